@@ -1,0 +1,154 @@
+/*
+ * krecycle_b200.h -- C ABI of the B200-native recycled hypergradient solve.
+ *
+ * The reference (arXiv 2412.08264, package `krecycle`) is pure Python and has
+ * no FFI; its "operator API" is a duck-typed protocol.  Each entry point below
+ * replaces one reference interface (cited as file:line under
+ * /root/reference/pkg/src/krecycle/) with plain pointers and sizes:
+ *
+ *   kr_op_prepare      <- the closures built by foe_hessian / mixed_jacobian
+ *                         (operators.py:363-383, 411-444): per-pixel curvature
+ *                         phi''(C_j xhat) and slope phi'(C_j xhat) cached once
+ *                         per (theta, xhat), like `kx_list` (operators.py:427)
+ *   kr_hvp             <- SymmetricOperator.__call__ / apply_matrix
+ *                         (operators.py:253-261): H v for t columns, B samples
+ *   kr_jadj            <- MixedJacobianOperator.apply_adjoint / _matrix
+ *                         (operators.py:290-298): J w for t columns, B samples
+ *   kr_lower_eval      <- foe_cost / foe_gradient (operators.py:329-353)
+ *   kr_rminres         <- rminres / minres (krylov.py:386-405) with
+ *                         _rminres_core (krylov.py:205-383), the residual
+ *                         recurrence (krylov.py:154-181) and the stop rules
+ *                         ResidualNormRule / NscRule (stopping.py:93-118)
+ *   kr_cg              <- cg (krylov.py:408-483)
+ *
+ * All array pointers are DEVICE pointers (fp64 unless stated), all calls are
+ * asynchronous on the given CUDA stream, and every function returns 0 on
+ * success or a negative KR_E* code; kr_last_error() gives the message.  The
+ * error codes map onto the reference's exceptions: KR_EINVAL -> ValueError,
+ * KR_ENONSPD -> NonSPDError, KR_ECUDA -> RuntimeError.
+ *
+ * Layout: image vectors are row-major (rows x cols), samples contiguous
+ * ([batch][n]); a block of t column vectors per sample is [batch][t][ld]
+ * (column j of sample b at ptr + b*bs + j*ld), i.e. the numpy n x t matrix of
+ * the reference stored column-major.
+ */
+#ifndef KRECYCLE_B200_H
+#define KRECYCLE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* kr_stream_t; /* == cudaStream_t */
+
+#define KR_ABI_VERSION 1
+
+#define KR_OK 0
+#define KR_EINVAL (-1)
+#define KR_ECUDA (-2)
+#define KR_ENONSPD (-3)
+#define KR_ENOMEM (-4)
+
+#define KR_MAX_BLUR 31
+#define KR_MAX_KSIZE 9
+#define KR_MAX_FILTERS 64
+
+/* data term: cost = data_scale/2 ||A x - y||^2 + ridge/2 ||x||^2 */
+#define KR_DATA_NONE 0
+#define KR_DATA_MASK 1  /* A = row subsampling; A^T A = diag(mask) (operators.py:187-235) */
+#define KR_DATA_BLUR 2  /* A = separable Gaussian, true convolution, zero boundary */
+#define KR_DATA_DENSE 3 /* H = explicit symmetric matrix (dense_operator, operators.py:269-274) */
+
+#define KR_REG_NONE 0
+#define KR_REG_FILTERS 1 /* sum_j w_j sum_p phi((c_j * x)_p) */
+#define KR_REG_TV 2      /* w sum_p sqrt(Dh^2 + Dv^2 + eps^2), Neumann forward differences */
+
+#define KR_POT_QUADRATIC 0  /* phi(t) = t^2 (reference FoE, operators.py:5-7) */
+#define KR_POT_SMOOTH_ABS 1 /* phi(t) = sqrt(t^2 + eps^2) */
+
+/* One Hessian / Jacobian family for a batch of samples sharing theta. */
+typedef struct kr_op {
+  int32_t rows, cols, batch;
+  int32_t data_kind;
+  double data_scale;
+  double ridge;
+  const double* mask;     /* KR_DATA_MASK: [batch][n] 0/1 (mask_bstride 0 = shared) */
+  int64_t mask_bstride;
+  const double* dense;    /* KR_DATA_DENSE: [batch][n][n] row-major */
+  int64_t dense_bstride;
+  int32_t blur_size;      /* odd, <= KR_MAX_BLUR */
+  double blur_taps[KR_MAX_BLUR]; /* 1-D normalised taps; blur = outer(taps, taps) */
+  int32_t reg_kind;
+  int32_t potential;
+  double eps;
+  int32_t num_filters, ksize;
+  const double* kernels;  /* [J][q][q] row-major (the theta layout of operators.py:150-172) */
+  const double* fweights; /* [J] exp(a_j) after the +/-30 clamp (operators.py:174-184); TV: [1] */
+  double* curv;           /* [batch][J][n] phi''(C_j xhat); TV: [batch][3][n] (m11, m12, m22) */
+  double* slope;          /* [batch][J][n] phi'(C_j xhat);  TV: [batch][2][n] (Dh xhat/s, Dv xhat/s) */
+  const double* xhat;     /* [batch][n] */
+} kr_op;
+
+/* Arguments of one batched recycled-MINRES solve (krylov.py:205-383). */
+typedef struct kr_solve_args {
+  int32_t max_iter;
+  int32_t s;               /* recycle columns (zero-padded columns are allowed) */
+  const double* g;         /* [batch][n] right-hand sides */
+  const double* w0;        /* [batch][n] initial guesses or NULL (zero) */
+  const double* U;         /* [batch][s][ld_uc] */
+  const double* C;         /* [batch][s][ld_uc], C^T C = I */
+  int64_t ld_uc, bs_uc;
+  int32_t stop_kind;       /* 0 = residual norm (stopping.py:93-99), 1 = NSC (stopping.py:102-118) */
+  double delta;            /* strict: stop when value < delta (stopping.py:89-90) */
+  int32_t nsc_s;           /* NSC columns */
+  const double* Z;         /* [batch][nsc_s][ld_z]: Z = W V_H,sel diag(mu_sel) (nsc_value, stopping.py:69-72) */
+  int64_t ld_z, bs_z;
+  const double* ZtC;       /* [batch][nsc_s][s]: Z^T C (row-major nsc_s x s) */
+  int32_t track_residual;  /* maintain r by the recurrence (krylov.py:154-181) */
+  double* w;               /* out [batch][n] solution */
+  double* r;               /* out [batch][n] tracked residual (if track_residual) */
+  double* basis;           /* out [batch][max_iter][ld_basis] Lanczos vectors, or NULL */
+  int64_t ld_basis, bs_basis;
+  double* res_norms;       /* out [batch][max_iter+1] */
+  double* stop_vals;       /* out [batch][max_iter+1] */
+  int32_t* iters;          /* out [batch] */
+  int32_t* reasons;        /* out [batch]: 0 tolerance, 1 max_iter, 2 breakdown */
+} kr_solve_args;
+
+int kr_abi_version(void);
+const char* kr_last_error(void);
+int kr_device_info(int32_t* num_sms, int32_t* cc_major, int32_t* cc_minor);
+/* sizeof(kr_op), sizeof(kr_solve_args): lets an FFI binding verify its struct mirror. */
+int kr_struct_sizes(int64_t* op_size, int64_t* args_size);
+
+int kr_op_prepare(const kr_op* op, kr_stream_t stream);
+
+int kr_hvp(const kr_op* op, const double* V, int64_t ldv, int64_t bsv, int32_t ncols,
+           double* HV, int64_t ldo, int64_t bso, kr_stream_t stream);
+
+int64_t kr_jadj_workspace(const kr_op* op, int32_t ncols);
+int kr_jadj(const kr_op* op, const double* W, int64_t ldw, int64_t bsw, int32_t ncols,
+            double* JW, int64_t ldo, int64_t bso, double* work, int64_t work_len,
+            kr_stream_t stream);
+
+/* Lower-level cost and gradient at X ([batch][n]) for data y ([batch][n] blur / [batch][n] masked-and-scattered):
+   cost[b] = data_scale/2 ||A x_b - y_b||^2 + ridge/2 ||x_b||^2 + R(x_b);  grad = d cost / d x. */
+int64_t kr_lower_workspace(const kr_op* op);
+int kr_lower_eval(const kr_op* op, const double* X, const double* Y, double* cost, double* grad,
+                  double* work, int64_t work_len, kr_stream_t stream);
+
+int64_t kr_rminres_workspace(const kr_op* op, const kr_solve_args* args);
+int kr_rminres(const kr_op* op, const kr_solve_args* args, double* work, int64_t work_len,
+               kr_stream_t stream);
+
+/* Plain CG (krylov.py:408-483); NonSPD curvature is reported through reasons[b] = 3. */
+int64_t kr_cg_workspace(const kr_op* op, const kr_solve_args* args);
+int kr_cg(const kr_op* op, const kr_solve_args* args, double* work, int64_t work_len,
+          kr_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KRECYCLE_B200_H */

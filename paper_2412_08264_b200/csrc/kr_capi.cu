@@ -1,0 +1,109 @@
+// kr_capi.cu -- ABI version, error state, operator validation, device queries.
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "kr_common.cuh"
+#include "kr_internal.h"
+
+namespace kr {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(KR_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return KR_OK;
+}
+
+int validate_op(const kr_op& op) {
+  if (op.rows <= 0 || op.cols <= 0) return fail(KR_EINVAL, "image shape must be positive");
+  if (op.batch < 0) return fail(KR_EINVAL, "batch must be nonnegative");
+  switch (op.data_kind) {
+    case KR_DATA_NONE:
+      break;
+    case KR_DATA_MASK:
+      if (!op.mask) return fail(KR_EINVAL, "mask data term without a mask");
+      break;
+    case KR_DATA_BLUR:
+      if (op.blur_size < 1 || op.blur_size % 2 == 0 || op.blur_size > KR_MAX_BLUR)
+        return fail(KR_EINVAL, "blur size must be odd and <= 31");
+      break;
+    case KR_DATA_DENSE:
+      if (!op.dense) return fail(KR_EINVAL, "dense operator without a matrix");
+      if (op.rows != 1) return fail(KR_EINVAL, "dense operators use rows = 1, cols = n");
+      return KR_OK;
+    default:
+      return fail(KR_EINVAL, "unknown data kind");
+  }
+  if (!(op.ridge >= 0.0)) return fail(KR_EINVAL, "ridge must be nonnegative");
+  switch (op.reg_kind) {
+    case KR_REG_NONE:
+      break;
+    case KR_REG_FILTERS:
+      if (op.num_filters < 1 || op.num_filters > KR_MAX_FILTERS) return fail(KR_EINVAL, "1 <= num_filters <= 64");
+      if (op.ksize < 1 || op.ksize % 2 == 0 || op.ksize > KR_MAX_KSIZE)
+        return fail(KR_EINVAL, "kernel size must be odd and <= 9");
+      if (!op.kernels || !op.fweights) return fail(KR_EINVAL, "filters without kernels / weights");
+      if (op.potential != KR_POT_QUADRATIC && op.potential != KR_POT_SMOOTH_ABS)
+        return fail(KR_EINVAL, "unknown potential");
+      if (op.potential == KR_POT_SMOOTH_ABS && !(op.eps > 0.0)) return fail(KR_EINVAL, "eps must be positive");
+      break;
+    case KR_REG_TV:
+      if (!op.fweights) return fail(KR_EINVAL, "TV without a weight");
+      if (!(op.eps > 0.0)) return fail(KR_EINVAL, "eps must be positive");
+      break;
+    default:
+      return fail(KR_EINVAL, "unknown regulariser kind");
+  }
+  return KR_OK;
+}
+
+int ensure_smem(const void* kernel, size_t bytes) {
+  if (bytes > 227 * 1024) return fail(KR_EINVAL, "tile needs more than 227 KB of shared memory");
+  if (bytes > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return fail(KR_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  }
+  return KR_OK;
+}
+
+int device_sms() {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+}  // namespace kr
+
+extern "C" int kr_abi_version(void) { return KR_ABI_VERSION; }
+
+extern "C" const char* kr_last_error(void) { return kr::g_last_error.c_str(); }
+
+extern "C" int kr_device_info(int32_t* num_sms, int32_t* cc_major, int32_t* cc_minor) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return kr::fail(KR_ECUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  if (num_sms) *num_sms = v;
+  cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMajor, dev);
+  if (cc_major) *cc_major = v;
+  cudaDeviceGetAttribute(&v, cudaDevAttrComputeCapabilityMinor, dev);
+  if (cc_minor) *cc_minor = v;
+  return KR_OK;
+}
+
+extern "C" int kr_struct_sizes(int64_t* op_size, int64_t* args_size) {
+  if (op_size) *op_size = (int64_t)sizeof(kr_op);
+  if (args_size) *args_size = (int64_t)sizeof(kr_solve_args);
+  return KR_OK;
+}

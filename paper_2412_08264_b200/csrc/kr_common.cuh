@@ -1,0 +1,341 @@
+// kr_common.cuh -- shared device code: operator descriptor access, tile
+// geometry, deterministic block reductions, and the shared-memory tile
+// stencils (Hessian-vector product and lower-level gradient).
+//
+// Reference semantics: operators.py:19-22 (true convolution, zero boundary),
+// operators.py:363-383 (H v), operators.py:329-353 (cost / gradient); the
+// blur / TV / phi_eps generalisation is documented in DESIGN.md.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/krecycle_b200.h"
+
+namespace kr {
+
+constexpr int TH = 16;        // tile rows
+constexpr int TW = 32;        // tile cols
+constexpr int TPX = TH * TW;  // pixels per tile
+constexpr int NT = 256;       // threads per block for tile kernels
+constexpr int PPT = TPX / NT; // tile pixels per thread
+constexpr int MAX_SLOTS = 160;
+
+struct Geom {
+  int rb;    // blur radius (0 if no blur)
+  int rq;    // filter radius (0 if no filters)
+  int H;     // halo of the input region
+  int RW;    // region width  = TW + 2H
+  int RH;    // region height = TH + 2H
+  int s0;    // doubles in S0 (input region)
+  int sa;    // doubles in SA (scratch A)
+  int sb;    // doubles in SB (scratch B)
+  int kw;    // doubles of kernel weights (J q^2)
+  int total; // total doubles of dynamic smem used by the stencil
+};
+
+__host__ __device__ inline int imax(int a, int b) { return a > b ? a : b; }
+
+__host__ __device__ inline Geom make_geom(const kr_op& op) {
+  Geom g;
+  g.rb = (op.data_kind == KR_DATA_BLUR) ? op.blur_size / 2 : 0;
+  g.rq = (op.reg_kind == KR_REG_FILTERS) ? op.ksize / 2 : 0;
+  g.H = imax(imax(2 * g.rb, 2 * g.rq), 1);
+  g.RW = TW + 2 * g.H;
+  g.RH = TH + 2 * g.H;
+  g.s0 = g.RH * g.RW;
+  int s1 = (op.data_kind == KR_DATA_BLUR) ? (TH + 4 * g.rb) * (TW + 2 * g.rb) : 0;
+  int s3 = (op.data_kind == KR_DATA_BLUR) ? (TH + 2 * g.rb) * TW : 0;
+  int s4 = (op.reg_kind == KR_REG_FILTERS) ? (TH + 2 * g.rq) * (TW + 2 * g.rq) : 0;
+  int s5 = (op.reg_kind == KR_REG_TV) ? 2 * (TH + 1) * (TW + 1) : 0;
+  g.sa = imax(imax(s1, s3), imax(s4, s5));
+  g.sb = (op.data_kind == KR_DATA_BLUR) ? (TH + 2 * g.rb) * (TW + 2 * g.rb) : 0;
+  g.kw = (op.reg_kind == KR_REG_FILTERS) ? op.num_filters * op.ksize * op.ksize : 0;
+  g.total = g.s0 + g.sa + g.sb + TPX + g.kw + KR_MAX_FILTERS + KR_MAX_BLUR + 1;
+  return g;
+}
+
+__host__ __device__ inline int64_t op_n(const kr_op& op) { return (int64_t)op.rows * op.cols; }
+
+__host__ __device__ inline int tiles_y(const kr_op& op) { return (op.rows + TH - 1) / TH; }
+__host__ __device__ inline int tiles_x(const kr_op& op) { return (op.cols + TW - 1) / TW; }
+__host__ __device__ inline int num_tiles(const kr_op& op) {
+  if (op.data_kind == KR_DATA_DENSE) return (int)((op_n(op) + TPX - 1) / TPX);
+  return tiles_y(op) * tiles_x(op);
+}
+
+// ---------------------------------------------------------------------------
+// deterministic reductions
+
+__device__ inline double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Sum NV per-thread values over the block; red is smem of >= NV*32 doubles.
+// Result in red[0..NV) after the call (visible to all threads).
+template <int NV>
+__device__ inline void block_sum(double (&v)[NV], double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) red[i * 32 + warp] = v[i];
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double acc = 0.0;
+    for (int w = 0; w < nw; ++w) acc += red[threadIdx.x * 32 + w];
+    red[NV * 32 + threadIdx.x] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) red[threadIdx.x] = red[NV * 32 + threadIdx.x];
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// tile stencil: H v on one TH x TW tile of sample b.
+//
+//   out = data_scale A^T A v + ridge v + sum_j w_j C_j^T (kappa_j . C_j v)   (filters)
+//   out = data_scale A^T A v + ridge v + w D^T M D v                         (TV)
+//
+// `in` describes the sample's input vector (TileIn: the solvers feed the
+// unnormalised Lanczos vector and beta, so H sees exactly v = u/beta).  The result is left
+// in `res` (smem, TPX doubles, row-major tile).  All threads must call.
+
+struct Smem {
+  double* S0;
+  double* SA;
+  double* SB;
+  double* res;
+  double* kw;  // kernels
+  double* fw;  // filter weights
+  double* taps;  // blur taps
+};
+
+__device__ inline Smem carve(const Geom& g, double* base) {
+  Smem s;
+  s.S0 = base;
+  s.SA = s.S0 + g.s0;
+  s.SB = s.SA + g.sa;
+  s.res = s.SB + g.sb;
+  s.kw = s.res + TPX;
+  s.fw = s.kw + g.kw;
+  s.taps = s.fw + KR_MAX_FILTERS;
+  return s;
+}
+
+// Load the filter bank into smem (call once per block).
+__device__ inline void load_weights(const kr_op& op, const Geom& g, Smem& sm) {
+  for (int i = threadIdx.x; i < g.kw; i += blockDim.x) sm.kw[i] = op.kernels[i];
+  int nf = (op.reg_kind == KR_REG_TV) ? 1 : (op.reg_kind == KR_REG_FILTERS ? op.num_filters : 0);
+  for (int i = threadIdx.x; i < nf; i += blockDim.x) sm.fw[i] = op.fweights[i];
+  for (int i = threadIdx.x; i < op.blur_size && op.data_kind == KR_DATA_BLUR; i += blockDim.x)
+    sm.taps[i] = op.blur_taps[i];
+  __syncthreads();
+}
+
+// Input of a tile stencil: v = a / div, or v = a + coef * b when b != nullptr
+// (CG's direction p = r + (rr_new/rr) p_old, formed on the fly).
+struct TileIn {
+  const double* a;
+  double div;
+  const double* b;
+  double coef;
+  __device__ inline double at(int64_t p) const { return b ? a[p] + coef * b[p] : a[p] / div; }
+};
+
+__device__ inline void load_region(const kr_op& op, const Geom& g, const TileIn& in, int y0, int x0,
+                                   double* S0) {
+  const int rows = op.rows, cols = op.cols;
+  for (int i = threadIdx.x; i < g.s0; i += blockDim.x) {
+    int yy = i / g.RW, xx = i - yy * g.RW;
+    int y = y0 - g.H + yy, x = x0 - g.H + xx;
+    double v = 0.0;
+    if (y >= 0 && y < rows && x >= 0 && x < cols) v = in.at((int64_t)y * cols + x);
+    S0[i] = v;
+  }
+}
+
+// Dense operator: res[l] = sum_j M[p][j] v[j] for the tile's flat rows.
+__device__ inline void tile_hvp_dense(const kr_op& op, int b, const TileIn& in, int tile, double* res) {
+  const int64_t n = op_n(op);
+  const double* M = op.dense + (int64_t)b * op.dense_bstride;
+  for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
+    int64_t p = (int64_t)tile * TPX + l;
+    double acc = 0.0;
+    if (p < n) {
+      const double* row = M + p * n;
+      for (int64_t j = 0; j < n; ++j) acc += row[j] * in.at(j);
+    }
+    res[l] = acc;
+  }
+  __syncthreads();
+}
+
+// Blur data term on the loaded region: res (+)= data_scale * A^T A v.
+__device__ inline void tile_blur_normal(const kr_op& op, const Geom& g, Smem& sm, int y0, int x0,
+                                        bool accumulate) {
+  const int rb = g.rb, bs = op.blur_size, H = g.H;
+  const int rows = op.rows, cols = op.cols;
+  const double* __restrict__ tp = sm.taps;
+  // S1: horizontal conv, rows [y0-2rb, y0+TH+2rb), cols [x0-rb, x0+TW+rb)
+  const int w1 = TW + 2 * rb, h1 = TH + 4 * rb;
+  double* S1 = sm.SA;
+  for (int i = threadIdx.x; i < h1 * w1; i += blockDim.x) {
+    int r1 = i / w1, c1 = i - r1 * w1;
+    const double* src = sm.S0 + (r1 + H - 2 * rb) * g.RW + c1 + H;
+    double acc = 0.0;
+    for (int u = 0; u < bs; ++u) acc += tp[u] * src[-u];
+    S1[i] = acc;
+  }
+  __syncthreads();
+  // S2 = A v (vertical conv), rows [y0-rb, y0+TH+rb), cols [x0-rb, x0+TW+rb); zero outside image
+  const int w2 = w1, h2 = TH + 2 * rb;
+  double* S2 = sm.SB;
+  for (int i = threadIdx.x; i < h2 * w2; i += blockDim.x) {
+    int r2 = i / w2, c2 = i - r2 * w2;
+    int y = y0 - rb + r2, x = x0 - rb + c2;
+    double acc = 0.0;
+    if (y >= 0 && y < rows && x >= 0 && x < cols) {
+      const double* src = S1 + (r2 + 2 * rb) * w1 + c2;
+      for (int u = 0; u < bs; ++u) acc += tp[u] * src[-u * w1];
+    }
+    S2[i] = acc;
+  }
+  __syncthreads();
+  // S3: horizontal correlation, rows [y0-rb, y0+TH+rb), cols [x0, x0+TW)
+  double* S3 = sm.SA;
+  for (int i = threadIdx.x; i < h2 * TW; i += blockDim.x) {
+    int r3 = i / TW, c3 = i - r3 * TW;
+    const double* src = S2 + r3 * w2 + c3;
+    double acc = 0.0;
+    for (int u = 0; u < bs; ++u) acc += tp[u] * src[u];
+    S3[i] = acc;
+  }
+  __syncthreads();
+  const double ds = op.data_scale;
+  for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
+    int ty = l / TW, tx = l - ty * TW;
+    const double* src = S3 + ty * TW + tx;
+    double acc = 0.0;
+    for (int u = 0; u < bs; ++u) acc += tp[u] * src[u * TW];
+    if (accumulate) sm.res[l] += ds * acc;
+    else sm.res[l] = ds * acc;
+  }
+  __syncthreads();
+}
+
+__device__ inline void tile_hvp(const kr_op& op, const Geom& g, Smem& sm, int b, const TileIn& in, int tile) {
+  if (op.data_kind == KR_DATA_DENSE) {
+    tile_hvp_dense(op, b, in, tile, sm.res);
+    return;
+  }
+  const int tyc = tiles_x(op);
+  const int y0 = (tile / tyc) * TH, x0 = (tile % tyc) * TW;
+  const int rows = op.rows, cols = op.cols, H = g.H;
+  const int64_t n = op_n(op);
+  load_region(op, g, in, y0, x0, sm.S0);
+  __syncthreads();
+
+  // pointwise part: mask data term + ridge
+  const double* mask = (op.data_kind == KR_DATA_MASK) ? op.mask + (int64_t)b * op.mask_bstride : nullptr;
+  for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
+    int ty = l / TW, tx = l - ty * TW;
+    int y = y0 + ty, x = x0 + tx;
+    double v = sm.S0[(ty + H) * g.RW + tx + H];
+    double acc = 0.0;
+    if (y < rows && x < cols) {
+      if (mask) acc = (op.data_scale == 1.0 ? mask[(int64_t)y * cols + x] : op.data_scale * mask[(int64_t)y * cols + x]) * v;
+      acc += op.ridge * v;
+    }
+    sm.res[l] = acc;
+  }
+  __syncthreads();
+  if (op.data_kind == KR_DATA_BLUR) tile_blur_normal(op, g, sm, y0, x0, true);
+
+  if (op.reg_kind == KR_REG_FILTERS) {
+    const int q = op.ksize, rq = g.rq;
+    const int w4 = TW + 2 * rq, h4 = TH + 2 * rq;
+    double* S4 = sm.SA;
+    const bool quad = (op.potential == KR_POT_QUADRATIC);
+    for (int j = 0; j < op.num_filters; ++j) {
+      const double* kj = sm.kw + j * q * q;
+      const double* cj = quad ? nullptr : op.curv + ((int64_t)b * op.num_filters + j) * n;
+      for (int i = threadIdx.x; i < h4 * w4; i += blockDim.x) {
+        int r4 = i / w4, c4 = i - r4 * w4;
+        int y = y0 - rq + r4, x = x0 - rq + c4;
+        double e = 0.0;
+        if (y >= 0 && y < rows && x >= 0 && x < cols) {
+          const double* src = sm.S0 + (r4 + H) * g.RW + c4 + H;
+          double acc = 0.0;
+          for (int a = 0; a < q; ++a)
+            for (int bb = 0; bb < q; ++bb) acc += kj[a * q + bb] * src[-a * g.RW - bb];
+          e = quad ? 2.0 * acc : cj[(int64_t)y * cols + x] * acc;
+        }
+        S4[i] = e;
+      }
+      __syncthreads();
+      const double wj = sm.fw[j];
+      for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
+        int ty = l / TW, tx = l - ty * TW;
+        const double* src = S4 + ty * w4 + tx;
+        double acc = 0.0;
+        for (int a = 0; a < q; ++a)
+          for (int bb = 0; bb < q; ++bb) acc += kj[a * q + bb] * src[a * w4 + bb];
+        sm.res[l] += wj * acc;
+      }
+      __syncthreads();
+    }
+  } else if (op.reg_kind == KR_REG_TV) {
+    // p = M D v on rows [y0-1, y0+TH), cols [x0-1, x0+TW); masked where D's row is zero
+    const int w5 = TW + 1, h5 = TH + 1;
+    double* PH = sm.SA;
+    double* PV = sm.SA + h5 * w5;
+    const double* M = op.curv + (int64_t)b * 3 * n;
+    for (int i = threadIdx.x; i < h5 * w5; i += blockDim.x) {
+      int r5 = i / w5, c5 = i - r5 * w5;
+      int y = y0 - 1 + r5, x = x0 - 1 + c5;
+      double ph = 0.0, pv = 0.0;
+      if (y >= 0 && y < rows && x >= 0 && x < cols) {
+        const double* c = sm.S0 + (y - y0 + H) * g.RW + (x - x0 + H);
+        double dh = (x < cols - 1) ? c[1] - c[0] : 0.0;
+        double dv = (y < rows - 1) ? c[g.RW] - c[0] : 0.0;
+        int64_t p = (int64_t)y * cols + x;
+        double m11 = M[p], m12 = M[n + p], m22 = M[2 * n + p];
+        if (x < cols - 1) ph = m11 * dh + m12 * dv;
+        if (y < rows - 1) pv = m12 * dh + m22 * dv;
+      }
+      PH[i] = ph;
+      PV[i] = pv;
+    }
+    __syncthreads();
+    const double wa = sm.fw[0];
+    for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
+      int ty = l / TW, tx = l - ty * TW;
+      int i = (ty + 1) * w5 + tx + 1;
+      // D_h^T p_h = -p_h[x] + p_h[x-1];  D_v^T p_v = -p_v[y] + p_v[y-1]
+      double dth = -PH[i] + PH[i - 1];
+      double dtv = -PV[i] + PV[i - w5];
+      sm.res[l] += wa * (dth + dtv);
+    }
+    __syncthreads();
+  }
+}
+
+// Global pixel index of tile-local pixel l, or -1 if outside the image.
+__device__ inline int64_t tile_pixel(const kr_op& op, int tile, int l) {
+  if (op.data_kind == KR_DATA_DENSE) {
+    int64_t p = (int64_t)tile * TPX + l;
+    return p < op_n(op) ? p : -1;
+  }
+  const int tyc = tiles_x(op);
+  int y = (tile / tyc) * TH + l / TW, x = (tile % tyc) * TW + l % TW;
+  if (y >= op.rows || x >= op.cols) return -1;
+  return (int64_t)y * op.cols + x;
+}
+
+}  // namespace kr

@@ -1,0 +1,31 @@
+// kr_internal.h -- host-side error plumbing shared by the C ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/krecycle_b200.h"
+
+namespace kr {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int check_launch(const char* what);
+int validate_op(const kr_op& op);
+int ensure_smem(const void* kernel, size_t bytes);
+int device_sms();
+
+}  // namespace kr
+
+#define KR_CHECK_ARG(cond, msg)                      \
+  do {                                               \
+    if (!(cond)) return ::kr::fail(KR_EINVAL, msg);  \
+  } while (0)
+
+#define KR_TRY(expr)              \
+  do {                            \
+    int _kr_rc = (expr);          \
+    if (_kr_rc != KR_OK) return _kr_rc; \
+  } while (0)

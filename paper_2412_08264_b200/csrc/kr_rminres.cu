@@ -1,0 +1,612 @@
+// kr_rminres.cu -- batched recycled MINRES as ONE persistent cooperative kernel.
+//
+// Algorithm: /root/reference/pkg/src/krecycle/krylov.py:205-383 (Alg. 3 with the
+// corrected sign w += c_k zeta_{k-1}(vt - bt)), stop rules stopping.py:69-118,
+// residual recurrence krylov.py:154-181.  B200 structure:
+//
+//  * one launch runs every iteration of every sample; blocks are partitioned
+//    by sample (Gs blocks per sample), grid-wide barriers separate the three
+//    reduction phases of an iteration:
+//      P1  finish iteration k-1 (Givens, vt / w / residual updates, stop test),
+//          v_k = u_{k-1}/beta_k, tile stencil hv_k = H v_k, partial C^T hv_k
+//      P2  NSC decision, u = hv_k - C chv_k, partial alpha = v_k . u
+//      P3  u -= alpha v_k; u -= beta v_{k-1}, partial ||u||^2
+//  * the recycle-space terms b = U chv and H b~ = C chv are carried in s-space
+//    (b~_k = U btc_k, btc_k = (chv_k - gamma btc_{k-2} - delta btc_{k-1})/eps~);
+//    the solution is w = w_v - U Omega and the residual r = r_v + C Omega with
+//    Omega = sum_k step_k btc_k, so U is read once per solve instead of once
+//    per iteration (exact in exact arithmetic);
+//  * NSC reads Z = W V_H,sel diag(mu_sel) (one n x s block) instead of W (n x t):
+//    Z^T r = Z^T r_v + (Z^T C) Omega;
+//  * every reduction is a fixed-order two-level sum (warp tree, block, then the
+//    sample's blocks in rank order), so results are bitwise reproducible.
+#include <cooperative_groups.h>
+
+#include <string>
+
+#include "kr_common.cuh"
+#include "kr_internal.h"
+#include "kr_solver.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace kr {
+
+struct SolverWork {
+  double* tmp;     // unnormalised next Lanczos vector u (global: read with halo)
+  double* u;       // hv - C chv
+  double* hv[2];   // H v_k (double-buffered by k parity)
+  double* vt[2];   // v~ recurrence
+  double* hvt[2];  // H v~ recurrence
+  double* rv;      // residual without the C Omega term
+  double* wv;      // solution without the -U Omega term
+  double* vr[2];   // Lanczos vectors when the basis is not tracked
+  double* part;    // [B][NSLOT][Gs] block partials
+  int* done;       // finished-sample counter
+};
+
+struct Params {
+  kr_op op;
+  kr_solve_args a;
+  SolverWork w;
+  int Gs;       // blocks per sample
+  int b0;       // first sample of this launch
+  int nb;       // samples in this launch
+  int nslot;
+  int64_t n;
+  __device__ inline Partials parts() const { return Partials{w.part, nslot, Gs}; }
+};
+
+struct Scalars {
+  double beta, beta_prev, alpha, alpha_prev;
+  double c1, s1, c2, s2, zeta;
+  double gamma, delta, eps_r, step;
+  double tol_bd, delta_stop;
+  int active, finished, counted, pending, pend_k, pend_broke, do_update, do_hvp, iters, reason;
+};
+
+__device__ inline double* vec(double* base, int64_t n, int b) { return base + (int64_t)b * n; }
+
+// Lanczos vector v_k (k >= 1)
+__device__ inline double* lanczos(const Params& P, int b, int k) {
+  if (P.a.basis) return P.a.basis + (int64_t)b * P.a.bs_basis + (int64_t)(k - 1) * P.a.ld_basis;
+  return vec(P.w.vr[k & 1], P.n, b);
+}
+
+__global__ void __launch_bounds__(NT) rminres_kernel(Params P) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double smem[];
+  const kr_op& op = P.op;
+  const kr_solve_args& A = P.a;
+  const Geom g = make_geom(op);
+  Smem sm = carve(g, smem);
+  double* tail = smem + g.total;
+  double* slot_acc = tail;               // MAX_SLOTS
+  double* chv = slot_acc + MAX_SLOTS;    // MAX_S (also the initial projection t)
+  double* btc1 = chv + MAX_S;
+  double* btc2 = btc1 + MAX_S;
+  double* omega = btc2 + MAX_S;
+  double* nscv = omega + MAX_S;          // MAX_NSC
+  double* red = nscv + MAX_NSC;          // 8*33+8
+  __shared__ Scalars sc;
+
+  const int bl = blockIdx.x / P.Gs;      // local sample index
+  const int j = blockIdx.x % P.Gs;       // rank within the sample
+  const int b = P.b0 + bl;               // global sample index
+  const int64_t n = P.n;
+  const int s = A.s, ns = (A.stop_kind == 1) ? A.nsc_s : 0;
+  const int SL_CHV = 0, SL_NSC = s, SL_ALPHA = s + ns, SL_BETA2 = s + ns + 1;
+  const int64_t lo = n * j / P.Gs, hi = n * (j + 1) / P.Gs;
+  const int ntiles = num_tiles(op);
+  const bool leader = (j == 0);
+  const bool track = A.track_residual != 0;
+  const Partials PP = P.parts();
+
+  const double* U = A.U ? A.U + (int64_t)b * A.bs_uc : nullptr;
+  const double* C = A.C ? A.C + (int64_t)b * A.bs_uc : nullptr;
+  const double* Z = (ns > 0) ? A.Z + (int64_t)b * A.bs_z : nullptr;
+  const double* ZtC = (ns > 0 && s > 0) ? A.ZtC + (int64_t)b * ns * s : nullptr;
+  const double* gb = A.g + (int64_t)b * n;
+  const double* w0 = A.w0 ? A.w0 + (int64_t)b * n : nullptr;
+  double* tmp = vec(P.w.tmp, n, b);
+  double* ub = vec(P.w.u, n, b);
+  double* rv = vec(P.w.rv, n, b);
+  double* wv = vec(P.w.wv, n, b);
+  double* res_norms = A.res_norms + (int64_t)b * (A.max_iter + 1);
+  double* stop_vals = A.stop_vals + (int64_t)b * (A.max_iter + 1);
+
+  load_weights(op, g, sm);
+  for (int i = threadIdx.x; i < MAX_SLOTS; i += blockDim.x) slot_acc[i] = 0.0;
+  for (int i = threadIdx.x; i < MAX_S; i += blockDim.x) {
+    chv[i] = 0.0;
+    btc1[i] = 0.0;
+    btc2[i] = 0.0;
+    omega[i] = 0.0;
+  }
+  if (threadIdx.x == 0) {
+    sc.active = 1;
+    sc.finished = 0;
+    sc.counted = 0;
+    sc.pending = 0;
+    sc.iters = 0;
+    sc.reason = R_MAXIT;
+    sc.c1 = 1.0;
+    sc.s1 = 0.0;
+    sc.c2 = 0.0;
+    sc.s2 = 0.0;
+    sc.beta_prev = 0.0;
+    sc.alpha_prev = 0.0;
+    sc.delta_stop = A.delta;
+  }
+  __syncthreads();
+
+  // ---------------- setup S1: r0 = g - H w0, partial C^T r0 ----------------
+  if (w0) {
+    for (int tile = j; tile < ntiles; tile += P.Gs) {
+      tile_hvp(op, g, sm, b, TileIn{w0, 1.0, nullptr, 0.0}, tile);
+      for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
+        int64_t p = tile_pixel(op, tile, l);
+        double r = 0.0;
+        if (p >= 0) {
+          r = gb[p] - sm.res[l];
+          tmp[p] = r;
+        }
+        sm.res[l] = r;
+      }
+      __syncthreads();
+    }
+  } else {
+    for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) tmp[p] = gb[p];  // g - H 0 == g exactly
+  }
+  // zero the recurrence state
+  for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+    vec(P.w.vt[0], n, b)[p] = 0.0;
+    vec(P.w.vt[1], n, b)[p] = 0.0;
+    if (track) {
+      vec(P.w.hvt[0], n, b)[p] = 0.0;
+      vec(P.w.hvt[1], n, b)[p] = 0.0;
+    }
+  }
+  grid.sync();  // tmp complete (written by tiles when w0 given)
+  if (s > 0) {
+    slot_dots(C, A.ld_uc, s, lo, hi, [&](int64_t p) { return tmp[p]; }, slot_acc, red);
+    write_partials(PP, bl, j, SL_CHV, s, slot_acc);
+  }
+  grid.sync();
+  // ---------------- setup S2: projection onto the recycle space ----------------
+  if (s > 0) {
+    reduce_slots(PP, bl, SL_CHV, s, chv);  // t = C^T r0
+    __syncthreads();
+  }
+  {
+    double bsq[1] = {0.0};
+    for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+      double r = tmp[p];
+      double w = w0 ? w0[p] : 0.0;
+      if (s > 0) {
+        double ut = 0.0, ct = 0.0;
+        for (int i = 0; i < s; ++i) {
+          ut += U[(int64_t)i * A.ld_uc + p] * chv[i];
+          ct += C[(int64_t)i * A.ld_uc + p] * chv[i];
+        }
+        w = w + ut;  // w = w + U t
+        r = r - ct;  // r = r - C t
+        tmp[p] = r;
+      }
+      wv[p] = w;
+      if (track) rv[p] = r;
+      bsq[0] += r * r;
+    }
+    block_sum<1>(bsq, red);
+    if (threadIdx.x == 0) P.w.part[((int64_t)bl * P.nslot + SL_BETA2) * P.Gs + j] = red[0];
+    if (ns > 0) {
+      for (int i = threadIdx.x; i < ns; i += blockDim.x) slot_acc[i] = 0.0;
+      __syncthreads();
+      slot_dots(Z, A.ld_z, ns, lo, hi, [&](int64_t p) { return tmp[p]; }, slot_acc, red);
+      write_partials(PP, bl, j, SL_NSC, ns, slot_acc);
+    }
+  }
+  // g-scale for the breakdown tolerance (krylov.py:236-237): ||g||
+  {
+    double gsq[1] = {0.0};
+    for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) gsq[0] += gb[p] * gb[p];
+    block_sum<1>(gsq, red);
+    if (threadIdx.x == 0) P.w.part[((int64_t)bl * P.nslot + SL_ALPHA) * P.Gs + j] = red[0];
+  }
+  grid.sync();
+  if (threadIdx.x == 0) {
+    double gg = 0.0;
+    const double* src = P.w.part + ((int64_t)bl * P.nslot + SL_ALPHA) * P.Gs;
+    for (int jj = 0; jj < P.Gs; ++jj) gg += src[jj];
+    double gn = sqrt(gg);
+    sc.tol_bd = BREAKDOWN_RTOL * (gn > 1e-300 ? gn : 1e-300);
+  }
+  __syncthreads();
+
+  // ---------------- main loop ----------------
+  for (int k = 1; k <= A.max_iter + 1; ++k) {
+    if (k > 1 && *((volatile int*)P.w.done) >= P.nb) break;
+    // ===== P1 =====
+    if (threadIdx.x == 0) {
+      sc.do_update = 0;
+      sc.do_hvp = 0;
+      if (sc.active) {
+        const double* src = P.w.part + ((int64_t)bl * P.nslot + SL_BETA2) * P.Gs;
+        double bb = 0.0;
+        for (int jj = 0; jj < P.Gs; ++jj) bb += src[jj];
+        double beta_k = sqrt(bb);
+        bool broke = beta_k <= sc.tol_bd;
+        if (k == 1) {
+          sc.beta = beta_k;
+          sc.zeta = beta_k;
+          if (leader) res_norms[0] = beta_k;
+          if (A.stop_kind == 0) {
+            if (leader) stop_vals[0] = beta_k;
+            if (beta_k < sc.delta_stop) {
+              sc.active = 0; sc.finished = 1; sc.iters = 0; sc.reason = R_TOL;
+            } else if (broke) {
+              sc.active = 0; sc.finished = 1; sc.iters = 0; sc.reason = R_BREAK;
+            }
+          } else {
+            sc.pending = 1; sc.pend_k = 0; sc.pend_broke = broke;
+          }
+        } else {
+          // finish iteration k-1 (krylov.py:298-338)
+          const double bp = sc.beta;  // beta_{k-1}
+          const double al = sc.alpha;
+          double gamma = sc.s2 * bp;
+          double delta = sc.c1 * sc.c2 * bp + sc.s1 * al;
+          double eps = -sc.s1 * sc.c2 * bp + sc.c1 * al;
+          double eps_r = hypot(eps, beta_k);
+          if (eps_r == 0.0) {
+            sc.active = 0; sc.finished = 1; sc.iters = k - 2; sc.reason = R_BREAK;
+          } else {
+            double s_new = beta_k / eps_r, c_new = eps / eps_r;
+            double zeta_prev = sc.zeta;
+            sc.zeta = -s_new * zeta_prev;
+            sc.gamma = gamma; sc.delta = delta; sc.eps_r = eps_r;
+            sc.step = c_new * zeta_prev;
+            sc.do_update = 1;
+            sc.c2 = sc.c1; sc.s2 = sc.s1; sc.c1 = c_new; sc.s1 = s_new;
+            sc.beta_prev = bp;
+            sc.beta = beta_k;
+            double rn = fabs(sc.zeta);
+            if (leader) res_norms[k - 1] = rn;
+            if (A.stop_kind == 0) {
+              if (leader) stop_vals[k - 1] = rn;
+              if (rn < sc.delta_stop) {
+                sc.active = 0; sc.finished = 1; sc.iters = k - 1; sc.reason = R_TOL;
+              } else if (broke) {
+                sc.active = 0; sc.finished = 1; sc.iters = k - 1; sc.reason = R_BREAK;
+              } else if (k - 1 == A.max_iter) {
+                sc.active = 0; sc.finished = 1; sc.iters = k - 1; sc.reason = R_MAXIT;
+              }
+            } else {
+              sc.pending = 1; sc.pend_k = k - 1; sc.pend_broke = broke;
+            }
+          }
+        }
+        if (sc.active && !(sc.pending && sc.pend_broke) && k <= A.max_iter) sc.do_hvp = 1;
+      }
+    }
+    __syncthreads();
+    if (sc.do_update) {
+      // s-space recurrences (thread per recycle column)
+      for (int i = threadIdx.x; i < s; i += blockDim.x) {
+        double bt = (chv[i] - sc.gamma * btc2[i] - sc.delta * btc1[i]) / sc.eps_r;
+        omega[i] += sc.step * bt;
+        btc2[i] = btc1[i];
+        btc1[i] = bt;
+      }
+      // pointwise updates of iteration k-1
+      const int km = k - 1;
+      const double* v = lanczos(P, b, km);
+      double* vtn = vec(P.w.vt[km & 1], n, b);        // holds vt_{k-3} -> becomes vt_{k-1}
+      const double* vto = vec(P.w.vt[(km + 1) & 1], n, b);  // vt_{k-2}
+      const double* hvk = vec(P.w.hv[km & 1], n, b);
+      double* hvtn = vec(P.w.hvt[km & 1], n, b);
+      const double* hvto = vec(P.w.hvt[(km + 1) & 1], n, b);
+      const double ga = sc.gamma, de = sc.delta, er = sc.eps_r, st = sc.step;
+      for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+        double vt = (v[p] - ga * vtn[p] - de * vto[p]) / er;
+        vtn[p] = vt;
+        wv[p] = wv[p] + st * vt;
+        if (track) {
+          double ht = (hvk[p] - de * hvto[p] - ga * hvtn[p]) / er;
+          hvtn[p] = ht;
+          rv[p] -= st * ht;
+        }
+      }
+    }
+    __syncthreads();
+    if (sc.pending && k > 1 && sc.do_update) {
+      for (int i = threadIdx.x; i < ns; i += blockDim.x) slot_acc[i] = 0.0;
+      __syncthreads();
+      slot_dots(Z, A.ld_z, ns, lo, hi, [&](int64_t p) { return rv[p]; }, slot_acc, red);
+      write_partials(PP, bl, j, SL_NSC, ns, slot_acc);
+    }
+    if (sc.finished && !sc.counted) {
+      // finalize: w = w_v - U Omega, r = r_v + C Omega (krylov.py:184-202 outputs)
+      double* wout = A.w + (int64_t)b * n;
+      double* rout = (track && A.r) ? A.r + (int64_t)b * n : nullptr;
+      for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+        double uo = 0.0, co = 0.0;
+        for (int i = 0; i < s; ++i) {
+          uo += U[(int64_t)i * A.ld_uc + p] * omega[i];
+          co += C[(int64_t)i * A.ld_uc + p] * omega[i];
+        }
+        wout[p] = wv[p] - uo;
+        if (rout) rout[p] = rv[p] + co;
+      }
+    }
+    if (sc.do_hvp) {
+      const double beta_k = sc.beta;
+      double* vk = lanczos(P, b, k);
+      for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) vk[p] = tmp[p] / beta_k;
+      for (int i = threadIdx.x; i < s; i += blockDim.x) slot_acc[i] = 0.0;
+      __syncthreads();
+      double* hvk = vec(P.w.hv[k & 1], n, b);
+      for (int tile = j; tile < ntiles; tile += P.Gs) {
+        tile_hvp(op, g, sm, b, TileIn{tmp, beta_k, nullptr, 0.0}, tile);
+        for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
+          int64_t p = tile_pixel(op, tile, l);
+          if (p >= 0) hvk[p] = sm.res[l];
+        }
+        if (s > 0) {
+          // partial C^T hv over this tile's pixels
+          for (int base = 0; base < s; base += 8) {
+            double v8[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v8[i] = 0.0;
+            for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
+              int64_t p = tile_pixel(op, tile, l);
+              if (p < 0) continue;
+              double h = sm.res[l];
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (base + i < s) v8[i] += C[(int64_t)(base + i) * A.ld_uc + p] * h;
+            }
+            block_sum<8>(v8, red);
+            if (threadIdx.x < 8 && base + threadIdx.x < s) slot_acc[base + threadIdx.x] += red[threadIdx.x];
+            __syncthreads();
+          }
+        }
+        __syncthreads();
+      }
+      if (s > 0) write_partials(PP, bl, j, SL_CHV, s, slot_acc);
+    }
+    grid.sync();
+    // ===== P2 =====
+    if (sc.pending) {
+      reduce_slots(PP, bl, SL_NSC, ns, nscv);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double ss = 0.0;
+        for (int i = 0; i < ns; ++i) {
+          double z = nscv[i];
+          if (ZtC) {
+            double corr = 0.0;
+            for (int l = 0; l < s; ++l) corr += ZtC[(int64_t)i * s + l] * omega[l];
+            z += corr;
+          }
+          ss += z * z;
+        }
+        double val = sqrt(ss);
+        const int kk = sc.pend_k;
+        if (leader) stop_vals[kk] = val;
+        sc.pending = 0;
+        if (val < sc.delta_stop) {
+          sc.active = 0; sc.finished = 1; sc.iters = kk; sc.reason = R_TOL;
+        } else if (sc.pend_broke) {
+          sc.active = 0; sc.finished = 1; sc.iters = kk; sc.reason = R_BREAK;
+        } else if (kk == A.max_iter) {
+          sc.active = 0; sc.finished = 1; sc.iters = kk; sc.reason = R_MAXIT;
+        }
+        sc.do_hvp = sc.do_hvp && sc.active;
+      }
+      __syncthreads();
+      if (sc.finished && !sc.counted) {
+        double* wout = A.w + (int64_t)b * n;
+        double* rout = (track && A.r) ? A.r + (int64_t)b * n : nullptr;
+        for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+          double uo = 0.0, co = 0.0;
+          for (int i = 0; i < s; ++i) {
+            uo += U[(int64_t)i * A.ld_uc + p] * omega[i];
+            co += C[(int64_t)i * A.ld_uc + p] * omega[i];
+          }
+          wout[p] = wv[p] - uo;
+          if (rout) rout[p] = rv[p] + co;
+        }
+      }
+    }
+    if (sc.do_hvp) {
+      if (s > 0) {
+        reduce_slots(PP, bl, SL_CHV, s, chv);
+        __syncthreads();
+      }
+      const double* vk = lanczos(P, b, k);
+      const double* hvk = vec(P.w.hv[k & 1], n, b);
+      double al[1] = {0.0};
+      for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+        double x = hvk[p];
+        if (s > 0) {
+          double cc = 0.0;
+          for (int i = 0; i < s; ++i) cc += C[(int64_t)i * A.ld_uc + p] * chv[i];
+          x = x - cc;  // vnext = hv - C chv
+        }
+        ub[p] = x;
+        al[0] += vk[p] * x;
+      }
+      block_sum<1>(al, red);
+      if (threadIdx.x == 0) P.w.part[((int64_t)bl * P.nslot + SL_ALPHA) * P.Gs + j] = red[0];
+    }
+    grid.sync();
+    // ===== P3 =====
+    if (sc.do_hvp) {
+      if (threadIdx.x == 0) {
+        const double* src = P.w.part + ((int64_t)bl * P.nslot + SL_ALPHA) * P.Gs;
+        double a = 0.0;
+        for (int jj = 0; jj < P.Gs; ++jj) a += src[jj];
+        sc.alpha = a;
+      }
+      __syncthreads();
+      const double al = sc.alpha, be = sc.beta;
+      const double* vk = lanczos(P, b, k);
+      const double* vkm = (k > 1) ? lanczos(P, b, k - 1) : nullptr;
+      double bsq[1] = {0.0};
+      for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+        double x = ub[p] - al * vk[p];
+        x = x - be * (vkm ? vkm[p] : 0.0);
+        tmp[p] = x;
+        bsq[0] += x * x;
+      }
+      block_sum<1>(bsq, red);
+      if (threadIdx.x == 0) P.w.part[((int64_t)bl * P.nslot + SL_BETA2) * P.Gs + j] = red[0];
+    }
+    if (sc.finished && !sc.counted) {
+      if (threadIdx.x == 0) {
+        sc.counted = 1;
+        if (leader) {
+          A.iters[b] = sc.iters;
+          A.reasons[b] = sc.reason;
+          atomicAdd(P.w.done, 1);
+        }
+      }
+      __syncthreads();
+    }
+    grid.sync();
+  }
+}
+
+}  // namespace kr
+
+using namespace kr;
+
+namespace {
+
+struct Layout {
+  int Gs, chunk, nslot;
+  int64_t vec_doubles;   // per-sample vector storage
+  int64_t part_doubles;  // partials
+  int64_t total;         // doubles (plus ints packed at the end)
+  size_t smem;
+};
+
+int plan(const kr_op& op, const kr_solve_args& a, Layout& L) {
+  const int64_t n = op_n(op);
+  Geom g = make_geom(op);
+  L.smem = sizeof(double) * ((size_t)g.total + MAX_SLOTS + 4 * MAX_S + MAX_NSC + 8 * 33 + 8);
+  int sms = device_sms();
+  int per_sm = 0;
+  if (sms > 0) {
+    if (L.smem > 48 * 1024)
+      cudaFuncSetAttribute((const void*)rminres_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rminres_kernel, NT, L.smem);
+  }
+  if (per_sm < 1) per_sm = 1;
+  if (sms < 1) sms = 148;
+  int max_blocks = per_sm * sms;
+  int B = op.batch;
+  L.chunk = B < max_blocks ? B : max_blocks;
+  if (L.chunk < 1) L.chunk = 1;
+  int want = (int)((n + 511) / 512);
+  int nt = num_tiles(op);
+  if (want < nt) want = nt;
+  int Gs = max_blocks / L.chunk;
+  if (Gs > want) Gs = want;
+  if (Gs < 1) Gs = 1;
+  L.Gs = Gs;
+  int ns = a.stop_kind == 1 ? a.nsc_s : 0;
+  L.nslot = a.s + ns + 2;
+  L.vec_doubles = (int64_t)B * n * (a.basis ? 11 : 13);
+  L.part_doubles = (int64_t)L.chunk * L.nslot * Gs;
+  L.total = L.vec_doubles + L.part_doubles + 2;
+  return KR_OK;
+}
+
+int check_args(const kr_op& op, const kr_solve_args& a) {
+  KR_CHECK_ARG(a.max_iter >= 1, "max_iter must be >= 1");
+  KR_CHECK_ARG(a.s >= 0 && a.s <= MAX_S, "recycle dimension must be in [0, 128]");
+  KR_CHECK_ARG(a.s == 0 || (a.U && a.C && a.ld_uc >= op_n(op)), "recycle space U/C missing or bad ld");
+  KR_CHECK_ARG(a.stop_kind == 0 || a.stop_kind == 1, "stop_kind must be 0 (residual) or 1 (NSC)");
+  KR_CHECK_ARG(a.delta > 0.0, "tolerance must be positive");
+  if (a.stop_kind == 1) {
+    KR_CHECK_ARG(a.nsc_s >= 1 && a.nsc_s <= MAX_NSC, "NSC needs 1..128 columns");
+    KR_CHECK_ARG(a.Z && a.ld_z >= op_n(op), "NSC needs Z");
+    KR_CHECK_ARG(a.s == 0 || a.ZtC, "NSC with recycling needs Z^T C");
+    KR_CHECK_ARG(a.track_residual, "NSC needs the tracked residual");
+  }
+  KR_CHECK_ARG(a.g && a.w && a.res_norms && a.stop_vals && a.iters && a.reasons, "missing output buffer");
+  KR_CHECK_ARG(!a.basis || a.ld_basis >= op_n(op), "basis leading dimension smaller than n");
+  KR_CHECK_ARG(!a.track_residual || a.r, "track_residual needs an r buffer");
+  KR_CHECK_ARG(op.reg_kind != KR_REG_FILTERS || op.potential == KR_POT_QUADRATIC || op.curv,
+               "operator not prepared (curv)");
+  KR_CHECK_ARG(op.reg_kind != KR_REG_TV || op.curv, "operator not prepared (curv)");
+  return KR_OK;
+}
+
+}  // namespace
+
+extern "C" int64_t kr_rminres_workspace(const kr_op* op, const kr_solve_args* a) {
+  if (!op || !a || validate_op(*op) != KR_OK) return -1;
+  Layout L;
+  plan(*op, *a, L);
+  return L.total;
+}
+
+extern "C" int kr_rminres(const kr_op* op, const kr_solve_args* a, double* work, int64_t work_len,
+                          kr_stream_t stream) {
+  KR_CHECK_ARG(op && a, "null argument");
+  KR_TRY(validate_op(*op));
+  if (op->batch == 0) return KR_OK;
+  KR_TRY(check_args(*op, *a));
+  Layout L;
+  plan(*op, *a, L);
+  KR_CHECK_ARG(work && work_len >= L.total, "rminres workspace too small");
+  const int64_t n = op_n(*op);
+  const int B = op->batch;
+  Params P;
+  P.op = *op;
+  P.a = *a;
+  P.n = n;
+  P.Gs = L.Gs;
+  P.nslot = L.nslot;
+  double* cur = work;
+  auto take = [&](int64_t cnt) {
+    double* r = cur;
+    cur += cnt;
+    return r;
+  };
+  P.w.tmp = take(B * n);
+  P.w.u = take(B * n);
+  P.w.hv[0] = take(B * n);
+  P.w.hv[1] = take(B * n);
+  P.w.vt[0] = take(B * n);
+  P.w.vt[1] = take(B * n);
+  P.w.hvt[0] = take(B * n);
+  P.w.hvt[1] = take(B * n);
+  P.w.rv = take(B * n);
+  P.w.wv = take(B * n);
+  if (!a->basis) {
+    P.w.vr[0] = take(B * n);
+    P.w.vr[1] = take(B * n);
+  } else {
+    P.w.vr[0] = P.w.vr[1] = nullptr;
+  }
+  take((a->basis ? 11 : 13) * (int64_t)B * n - (cur - work));  // keep layout == plan
+  P.w.part = take(L.part_doubles);
+  P.w.done = reinterpret_cast<int*>(take(2));
+  cudaStream_t st = (cudaStream_t)stream;
+  KR_TRY(ensure_smem((const void*)rminres_kernel, L.smem));
+  for (int b0 = 0; b0 < B; b0 += L.chunk) {
+    P.b0 = b0;
+    P.nb = (B - b0) < L.chunk ? (B - b0) : L.chunk;
+    cudaMemsetAsync(P.w.done, 0, sizeof(int), st);
+    dim3 grid(P.nb * P.Gs), block(NT);
+    void* args[] = {&P};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)rminres_kernel, grid, block, args, L.smem, st);
+    if (e != cudaSuccess) return fail(KR_ECUDA, std::string("rminres cooperative launch: ") + cudaGetErrorString(e));
+  }
+  return check_launch("kr_rminres");
+}
+

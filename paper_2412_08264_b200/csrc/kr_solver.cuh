@@ -1,0 +1,74 @@
+// kr_solver.cuh -- helpers shared by the persistent Krylov kernels: block
+// partial sums per sample and their fixed-order (deterministic) reduction.
+#pragma once
+
+#include "kr_common.cuh"
+
+namespace kr {
+
+constexpr int MAX_S = 128;                // recycle columns
+constexpr int MAX_NSC = 128;              // NSC columns
+constexpr double BREAKDOWN_RTOL = 1e-13;  // krylov.py:50
+
+enum Reason { R_TOL = 0, R_MAXIT = 1, R_BREAK = 2, R_NONSPD = 3 };
+
+// Block partials of one launch: part[sample][slot][rank].
+struct Partials {
+  double* part;
+  int nslot;
+  int Gs;
+  __device__ inline double* at(int bl, int slot) const { return part + ((int64_t)bl * nslot + slot) * Gs; }
+};
+
+// acc_out[i] += sum_{p in [lo,hi)} A_i[p] * x(p), i < S; A_i = A + i*lda (8 columns per pass).
+template <typename XF>
+__device__ inline void slot_dots(const double* __restrict__ A, int64_t lda, int S, int64_t lo, int64_t hi,
+                                 XF xf, double* acc_out, double* red) {
+  for (int base = 0; base < S; base += 8) {
+    double v8[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v8[i] = 0.0;
+    for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+      double x = xf(p);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (base + i < S) v8[i] += A[(int64_t)(base + i) * lda + p] * x;
+    }
+    block_sum<8>(v8, red);
+    if (threadIdx.x < 8 && base + threadIdx.x < S) acc_out[base + threadIdx.x] += red[threadIdx.x];
+    __syncthreads();
+  }
+}
+
+__device__ inline void write_partials(const Partials& P, int bl, int j, int slot0, int S, const double* acc) {
+  for (int i = threadIdx.x; i < S; i += blockDim.x) P.at(bl, slot0 + i)[j] = acc[i];
+}
+
+__device__ inline void write_partial1(const Partials& P, int bl, int j, int slot, double v) {
+  if (threadIdx.x == 0) P.at(bl, slot)[j] = v;
+}
+
+// out[i] = sum over the sample's blocks, rank order (deterministic).
+__device__ inline void reduce_slots(const Partials& P, int bl, int slot0, int S, double* out) {
+  for (int i = threadIdx.x; i < S; i += blockDim.x) {
+    const double* src = P.at(bl, slot0 + i);
+    double acc = 0.0;
+    for (int jj = 0; jj < P.Gs; ++jj) acc += src[jj];
+    out[i] = acc;
+  }
+}
+
+__device__ inline double reduce_slot1(const Partials& P, int bl, int slot) {
+  const double* src = P.at(bl, slot);
+  double acc = 0.0;
+  for (int jj = 0; jj < P.Gs; ++jj) acc += src[jj];
+  return acc;
+}
+
+// Blocks per sample and samples per launch for a cooperative launch.
+struct LaunchPlan {
+  int Gs;
+  int chunk;
+};
+
+}  // namespace kr

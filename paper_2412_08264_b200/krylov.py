@@ -1,0 +1,331 @@
+"""MINRES / RMINRES / CG mirroring ``krecycle.krylov`` (reference krylov.py).
+
+Each call is ONE persistent cooperative kernel (``kr_rminres`` / ``kr_cg``)
+that runs every iteration of every sample of a batch on the device; the host
+sees the result once.  Semantics follow krylov.py:205-483: Alg. 3 with the
+corrected sign, breakdown at 1e-13 ||g||, stop test before breakdown test,
+the 5-vector residual recurrence when the rule needs r, and the closed-form
+FLOP model (krylov.py:119-135) in ``SolveResult.flops``.
+
+Batching: ``g`` of shape (B, n) with a batched operator solves B independent
+systems in one launch and returns a list of results; ``recycle`` and the
+stop rule may then be per-sample lists.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import KrSolveArgs, NonSPDError
+from .operators import as_device, columns, new_columns
+from .stopping import NscRule, ResidualNormRule, StopRule
+
+__all__ = ["BREAKDOWN_RTOL", "NonSPDError", "SolveOptions", "SolveResult", "TridiagState", "cg", "flops_cg",
+           "flops_minres", "flops_rminres", "minres", "rminres"]
+
+BREAKDOWN_RTOL = 1e-13
+
+
+@dataclass
+class SolveOptions:
+    """krylov.py:57-82.  The per-iteration diagnostics (reorthogonalize,
+    collect_*) are host-loop test hooks of the reference; the persistent
+    kernel does not produce them and raises if they are requested."""
+
+    max_iter: int = 500
+    initial_guess: object = None
+    stop_rule: StopRule | None = None
+    track_basis: bool = False
+    track_residual_vector: bool = False
+    reorthogonalize: bool = False
+    collect_states: bool = False
+    collect_iterates: bool = False
+    collect_residual_history: bool = False
+
+    def __post_init__(self):
+        if self.max_iter < 1:
+            raise ValueError(f"max_iter must be >= 1, got {self.max_iter}")
+
+    def rule(self) -> StopRule:
+        return self.stop_rule if self.stop_rule is not None else ResidualNormRule(1e-2)
+
+
+@dataclass(frozen=True)
+class TridiagState:
+    """krylov.py:85-99 (kept for API compatibility)."""
+
+    alpha: float
+    beta: float
+    beta_next: float
+    gamma: float
+    delta: float
+    epsilon: float
+    epsilon_rot: float
+    givens: tuple
+    givens_prev: tuple
+    givens_prev2: tuple
+    zeta: float
+
+
+@dataclass
+class SolveResult:
+    """krylov.py:102-116; solution / basis / residual_vector are device tensors."""
+
+    solution: torch.Tensor
+    iterations: int
+    residual_norms: np.ndarray
+    flops: int
+    stop_reason: str
+    stop_values: np.ndarray
+    basis: torch.Tensor | None = None
+    residual_vector: torch.Tensor | None = None
+    states: list | None = None
+    iterates: list | None = None
+    residual_history: list | None = None
+
+
+def _check_counts(**kw):
+    for name, v in kw.items():
+        if v < 0:
+            raise ValueError(f"{name} must be nonnegative, got {v}")
+
+
+def flops_minres(k_total: int, n: int, h_cost: int) -> int:
+    """krylov.py:119-122"""
+    _check_counts(k_total=k_total, n=n, h_cost=h_cost)
+    return h_cost + 4 * n + k_total * (h_cost + 16 * n)
+
+
+def flops_rminres(k_total: int, n: int, s: int, h_cost: int) -> int:
+    """krylov.py:125-128"""
+    _check_counts(k_total=k_total, n=n, s=s, h_cost=h_cost)
+    return h_cost + 4 * n + 6 * n * s + k_total * (h_cost + 21 * n + 6 * n * s - s)
+
+
+def flops_cg(k_total: int, n: int, h_cost: int) -> int:
+    """krylov.py:131-135"""
+    _check_counts(k_total=k_total, n=n, h_cost=h_cost)
+    return h_cost + 3 * n + k_total * (h_cost + 10 * n)
+
+
+def _unsupported(opts: SolveOptions):
+    for flag in ("reorthogonalize", "collect_states", "collect_iterates", "collect_residual_history"):
+        if getattr(opts, flag):
+            raise NotImplementedError(f"SolveOptions.{flag} is a host-loop diagnostic; the device solver "
+                                      "runs the whole iteration in one kernel and does not record it")
+
+
+def _as_batch(H, g):
+    g = as_device(g)
+    single = g.dim() == 1
+    G = g.reshape(1, -1) if single else g
+    if G.shape[1] != H.dim:
+        raise ValueError(f"right-hand side of shape {tuple(g.shape)}, operator dim {H.dim}")
+    if G.shape[0] != H.batch:
+        raise ValueError(f"{G.shape[0]} right-hand sides for an operator batch of {H.batch}")
+    if not bool(torch.isfinite(G).all()):
+        raise ValueError("right-hand side contains non-finite entries")
+    return G.contiguous(), single
+
+
+def _per_sample(x, B):
+    if isinstance(x, (list, tuple)):
+        if len(x) != B:
+            raise ValueError(f"expected {B} per-sample entries, got {len(x)}")
+        return list(x)
+    return [x] * B
+
+
+def _rule_kind(rule) -> int:
+    if isinstance(rule, NscRule):
+        return 1
+    if isinstance(rule, ResidualNormRule):
+        return 0
+    raise NotImplementedError(f"the device solver evaluates residual and NSC rules only, got {type(rule).__name__}")
+
+
+class _Launch:
+    """Device buffers + kr_solve_args for one batched solve."""
+
+    def __init__(self, H, G, recycles, rules, opts, want_basis):
+        B, n = G.shape
+        dev = G.device
+        self.B, self.n = B, n
+        self.max_iter = opts.max_iter
+        a = KrSolveArgs()
+        a.max_iter = opts.max_iter
+        a.g = G.data_ptr()
+        self.keep = [G]
+        w0 = opts.initial_guess
+        if w0 is not None:
+            w0 = as_device(w0).reshape(B, n).contiguous()
+            self.keep.append(w0)
+            a.w0 = w0.data_ptr()
+        dims = [0 if r is None else r.dim for r in recycles]
+        s = max(dims) if dims else 0
+        self.dims = dims
+        a.s = s
+        if s:
+            U = torch.zeros(B, s, n, dtype=torch.float64, device=dev)
+            C = torch.zeros(B, s, n, dtype=torch.float64, device=dev)
+            for b, r in enumerate(recycles):
+                if r is not None and r.dim:
+                    U[b, : r.dim] = r.U.T
+                    C[b, : r.dim] = r.C.T
+            self.U, self.C = U, C
+            self.keep += [U, C]
+            a.U, a.C, a.ld_uc, a.bs_uc = U.data_ptr(), C.data_ptr(), n, s * n
+        kinds = {_rule_kind(r) for r in rules}
+        if len(kinds) != 1:
+            raise ValueError("one launch needs one rule kind; split the batch")
+        kind = kinds.pop()
+        deltas = {float(r.delta) for r in rules}
+        if len(deltas) != 1:
+            raise ValueError("one launch needs one tolerance")
+        a.stop_kind = kind
+        a.delta = deltas.pop()
+        track = opts.track_residual_vector or kind == 1
+        a.track_residual = int(track)
+        if kind == 1:
+            zs = [r.data.z_block() for r in rules]
+            ns = max(z.shape[1] for z in zs)
+            Z = torch.zeros(B, ns, n, dtype=torch.float64, device=dev)
+            for b, z in enumerate(zs):
+                Z[b, : z.shape[1]] = z.T
+            a.nsc_s, a.Z, a.ld_z, a.bs_z = ns, Z.data_ptr(), n, ns * n
+            self.keep.append(Z)
+            if s:
+                ZtC = torch.bmm(Z, self.C.transpose(1, 2)).contiguous()  # (B, ns, s)
+                a.ZtC = ZtC.data_ptr()
+                self.keep.append(ZtC)
+        self.w = torch.empty(B, n, dtype=torch.float64, device=dev)
+        a.w = self.w.data_ptr()
+        self.r = torch.empty(B, n, dtype=torch.float64, device=dev) if track else None
+        if track:
+            a.r = self.r.data_ptr()
+        self.basis = None
+        if want_basis:
+            self.basis = torch.empty(B, opts.max_iter, n, dtype=torch.float64, device=dev)
+            a.basis, a.ld_basis, a.bs_basis = self.basis.data_ptr(), n, opts.max_iter * n
+        self.res = torch.empty(B, opts.max_iter + 1, dtype=torch.float64, device=dev)
+        self.vals = torch.empty(B, opts.max_iter + 1, dtype=torch.float64, device=dev)
+        self.iters = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.reasons = torch.zeros(B, dtype=torch.int32, device=dev)
+        a.res_norms, a.stop_vals = self.res.data_ptr(), self.vals.data_ptr()
+        a.iters, a.reasons = self.iters.data_ptr(), self.reasons.data_ptr()
+        self.args = a
+        self.track = track
+
+    def run(self, H, fn_ws, fn):
+        L = _lib.lib()
+        wl = fn_ws(ctypes.byref(H.op), ctypes.byref(self.args))
+        if wl < 0:
+            _lib.check(-1, "workspace query")
+        ws = torch.empty(max(int(wl), 1), dtype=torch.float64, device=self.w.device)
+        _lib.check(fn(ctypes.byref(H.op), ctypes.byref(self.args), ws.data_ptr(), int(wl), _lib.stream_ptr()),
+                   "solver")
+        self.ws = ws
+
+    def results(self, H, flop_fn):
+        iters = self.iters.cpu().numpy()
+        reasons = self.reasons.cpu().numpy()
+        res = self.res.cpu().numpy()
+        vals = self.vals.cpu().numpy()
+        out = []
+        for b in range(self.B):
+            k = int(iters[b])
+            why = _lib.REASONS[int(reasons[b])]
+            if why == "nonspd":
+                raise NonSPDError(f"curvature p^T H p <= 0 at iteration {k}; operator is not SPD")
+            basis = None
+            if self.basis is not None:
+                basis = self.basis[b, :k].T  # (n, k), contiguous columns
+            out.append(SolveResult(
+                solution=self.w[b], iterations=k, residual_norms=res[b, : k + 1].copy(),
+                flops=flop_fn(k, self.dims[b] if hasattr(self, "dims") else 0),
+                stop_reason=why, stop_values=vals[b, : k + 1].copy(), basis=basis,
+                residual_vector=None if self.r is None else self.r[b]))
+        return out
+
+
+def _split_by_rule(rules):
+    groups: dict = {}
+    for b, r in enumerate(rules):
+        groups.setdefault((_rule_kind(r), float(r.delta)), []).append(b)
+    return list(groups.values())
+
+
+def _solve(H, g, recycle, opts, kind):
+    opts = opts or SolveOptions()
+    _unsupported(opts)
+    G, single = _as_batch(H, g)
+    B, n = G.shape
+    recycles = _per_sample(recycle, B)
+    rule = opts.stop_rule if isinstance(opts.stop_rule, (list, tuple)) else opts.rule()
+    rules = _per_sample(rule, B)
+    for r in recycles:
+        if r is None or r.dim == 0:
+            continue
+        if r.U.shape != r.C.shape or r.U.shape[0] != H.dim:
+            raise ValueError(f"recycle space shapes U{tuple(r.U.shape)} / C{tuple(r.C.shape)} "
+                             f"do not match operator dim {H.dim}")
+        ctc = r.C.T @ r.C
+        if float((ctc - torch.eye(r.dim, dtype=ctc.dtype, device=ctc.device)).abs().max()) > 1e-8:
+            raise ValueError("recycle space violates C^T C = I beyond 1e-8")
+    groups = _split_by_rule(rules)
+    results: list = [None] * B
+    L = _lib.lib()
+    for idx in groups:
+        if len(groups) == 1:
+            Hs, Gs, rs, rec = H, G, [rules[b] for b in idx], [recycles[b] for b in idx]
+        else:
+            Hs = _subbatch(H, idx)
+            Gs = G[idx].contiguous()
+            rs, rec = [rules[b] for b in idx], [recycles[b] for b in idx]
+        sub_opts = opts
+        if opts.initial_guess is not None:
+            w0 = as_device(opts.initial_guess).reshape(B, n)
+            sub_opts = SolveOptions(**{**opts.__dict__, "initial_guess": w0[idx].contiguous(), "stop_rule": None})
+        if kind == "cg":
+            if any(r is not None and r.dim for r in rec):
+                raise ValueError("plain CG takes no recycle space")
+            launch = _Launch(Hs, Gs, [None] * len(idx), rs, sub_opts, opts.track_basis)
+            launch.run(Hs, L.kr_cg_workspace, L.kr_cg)
+            res = launch.results(Hs, lambda k, s: flops_cg(k, n, H.apply_cost))
+        else:
+            launch = _Launch(Hs, Gs, rec, rs, sub_opts, opts.track_basis)
+            launch.run(Hs, L.kr_rminres_workspace, L.kr_rminres)
+            res = launch.results(
+                Hs, lambda k, s: flops_rminres(k, n, s, H.apply_cost) if s else flops_minres(k, n, H.apply_cost))
+        for b, r in zip(idx, res):
+            results[b] = r
+    return results[0] if single else results
+
+
+def _subbatch(H, idx):
+    """Operator restricted to samples idx (one sample at a time when idx is not contiguous)."""
+    if len(idx) == 1:
+        return H.sample(idx[0])
+    if idx == list(range(idx[0], idx[0] + len(idx))) and hasattr(H, "slice"):
+        return H.slice(idx[0], idx[0] + len(idx))
+    raise NotImplementedError("mixed stop rules inside one batch need contiguous sample groups")
+
+
+def minres(H, g, opts: SolveOptions | None = None):
+    """krylov.py:386-388"""
+    return _solve(H, g, None, opts, "rminres")
+
+
+def rminres(H, g, recycle, opts: SolveOptions | None = None):
+    """krylov.py:391-405: empty recycle space -> the MINRES path of the same kernel."""
+    return _solve(H, g, recycle, opts, "rminres")
+
+
+def cg(H, g, opts: SolveOptions | None = None):
+    """krylov.py:408-483"""
+    return _solve(H, g, None, opts, "cg")
