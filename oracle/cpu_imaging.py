@@ -607,3 +607,11 @@ def deblur_theta0(cfg: DeblurConfig) -> np.ndarray:
         k = cfg.filter_std * rng.standard_normal((cfg.kernel_size, cfg.kernel_size))
         kernels.append(k - k.mean())
     return pack_theta(np.full(cfg.num_filters, cfg.alpha0), kernels)
+
+
+def perturbed(H: SymOp, rel: float = 2e-16, seed: int = 0) -> SymOp:
+    """H with each output entry multiplied by (1 + rel * N(0,1)): a roundoff-level
+    perturbation used to measure the reference algorithm's own sensitivity
+    (its "roundoff floor") -- the SURVEY App. B roundoff-sensitivity probe."""
+    rng = np.random.default_rng(seed)
+    return SymOp(H.dim, lambda v: H(v) * (1.0 + rel * rng.standard_normal(v.size)), H.apply_cost)

@@ -150,3 +150,18 @@ def ptr(t: torch.Tensor | None) -> int | None:
 
 def stream_ptr(device=None) -> int:
     return torch.cuda.current_stream(device).cuda_stream
+
+
+# --------------------------------------------------------------------------
+# instrumentation used by bench.py: launch counts and CUDA-event kernel timing
+
+LAUNCHES: dict = {}
+PROFILE: list | None = None  # when a list, solver launches append (start_event, end_event, info)
+
+
+def note_launch(name: str, count: int = 1) -> None:
+    LAUNCHES[name] = LAUNCHES.get(name, 0) + count
+
+
+def total_launches() -> int:
+    return sum(LAUNCHES.values())

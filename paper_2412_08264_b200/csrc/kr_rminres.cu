@@ -463,8 +463,11 @@ __global__ void __launch_bounds__(NT) rminres_kernel(Params P) {
       block_sum<1>(bsq, red);
       if (threadIdx.x == 0) P.w.part[((int64_t)bl * P.nslot + SL_BETA2) * P.Gs + j] = red[0];
     }
-    if (sc.finished && !sc.counted) {
-      if (threadIdx.x == 0) {
+    {
+      // evaluate before thread 0 flips `counted` (keeps the barrier below uniform)
+      const bool count_now = sc.finished && !sc.counted;
+      __syncthreads();
+      if (count_now && threadIdx.x == 0) {
         sc.counted = 1;
         if (leader) {
           A.iters[b] = sc.iters;

@@ -227,8 +227,18 @@ class _Launch:
         if wl < 0:
             _lib.check(-1, "workspace query")
         ws = torch.empty(max(int(wl), 1), dtype=torch.float64, device=self.w.device)
+        ev = None
+        if _lib.PROFILE is not None:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
         _lib.check(fn(ctypes.byref(H.op), ctypes.byref(self.args), ws.data_ptr(), int(wl), _lib.stream_ptr()),
                    "solver")
+        _lib.note_launch(fn.__name__, 1)
+        if ev is not None:
+            ev[1].record()
+            _lib.PROFILE.append((ev[0], ev[1], {"kernel": fn.__name__, "B": self.B, "n": self.n,
+                                                "s": int(self.args.s), "nsc": int(self.args.nsc_s),
+                                                "iters": self.iters}))
         self.ws = ws
 
     def results(self, H, flop_fn):

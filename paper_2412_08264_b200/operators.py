@@ -376,6 +376,7 @@ class Model:
         op = self._kr_op(theta, x_hat, keep)
         if x_hat is not None:
             _lib.check(_lib.lib().kr_op_prepare(ctypes.byref(op), _lib.stream_ptr()), "kr_op_prepare")
+            _lib.note_launch("kr_op_prepare")
         H = HessianOperator(self, op, keep)
         J = StencilJacobian(self, op, keep) if x_hat is not None else None
         return H, J
@@ -394,6 +395,7 @@ class Model:
         ws = torch.empty(max(wl, 1), dtype=torch.float64, device=self.device)
         _lib.check(L.kr_lower_eval(ctypes.byref(op), X.data_ptr(), self.y.data_ptr(), cost.data_ptr(),
                                    grad.data_ptr(), ws.data_ptr(), wl, _lib.stream_ptr()), "kr_lower_eval")
+        _lib.note_launch("kr_lower_eval", 2)
         return cost, grad
 
 
@@ -467,6 +469,7 @@ class HessianOperator(SymmetricOperator):
         _lib.check(_lib.lib().kr_hvp(ctypes.byref(self.op), M.data_ptr(), M.stride(2) if t > 1 else n,
                                      M.stride(0), t, out.data_ptr(), out.stride(2) if t > 1 else n,
                                      out.stride(0), _lib.stream_ptr()), "kr_hvp")
+        _lib.note_launch("kr_hvp")
         return out
 
     def __call__(self, v):
@@ -574,6 +577,7 @@ class StencilJacobian(MixedJacobianOperator):
         _lib.check(L.kr_jadj(ctypes.byref(self.op), W.data_ptr(), W.stride(2) if t > 1 else n, W.stride(0), t,
                              out.data_ptr(), out.stride(2) if t > 1 else p, out.stride(0), ws.data_ptr(), wl,
                              _lib.stream_ptr()), "kr_jadj")
+        _lib.note_launch("kr_jadj", 2)
         return out
 
     def apply_adjoint(self, w):
