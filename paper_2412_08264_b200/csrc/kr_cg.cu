@@ -30,7 +30,8 @@ struct CgParams {
   int64_t n;
 };
 
-__global__ void __launch_bounds__(NT) cg_kernel(CgParams P) {
+template <int Q>
+__global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double smem[];
   const kr_op& op = P.op;
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(NT) cg_kernel(CgParams P) {
   // r = g - H w0
   if (w0) {
     for (int tile = j; tile < ntiles; tile += P.Gs) {
-      tile_hvp(op, g, sm, b, TileIn{w0, 1.0, nullptr, 0.0}, tile);
+      tile_hvp_t<Q>(op, g, sm, b, TileIn{w0, 1.0, nullptr, 0.0}, tile);
       for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
         int64_t p = tile_pixel(op, tile, l);
         if (p >= 0) r[p] = gb[p] - sm.res[l];
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(NT) cg_kernel(CgParams P) {
       }
       double php[1] = {0.0};
       for (int tile = j; tile < ntiles; tile += P.Gs) {
-        tile_hvp(op, g, sm, b, TileIn{r, 1.0, po, coef}, tile);
+        tile_hvp_t<Q>(op, g, sm, b, TileIn{r, 1.0, po, coef}, tile);
         const int tyc = tiles_x(op);
         for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
           int64_t p = tile_pixel(op, tile, l);
@@ -238,8 +239,8 @@ void cg_plan(const kr_op& op, const kr_solve_args& a, CgLayout& L) {
   int sms = device_sms(), per_sm = 0;
   if (sms > 0) {
     if (L.smem > 48 * 1024)
-      cudaFuncSetAttribute((const void*)cg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_kernel, NT, L.smem);
+      cudaFuncSetAttribute(KR_PICK_Q(cg_kernel, q_variant(op)), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, KR_PICK_Q(cg_kernel, q_variant(op)), NT, L.smem);
   }
   if (per_sm < 1) per_sm = 1;
   if (sms < 1) sms = 148;
@@ -290,13 +291,14 @@ extern "C" int kr_cg(const kr_op* op, const kr_solve_args* a, double* work, int6
   P.part = P.wv + (int64_t)B * n;
   P.done = reinterpret_cast<int*>(P.part + (int64_t)L.chunk * L.nslot * L.Gs);
   cudaStream_t st = (cudaStream_t)stream;
-  KR_TRY(ensure_smem((const void*)cg_kernel, L.smem));
+  const void* kfn = KR_PICK_Q(cg_kernel, q_variant(*op));
+  KR_TRY(ensure_smem(kfn, L.smem));
   for (int b0 = 0; b0 < B; b0 += L.chunk) {
     P.b0 = b0;
     P.nb = (B - b0) < L.chunk ? (B - b0) : L.chunk;
     cudaMemsetAsync(P.done, 0, sizeof(int), st);
     void* args[] = {&P};
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)cg_kernel, dim3(P.nb * P.Gs), dim3(NT), args, L.smem, st);
+    cudaError_t e = cudaLaunchCooperativeKernel(kfn, dim3(P.nb * P.Gs), dim3(NT), args, L.smem, st);
     if (e != cudaSuccess) return fail(KR_ECUDA, std::string("cg cooperative launch: ") + cudaGetErrorString(e));
   }
   return check_launch("kr_cg");

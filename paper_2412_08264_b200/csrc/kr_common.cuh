@@ -57,6 +57,18 @@ __host__ __device__ inline Geom make_geom(const kr_op& op) {
 
 __host__ __device__ inline int64_t op_n(const kr_op& op) { return (int64_t)op.rows * op.cols; }
 
+// Compile-time filter-size variant of the stencil kernels (0 = generic runtime path).
+inline int q_variant(const kr_op& op) {
+  if (op.reg_kind == KR_REG_FILTERS && op.data_kind != KR_DATA_DENSE &&
+      (op.ksize == 3 || op.ksize == 5 || op.ksize == 7))
+    return op.ksize;
+  return 0;
+}
+
+#define KR_PICK_Q(kernel, q) \
+  ((q) == 3 ? (const void*)kernel<3> : (q) == 5 ? (const void*)kernel<5> : (q) == 7 ? (const void*)kernel<7> \
+                                                                              : (const void*)kernel<0>)
+
 __host__ __device__ inline int tiles_y(const kr_op& op) { return (op.rows + TH - 1) / TH; }
 __host__ __device__ inline int tiles_x(const kr_op& op) { return (op.cols + TW - 1) / TW; }
 __host__ __device__ inline int num_tiles(const kr_op& op) {
@@ -229,7 +241,105 @@ __device__ inline void tile_blur_normal(const kr_op& op, const Geom& g, Smem& sm
   __syncthreads();
 }
 
+// Learned-filter part of H v for a compile-time filter size Q (register-blocked):
+//   stage 1: e_j = kappa_j . (c_j * v) on the (TH+2R) x (TW+2R) extended tile, each
+//            thread a strip of RB1 rows of one column (loads (RB1+Q-1)Q, FMAs RB1 Q^2);
+//   stage 2: out += w_j corr(e_j, c_j) on the tile, each thread RB2 rows of one column;
+//   the filter weights live in registers, the per-thread outputs accumulate over all
+//   J filters in registers and are added to sm.res once.
+template <int Q>
+__device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, int b, int y0, int x0) {
+  constexpr int R = Q / 2;
+  constexpr int EW = TW + 2 * R, EH = TH + 2 * R;
+  constexpr int RB1 = 3;
+  constexpr int NCH1 = (EH + RB1 - 1) / RB1;
+  constexpr int RB2 = TPX / NT;
+  const int rows = op.rows, cols = op.cols, H = g.H, RW = g.RW;
+  const int64_t n = op_n(op);
+  double* S4 = sm.SA;
+  const bool quad = op.potential == KR_POT_QUADRATIC;
+  const int tid = threadIdx.x;
+  const int tx2 = tid % TW, r2 = (tid / TW) * RB2;
+  double out[RB2];
+#pragma unroll
+  for (int i = 0; i < RB2; ++i) out[i] = 0.0;
+  for (int j = 0; j < op.num_filters; ++j) {
+    double k[Q][Q];
+    const double* kj = sm.kw + j * Q * Q;
+#pragma unroll
+    for (int a = 0; a < Q; ++a)
+#pragma unroll
+      for (int bb = 0; bb < Q; ++bb) k[a][bb] = kj[a * Q + bb];
+    const double* cj = quad ? nullptr : op.curv + ((int64_t)b * op.num_filters + j) * n;
+    for (int item = tid; item < EW * NCH1; item += NT) {
+      const int c = item % EW, r0 = (item / EW) * RB1;
+      double acc[RB1];
+#pragma unroll
+      for (int i = 0; i < RB1; ++i) acc[i] = 0.0;
+#pragma unroll
+      for (int sr = 0; sr < RB1 + Q - 1; ++sr) {
+        const double* src = sm.S0 + (r0 + H - (Q - 1) + sr) * RW + c + H;
+        double v[Q];
+#pragma unroll
+        for (int bb = 0; bb < Q; ++bb) v[bb] = src[-bb];
+#pragma unroll
+        for (int i = 0; i < RB1; ++i) {
+          const int a = i + Q - 1 - sr;  // conv tap row: output row r0+i reads S0 row r0+i+H-a
+          if (a >= 0 && a < Q) {
+#pragma unroll
+            for (int bb = 0; bb < Q; ++bb) acc[i] = fma(k[a][bb], v[bb], acc[i]);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < RB1; ++i) {
+        const int r = r0 + i;
+        if (r < EH) {
+          const int y = y0 - R + r, x = x0 - R + c;
+          double e = 0.0;
+          if (y >= 0 && y < rows && x >= 0 && x < cols) e = quad ? 2.0 * acc[i] : cj[(int64_t)y * cols + x] * acc[i];
+          S4[r * EW + c] = e;
+        }
+      }
+    }
+    __syncthreads();
+    double acc2[RB2];
+#pragma unroll
+    for (int i = 0; i < RB2; ++i) acc2[i] = 0.0;
+#pragma unroll
+    for (int sr = 0; sr < RB2 + Q - 1; ++sr) {
+      const double* src = S4 + (r2 + sr) * EW + tx2;
+      double v[Q];
+#pragma unroll
+      for (int bb = 0; bb < Q; ++bb) v[bb] = src[bb];
+#pragma unroll
+      for (int i = 0; i < RB2; ++i) {
+        const int a = sr - i;  // correlation tap row
+        if (a >= 0 && a < Q) {
+#pragma unroll
+          for (int bb = 0; bb < Q; ++bb) acc2[i] = fma(k[a][bb], v[bb], acc2[i]);
+        }
+      }
+    }
+    const double wj = sm.fw[j];
+#pragma unroll
+    for (int i = 0; i < RB2; ++i) out[i] = fma(wj, acc2[i], out[i]);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < RB2; ++i) sm.res[(r2 + i) * TW + tx2] += out[i];
+  __syncthreads();
+}
+
+template <int Q>
+__device__ inline void tile_hvp_t(const kr_op& op, const Geom& g, Smem& sm, int b, const TileIn& in, int tile);
+
 __device__ inline void tile_hvp(const kr_op& op, const Geom& g, Smem& sm, int b, const TileIn& in, int tile) {
+  tile_hvp_t<0>(op, g, sm, b, in, tile);
+}
+
+template <int Q>
+__device__ inline void tile_hvp_t(const kr_op& op, const Geom& g, Smem& sm, int b, const TileIn& in, int tile) {
   if (op.data_kind == KR_DATA_DENSE) {
     tile_hvp_dense(op, b, in, tile, sm.res);
     return;
@@ -257,7 +367,9 @@ __device__ inline void tile_hvp(const kr_op& op, const Geom& g, Smem& sm, int b,
   __syncthreads();
   if (op.data_kind == KR_DATA_BLUR) tile_blur_normal(op, g, sm, y0, x0, true);
 
-  if (op.reg_kind == KR_REG_FILTERS) {
+  if (Q > 0 && op.reg_kind == KR_REG_FILTERS) {
+    tile_filters_q<(Q > 0 ? Q : 1)>(op, g, sm, b, y0, x0);
+  } else if (op.reg_kind == KR_REG_FILTERS) {
     const int q = op.ksize, rq = g.rq;
     const int w4 = TW + 2 * rq, h4 = TH + 2 * rq;
     double* S4 = sm.SA;

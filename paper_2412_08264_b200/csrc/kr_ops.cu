@@ -71,6 +71,7 @@ __global__ void prepare_tv_kernel(kr_op op) {
 // ---------------------------------------------------------------------------
 // H V
 
+template <int Q>
 __global__ void __launch_bounds__(NT) hvp_kernel(kr_op op, const double* __restrict__ V, int64_t ldv,
                                                  int64_t bsv, double* __restrict__ HV, int64_t ldo,
                                                  int64_t bso) {
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(NT) hvp_kernel(kr_op op, const double* __restr
   load_weights(op, g, sm);
   const int tile = blockIdx.x, col = blockIdx.y, b = blockIdx.z;
   const double* in = V + b * bsv + col * ldv;
-  tile_hvp(op, g, sm, b, TileIn{in, 1.0, nullptr, 0.0}, tile);
+  tile_hvp_t<Q>(op, g, sm, b, TileIn{in, 1.0, nullptr, 0.0}, tile);
   double* out = HV + b * bso + col * ldo;
   for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
     int64_t p = tile_pixel(op, tile, l);
@@ -417,9 +418,13 @@ extern "C" int kr_hvp(const kr_op* op, const double* V, int64_t ldv, int64_t bsv
   KR_CHECK_ARG(ldv >= op_n(*op) && ldo >= op_n(*op), "leading dimension smaller than n");
   Geom g = make_geom(*op);
   size_t smem = (size_t)g.total * sizeof(double);
-  KR_TRY(ensure_smem((const void*)hvp_kernel, smem));
+  const void* fn = KR_PICK_Q(hvp_kernel, q_variant(*op));
+  KR_TRY(ensure_smem(fn, smem));
   dim3 grid(num_tiles(*op), ncols, op->batch);
-  hvp_kernel<<<grid, NT, smem, (cudaStream_t)stream>>>(*op, V, ldv, bsv, HV, ldo, bso);
+  kr_op opv = *op;
+  void* args[] = {&opv, (void*)&V, &ldv, &bsv, &HV, &ldo, &bso};
+  cudaError_t e = cudaLaunchKernel(fn, grid, dim3(NT), args, smem, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(KR_ECUDA, std::string("kr_hvp launch: ") + cudaGetErrorString(e));
   return check_launch("kr_hvp");
 }
 

@@ -73,7 +73,8 @@ __device__ inline double* lanczos(const Params& P, int b, int k) {
   return vec(P.w.vr[k & 1], P.n, b);
 }
 
-__global__ void __launch_bounds__(NT) rminres_kernel(Params P) {
+template <int Q>
+__global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double smem[];
   const kr_op& op = P.op;
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(NT) rminres_kernel(Params P) {
   // ---------------- setup S1: r0 = g - H w0, partial C^T r0 ----------------
   if (w0) {
     for (int tile = j; tile < ntiles; tile += P.Gs) {
-      tile_hvp(op, g, sm, b, TileIn{w0, 1.0, nullptr, 0.0}, tile);
+      tile_hvp_t<Q>(op, g, sm, b, TileIn{w0, 1.0, nullptr, 0.0}, tile);
       for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
         int64_t p = tile_pixel(op, tile, l);
         double r = 0.0;
@@ -347,7 +348,7 @@ __global__ void __launch_bounds__(NT) rminres_kernel(Params P) {
       __syncthreads();
       double* hvk = vec(P.w.hv[k & 1], n, b);
       for (int tile = j; tile < ntiles; tile += P.Gs) {
-        tile_hvp(op, g, sm, b, TileIn{tmp, beta_k, nullptr, 0.0}, tile);
+        tile_hvp_t<Q>(op, g, sm, b, TileIn{tmp, beta_k, nullptr, 0.0}, tile);
         for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
           int64_t p = tile_pixel(op, tile, l);
           if (p >= 0) hvk[p] = sm.res[l];
@@ -503,8 +504,8 @@ int plan(const kr_op& op, const kr_solve_args& a, Layout& L) {
   int per_sm = 0;
   if (sms > 0) {
     if (L.smem > 48 * 1024)
-      cudaFuncSetAttribute((const void*)rminres_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rminres_kernel, NT, L.smem);
+      cudaFuncSetAttribute(KR_PICK_Q(rminres_kernel, q_variant(op)), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, KR_PICK_Q(rminres_kernel, q_variant(op)), NT, L.smem);
   }
   if (per_sm < 1) per_sm = 1;
   if (sms < 1) sms = 148;
@@ -600,14 +601,15 @@ extern "C" int kr_rminres(const kr_op* op, const kr_solve_args* a, double* work,
   P.w.part = take(L.part_doubles);
   P.w.done = reinterpret_cast<int*>(take(2));
   cudaStream_t st = (cudaStream_t)stream;
-  KR_TRY(ensure_smem((const void*)rminres_kernel, L.smem));
+  const void* kfn = KR_PICK_Q(rminres_kernel, q_variant(*op));
+  KR_TRY(ensure_smem(kfn, L.smem));
   for (int b0 = 0; b0 < B; b0 += L.chunk) {
     P.b0 = b0;
     P.nb = (B - b0) < L.chunk ? (B - b0) : L.chunk;
     cudaMemsetAsync(P.w.done, 0, sizeof(int), st);
     dim3 grid(P.nb * P.Gs), block(NT);
     void* args[] = {&P};
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)rminres_kernel, grid, block, args, L.smem, st);
+    cudaError_t e = cudaLaunchCooperativeKernel(kfn, grid, block, args, L.smem, st);
     if (e != cudaSuccess) return fail(KR_ECUDA, std::string("rminres cooperative launch: ") + cudaGetErrorString(e));
   }
   return check_launch("kr_rminres");
