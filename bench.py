@@ -137,13 +137,11 @@ def run_ours(args):
     solver_cfg = HessianSolveConfig.from_strategy(args.strategy, recycle_dim=cfg.recycle_dim, delta=args.delta,
                                                   max_iter=cfg.max_iter)
 
+    from paper_2412_08264_b200.distributed import allgather_sum
+
     def step(seq, i, X):
         hg, res, rec = hypergradients(model, thetas[i], X, seq)
-        d = hg[0].clone()
-        for k in range(1, hg.shape[0]):
-            d += hg[k]
-        if world > 1:
-            dist.all_reduce(d)
+        d = allgather_sum(hg, B * world)  # sample-ordered sum, bitwise equal for any world size
         return d, res
 
     # ---- device-resident run: warmup + timed ----
