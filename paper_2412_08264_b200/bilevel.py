@@ -9,6 +9,7 @@ launch per upper step.  ``hypergradient`` is bilevel.py:291-305.
 from __future__ import annotations
 
 import warnings
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
 import torch
@@ -51,6 +52,28 @@ class HessianSolveConfig:
         return cls(strategy=strategy, **kwargs)
 
 
+_LINALG_WARM = False
+
+
+def _warm_linalg():
+    """torch initialises its cuSOLVER / linalg backends lazily and not thread-safely;
+    touch every routine next_recycle uses once on the calling thread first."""
+    global _LINALG_WARM
+    if _LINALG_WARM:
+        return
+    a = torch.eye(4, dtype=torch.float64, device="cuda") * 2.0
+    torch.linalg.cholesky_ex(a)
+    torch.linalg.qr(a)
+    torch.linalg.eigh(a)
+    torch.linalg.eigvalsh(a)
+    torch.linalg.svdvals(a)
+    torch.linalg.solve_triangular(a, a, upper=True)
+    torch.linalg.cholesky(a)
+    torch.argsort(a[0], stable=True)
+    torch.cuda.synchronize()
+    _LINALG_WARM = True
+
+
 class SequenceSolver:
     """Solves consecutive Hessian systems of a batch of samples, carrying the
     recycling state of each sample (bilevel.py:225-288).
@@ -70,9 +93,66 @@ class SequenceSolver:
         self._prev_h = None
         self._prev_jac = None
         self._prev_solution = None
+        self.max_workers = 8
+        self._streams = None
+        self._pool = None
 
     def _needs_basis(self) -> bool:
         return not self.cfg.strategy.is_none
+
+    def reserve(self, batch: int, nbytes: int) -> None:
+        """Pre-size the caching-allocator pools of the per-sample worker streams (each
+        stream has its own pool) so steady-state steps never call cudaMalloc."""
+        if batch <= 1 or self.max_workers <= 1:
+            return
+        _warm_linalg()
+        if self._streams is None or len(self._streams) < batch:
+            self._streams = [torch.cuda.Stream() for _ in range(batch)]
+            self._pool = ThreadPoolExecutor(max_workers=min(batch, self.max_workers))
+        for st in self._streams:
+            with torch.cuda.stream(st):
+                torch.empty(nbytes // 8, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+
+    def _recycle_one(self, hessian, jac, B, b):
+        cfg = self.cfg
+        hb = hessian if B == 1 else hessian.sample(b)
+        jb = jac if (B == 1 or jac is None) else jac.sample(b)
+        hp = None if self._prev_h is None else (self._prev_h if B == 1 else self._prev_h.sample(b))
+        jp = None if self._prev_jac is None else (self._prev_jac if B == 1 else self._prev_jac.sample(b))
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)
+            return next_recycle(cfg.strategy, h_current=hb, h_previous=hp, jac_current=jb, jac_previous=jp,
+                                prev_basis=self._prev_basis[b], prev_recycle=self._prev_recycle[b],
+                                s=cfg.recycle_dim, dense_limit=cfg.dense_limit, reuse_products=cfg.reuse_products)
+
+    def _recycle_all(self, hessian, jac, B):
+        """next_recycle for every sample.  The per-sample updates are independent and
+        dominated by latency-bound t x t decompositions, so with B > 1 each sample runs
+        on its own host thread and CUDA stream (torch releases the GIL inside ops);
+        the caller's stream waits for all of them."""
+        if B == 1 or self.max_workers <= 1:
+            return [self._recycle_one(hessian, jac, B, b) for b in range(B)]
+        main = torch.cuda.current_stream()
+        if self._streams is None or len(self._streams) < B:
+            _warm_linalg()
+            self._streams = [torch.cuda.Stream() for _ in range(B)]
+            self._pool = ThreadPoolExecutor(max_workers=min(B, self.max_workers))
+
+        def work(b):
+            st = self._streams[b]
+            st.wait_stream(main)
+            with torch.cuda.stream(st):
+                rec = self._recycle_one(hessian, jac, B, b)
+            for t in (rec.U, rec.C) + ((rec.nsc_data.values, rec.nsc_data.v_h, rec.nsc_data.w)
+                                       if rec.nsc_data is not None and rec.nsc_data.w is not None else ()):
+                t.record_stream(main)
+            return rec
+
+        recs = list(self._pool.map(work, range(B)))
+        for b in range(B):
+            main.wait_stream(self._streams[b])
+        return recs
 
     def solve(self, hessian, g, jac):
         cfg = self.cfg
@@ -83,18 +163,7 @@ class SequenceSolver:
         if cfg.strategy.is_none or self._first:
             recycles = [RecycleSpace.empty(n) for _ in range(B)]
         else:
-            recycles = []
-            for b in range(B):
-                hb = hessian if B == 1 else hessian.sample(b)
-                jb = jac if (B == 1 or jac is None) else jac.sample(b)
-                hp = None if self._prev_h is None else (self._prev_h if B == 1 else self._prev_h.sample(b))
-                jp = None if self._prev_jac is None else (self._prev_jac if B == 1 else self._prev_jac.sample(b))
-                with warnings.catch_warnings():
-                    warnings.simplefilter("ignore", UserWarning)
-                    recycles.append(next_recycle(
-                        cfg.strategy, h_current=hb, h_previous=hp, jac_current=jb, jac_previous=jp,
-                        prev_basis=self._prev_basis[b], prev_recycle=self._prev_recycle[b],
-                        s=cfg.recycle_dim, dense_limit=cfg.dense_limit, reuse_products=cfg.reuse_products))
+            recycles = self._recycle_all(hessian, jac, B)
         self._first = False
         rules = []
         for rec in recycles:

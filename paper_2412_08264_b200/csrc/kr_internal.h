@@ -1,6 +1,7 @@
 // kr_internal.h -- host-side error plumbing shared by the C ABI translation units.
 #pragma once
 
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -16,6 +17,8 @@ int check_launch(const char* what);
 int validate_op(const kr_op& op);
 int ensure_smem(const void* kernel, size_t bytes);
 int device_sms();
+int cublas_handle(cublasHandle_t* out, cudaStream_t st);
+int cublas_check(cublasStatus_t s, const char* what);
 
 }  // namespace kr
 

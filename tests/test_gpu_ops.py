@@ -41,13 +41,13 @@ def test_hvp_matches_oracle(cuda, kind, rows, cols, batch, kw):
             assert rel(HV[b, :, j], ref) <= 1e-12, (b, j, rel(HV[b, :, j], ref))
 
 
+@pytest.mark.parametrize("t", [3, 70, 260])  # 3: per-tile kernel; 70, 260: conv + split-K DGEMM (1 and 2 column chunks)
 @pytest.mark.parametrize("kind,rows,cols,batch,kw", CASES)
-def test_jadj_matches_oracle(cuda, kind, rows, cols, batch, kw):
+def test_jadj_matches_oracle(cuda, kind, rows, cols, batch, kw, t):
     models, theta, xh, _ = oracle_models(kind, rows, cols, batch, seed=7 + rows, **kw)
     dm = device_model(models)
     _, J = dm.at(theta, xh)
     rng = np.random.default_rng(2)
-    t = 3
     W = rng.standard_normal((batch, rows * cols, t))
     JW = to_np(J.apply_adjoint_matrix(torch.as_tensor(W, device=cuda)))
     for b in range(batch):
