@@ -5,7 +5,6 @@
 // evaluated on the explicit residual (stopping.py:93-118).  Two grid barriers
 // per iteration: the direction p_k = r_{k-1} + (rr_{k-1}/rr_{k-2}) p_{k-1} is
 // formed on the fly inside the stencil load, so it needs no barrier of its own.
-#include <cooperative_groups.h>
 
 #include <string>
 
@@ -13,7 +12,6 @@
 #include "kr_internal.h"
 #include "kr_solver.cuh"
 
-namespace cg = cooperative_groups;
 
 namespace kr {
 
@@ -32,7 +30,7 @@ struct CgParams {
 
 template <int Q>
 __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
-  cg::grid_group grid = cg::this_grid();
+  unsigned int grid_target = 0;
   extern __shared__ double smem[];
   const kr_op& op = P.op;
   const kr_solve_args& A = P.a;
@@ -70,7 +68,7 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
     s_reason = R_MAXIT;
     s_rr_old = 1.0;
   }
-  __syncthreads();
+  block_barrier();
   // r = g - H w0
   if (w0) {
     for (int tile = j; tile < ntiles; tile += P.Gs) {
@@ -79,13 +77,13 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
         int64_t p = tile_pixel(op, tile, l);
         if (p >= 0) r[p] = gb[p] - sm.res[l];
       }
-      __syncthreads();
+      block_barrier();
     }
   } else {
     for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) r[p] = gb[p];
   }
   for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) w[p] = w0 ? w0[p] : 0.0;
-  grid.sync();
+  grid_barrier(reinterpret_cast<unsigned int*>(P.done) + 1, gridDim.x, grid_target);
   {
     double v[1] = {0.0};
     for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) v[0] += r[p] * r[p];
@@ -93,19 +91,19 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
     write_partial1(PP, bl, j, SL_RR, red[0]);
     if (ns) {
       for (int i = threadIdx.x; i < ns; i += blockDim.x) slot_acc[i] = 0.0;
-      __syncthreads();
+      block_barrier();
       slot_dots(Z, A.ld_z, ns, lo, hi, [&](int64_t p) { return r[p]; }, slot_acc, red);
       write_partials(PP, bl, j, SL_NSC, ns, slot_acc);
     }
   }
-  grid.sync();
+  grid_barrier(reinterpret_cast<unsigned int*>(P.done) + 1, gridDim.x, grid_target);
 
   for (int k = 1; k <= A.max_iter + 1; ++k) {
-    if (k > 1 && *((volatile int*)P.done) >= P.nb) break;
+    if (k > 1 && __syncthreads_or(threadIdx.x == 0 && *((volatile int*)P.done) >= P.nb)) break;
     // ===== P1: stop test on r_{k-1}, then hp = H p_k =====
     if (ns && s_active) {
       reduce_slots(PP, bl, SL_NSC, ns, nscv);
-      __syncthreads();
+      block_barrier();
     }
     if (threadIdx.x == 0) {
       s_hvp = 0;
@@ -134,7 +132,7 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
         }
       }
     }
-    __syncthreads();
+    block_barrier();
     if (s_hvp) {
       double* pk = P.p[k & 1] + (int64_t)b * n;
       const double* po = (k == 1) ? nullptr : P.p[(k + 1) & 1] + (int64_t)b * n;
@@ -162,12 +160,12 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
           php[0] += pv * sm.res[l];
           (void)tyc;
         }
-        __syncthreads();
+        block_barrier();
       }
       block_sum<1>(php, red);
       write_partial1(PP, bl, j, SL_PHP, red[0]);
     }
-    grid.sync();
+    grid_barrier(reinterpret_cast<unsigned int*>(P.done) + 1, gridDim.x, grid_target);
     // ===== P2: step =====
     if (s_hvp) {
       if (threadIdx.x == 0) {
@@ -177,7 +175,7 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
           s_active = 0; s_finished = 1; s_iters = k; s_reason = R_NONSPD;
         }
       }
-      __syncthreads();
+      block_barrier();
       if (s_active) {
         const double a = s_rr_old / s_php;
         const double* pk = P.p[k & 1] + (int64_t)b * n;
@@ -192,7 +190,7 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
         write_partial1(PP, bl, j, SL_RR, red[0]);
         if (ns) {
           for (int i = threadIdx.x; i < ns; i += blockDim.x) slot_acc[i] = 0.0;
-          __syncthreads();
+          block_barrier();
           slot_dots(Z, A.ld_z, ns, lo, hi, [&](int64_t p) { return r[p]; }, slot_acc, red);
           write_partials(PP, bl, j, SL_NSC, ns, slot_acc);
         }
@@ -205,7 +203,7 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
         wout[p] = w[p];
         if (rout) rout[p] = r[p];
       }
-      __syncthreads();
+      block_barrier();
       if (threadIdx.x == 0) {
         s_counted = 1;
         if (leader) {
@@ -214,9 +212,9 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
           atomicAdd(P.done, 1);
         }
       }
-      __syncthreads();
+      block_barrier();
     }
-    grid.sync();
+    grid_barrier(reinterpret_cast<unsigned int*>(P.done) + 1, gridDim.x, grid_target);
   }
 }
 
@@ -235,7 +233,7 @@ struct CgLayout {
 void cg_plan(const kr_op& op, const kr_solve_args& a, CgLayout& L) {
   const int64_t n = op_n(op);
   Geom g = make_geom(op);
-  L.smem = sizeof(double) * ((size_t)g.total + MAX_SLOTS + MAX_NSC + 8 * 33 + 8);
+  L.smem = sizeof(double) * ((size_t)g.total + MAX_SLOTS + MAX_NSC + 16 * 33 + 16);
   int sms = device_sms(), per_sm = 0;
   if (sms > 0) {
     if (L.smem > 48 * 1024)
@@ -296,7 +294,7 @@ extern "C" int kr_cg(const kr_op* op, const kr_solve_args* a, double* work, int6
   for (int b0 = 0; b0 < B; b0 += L.chunk) {
     P.b0 = b0;
     P.nb = (B - b0) < L.chunk ? (B - b0) : L.chunk;
-    cudaMemsetAsync(P.done, 0, sizeof(int), st);
+    cudaMemsetAsync(P.done, 0, 2 * sizeof(int), st);
     void* args[] = {&P};
     cudaError_t e = cudaLaunchCooperativeKernel(kfn, dim3(P.nb * P.Gs), dim3(NT), args, L.smem, st);
     if (e != cudaSuccess) return fail(KR_ECUDA, std::string("cg cooperative launch: ") + cudaGetErrorString(e));

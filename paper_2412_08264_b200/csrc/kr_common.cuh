@@ -14,12 +14,20 @@
 
 namespace kr {
 
+// Block barrier preceded by a full-warp reconvergence: thread-0-only sections
+// (scalar recurrences, partial reductions) leave warp 0 diverged, and the
+// .aligned bar.sync behind __syncthreads() must be reached by converged warps.
+__device__ __forceinline__ void block_barrier() {
+  __syncwarp();
+  __syncthreads();
+}
+
 constexpr int TH = 16;        // tile rows
 constexpr int TW = 32;        // tile cols
 constexpr int TPX = TH * TW;  // pixels per tile
 constexpr int NT = 256;       // threads per block for tile kernels
 constexpr int PPT = TPX / NT; // tile pixels per thread
-constexpr int MAX_SLOTS = 160;
+constexpr int MAX_SLOTS = 272;
 
 struct Geom {
   int rb;    // blur radius (0 if no blur)
@@ -85,27 +93,82 @@ __device__ inline double warp_sum(double v) {
   return v;
 }
 
-// Sum NV per-thread values over the block; red is smem of >= NV*32 doubles.
+// Warp sum of NV values at once by recursive halving ("transpose" reduction):
+// at each level a lane keeps half of its values and adds its partner's other half,
+// so NV=32 costs 16+8+4+2+1 = 31 shuffles instead of 32*5.  Afterwards value i
+// (i < NV) is complete in lane  lane_of(i)  (returned through `owner`).
+template <int W, int OFF, int P>
+__device__ inline void msum_level(double (&a)[P], int lane) {
+  if constexpr (OFF >= 1) {
+    if constexpr (W >= 2) {
+      constexpr int H = W / 2;
+      const bool upper = (lane & OFF) != 0;
+#pragma unroll
+      for (int i = 0; i < H; ++i) {
+        const double keep = upper ? a[i + H] : a[i];
+        const double send = upper ? a[i] : a[i + H];
+        a[i] = keep + __shfl_xor_sync(0xffffffffu, send, OFF);
+      }
+    } else {
+      a[0] += __shfl_xor_sync(0xffffffffu, a[0], OFF);
+    }
+    msum_level<(W >= 2 ? W / 2 : 1), OFF / 2, P>(a, lane);
+  }
+}
+
+template <int NV>
+struct MultiSum {
+  static constexpr int P = NV <= 1 ? 1 : NV <= 2 ? 2 : NV <= 4 ? 4 : NV <= 8 ? 8 : NV <= 16 ? 16 : 32;
+  // value index this lane ends up holding (fully reduced over the warp)
+  __device__ static inline int owner(int lane) {
+    int idx = 0, w = P;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      if (w > 1) {
+        if (lane & off) idx += w / 2;
+        w /= 2;
+      }
+    }
+    return idx;
+  }
+  __device__ static inline double reduce(const double (&v)[NV], int lane) {
+    double a[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) a[i] = i < NV ? v[i] : 0.0;
+    msum_level<P, 16, P>(a, lane);
+    return a[0];
+  }
+};
+
+// Sum NV per-thread values over the block; red is smem of >= NV*33 doubles.
 // Result in red[0..NV) after the call (visible to all threads).
 template <int NV>
 __device__ inline void block_sum(double (&v)[NV], double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if constexpr (NV >= 4) {
+    using M = MultiSum<NV>;
+    const double s = M::reduce(v, lane);  // lane holds the warp sum of value owner(lane)
+    const int idx = M::owner(lane);
+    block_barrier();
+    if (idx < NV && (lane & ((32 / M::P) - 1)) == 0) red[idx * 32 + warp] = s;
+  } else {
 #pragma unroll
-  for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
-  __syncthreads();
-  if (lane == 0) {
+    for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
+    block_barrier();
+    if (lane == 0) {
 #pragma unroll
-    for (int i = 0; i < NV; ++i) red[i * 32 + warp] = v[i];
+      for (int i = 0; i < NV; ++i) red[i * 32 + warp] = v[i];
+    }
   }
-  __syncthreads();
+  block_barrier();
   if (threadIdx.x < NV) {
     double acc = 0.0;
     for (int w = 0; w < nw; ++w) acc += red[threadIdx.x * 32 + w];
     red[NV * 32 + threadIdx.x] = acc;
   }
-  __syncthreads();
+  block_barrier();
   if (threadIdx.x < NV) red[threadIdx.x] = red[NV * 32 + threadIdx.x];
-  __syncthreads();
+  block_barrier();
 }
 
 // ---------------------------------------------------------------------------
@@ -147,7 +210,7 @@ __device__ inline void load_weights(const kr_op& op, const Geom& g, Smem& sm) {
   for (int i = threadIdx.x; i < nf; i += blockDim.x) sm.fw[i] = op.fweights[i];
   for (int i = threadIdx.x; i < op.blur_size && op.data_kind == KR_DATA_BLUR; i += blockDim.x)
     sm.taps[i] = op.blur_taps[i];
-  __syncthreads();
+  block_barrier();
 }
 
 // Input of a tile stencil: v = a / div, or v = a + coef * b when b != nullptr
@@ -185,7 +248,7 @@ __device__ inline void tile_hvp_dense(const kr_op& op, int b, const TileIn& in, 
     }
     res[l] = acc;
   }
-  __syncthreads();
+  block_barrier();
 }
 
 // Blur data term on the loaded region: res (+)= data_scale * A^T A v.
@@ -204,7 +267,7 @@ __device__ inline void tile_blur_normal(const kr_op& op, const Geom& g, Smem& sm
     for (int u = 0; u < bs; ++u) acc += tp[u] * src[-u];
     S1[i] = acc;
   }
-  __syncthreads();
+  block_barrier();
   // S2 = A v (vertical conv), rows [y0-rb, y0+TH+rb), cols [x0-rb, x0+TW+rb); zero outside image
   const int w2 = w1, h2 = TH + 2 * rb;
   double* S2 = sm.SB;
@@ -218,7 +281,7 @@ __device__ inline void tile_blur_normal(const kr_op& op, const Geom& g, Smem& sm
     }
     S2[i] = acc;
   }
-  __syncthreads();
+  block_barrier();
   // S3: horizontal correlation, rows [y0-rb, y0+TH+rb), cols [x0, x0+TW)
   double* S3 = sm.SA;
   for (int i = threadIdx.x; i < h2 * TW; i += blockDim.x) {
@@ -228,7 +291,7 @@ __device__ inline void tile_blur_normal(const kr_op& op, const Geom& g, Smem& sm
     for (int u = 0; u < bs; ++u) acc += tp[u] * src[u];
     S3[i] = acc;
   }
-  __syncthreads();
+  block_barrier();
   const double ds = op.data_scale;
   for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
     int ty = l / TW, tx = l - ty * TW;
@@ -238,7 +301,7 @@ __device__ inline void tile_blur_normal(const kr_op& op, const Geom& g, Smem& sm
     if (accumulate) sm.res[l] += ds * acc;
     else sm.res[l] = ds * acc;
   }
-  __syncthreads();
+  block_barrier();
 }
 
 // Learned-filter part of H v for a compile-time filter size Q (register-blocked):
@@ -251,15 +314,16 @@ template <int Q>
 __device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, int b, int y0, int x0) {
   constexpr int R = Q / 2;
   constexpr int EW = TW + 2 * R, EH = TH + 2 * R;
-  constexpr int RB1 = 3;
+  constexpr int RB1 = Q <= 3 ? 6 : (Q <= 5 ? 5 : 4);  // taller strips: fewer smem loads per FMA
   constexpr int NCH1 = (EH + RB1 - 1) / RB1;
-  constexpr int RB2 = TPX / NT;
+  constexpr int RB2 = 4;  // stage-2 rows per thread: TW * TH / RB2 = 128 active threads
   const int rows = op.rows, cols = op.cols, H = g.H, RW = g.RW;
   const int64_t n = op_n(op);
   double* S4 = sm.SA;
   const bool quad = op.potential == KR_POT_QUADRATIC;
   const int tid = threadIdx.x;
   const int tx2 = tid % TW, r2 = (tid / TW) * RB2;
+  const bool active2 = tid < TW * (TH / RB2);
   double out[RB2];
 #pragma unroll
   for (int i = 0; i < RB2; ++i) out[i] = 0.0;
@@ -302,33 +366,37 @@ __device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, 
         }
       }
     }
-    __syncthreads();
-    double acc2[RB2];
+    block_barrier();
+    if (active2) {
+      double acc2[RB2];
 #pragma unroll
-    for (int i = 0; i < RB2; ++i) acc2[i] = 0.0;
+      for (int i = 0; i < RB2; ++i) acc2[i] = 0.0;
 #pragma unroll
-    for (int sr = 0; sr < RB2 + Q - 1; ++sr) {
-      const double* src = S4 + (r2 + sr) * EW + tx2;
-      double v[Q];
+      for (int sr = 0; sr < RB2 + Q - 1; ++sr) {
+        const double* src = S4 + (r2 + sr) * EW + tx2;
+        double v[Q];
 #pragma unroll
-      for (int bb = 0; bb < Q; ++bb) v[bb] = src[bb];
+        for (int bb = 0; bb < Q; ++bb) v[bb] = src[bb];
 #pragma unroll
-      for (int i = 0; i < RB2; ++i) {
-        const int a = sr - i;  // correlation tap row
-        if (a >= 0 && a < Q) {
+        for (int i = 0; i < RB2; ++i) {
+          const int a = sr - i;  // correlation tap row
+          if (a >= 0 && a < Q) {
 #pragma unroll
-          for (int bb = 0; bb < Q; ++bb) acc2[i] = fma(k[a][bb], v[bb], acc2[i]);
+            for (int bb = 0; bb < Q; ++bb) acc2[i] = fma(k[a][bb], v[bb], acc2[i]);
+          }
         }
       }
+      const double wj = sm.fw[j];
+#pragma unroll
+      for (int i = 0; i < RB2; ++i) out[i] = fma(wj, acc2[i], out[i]);
     }
-    const double wj = sm.fw[j];
-#pragma unroll
-    for (int i = 0; i < RB2; ++i) out[i] = fma(wj, acc2[i], out[i]);
-    __syncthreads();
+    block_barrier();
   }
+  if (active2) {
 #pragma unroll
-  for (int i = 0; i < RB2; ++i) sm.res[(r2 + i) * TW + tx2] += out[i];
-  __syncthreads();
+    for (int i = 0; i < RB2; ++i) sm.res[(r2 + i) * TW + tx2] += out[i];
+  }
+  block_barrier();
 }
 
 template <int Q>
@@ -349,7 +417,7 @@ __device__ inline void tile_hvp_t(const kr_op& op, const Geom& g, Smem& sm, int 
   const int rows = op.rows, cols = op.cols, H = g.H;
   const int64_t n = op_n(op);
   load_region(op, g, in, y0, x0, sm.S0);
-  __syncthreads();
+  block_barrier();
 
   // pointwise part: mask data term + ridge
   const double* mask = (op.data_kind == KR_DATA_MASK) ? op.mask + (int64_t)b * op.mask_bstride : nullptr;
@@ -364,7 +432,7 @@ __device__ inline void tile_hvp_t(const kr_op& op, const Geom& g, Smem& sm, int 
     }
     sm.res[l] = acc;
   }
-  __syncthreads();
+  block_barrier();
   if (op.data_kind == KR_DATA_BLUR) tile_blur_normal(op, g, sm, y0, x0, true);
 
   if (Q > 0 && op.reg_kind == KR_REG_FILTERS) {
@@ -390,7 +458,7 @@ __device__ inline void tile_hvp_t(const kr_op& op, const Geom& g, Smem& sm, int 
         }
         S4[i] = e;
       }
-      __syncthreads();
+      block_barrier();
       const double wj = sm.fw[j];
       for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
         int ty = l / TW, tx = l - ty * TW;
@@ -400,7 +468,7 @@ __device__ inline void tile_hvp_t(const kr_op& op, const Geom& g, Smem& sm, int 
           for (int bb = 0; bb < q; ++bb) acc += kj[a * q + bb] * src[a * w4 + bb];
         sm.res[l] += wj * acc;
       }
-      __syncthreads();
+      block_barrier();
     }
   } else if (op.reg_kind == KR_REG_TV) {
     // p = M D v on rows [y0-1, y0+TH), cols [x0-1, x0+TW); masked where D's row is zero
@@ -424,7 +492,7 @@ __device__ inline void tile_hvp_t(const kr_op& op, const Geom& g, Smem& sm, int 
       PH[i] = ph;
       PV[i] = pv;
     }
-    __syncthreads();
+    block_barrier();
     const double wa = sm.fw[0];
     for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
       int ty = l / TW, tx = l - ty * TW;
@@ -434,7 +502,7 @@ __device__ inline void tile_hvp_t(const kr_op& op, const Geom& g, Smem& sm, int 
       double dtv = -PV[i] + PV[i - w5];
       sm.res[l] += wa * (dth + dtv);
     }
-    __syncthreads();
+    block_barrier();
   }
 }
 

@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(NT) jadj_filters_kernel(kr_op op, const double
     Sx[i] = (y >= 0 && y < op.rows && x >= 0 && x < op.cols) ? xh[(int64_t)y * op.cols + x] : 0.0;
   }
   for (int i = threadIdx.x; i < J * q2; i += blockDim.x) Sk[i] = op.kernels[i];
-  __syncthreads();
+  block_barrier();
   const int P = J * (1 + q2);
   double* outp = part + (((int64_t)b * ncols + col) * ntiles + tile) * P;
   for (int j = 0; j < J; ++j) {
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(NT) jadj_filters_kernel(kr_op op, const double
       for (int i = 0; i < 8; ++i) v8[i] = (base + i <= q2) ? acc[base + i] : 0.0;
       block_sum<8>(v8, red);
       if (threadIdx.x < 8 && base + threadIdx.x <= q2) outp[j * (1 + q2) + base + threadIdx.x] = red[threadIdx.x];
-      __syncthreads();
+      block_barrier();
     }
   }
 }
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(NT) lower_eval_kernel(kr_op op, const double* 
   const double* x = X + (int64_t)b * n;
   const double* yv = Y + (int64_t)b * n;
   load_region(op, g, TileIn{x, 1.0, nullptr, 0.0}, y0, x0, sm.S0);
-  __syncthreads();
+  block_barrier();
   double c_data = 0.0, c_ridge = 0.0, c_reg = 0.0;
   const double* mask = (op.data_kind == KR_DATA_MASK) ? op.mask + (int64_t)b * op.mask_bstride : nullptr;
   for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(NT) lower_eval_kernel(kr_op op, const double* 
     }
     sm.res[l] = acc;
   }
-  __syncthreads();
+  block_barrier();
   if (op.data_kind == KR_DATA_BLUR) {
     // residual A x - y on rows [y0-rb, y0+TH+rb) ... computed like tile_blur_normal but subtracting y
     const int rb = g.rb, bs = op.blur_size;
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(NT) lower_eval_kernel(kr_op op, const double* 
       for (int u = 0; u < bs; ++u) acc += tp[u] * src[-u];
       S1[i] = acc;
     }
-    __syncthreads();
+    block_barrier();
     const int w2 = w1, h2 = TH + 2 * rb;
     double* S2 = sm.SB;
     for (int i = threadIdx.x; i < h2 * w2; i += blockDim.x) {
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(NT) lower_eval_kernel(kr_op op, const double* 
       }
       S2[i] = acc;
     }
-    __syncthreads();
+    block_barrier();
     double* S3 = sm.SA;
     for (int i = threadIdx.x; i < h2 * TW; i += blockDim.x) {
       int r3 = i / TW, c3 = i - r3 * TW;
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(NT) lower_eval_kernel(kr_op op, const double* 
       for (int u = 0; u < bs; ++u) acc += tp[u] * src[u];
       S3[i] = acc;
     }
-    __syncthreads();
+    block_barrier();
     for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
       int ty = l / TW, tx = l - ty * TW;
       const double* src = S3 + ty * TW + tx;
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(NT) lower_eval_kernel(kr_op op, const double* 
       for (int u = 0; u < bs; ++u) acc += tp[u] * src[u * TW];
       sm.res[l] += op.data_scale * acc;
     }
-    __syncthreads();
+    block_barrier();
   }
   if (op.reg_kind == KR_REG_FILTERS) {
     const int q = op.ksize, rq = g.rq;
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(NT) lower_eval_kernel(kr_op op, const double* 
         S4[i] = e;
       }
       c_reg += wj * cj;
-      __syncthreads();
+      block_barrier();
       for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
         int ty = l / TW, tx = l - ty * TW;
         const double* src = S4 + ty * w4 + tx;
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(NT) lower_eval_kernel(kr_op op, const double* 
           for (int bb = 0; bb < q; ++bb) acc += kj[a * q + bb] * src[a * w4 + bb];
         sm.res[l] += wj * acc;
       }
-      __syncthreads();
+      block_barrier();
     }
   } else if (op.reg_kind == KR_REG_TV) {
     const int w5 = TW + 1, h5 = TH + 1;
@@ -353,14 +353,14 @@ __global__ void __launch_bounds__(NT) lower_eval_kernel(kr_op op, const double* 
       PV[i] = pv;
     }
     c_reg *= sm.fw[0];
-    __syncthreads();
+    block_barrier();
     const double wa = sm.fw[0];
     for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
       int ty = l / TW, tx = l - ty * TW;
       int i = (ty + 1) * w5 + tx + 1;
       sm.res[l] += wa * ((-PH[i] + PH[i - 1]) + (-PV[i] + PV[i - w5]));
     }
-    __syncthreads();
+    block_barrier();
   }
   double* gout = grad + (int64_t)b * n;
   for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(NT) jw_conv_kernel(kr_op op, int b, const doub
   for (int a = 0; a < Q; ++a)
 #pragma unroll
     for (int bb = 0; bb < Q; ++bb) k[a][bb] = kj[a * Q + bb];
-  __syncthreads();
+  block_barrier();
   const int tx = threadIdx.x % TW, r0 = (threadIdx.x / TW) * RB;
   double acc[RB];
 #pragma unroll

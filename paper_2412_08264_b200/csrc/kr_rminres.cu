@@ -20,7 +20,6 @@
 //    Z^T r = Z^T r_v + (Z^T C) Omega;
 //  * every reduction is a fixed-order two-level sum (warp tree, block, then the
 //    sample's blocks in rank order), so results are bitwise reproducible.
-#include <cooperative_groups.h>
 
 #include <string>
 
@@ -28,7 +27,6 @@
 #include "kr_internal.h"
 #include "kr_solver.cuh"
 
-namespace cg = cooperative_groups;
 
 namespace kr {
 
@@ -68,14 +66,24 @@ struct Scalars {
 __device__ inline double* vec(double* base, int64_t n, int b) { return base + (int64_t)b * n; }
 
 // Lanczos vector v_k (k >= 1)
-__device__ inline double* lanczos(const Params& P, int b, int k) {
+__device__ inline double* lanczos(const Params& P, int b, int k, int site = 0) {
+#ifdef KR_GUARD
+  assert(site != 1 || k >= 1);
+  assert(site != 1 || k <= P.a.max_iter);
+  assert(site != 2 || k <= P.a.max_iter);
+  assert(site != 3 || k <= P.a.max_iter);
+  assert(site != 4 || k >= 1);
+  assert(b >= 0 && b < P.op.batch);
+#endif
   if (P.a.basis) return P.a.basis + (int64_t)b * P.a.bs_basis + (int64_t)(k - 1) * P.a.ld_basis;
   return vec(P.w.vr[k & 1], P.n, b);
 }
 
+#define KR_GRID_SYNC() grid_barrier(reinterpret_cast<unsigned int*>(P.w.done) + 1, gridDim.x, grid_target)
+
 template <int Q>
 __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
-  cg::grid_group grid = cg::this_grid();
+  unsigned int grid_target = 0;
   extern __shared__ double smem[];
   const kr_op& op = P.op;
   const kr_solve_args& A = P.a;
@@ -84,24 +92,29 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
   double* tail = smem + g.total;
   double* slot_acc = tail;               // MAX_SLOTS
   double* chv = slot_acc + MAX_SLOTS;    // MAX_S (also the initial projection t)
-  double* btc1 = chv + MAX_S;
+  double* btc1 = chv + 2 * MAX_S;  // chv holds C^T hv [0,s) and C^T v [s,2s)
   double* btc2 = btc1 + MAX_S;
   double* omega = btc2 + MAX_S;
   double* nscv = omega + MAX_S;          // MAX_NSC
   double* red = nscv + MAX_NSC;          // 8*33+8
+#ifdef KR_VOLATILE_SC
+  __shared__ volatile Scalars sc;
+#else
   __shared__ Scalars sc;
+#endif
 
   const int bl = blockIdx.x / P.Gs;      // local sample index
   const int j = blockIdx.x % P.Gs;       // rank within the sample
   const int b = P.b0 + bl;               // global sample index
   const int64_t n = P.n;
   const int s = A.s, ns = (A.stop_kind == 1) ? A.nsc_s : 0;
-  const int SL_CHV = 0, SL_NSC = s, SL_ALPHA = s + ns, SL_BETA2 = s + ns + 1;
+  const int SL_CHV = 0, SL_NSC = 2 * s, SL_ALPHA = 2 * s + ns, SL_BETA2 = 2 * s + ns + 1;
   const int64_t lo = n * j / P.Gs, hi = n * (j + 1) / P.Gs;
   const int ntiles = num_tiles(op);
   const bool leader = (j == 0);
   const bool track = A.track_residual != 0;
   const Partials PP = P.parts();
+  KR_ASSERT(b < op.batch && bl < P.nb && s <= MAX_S && 2 * s + 1 <= MAX_SLOTS && ns <= MAX_NSC && hi <= n);
 
   const double* U = A.U ? A.U + (int64_t)b * A.bs_uc : nullptr;
   const double* C = A.C ? A.C + (int64_t)b * A.bs_uc : nullptr;
@@ -139,7 +152,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
     sc.alpha_prev = 0.0;
     sc.delta_stop = A.delta;
   }
-  __syncthreads();
+  block_barrier();
 
   // ---------------- setup S1: r0 = g - H w0, partial C^T r0 ----------------
   if (w0) {
@@ -154,7 +167,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
         }
         sm.res[l] = r;
       }
-      __syncthreads();
+      block_barrier();
     }
   } else {
     for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) tmp[p] = gb[p];  // g - H 0 == g exactly
@@ -168,16 +181,16 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
       vec(P.w.hvt[1], n, b)[p] = 0.0;
     }
   }
-  grid.sync();  // tmp complete (written by tiles when w0 given)
+  KR_GRID_SYNC();  // tmp complete (written by tiles when w0 given)
   if (s > 0) {
     slot_dots(C, A.ld_uc, s, lo, hi, [&](int64_t p) { return tmp[p]; }, slot_acc, red);
     write_partials(PP, bl, j, SL_CHV, s, slot_acc);
   }
-  grid.sync();
+  KR_GRID_SYNC();
   // ---------------- setup S2: projection onto the recycle space ----------------
   if (s > 0) {
     reduce_slots(PP, bl, SL_CHV, s, chv);  // t = C^T r0
-    __syncthreads();
+    block_barrier();
   }
   {
     double bsq[1] = {0.0};
@@ -202,7 +215,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
     if (threadIdx.x == 0) P.w.part[((int64_t)bl * P.nslot + SL_BETA2) * P.Gs + j] = red[0];
     if (ns > 0) {
       for (int i = threadIdx.x; i < ns; i += blockDim.x) slot_acc[i] = 0.0;
-      __syncthreads();
+      block_barrier();
       slot_dots(Z, A.ld_z, ns, lo, hi, [&](int64_t p) { return tmp[p]; }, slot_acc, red);
       write_partials(PP, bl, j, SL_NSC, ns, slot_acc);
     }
@@ -214,7 +227,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
     block_sum<1>(gsq, red);
     if (threadIdx.x == 0) P.w.part[((int64_t)bl * P.nslot + SL_ALPHA) * P.Gs + j] = red[0];
   }
-  grid.sync();
+  KR_GRID_SYNC();
   if (threadIdx.x == 0) {
     double gg = 0.0;
     const double* src = P.w.part + ((int64_t)bl * P.nslot + SL_ALPHA) * P.Gs;
@@ -222,11 +235,22 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
     double gn = sqrt(gg);
     sc.tol_bd = BREAKDOWN_RTOL * (gn > 1e-300 ? gn : 1e-300);
   }
-  __syncthreads();
+  block_barrier();
 
   // ---------------- main loop ----------------
   for (int k = 1; k <= A.max_iter + 1; ++k) {
-    if (k > 1 && *((volatile int*)P.w.done) >= P.nb) break;
+    // every sample counted: leave together (one read, broadcast -> block-uniform)
+    if (k > 1 && __syncthreads_or(threadIdx.x == 0 && *((volatile int*)P.w.done) >= P.nb)) break;
+#ifdef KR_GUARD
+    {
+      __shared__ int guard_k[NT];
+      guard_k[threadIdx.x] = k;
+      block_barrier();
+      assert(guard_k[0] == k);                                  // warp 0 at the same iteration
+      assert(guard_k[(threadIdx.x + 32) % blockDim.x] == k);    // neighbouring warp too
+      block_barrier();
+    }
+#endif
     // ===== P1 =====
     if (threadIdx.x == 0) {
       sc.do_update = 0;
@@ -290,7 +314,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
         if (sc.active && !(sc.pending && sc.pend_broke) && k <= A.max_iter) sc.do_hvp = 1;
       }
     }
-    __syncthreads();
+    block_barrier();
     if (sc.do_update) {
       // s-space recurrences (thread per recycle column)
       for (int i = threadIdx.x; i < s; i += blockDim.x) {
@@ -301,7 +325,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
       }
       // pointwise updates of iteration k-1
       const int km = k - 1;
-      const double* v = lanczos(P, b, km);
+      const double* v = lanczos(P, b, km, 1);
       double* vtn = vec(P.w.vt[km & 1], n, b);        // holds vt_{k-3} -> becomes vt_{k-1}
       const double* vto = vec(P.w.vt[(km + 1) & 1], n, b);  // vt_{k-2}
       const double* hvk = vec(P.w.hv[km & 1], n, b);
@@ -319,10 +343,10 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
         }
       }
     }
-    __syncthreads();
+    block_barrier();
     if (sc.pending && k > 1 && sc.do_update) {
       for (int i = threadIdx.x; i < ns; i += blockDim.x) slot_acc[i] = 0.0;
-      __syncthreads();
+      block_barrier();
       slot_dots(Z, A.ld_z, ns, lo, hi, [&](int64_t p) { return rv[p]; }, slot_acc, red);
       write_partials(PP, bl, j, SL_NSC, ns, slot_acc);
     }
@@ -342,10 +366,10 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
     }
     if (sc.do_hvp) {
       const double beta_k = sc.beta;
-      double* vk = lanczos(P, b, k);
+      double* vk = lanczos(P, b, k, 2);
       for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) vk[p] = tmp[p] / beta_k;
-      for (int i = threadIdx.x; i < s; i += blockDim.x) slot_acc[i] = 0.0;
-      __syncthreads();
+      for (int i = threadIdx.x; i < 2 * s + 1; i += blockDim.x) slot_acc[i] = 0.0;
+      block_barrier();
       double* hvk = vec(P.w.hv[k & 1], n, b);
       for (int tile = j; tile < ntiles; tile += P.Gs) {
         tile_hvp_t<Q>(op, g, sm, b, TileIn{tmp, beta_k, nullptr, 0.0}, tile);
@@ -353,34 +377,49 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
           int64_t p = tile_pixel(op, tile, l);
           if (p >= 0) hvk[p] = sm.res[l];
         }
-        if (s > 0) {
-          // partial C^T hv over this tile's pixels
-          for (int base = 0; base < s; base += 8) {
-            double v8[8];
+        // partials over this tile: C^T hv, C^T v and v . hv (alpha = v.hv - (C^T v).(C^T hv))
+        for (int base = 0; base < (s > 0 ? s : 1); base += 8) {
+          double v16[17];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) v8[i] = 0.0;
-            for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
-              int64_t p = tile_pixel(op, tile, l);
-              if (p < 0) continue;
-              double h = sm.res[l];
-#pragma unroll
-              for (int i = 0; i < 8; ++i)
-                if (base + i < s) v8[i] += C[(int64_t)(base + i) * A.ld_uc + p] * h;
+          for (int i = 0; i < 17; ++i) v16[i] = 0.0;
+          for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
+            int64_t p = tile_pixel(op, tile, l);
+            if (p < 0) continue;
+            const double h = sm.res[l];
+            double v;
+            if (op.data_kind == KR_DATA_DENSE) {
+              v = tmp[p] / beta_k;
+            } else {
+              const int ty = l / TW, tx = l - ty * TW;
+              v = sm.S0[(ty + g.H) * g.RW + tx + g.H];
             }
-            block_sum<8>(v8, red);
-            if (threadIdx.x < 8 && base + threadIdx.x < s) slot_acc[base + threadIdx.x] += red[threadIdx.x];
-            __syncthreads();
+            if (base == 0) v16[16] += v * h;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (base + i < s) {
+                const double c = C[(int64_t)(base + i) * A.ld_uc + p];
+                v16[i] += c * h;
+                v16[8 + i] += c * v;
+              }
           }
+          block_sum<17>(v16, red);
+          if (threadIdx.x < 8 && base + threadIdx.x < s) {
+            slot_acc[base + threadIdx.x] += red[threadIdx.x];
+            slot_acc[s + base + threadIdx.x] += red[8 + threadIdx.x];
+          }
+          if (threadIdx.x == 0 && base == 0) slot_acc[2 * s] += red[16];
+          block_barrier();
         }
-        __syncthreads();
+        block_barrier();
       }
-      if (s > 0) write_partials(PP, bl, j, SL_CHV, s, slot_acc);
+      write_partials(PP, bl, j, SL_CHV, 2 * s, slot_acc);
+      write_partial1(PP, bl, j, SL_ALPHA, slot_acc[2 * s]);
     }
-    grid.sync();
+    KR_GRID_SYNC();
     // ===== P2 =====
     if (sc.pending) {
       reduce_slots(PP, bl, SL_NSC, ns, nscv);
-      __syncthreads();
+      block_barrier();
       if (threadIdx.x == 0) {
         double ss = 0.0;
         for (int i = 0; i < ns; ++i) {
@@ -405,7 +444,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
         }
         sc.do_hvp = sc.do_hvp && sc.active;
       }
-      __syncthreads();
+      block_barrier();
       if (sc.finished && !sc.counted) {
         double* wout = A.w + (int64_t)b * n;
         double* rout = (track && A.r) ? A.r + (int64_t)b * n : nullptr;
@@ -421,13 +460,21 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
       }
     }
     if (sc.do_hvp) {
-      if (s > 0) {
-        reduce_slots(PP, bl, SL_CHV, s, chv);
-        __syncthreads();
+      // chv = C^T hv, cv = C^T v, alpha = v.hv - cv.chv  (== v.(hv - C chv), krylov.py:269-283)
+      reduce_slots(PP, bl, SL_CHV, 2 * s, chv);  // chv[0..s) and cv at chv[s..2s) (MAX_S >= 2s is checked)
+      block_barrier();
+      if (threadIdx.x == 0) {
+        double a = reduce_slot1(PP, bl, SL_ALPHA);
+        double corr = 0.0;
+        for (int i = 0; i < s; ++i) corr += chv[s + i] * chv[i];
+        sc.alpha = a - corr;
       }
-      const double* vk = lanczos(P, b, k);
+      block_barrier();
+      const double al = sc.alpha, be = sc.beta;
+      const double* vk = lanczos(P, b, k, 3);
+      const double* vkm = (k > 1) ? lanczos(P, b, k - 1, 4) : nullptr;
       const double* hvk = vec(P.w.hv[k & 1], n, b);
-      double al[1] = {0.0};
+      double bsq[1] = {0.0};
       for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
         double x = hvk[p];
         if (s > 0) {
@@ -435,29 +482,8 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
           for (int i = 0; i < s; ++i) cc += C[(int64_t)i * A.ld_uc + p] * chv[i];
           x = x - cc;  // vnext = hv - C chv
         }
-        ub[p] = x;
-        al[0] += vk[p] * x;
-      }
-      block_sum<1>(al, red);
-      if (threadIdx.x == 0) P.w.part[((int64_t)bl * P.nslot + SL_ALPHA) * P.Gs + j] = red[0];
-    }
-    grid.sync();
-    // ===== P3 =====
-    if (sc.do_hvp) {
-      if (threadIdx.x == 0) {
-        const double* src = P.w.part + ((int64_t)bl * P.nslot + SL_ALPHA) * P.Gs;
-        double a = 0.0;
-        for (int jj = 0; jj < P.Gs; ++jj) a += src[jj];
-        sc.alpha = a;
-      }
-      __syncthreads();
-      const double al = sc.alpha, be = sc.beta;
-      const double* vk = lanczos(P, b, k);
-      const double* vkm = (k > 1) ? lanczos(P, b, k - 1) : nullptr;
-      double bsq[1] = {0.0};
-      for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
-        double x = ub[p] - al * vk[p];
-        x = x - be * (vkm ? vkm[p] : 0.0);
+        x = x - al * vk[p];                // vnext -= alpha v
+        x = x - be * (vkm ? vkm[p] : 0.0);  // vnext -= beta v_prev
         tmp[p] = x;
         bsq[0] += x * x;
       }
@@ -467,7 +493,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
     {
       // evaluate before thread 0 flips `counted` (keeps the barrier below uniform)
       const bool count_now = sc.finished && !sc.counted;
-      __syncthreads();
+      block_barrier();
       if (count_now && threadIdx.x == 0) {
         sc.counted = 1;
         if (leader) {
@@ -476,9 +502,9 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
           atomicAdd(P.w.done, 1);
         }
       }
-      __syncthreads();
+      block_barrier();
     }
-    grid.sync();
+    KR_GRID_SYNC();
   }
 }
 
@@ -499,7 +525,7 @@ struct Layout {
 int plan(const kr_op& op, const kr_solve_args& a, Layout& L) {
   const int64_t n = op_n(op);
   Geom g = make_geom(op);
-  L.smem = sizeof(double) * ((size_t)g.total + MAX_SLOTS + 4 * MAX_S + MAX_NSC + 8 * 33 + 8);
+  L.smem = sizeof(double) * ((size_t)g.total + MAX_SLOTS + 5 * MAX_S + MAX_NSC + 17 * 33 + 17);
   int sms = device_sms();
   int per_sm = 0;
   if (sms > 0) {
@@ -521,7 +547,7 @@ int plan(const kr_op& op, const kr_solve_args& a, Layout& L) {
   if (Gs < 1) Gs = 1;
   L.Gs = Gs;
   int ns = a.stop_kind == 1 ? a.nsc_s : 0;
-  L.nslot = a.s + ns + 2;
+  L.nslot = 2 * a.s + ns + 2;
   L.vec_doubles = (int64_t)B * n * (a.basis ? 11 : 13);
   L.part_doubles = (int64_t)L.chunk * L.nslot * Gs;
   L.total = L.vec_doubles + L.part_doubles + 2;
@@ -606,7 +632,7 @@ extern "C" int kr_rminres(const kr_op* op, const kr_solve_args* a, double* work,
   for (int b0 = 0; b0 < B; b0 += L.chunk) {
     P.b0 = b0;
     P.nb = (B - b0) < L.chunk ? (B - b0) : L.chunk;
-    cudaMemsetAsync(P.w.done, 0, sizeof(int), st);
+    cudaMemsetAsync(P.w.done, 0, 4 * sizeof(int), st);
     dim3 grid(P.nb * P.Gs), block(NT);
     void* args[] = {&P};
     cudaError_t e = cudaLaunchCooperativeKernel(kfn, grid, block, args, L.smem, st);

@@ -2,7 +2,15 @@
 // partial sums per sample and their fixed-order (deterministic) reduction.
 #pragma once
 
+#include <cassert>
+
 #include "kr_common.cuh"
+
+#ifdef KR_GUARD
+#define KR_ASSERT(c) assert(c)
+#else
+#define KR_ASSERT(c) ((void)0)
+#endif
 
 namespace kr {
 
@@ -17,30 +25,34 @@ struct Partials {
   double* part;
   int nslot;
   int Gs;
-  __device__ inline double* at(int bl, int slot) const { return part + ((int64_t)bl * nslot + slot) * Gs; }
+  __device__ inline double* at(int bl, int slot) const {
+    KR_ASSERT(bl >= 0 && slot >= 0 && slot < nslot);
+    return part + ((int64_t)bl * nslot + slot) * Gs;
+  }
 };
 
-// acc_out[i] += sum_{p in [lo,hi)} A_i[p] * x(p), i < S; A_i = A + i*lda (8 columns per pass).
+// acc_out[i] += sum_{p in [lo,hi)} A_i[p] * x(p), i < S; A_i = A + i*lda (16 columns per pass).
 template <typename XF>
 __device__ inline void slot_dots(const double* __restrict__ A, int64_t lda, int S, int64_t lo, int64_t hi,
                                  XF xf, double* acc_out, double* red) {
-  for (int base = 0; base < S; base += 8) {
-    double v8[8];
+  for (int base = 0; base < S; base += 16) {
+    double v16[16];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v8[i] = 0.0;
+    for (int i = 0; i < 16; ++i) v16[i] = 0.0;
     for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
       double x = xf(p);
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (base + i < S) v8[i] += A[(int64_t)(base + i) * lda + p] * x;
+      for (int i = 0; i < 16; ++i)
+        if (base + i < S) v16[i] += A[(int64_t)(base + i) * lda + p] * x;
     }
-    block_sum<8>(v8, red);
-    if (threadIdx.x < 8 && base + threadIdx.x < S) acc_out[base + threadIdx.x] += red[threadIdx.x];
-    __syncthreads();
+    block_sum<16>(v16, red);
+    if (threadIdx.x < 16 && base + threadIdx.x < S) acc_out[base + threadIdx.x] += red[threadIdx.x];
+    block_barrier();
   }
 }
 
 __device__ inline void write_partials(const Partials& P, int bl, int j, int slot0, int S, const double* acc) {
+  KR_ASSERT(j >= 0 && j < P.Gs && S >= 0 && slot0 + S <= P.nslot && S <= MAX_SLOTS);
   for (int i = threadIdx.x; i < S; i += blockDim.x) P.at(bl, slot0 + i)[j] = acc[i];
 }
 
@@ -63,6 +75,26 @@ __device__ inline double reduce_slot1(const Partials& P, int bl, int slot) {
   double acc = 0.0;
   for (int jj = 0; jj < P.Gs; ++jj) acc += src[jj];
   return acc;
+}
+
+// Grid-wide barrier for a cooperative launch.  Thread 0 of every block arrives
+// with a release add on a monotone counter and polls it with acquire loads
+// (ld.acquire.gpu also invalidates the SM's L1, so the block's later plain loads
+// see the other blocks' writes).  The __syncwarp inside block_barrier() keeps
+// lanes 1..31 of warp 0 from entering the aligned bar.sync while lane 0 is still
+// polling -- cooperative_groups' grid.sync() does not, and on sm_100 that let
+// warp 0 fall one block barrier behind its siblings.
+__device__ __forceinline__ void grid_barrier(unsigned int* counter, unsigned int nblocks, unsigned int& target) {
+  block_barrier();
+  if (threadIdx.x == 0) {
+    target += nblocks;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+    } while ((int)(v - target) < 0);
+  }
+  block_barrier();
 }
 
 // Blocks per sample and samples per launch for a cooperative launch.

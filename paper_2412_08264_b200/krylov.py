@@ -149,6 +149,26 @@ def _rule_kind(rule) -> int:
     raise NotImplementedError(f"the device solver evaluates residual and NSC rules only, got {type(rule).__name__}")
 
 
+import os as _os
+
+_PAD = int(_os.environ.get("KR_PAD", "0"))  # debug: guard-pad solver buffers (doubles each side)
+_PAD_ONLY = set(filter(None, _os.environ.get("KR_PAD_ONLY", "").split(",")))
+
+
+def _buf(tag, *shape, zero=False, dev=None):
+    if _PAD and (not _PAD_ONLY or tag in _PAD_ONLY):
+        numel = 1
+        for d in shape:
+            numel *= d
+        flat = torch.full((numel + 2 * _PAD,), float("nan"), dtype=torch.float64, device=dev)
+        t = flat[_PAD: _PAD + numel].view(*shape)
+        if zero:
+            t.zero_()
+        return t
+    f = torch.zeros if zero else torch.empty
+    return f(*shape, dtype=torch.float64, device=dev)
+
+
 class _Launch:
     """Device buffers + kr_solve_args for one batched solve."""
 
@@ -171,8 +191,8 @@ class _Launch:
         self.dims = dims
         a.s = s
         if s:
-            U = torch.zeros(B, s, n, dtype=torch.float64, device=dev)
-            C = torch.zeros(B, s, n, dtype=torch.float64, device=dev)
+            U = _buf("U", B, s, n, zero=True, dev=dev)
+            C = _buf("C", B, s, n, zero=True, dev=dev)
             for b, r in enumerate(recycles):
                 if r is not None and r.dim:
                     U[b, : r.dim] = r.U.T
@@ -194,7 +214,7 @@ class _Launch:
         if kind == 1:
             zs = [r.data.z_block() for r in rules]
             ns = max(z.shape[1] for z in zs)
-            Z = torch.zeros(B, ns, n, dtype=torch.float64, device=dev)
+            Z = _buf("Z", B, ns, n, zero=True, dev=dev)
             for b, z in enumerate(zs):
                 Z[b, : z.shape[1]] = z.T
             a.nsc_s, a.Z, a.ld_z, a.bs_z = ns, Z.data_ptr(), n, ns * n
@@ -203,17 +223,17 @@ class _Launch:
                 ZtC = torch.bmm(Z, self.C.transpose(1, 2)).contiguous()  # (B, ns, s)
                 a.ZtC = ZtC.data_ptr()
                 self.keep.append(ZtC)
-        self.w = torch.empty(B, n, dtype=torch.float64, device=dev)
+        self.w = _buf("w", B, n, dev=dev)
         a.w = self.w.data_ptr()
-        self.r = torch.empty(B, n, dtype=torch.float64, device=dev) if track else None
+        self.r = _buf("r", B, n, dev=dev) if track else None
         if track:
             a.r = self.r.data_ptr()
         self.basis = None
         if want_basis:
-            self.basis = torch.empty(B, opts.max_iter, n, dtype=torch.float64, device=dev)
+            self.basis = _buf("basis", B, opts.max_iter, n, dev=dev)
             a.basis, a.ld_basis, a.bs_basis = self.basis.data_ptr(), n, opts.max_iter * n
-        self.res = torch.empty(B, opts.max_iter + 1, dtype=torch.float64, device=dev)
-        self.vals = torch.empty(B, opts.max_iter + 1, dtype=torch.float64, device=dev)
+        self.res = _buf("res", B, opts.max_iter + 1, dev=dev)
+        self.vals = _buf("vals", B, opts.max_iter + 1, dev=dev)
         self.iters = torch.zeros(B, dtype=torch.int32, device=dev)
         self.reasons = torch.zeros(B, dtype=torch.int32, device=dev)
         a.res_norms, a.stop_vals = self.res.data_ptr(), self.vals.data_ptr()
@@ -226,7 +246,7 @@ class _Launch:
         wl = fn_ws(ctypes.byref(H.op), ctypes.byref(self.args))
         if wl < 0:
             _lib.check(-1, "workspace query")
-        ws = torch.empty(max(int(wl), 1), dtype=torch.float64, device=self.w.device)
+        ws = _buf("ws", max(int(wl), 1), dev=self.w.device)
         ev = None
         if _lib.PROFILE is not None:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
