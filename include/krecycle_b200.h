@@ -20,6 +20,8 @@
  *                         recurrence (krylov.py:154-181) and the stop rules
  *                         ResidualNormRule / NscRule (stopping.py:93-118)
  *   kr_cg              <- cg (krylov.py:408-483)
+ *   kr_syev_select     <- the t x t eigen-selection inside ritz_select / gsvd_pair /
+ *                         rgen_select (recycling.py:202-213, 226-236, 275-359)
  *
  * All array pointers are DEVICE pointers (fp64 unless stated), all calls are
  * asynchronous on the given CUDA stream, and every function returns 0 on
@@ -147,6 +149,21 @@ int kr_rminres(const kr_op* op, const kr_solve_args* args, double* work, int64_t
 int64_t kr_cg_workspace(const kr_op* op, const kr_solve_args* args);
 int kr_cg(const kr_op* op, const kr_solve_args* args, double* work, int64_t work_len,
           kr_stream_t stream);
+
+/* Selected eigenpairs of a batch of symmetric t_b x t_b matrices (t_b <= tmax <= 228),
+ * the eigen-selection step of ritz_select (recycling.py:226-236, _select_indices
+ * :202-213, _clamp_dim) and of gsvd_pair's right singular vectors
+ * (recycling.py:275-313, through Q1^T Q1).  Matrix b: element (i, j) at
+ * A + b*bsa + j*lda + i (symmetrised as (A + A^T)/2), t_b = dims[b] (DEVICE int32).
+ * size_code 0/1/2 = S/L/M: s_b = min(s, t_b) pairs, the s_b smallest (S), the s_b
+ * largest (L), or s_b/2 smallest then the rest largest (M), ascending.  Outputs:
+ * lam[b*bsl + q], eigenvector q of sample b at Z + b*bsz + q*ldz (rows >= t_b and
+ * columns >= s_b zeroed, largest-|component| positive), nsel[b] = s_b (optional). */
+int64_t kr_syev_select_workspace(int32_t batch, int32_t tmax);
+int kr_syev_select(const double* A, int64_t lda, int64_t bsa, const int32_t* dims, int32_t batch,
+                   int32_t tmax, int32_t size_code, int32_t s, double* lam, int64_t bsl, double* Z,
+                   int64_t ldz, int64_t bsz, int32_t* nsel, double* work, int64_t work_len,
+                   kr_stream_t stream);
 
 #ifdef __cplusplus
 }

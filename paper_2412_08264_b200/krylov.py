@@ -284,10 +284,16 @@ class _Launch:
 
 
 def _split_by_rule(rules):
-    groups: dict = {}
+    """Contiguous runs of samples sharing (rule kind, tolerance): one launch per run."""
+    runs: list = []
+    key_prev = None
     for b, r in enumerate(rules):
-        groups.setdefault((_rule_kind(r), float(r.delta)), []).append(b)
-    return list(groups.values())
+        key = (_rule_kind(r), float(r.delta))
+        if key != key_prev:
+            runs.append([])
+            key_prev = key
+        runs[-1].append(b)
+    return runs
 
 
 def _solve(H, g, recycle, opts, kind):
@@ -338,12 +344,10 @@ def _solve(H, g, recycle, opts, kind):
 
 
 def _subbatch(H, idx):
-    """Operator restricted to samples idx (one sample at a time when idx is not contiguous)."""
+    """Operator restricted to the contiguous sample run idx."""
     if len(idx) == 1:
         return H.sample(idx[0])
-    if idx == list(range(idx[0], idx[0] + len(idx))) and hasattr(H, "slice"):
-        return H.slice(idx[0], idx[0] + len(idx))
-    raise NotImplementedError("mixed stop rules inside one batch need contiguous sample groups")
+    return H.slice(idx[0], idx[0] + len(idx))
 
 
 def minres(H, g, opts: SolveOptions | None = None):

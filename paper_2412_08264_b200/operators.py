@@ -295,8 +295,12 @@ class Model:
 
     def sample(self, b: int) -> "Model":
         """Single-sample view (shares device storage)."""
-        sl = slice(b, b + 1)
-        return Model(self.shape, 1, self.data_kind, self.data_scale, self.ridge, self.y[sl],
+        return self.slice(b, b + 1)
+
+    def slice(self, lo: int, hi: int) -> "Model":
+        """View of samples [lo, hi) (shares device storage)."""
+        sl = slice(lo, hi)
+        return Model(self.shape, hi - lo, self.data_kind, self.data_scale, self.ridge, self.y[sl],
                      None if self.x_true is None else self.x_true[sl],
                      None if self.mask is None else (self.mask[sl] if self.mask.shape[0] > 1 else self.mask),
                      self.taps, self.reg_kind, self.potential, self.eps, self.num_filters, self.ksize)
@@ -447,18 +451,24 @@ class HessianOperator(SymmetricOperator):
     def sample(self, b: int) -> "HessianOperator":
         if not 0 <= b < self.batch:
             raise IndexError(f"sample {b} out of range for batch {self.batch}")
+        return self.slice(b, b + 1)
+
+    def slice(self, lo: int, hi: int) -> "HessianOperator":
+        """Operator over samples [lo, hi): the same kr_op with shifted per-sample pointers."""
+        if not 0 <= lo < hi <= self.batch:
+            raise IndexError(f"samples [{lo}, {hi}) out of range for batch {self.batch}")
         op = KrOp.from_buffer_copy(self.op)
-        op.batch = 1
+        op.batch = hi - lo
         k = self._keep
         if op.mask_bstride:
-            op.mask = k["mask"][b].data_ptr()
+            op.mask = k["mask"][lo].data_ptr()
         if "curv" in k:
-            op.curv = k["curv"][b].data_ptr()
+            op.curv = k["curv"][lo].data_ptr()
         if "slope" in k:
-            op.slope = k["slope"][b].data_ptr()
+            op.slope = k["slope"][lo].data_ptr()
         if "xhat" in k:
-            op.xhat = k["xhat"][b].data_ptr()
-        return HessianOperator(self.model.sample(b), op, self._keep)
+            op.xhat = k["xhat"][lo].data_ptr()
+        return HessianOperator(self.model.slice(lo, hi), op, self._keep)
 
     def _apply_cols(self, M: torch.Tensor) -> torch.Tensor:
         # M: (B, n, t) with contiguous columns
@@ -518,6 +528,9 @@ class DenseOperator(HessianOperator):
 
     def sample(self, b: int) -> "DenseOperator":
         return DenseOperator(self.matrix[b], self.apply_cost)
+
+    def slice(self, lo: int, hi: int) -> "DenseOperator":
+        return DenseOperator(self.matrix[lo:hi], self.apply_cost)
 
 
 def dense_operator(M, apply_cost=None) -> DenseOperator:
