@@ -22,6 +22,9 @@
  *   kr_cg              <- cg (krylov.py:408-483)
  *   kr_syev_select     <- the t x t eigen-selection inside ritz_select / gsvd_pair /
  *                         rgen_select (recycling.py:202-213, 226-236, 275-359)
+ *   kr_chol_inv        <- the t x t factorizations of the QRs in build_candidate_basis,
+ *                         gsvd_pair, prepare_recycle and the condition check
+ *                         (recycling.py:187-199, 290-313, 362-383)
  *
  * All array pointers are DEVICE pointers (fp64 unless stated), all calls are
  * asynchronous on the given CUDA stream, and every function returns 0 on
@@ -164,6 +167,20 @@ int kr_syev_select(const double* A, int64_t lda, int64_t bsa, const int32_t* dim
                    int32_t tmax, int32_t size_code, int32_t s, double* lam, int64_t bsl, double* Z,
                    int64_t ldz, int64_t bsz, int32_t* nsel, double* work, int64_t work_len,
                    kr_stream_t stream);
+
+/* Batched Cholesky + triangular inverse of the t_b x t_b Gram blocks of the
+ * Cholesky-QR passes (recycling._cholqr2 batched; the reference's pivoted QR at
+ * recycling.py:187-199, 362-383 and the QR of [Jt; Ht] at :305) and of the
+ * W^T H W condition screen (recycling.py:290-296).  G b: element (i, j) at
+ * G + b*bsg + i*ldg + j (symmetrised), t_b = dims[b] <= tmax <= 228 (DEVICE int32).
+ * flags bit 0: scale by D = sqrt(diag G); bit 1: write F.  shift (nullable,
+ * DEVICE, per sample) is added to the scaled diagonal.  G_s = L L^T; F = L^{-1} D^{-1}
+ * row-major (F + b*bsf + i*ldf + j), zero upper triangle, identity pad block.
+ * info[b] = -1 or the first row whose pivot is not positive; stats[4b..4b+3] =
+ * (min L_jj, max L_jj, min D, 0) (nullable). */
+int kr_chol_inv(const double* G, int64_t ldg, int64_t bsg, const int32_t* dims, int32_t batch,
+                int32_t tmax, int32_t flags, const double* shift, double* F, int64_t ldf, int64_t bsf,
+                double* stats, int32_t* info, kr_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -50,3 +50,305 @@ def syev_select(M: torch.Tensor, dims: torch.Tensor, size: str, s: int):
                                 ws.data_ptr(), wl, _lib.stream_ptr()), "kr_syev_select")
     _lib.note_launch("kr_syev_select")
     return lam[:, :s], Z[:, :s], nsel
+
+
+STATS: dict | None = None  # set to {} to count declined samples per check
+
+CHOLQR_TOL = 1e-7   # recycling.CHOLQR_TOL
+COND_SCREEN = 1e6   # recycling.COND_SCREEN
+COND_LIMIT = 1e12   # recycling.COND_LIMIT
+
+
+def _row_mask(dims, T: int, device) -> torch.Tensor:
+    d = torch.as_tensor(dims, device=device).reshape(-1, 1)
+    return (torch.arange(T, device=device).reshape(1, -1) < d).to(torch.float64)
+
+
+def _identity_pad(G: torch.Tensor, mask: torch.Tensor) -> torch.Tensor:
+    """G with the pad rows/columns replaced by those of the identity."""
+    return G * (mask.unsqueeze(2) * mask.unsqueeze(1)) + torch.diag_embed(1.0 - mask)
+
+
+def _masked_extrema(d: torch.Tensor, mask: torch.Tensor):
+    live = mask > 0
+    big = torch.finfo(d.dtype).max
+    return torch.where(live, d, -big).amax(1), torch.where(live, d, big).amin(1)
+
+
+CHOL_TMAX = 228          # kr_chol_inv's shared-memory limit
+SHIFTED_COND_MAX = 1e14  # shifted CholeskyQR3 is backward stable below ~1/u; keep a margin
+
+
+def _chol_inv(G: torch.Tensor, dims: torch.Tensor, scale: bool, shift: torch.Tensor | None = None,
+              inverse: bool = True):
+    """Per sample: D = sqrt(diag G) (scale) or 1, G_s = D^-1 G D^-1 + shift I on the
+    leading dims[b] block, G_s = L L^T.  Returns (F, info, stats): F = L^-1 D^-1
+    (row-major, identity pad; None unless inverse), info[b] = first failing row or
+    -1, stats[b] = (min L_jj, max L_jj, min D).  kr_chol_inv (one CTA per matrix)
+    for T <= 228, torch.linalg otherwise."""
+    B, T, _ = G.shape
+    dev = G.device
+    dims = dims.to(device=dev, dtype=torch.int32).contiguous()
+    if T <= CHOL_TMAX:
+        G = G.contiguous()
+        F = torch.empty_like(G) if inverse else None
+        stats = torch.empty(B, 4, dtype=torch.float64, device=dev)
+        info = torch.empty(B, dtype=torch.int32, device=dev)
+        sh = None if shift is None else shift.to(torch.float64).contiguous()
+        _lib.check(_lib.lib().kr_chol_inv(G.data_ptr(), T, T * T, dims.data_ptr(), B, T,
+                                          int(scale) | (2 if inverse else 0), 0 if sh is None else sh.data_ptr(),
+                                          0 if F is None else F.data_ptr(), T, T * T, stats.data_ptr(),
+                                          info.data_ptr(), _lib.stream_ptr()), "kr_chol_inv")
+        _lib.note_launch("kr_chol_inv")
+        return F, info, stats
+    mask = _row_mask(dims, T, dev)
+    live = mask > 0
+    g = G.diagonal(dim1=1, dim2=2)
+    D = torch.where(live & (g > 0), g.clamp_min(0.0).sqrt(), torch.ones_like(g)) if scale else torch.ones_like(g)
+    Gs = _identity_pad(0.5 * (G + G.transpose(1, 2)) / (D.unsqueeze(2) * D.unsqueeze(1)), mask)
+    if shift is not None:
+        Gs = Gs + shift.reshape(-1, 1, 1) * torch.diag_embed(mask)
+    L, inf = torch.linalg.cholesky_ex(Gs)
+    info = torch.where(inf > 0, inf - 1, torch.full_like(inf, -1)).to(torch.int32)
+    # kr_chol_inv's breakdown rule: a pivot L_jj^2 <= 4 t eps Gs_jj is a dependent row
+    piv_rtol = 4.0 * dims.to(torch.float64).reshape(-1, 1) * torch.finfo(torch.float64).eps
+    tiny = (L.diagonal(dim1=1, dim2=2) ** 2 <= piv_rtol * Gs.diagonal(dim1=1, dim2=2)) & live
+    first_tiny = torch.where(tiny, torch.arange(T, device=dev).reshape(1, -1), T).amin(1).to(torch.int32)
+    info = torch.where((first_tiny < T) & ((info < 0) | (first_tiny < info)), first_tiny, info)
+    hi, lo = _masked_extrema(L.diagonal(dim1=1, dim2=2), mask)
+    dmin = torch.where(live, g.clamp_min(0.0).sqrt(), torch.full_like(g, 1e308)).amin(1) if scale \
+        else torch.ones_like(lo)
+    stats = torch.stack([lo, hi, dmin, torch.zeros_like(lo)], dim=1)
+    stats[:, :3] = torch.where((dims > 0).reshape(-1, 1), stats[:, :3], torch.ones_like(stats[:, :3]))
+    F = None
+    if inverse:
+        eye = torch.eye(T, dtype=G.dtype, device=dev).expand(B, T, T)
+        F = torch.linalg.solve_triangular(L, eye, upper=False) / D.unsqueeze(1)
+    return F, info, stats
+
+
+def cholqr2_rows(A: torch.Tensor, mask: torch.Tensor, robust: bool = False, want_f: bool = True):
+    """Orthonormalise rows [0, t_b) of A (B, T, n) (pad rows zero) by two
+    Cholesky-QR passes, the first on the row-scaled block (recycling._cholqr2).
+
+    Returns (Q, F, ok): Q = F @ A with orthonormal live rows and zero pad rows;
+    F = R^{-T} for the column form A_col = Q_col R (so |R_jj| = 1 / |F_jj|); ok[b]
+    is False where the block is too ill-conditioned or rank deficient.  With
+    want_f=False, F is replaced by its diagonal (B, T).
+
+    robust=True: samples CholQR2 declines are redone as shifted CholeskyQR3
+    (Fukaya, Kannan, Nakatsukasa, Zhang, Yamamoto, SIAM J. Sci. Comput. 2020: a
+    first pass on G + sigma I, sigma = 11 (n t + t(t+1)) u ||A_s||^2, then CholQR2),
+    backward stable up to cond ~ 1/u; declined only when the bound
+    cond(A) <= ||A||_F ||R^{-1}||_F exceeds SHIFTED_COND_MAX.  Also returns the
+    first row where a Cholesky broke down (-1 if none)."""
+    B, T, n = A.shape
+    dims = mask.sum(1).to(torch.int32)
+    G = A @ A.transpose(1, 2)
+    F1, i1, st = _chol_inv(G, dims, scale=True)
+    ok1 = (i1 < 0) & (st[:, 0] > CHOLQR_TOL * st[:, 1]) & (st[:, 2] > 0)
+    shifted = robust and not bool(ok1.all())
+    if shifted:
+        tb = dims.to(torch.float64)  # ||A_s||_2^2 <= ||A_s||_F^2 = t_b after row scaling
+        sigma = 11.0 * (n * tb + tb * (tb + 1)) * torch.finfo(A.dtype).eps * tb
+        F1, i1, _ = _chol_inv(G, dims, scale=True, shift=torch.where(ok1, torch.zeros_like(sigma), sigma))
+    Q = F1 @ A
+    ok = i1 < 0
+    fail_row = i1.clone()
+    Fs = [F1]
+    for _ in range(2 if shifted else 1):
+        Fk, ik, _ = _chol_inv(Q @ Q.transpose(1, 2), dims, scale=False)
+        Q = Fk @ Q
+        Fs.append(Fk)
+        fail_row = torch.where((fail_row < 0) & (ik >= 0), ik, fail_row)
+        ok = ok & (ik < 0)
+    if want_f or shifted:
+        F = Fs[0]
+        for Fk in Fs[1:]:
+            F = Fk @ F
+    if shifted:
+        cond_bound = torch.linalg.vector_norm(A, dim=(1, 2)) * torch.linalg.matrix_norm(F)
+        ok = ok & (ok1 | (cond_bound <= SHIFTED_COND_MAX))
+    else:
+        ok = ok & ok1
+    if not want_f:
+        F = Fs[0].diagonal(dim1=1, dim2=2)
+        for Fk in Fs[1:]:
+            F = F * Fk.diagonal(dim1=1, dim2=2)
+    if robust:
+        return Q, F, ok, fail_row
+    return Q, F, ok
+
+
+def _compact_rows(A: torch.Tensor, keep: torch.Tensor):
+    """Move the kept rows of every sample to the front (order preserved), zero the rest."""
+    B, T, n = A.shape
+    ar = torch.arange(T, device=A.device).expand(B, T)
+    order = torch.argsort(torch.where(keep, ar, ar + T), dim=1, stable=True)
+    out = torch.gather(A, 1, order.unsqueeze(2).expand(B, T, n))
+    cnt = keep.sum(1)
+    out = out * (ar < cnt.unsqueeze(1)).unsqueeze(2).to(A.dtype)
+    return out, cnt
+
+
+def orth_rows_drop(A: torch.Tensor, dims: list[int], rounds: int = 8):
+    """Candidate basis with the reference's rank drop, batched: (W, dims_after, ok).
+
+    recycling._orth_drop removes the rows (columns of the n x t block) whose
+    unpivoted |R_jj| <= RANK_TOL max |R_ii| and redoes the QR.  Here a round of
+    (shifted) Cholesky QR either succeeds -- then that rule is applied to R's
+    diagonal (|R_jj| = 1 / |F_jj|) -- or its Cholesky breaks down at the first
+    numerically dependent row (the later row of a dependent set, the one the
+    unpivoted rule drops), which is removed; rows are compacted and the QR redone."""
+    from .recycling import RANK_TOL
+
+    B, T, _ = A.shape
+    mask = _row_mask(dims, T, A.device)
+    ar = torch.arange(T, device=A.device).reshape(1, -1)
+    for _ in range(rounds):
+        W, Fd, ok, fail_row = cholqr2_rows(A, mask, robust=True, want_f=False)
+        rd = 1.0 / Fd.abs()
+        rmax, _ = _masked_extrema(rd, mask)
+        live = mask > 0
+        factored = (fail_row < 0) & torch.isfinite(rmax)
+        drop = live & (rd <= RANK_TOL * rmax.unsqueeze(1)) & factored.unsqueeze(1)
+        drop = drop | (live & (ar == fail_row.unsqueeze(1)))
+        if not bool(drop.any()):
+            return W, dims, ok
+        A, cnt = _compact_rows(A, live & ~drop)
+        dims = cnt.cpu().tolist()
+        mask = _row_mask(dims, T, A.device)
+    W, _, ok, _ = cholqr2_rows(A, mask, robust=True, want_f=False)
+    return W, dims, ok
+
+
+def supports(strategy) -> bool:
+    """Strategies the whole-batch update computes to the reference's accuracy.
+
+    RGen takes its vectors from the eigenpairs of Q1^T Q1 (alpha^2), which are as
+    accurate as the reference's SVD of Q1 for alpha near 1 -- the largest mu,
+    size L -- but square the gaps between small alpha (sizes S, M); those stay on
+    the per-sample SVD path.  Ritz uses eigh(W^T H W) exactly as the reference."""
+    if strategy.placement != "outer":
+        return False
+    return strategy.vec_type == "Ritz" or (strategy.vec_type == "RGen" and strategy.size == "L")
+
+
+def recycle_update(strategy, s: int, H, J, bases, recycles, reuse_products: bool = True):
+    """``next_recycle`` (recycling.py:386-465) for every sample of a batch at once.
+
+    Outer placement, vector types RGen (``rgen_select`` :316-359 + ``gsvd_pair``
+    :275-313) and Ritz (``ritz_select`` :226-236); H, J are the batched operators of
+    the upcoming system; bases[b] is the previous Lanczos basis (n x k_b) and
+    recycles[b] the previous RecycleSpace of sample b.  Returns one RecycleSpace per
+    sample, or None where the batched path declines -- CholQR2 conditioning, the
+    Hessian-condition screen (recycling._hessian_condition), t_b > EIG_TMAX -- and
+    the caller runs the per-sample path of ``recycling.next_recycle`` instead.
+
+    Candidate order is the reference's [V_prev, U_prev]; every downstream quantity
+    depends on the candidate span only (exact arithmetic)."""
+    import warnings
+
+    from .recycling import RecycleSpace
+    from .stopping import NscData
+
+    if not supports(strategy):
+        raise ValueError(f"the batched recycle update covers outer RGen-L / Ritz, not {strategy}")
+    B = len(bases)
+    n = H.dim
+    k = [0 if V is None else int(V.shape[1]) for V in bases]
+    sp = [0 if r is None else int(r.dim) for r in recycles]
+    t = [a + c for a, c in zip(k, sp)]
+    T = max(t) if t else 0
+    if T == 0 or s == 0:
+        return [RecycleSpace.empty(n) for _ in range(B)]
+    if T > EIG_TMAX:
+        return [None] * B
+    if any(s > tb > 0 for tb in t):
+        warnings.warn(f"requested {s} recycle vectors but only {min(tb for tb in t if tb > 0)} candidates; "
+                      "clamping", stacklevel=3)
+    dev = H.model.y.device if getattr(H, "model", None) is not None else bases[0].device
+    A = torch.zeros(B, T, n, dtype=torch.float64, device=dev)
+    for b in range(B):
+        if k[b]:
+            A[b, : k[b]] = bases[b].T
+        if sp[b]:
+            A[b, k[b]: t[b]] = recycles[b].U.T
+    # candidate basis W = orth([V_prev, U_prev]) with the rank drop (recycling.py:187-199)
+    W, t, ok = orth_rows_drop(A, t)
+    mask = _row_mask(t, T, dev)
+    tt = torch.tensor(t, dtype=torch.int32, device=dev)
+    checks = {"candidates": ok}
+    HW = H.apply_matrix(W.transpose(1, 2)).transpose(1, 2)          # (B, T, n)
+    Ht = W @ HW.transpose(1, 2)
+    Ht = 0.5 * (Ht + Ht.transpose(1, 2))                            # _sym(W^T H W)
+    mu = VH = None
+    if strategy.vec_type == "Ritz":
+        _, Z, nsel = syev_select(Ht, tt, strategy.size, s)
+        coeffs = Z
+    else:
+        Jt = J.apply_adjoint_matrix(W.transpose(1, 2)).transpose(1, 2)  # (B, T, p): row j = J w_j
+        p = Jt.shape[2]
+        # _hessian_condition: Cholesky-pivot screen, exact extreme eigenvalues where it fails
+        _, ih, hst = _chol_inv(Ht, tt, scale=False, inverse=False)
+        screen = (ih < 0) & (hst[:, 0] > 0) & ((hst[:, 1] / hst[:, 0]) ** 2 < COND_SCREEN)
+        if not bool(screen.all()):
+            ext, _, _ = syev_select(Ht, tt, "M", 2)
+            lo_, hi_ = ext[:, 0], ext[:, -1]
+            # all eigenvalues are in [lo_, hi_]; |.| extremes as in the reference
+            smax = torch.maximum(lo_.abs(), hi_.abs())
+            exact_ok = (lo_ > 0) & (lo_ >= COND_LIMIT ** -1 * smax)
+            screen = screen | exact_ok
+        checks["cond_screen"] = screen
+        ok = ok & screen
+        # gsvd_pair: [Jt; Ht] = Q R, Z from Q1^T Q1, alpha/beta as column norms
+        QS, FS, okS = cholqr2_rows(torch.cat([Jt, Ht], dim=2), mask)
+        checks["gsvd_qr"] = okS
+        ok = ok & okS
+        Q1 = QS[:, :, :p]
+        _, Z, nsel = syev_select(Q1 @ Q1.transpose(1, 2), tt, strategy.size, s)
+        Y = Z @ QS                                                  # (B, s, p + T)
+        alpha = torch.linalg.vector_norm(Y[..., :p], dim=2).clamp(0.0, 1.0)
+        beta = torch.linalg.vector_norm(Y[..., p:], dim=2)
+        ok = ok & ((beta > 0) | (torch.arange(s, device=dev).reshape(1, -1) >= nsel.reshape(-1, 1))).all(1)
+        beta_safe = torch.where(beta > 0, beta, torch.ones_like(beta))
+        mu = alpha / beta_safe
+        VH = Y[..., p:] / beta_safe.unsqueeze(2)                    # rows = V_H columns
+        X = Z @ FS                                                  # rows = R^{-1} z
+        coeffs = {"R": X, "L": VH, "M": None}[strategy.side]
+    if coeffs is None:  # side M: normalised mean of both candidate sets, H applied explicitly
+        cand = 0.5 * (VH @ W + X @ W)
+        nr = torch.linalg.vector_norm(cand, dim=2, keepdim=True)
+        cand = cand / torch.where(nr > 0, nr, torch.ones_like(nr))
+        HU = H.apply_matrix(cand.transpose(1, 2)).transpose(1, 2)
+    else:
+        cand = coeffs @ W
+        HU = coeffs @ HW if reuse_products else H.apply_matrix(cand.transpose(1, 2)).transpose(1, 2)
+    # prepare_recycle (recycling.py:362-383): H U~ = C R, U = U~ R^{-1}
+    smask = _row_mask(nsel, s, dev)
+    C, Fu, okU = cholqr2_rows(HU, smask)
+    U = Fu @ cand
+    checks["prepare_qr"] = okU
+    ok = ok & okU
+    Znsc = None if mu is None else (mu.unsqueeze(2) * VH) @ W        # rows of W V_H diag(mu)
+    ok_h = ok.cpu().tolist()
+    if STATS is not None:
+        for name, flag in checks.items():
+            STATS[name] = STATS.get(name, 0) + int((~flag).sum())
+        STATS["declined"] = STATS.get("declined", 0) + sum(1 for b in range(B) if not ok_h[b])
+        STATS["samples"] = STATS.get("samples", 0) + B
+    nsel_h = nsel.cpu().tolist()
+    out = []
+    for b in range(B):
+        sb = nsel_h[b]
+        if t[b] == 0 or sb == 0:
+            out.append(RecycleSpace.empty(n))
+            continue
+        if not ok_h[b]:
+            out.append(None)
+            continue
+        nsc = None
+        if mu is not None:
+            nsc = NscData(values=mu[b, :sb], v_h=VH[b, :sb, : t[b]].T, w=W[b, : t[b]].T, z=Znsc[b, :sb].T)
+        out.append(RecycleSpace(U=U[b, :sb].T, C=C[b, :sb].T, nsc_data=nsc))
+    return out

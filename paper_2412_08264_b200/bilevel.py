@@ -14,8 +14,10 @@ from dataclasses import dataclass, field
 
 import torch
 
+from .batched import recycle_update, supports as batched_supports
 from .krylov import SolveOptions, SolveResult, rminres
-from .operators import FoEParams, ImageVector, InpaintingProblem, Model, as_device, _foe_model
+from .operators import (DenseOperator, FoEParams, HessianOperator, ImageVector, InpaintingProblem, Model,
+                        StencilJacobian, as_device, _foe_model)
 from .recycling import RecycleSpace, StrategyDescriptor, next_recycle
 from .stopping import ConfigurationError, NscRule, ResidualNormRule
 
@@ -94,6 +96,7 @@ class SequenceSolver:
         self._prev_jac = None
         self._prev_solution = None
         self.max_workers = 8
+        self.batched_update = True
         self._streams = None
         self._pool = None
 
@@ -114,6 +117,15 @@ class SequenceSolver:
                 torch.empty(nbytes // 8, dtype=torch.float64, device="cuda")
         torch.cuda.synchronize()
 
+    def _batched(self, hessian, jac) -> bool:
+        """Whether the whole-batch recycle update (batched.recycle_update) applies."""
+        st = self.cfg.strategy
+        if not self.batched_update or not batched_supports(st):
+            return False
+        if not isinstance(hessian, HessianOperator) or isinstance(hessian, DenseOperator):
+            return False
+        return st.vec_type == "Ritz" or isinstance(jac, StencilJacobian)
+
     def _recycle_one(self, hessian, jac, B, b):
         cfg = self.cfg
         hb = hessian if B == 1 else hessian.sample(b)
@@ -131,6 +143,11 @@ class SequenceSolver:
         dominated by latency-bound t x t decompositions, so with B > 1 each sample runs
         on its own host thread and CUDA stream (torch releases the GIL inside ops);
         the caller's stream waits for all of them."""
+        if self._batched(hessian, jac):
+            recs = recycle_update(self.cfg.strategy, self.cfg.recycle_dim, hessian, jac, self._prev_basis,
+                                  self._prev_recycle, self.cfg.reuse_products)
+            # samples the batched path declined take the per-sample reference path
+            return [r if r is not None else self._recycle_one(hessian, jac, B, b) for b, r in enumerate(recs)]
         if B == 1 or self.max_workers <= 1:
             return [self._recycle_one(hessian, jac, B, b) for b in range(B)]
         main = torch.cuda.current_stream()

@@ -221,9 +221,19 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
   double* yv = R + T;
   double* Ap = R + 2 * T;
   const double* Ab = P.A + (int64_t)b * P.bsa;
-  for (int i = warp; i < t; i += EW)
-    for (int j = lane; j <= i; j += 32)
-      Ap[pk(i, j)] = 0.5 * (Ab[(int64_t)j * P.lda + i] + Ab[(int64_t)i * P.lda + j]);
+  // (A + A^T) / 2 with coalesced reads: storage rows into the lower triangle, then
+  // storage rows again onto the transposed positions
+  for (int i = warp; i < t; i += EW) {
+    const double* ai = Ab + (int64_t)i * P.lda;
+#pragma unroll 4
+    for (int j = lane; j <= i; j += 32) Ap[pk(i, j)] = __ldg(ai + j);
+  }
+  __syncthreads();
+  for (int j = warp; j < t; j += EW) {
+    const double* aj = Ab + (int64_t)j * P.lda;
+#pragma unroll 4
+    for (int i = j + 1 + lane; i < t; i += 32) Ap[pk(i, j)] = 0.5 * (Ap[pk(i, j)] + __ldg(aj + i));
+  }
   __syncthreads();
   for (int k = 0; k + 1 < t; ++k) {
     const int m = t - k - 1;

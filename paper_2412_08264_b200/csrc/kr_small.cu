@@ -1,0 +1,263 @@
+// kr_small.cu -- batched Cholesky + triangular inverse of the small Gram matrices
+// of the recycle update (the Cholesky-QR passes of recycling._cholqr2 and the
+// batched path, and the _hessian_condition screen, recycling.py:290-296).
+//
+// One CTA per matrix, the t x t lower triangle packed in shared memory
+// (t <= CHOL_TMAX): scale by D = sqrt(diag G) (optional), add a diagonal shift
+// (optional, shifted CholeskyQR), factor G = L L^T (blocked right-looking),
+// report the first failing row and the extreme pivots, and overwrite L by
+// L^{-1} (blocked forward substitution, one thread per column).  Output F = L^{-1} D^{-1}, a full
+// row-major T x T matrix: lower triangle F, zero upper triangle, identity in the
+// pad block (rows/columns >= t_b), ready to be the left GEMM operand F @ A.
+
+#include "kr_common.cuh"
+#include "kr_internal.h"
+
+namespace kr {
+namespace {
+
+constexpr int CNT = 512;
+constexpr int CHOL_TMAX = 228;
+constexpr int NB = 16;
+
+struct CholParams {
+  const double* G;
+  int64_t ldg, bsg;
+  const int32_t* dims;
+  int T, flags;
+  const double* shift;
+  double* F;
+  int64_t ldf, bsf;
+  double* stats;  // per sample: [min L_jj, max L_jj, min D, 0]
+  int32_t* info;  // per sample: -1 = factored, else the first failing row
+};
+
+__device__ __forceinline__ int64_t pk(int i, int j) { return (int64_t)i * (i + 1) / 2 + j; }
+
+// 1/sqrt(d) for d > 0 without the sqrt/div slow-path calls (which force spills in
+// fully unrolled register code): hardware approximation + three Newton steps.
+__device__ __forceinline__ double rsqrt_nr(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+#pragma unroll
+  for (int it = 0; it < 3; ++it) {
+    const double h = 0.5 * d * y;
+    y = fma(y, fma(-h, y, 0.5), y);
+  }
+  return y;
+}
+
+__global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
+  extern __shared__ double sm[];
+  const int tid = threadIdx.x;
+  const int b = blockIdx.x;
+  const int t = P.dims[b];
+  const int T = P.T;
+  double* D = sm;                 // T
+  double* col = D + T;            // T (cached column)
+  double* rdiag = col + T;        // NB reciprocal pivots of the current block
+  double* Lbb = rdiag + NB;       // NB x (NB + 1) copy of a diagonal block
+  double* A = Lbb + NB * (NB + 1);  // packed lower t(t+1)/2
+  __shared__ int s_fail;
+  const double* Gb = P.G + (int64_t)b * P.bsg;
+  const bool scale = P.flags & 1, inv = P.flags & 2;
+  for (int i = tid; i < t; i += CNT) {
+    const double g = Gb[(int64_t)i * P.ldg + i];
+    D[i] = (scale && g > 0.0) ? sqrt(g) : 1.0;
+  }
+  if (tid == 0) s_fail = -1;
+  __syncthreads();
+  const double sh = P.shift ? P.shift[b] : 0.0;
+  // lower triangle (as potrf 'L'), rows coalesced, independent loads in flight
+  for (int i = tid >> 5; i < t; i += CNT / 32) {
+    const double* gi = Gb + (int64_t)i * P.ldg;
+    const double di = D[i];
+#pragma unroll 4
+    for (int j = tid & 31; j <= i; j += 32) A[pk(i, j)] = __ldg(gi + j) / (di * D[j]) + (i == j ? sh : 0.0);
+  }
+  __syncthreads();
+  for (int i = tid; i < t; i += CNT) col[i] = A[pk(i, i)];  // diagonal before factoring
+  __syncthreads();
+  // a pivot below PIV_RTOL * (its original diagonal) is a breakdown: the row is
+  // numerically dependent on the previous ones (exact dependence rounds either way)
+  const double piv_rtol = 4.0 * t * 1.1102230246251565e-16;
+  // ---- blocked Cholesky (right-looking, NB = 32) ----
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int kb = 0; kb < t; kb += NB) {
+    const int nb = min(NB, t - kb);
+    if (warp == 0) {  // diagonal block in registers: lane = row, column j broadcast by shuffles
+      double a[NB];
+#pragma unroll
+      for (int k = 0; k < NB; ++k) a[k] = (lane < nb && k <= lane) ? A[pk(kb + lane, kb + k)] : 0.0;
+      int bad = -1;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        if (j < nb && bad < 0) {
+          const double d = __shfl_sync(0xffffffffu, a[j], j);
+          if (!(d > piv_rtol * col[kb + j])) {
+            bad = kb + j;
+          } else {
+            const double rl = rsqrt_nr(d), ljj = d * rl;
+            const double lij = lane == j ? ljj : a[j] * rl;
+            if (lane >= j) a[j] = lij;
+#pragma unroll
+            for (int k = j + 1; k < NB; ++k) {
+              const double lkj = __shfl_sync(0xffffffffu, lij, k);
+              if (lane >= k) a[k] -= lij * lkj;
+            }
+          }
+        }
+      }
+      if (lane < nb) {
+#pragma unroll
+        for (int k = 0; k < NB; ++k)
+          if (k <= lane) A[pk(kb + lane, kb + k)] = a[k];
+        rdiag[lane] = 1.0 / a[lane];  // (outside the unrolled code)
+      }
+      if (lane == 0 && bad >= 0) s_fail = bad;
+    }
+    __syncthreads();
+    if (s_fail >= 0) break;
+    // panel: rows below solve x L_kk^T = a (forward substitution over the block columns)
+    for (int r = kb + nb + tid; r < t; r += CNT) {
+      double x[NB];
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        if (c < nb) {
+          double v = A[pk(r, kb + c)];
+          for (int m = 0; m < c; ++m) v -= x[m] * A[pk(kb + c, kb + m)];
+          x[c] = v * rdiag[c];
+          A[pk(r, kb + c)] = x[c];
+        }
+      }
+    }
+    __syncthreads();
+    // trailing update A_ij -= L_i,panel . L_j,panel (lower part), warp per row, lanes over j
+    for (int i = kb + nb + warp; i < t; i += CNT / 32) {
+      const double* Li = A + pk(i, kb);
+      for (int j = kb + nb + lane; j <= i; j += 32) {
+        const double* Lj = A + pk(j, kb);
+        double acc = 0.0;
+#pragma unroll 8
+        for (int c = 0; c < nb; ++c) acc += Li[c] * Lj[c];
+        A[pk(i, j)] -= acc;
+      }
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  const int fail = s_fail;
+  if (P.stats) {  // extreme pivots and the smallest row norm, warp 0
+    if (warp == 0) {
+      double lo = 1e308, hi = 0.0, dm = 1e308;
+      for (int j = lane; j < t; j += 32) {
+        if (fail < 0) {
+          lo = fmin(lo, A[pk(j, j)]);
+          hi = fmax(hi, A[pk(j, j)]);
+        }
+        dm = fmin(dm, scale ? sqrt(fmax(Gb[(int64_t)j * P.ldg + j], 0.0)) : 1.0);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        dm = fmin(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+      }
+      if (lane == 0) {
+        P.stats[4 * b + 0] = t ? lo : 1.0;
+        P.stats[4 * b + 1] = t ? hi : 1.0;
+        P.stats[4 * b + 2] = t ? dm : 1.0;
+        P.stats[4 * b + 3] = 0.0;
+      }
+    }
+  }
+  if (tid == 0) P.info[b] = fail;
+  if (!inv) return;
+  double* Fb = P.F + (int64_t)b * P.bsf;
+  if (fail >= 0) {  // no factor: identity (callers discard the sample)
+    for (int64_t e = tid; e < (int64_t)T * T; e += CNT) {
+      const int i = (int)(e / T), j = (int)(e % T);
+      Fb[(int64_t)i * P.ldf + j] = i == j ? 1.0 : 0.0;
+    }
+    return;
+  }
+  // ---- X = L^{-1} by blocked forward substitution ----
+  // block row I: V = E_I - L_I,<I X_<I over (row, column) pairs spread across the
+  // CTA, staged in the (not yet written) output rows of F, then X_I = L_II^{-1} V,
+  // one thread per column, from a copy of L_II; X_I overwrites L_I.
+  for (int ib = 0; ib < t; ib += NB) {
+    const int nb = min(NB, t - ib);
+    const int w = ib + nb;  // columns 0 .. w-1 are nonzero in block row I
+    for (int e = tid; e < nb * nb; e += CNT) {
+      const int r = e / nb, m = e % nb;
+      Lbb[r * (NB + 1) + m] = m <= r ? A[pk(ib + r, ib + m)] : 0.0;
+      if (m == r) rdiag[r] = 1.0 / A[pk(ib + r, ib + r)];
+    }
+    for (int r = warp; r < nb; r += CNT / 32) {
+      const double* Li = A + pk(ib + r, 0);
+      double* vr = Fb + (int64_t)(ib + r) * P.ldf;
+      for (int c = lane; c < w; c += 32) {
+        double acc = 0.0, a1 = 0.0;
+        if (c < ib) {
+          int k = c;
+          for (; k + 1 < ib; k += 2) {
+            acc += Li[k] * A[pk(k, c)];
+            a1 += Li[k + 1] * A[pk(k + 1, c)];
+          }
+          if (k < ib) acc += Li[k] * A[pk(k, c)];
+        }
+        vr[c] = (c == ib + r ? 1.0 : 0.0) - (acc + a1);
+      }
+    }
+    __syncthreads();
+    if (tid < w) {  // column c: forward substitution with L_II
+      const int c = tid;
+      double x[NB];
+#pragma unroll
+      for (int r = 0; r < NB; ++r) {
+        if (r < nb) {
+          double s = (c <= ib + r) ? Fb[(int64_t)(ib + r) * P.ldf + c] : 0.0;
+          for (int m = 0; m < r; ++m) s -= Lbb[r * (NB + 1) + m] * x[m];
+          x[r] = s * rdiag[r];
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < NB; ++r)
+        if (r < nb && c <= ib + r) A[pk(ib + r, c)] = x[r];
+    }
+    __syncthreads();
+  }
+  // ---- F = L^{-1} D^{-1}, full row-major T x T ----
+  for (int i = warp; i < T; i += CNT / 32) {
+    double* fi = Fb + (int64_t)i * P.ldf;
+    for (int j = lane; j < T; j += 32) {
+      double v;
+      if (i < t && j < t)
+        v = j <= i ? A[pk(i, j)] / D[j] : 0.0;
+      else
+        v = i == j ? 1.0 : 0.0;
+      fi[j] = v;
+    }
+  }
+}
+
+}  // namespace
+}  // namespace kr
+
+using namespace kr;
+
+extern "C" int kr_chol_inv(const double* G, int64_t ldg, int64_t bsg, const int32_t* dims, int32_t batch,
+                           int32_t tmax, int32_t flags, const double* shift, double* F, int64_t ldf, int64_t bsf,
+                           double* stats, int32_t* info, kr_stream_t stream) {
+  KR_CHECK_ARG(batch >= 0 && tmax >= 0, "negative size");
+  KR_CHECK_ARG(tmax <= CHOL_TMAX, "kr_chol_inv: t exceeds the shared-memory limit (228)");
+  KR_CHECK_ARG(ldg >= tmax, "leading dimension smaller than t");
+  KR_CHECK_ARG(!(flags & 2) || (F && ldf >= tmax), "inverse requested without an output");
+  if (batch == 0) return KR_OK;
+  KR_CHECK_ARG(G && dims && info, "null pointer");
+  CholParams P{G, ldg, bsg, dims, tmax, flags, shift, F, ldf, bsf, stats, info};
+  const size_t smem = (size_t)(2 * tmax + NB + NB * (NB + 1) + (int64_t)tmax * (tmax + 1) / 2) * sizeof(double);
+  KR_TRY(ensure_smem((const void*)chol_inv_kernel, smem));
+  chol_inv_kernel<<<batch, CNT, smem, (cudaStream_t)stream>>>(P);
+  return check_launch("chol_inv_kernel");
+}

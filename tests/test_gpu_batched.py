@@ -1,0 +1,227 @@
+"""Whole-batch recycle update (batched.recycle_update) against the per-sample
+path (recycling.next_recycle, itself pinned to the oracle in test_gpu_bilevel /
+test_gpu_replay), and batched CholQR2 with padding.
+
+Equal in exact arithmetic; compared through basis-independent quantities:
+the spanned projectors of U and C, the selected mu values, and Z = W V_H diag(mu)
+(sign-free up to column order: Z's columns carry the eigenvector sign, so the
+projector of Z and the mu values are compared)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _proj(M):
+    Q, _ = torch.linalg.qr(M)
+    return Q @ Q.T
+
+
+def test_cholqr2_rows_padding():
+    from paper_2412_08264_b200.batched import _row_mask, cholqr2_rows
+
+    g = torch.Generator(device="cuda").manual_seed(0)
+    B, T, n = 3, 12, 500
+    dims = [12, 7, 0]
+    A = torch.randn(B, T, n, generator=g, dtype=torch.float64, device="cuda")
+    for b, d in enumerate(dims):
+        A[b, d:] = 0
+    mask = _row_mask(dims, T, "cuda")
+    Q, F, ok = cholqr2_rows(A, mask)
+    assert ok.tolist() == [True, True, True]
+    for b, d in enumerate(dims):
+        Qb = Q[b, :d]
+        assert torch.allclose(Qb @ Qb.T, torch.eye(d, dtype=torch.float64, device="cuda"), atol=1e-14)
+        assert torch.all(Q[b, d:] == 0)
+        assert torch.allclose(F[b] @ A[b], Q[b], atol=1e-12)
+        # A_col = Q_col R with R = F^{-T} upper triangular (positive diagonal)
+        R = torch.linalg.inv(F[b, :d, :d]).T
+        assert torch.allclose(torch.triu(R), R, atol=1e-12) and bool((R.diagonal() > 0).all())
+    # ill-conditioned and rank-deficient blocks are declined
+    A2 = A.clone()
+    A2[0, 5] = A2[0, 4] * (1 + 1e-12)
+    A2[1, 3] = 0
+    _, _, ok2 = cholqr2_rows(A2, mask)
+    assert ok2.tolist() == [False, False, True]
+    # shifted CholeskyQR3 takes cond ~ 1e8 blocks (which CholQR2 declines) ...
+    A3 = A.clone()
+    A3[0, 5] = A3[0, 4] + 1e-8 * A3[0, 5]
+    _, _, ok3 = cholqr2_rows(A3, mask)
+    Q3, F3, ok3r, _ = cholqr2_rows(A3, mask, robust=True)
+    assert ok3.tolist() == [False, True, True] and ok3r.tolist() == [True, True, True]
+    Qb = Q3[0, :12]
+    assert torch.allclose(Qb @ Qb.T, torch.eye(12, dtype=torch.float64, device="cuda"), atol=1e-14)
+    assert torch.dist(F3[0] @ A3[0], Q3[0]) <= 1e-6 * torch.linalg.norm(Q3[0])  # forward error ~ cond * eps
+    # ... and still declines near-dependent ones (the reference's pivoted QR drops a column)
+    _, _, ok2r, fr = cholqr2_rows(A2, mask, robust=True)
+    assert ok2r.tolist() == [False, False, True] and fr.tolist()[2] == -1
+
+
+def _setup(strategy, s=6, size=32, B=4, steps=2):
+    from paper_2412_08264_b200 import HessianSolveConfig, SequenceSolver
+    from paper_2412_08264_b200.bilevel import hypergradients
+    from paper_2412_08264_b200.problems import DeblurConfig, make_batch, synthetic_sequence
+
+    cfg = DeblurConfig(size, B, 5, 1.0, 0.01, "filters", 4, 3)
+    model = make_batch(cfg)
+    th, xh = synthetic_sequence(cfg, model.x_true.cpu().numpy(), steps + 1)
+    seq = SequenceSolver(HessianSolveConfig.from_strategy(strategy, recycle_dim=s, delta=1e-8, max_iter=40))
+    seq.batched_update = False
+    for i in range(steps):
+        hypergradients(model, th[i], torch.as_tensor(xh[i], device="cuda"), seq)
+    H, J = model.at(th[steps], torch.as_tensor(xh[steps], device="cuda"))
+    return model, seq, H, J
+
+
+def _selection_well_posed(st, Hb, Jb, seq, b):
+    """False when the S/L/M cut splits a cluster of equal selection keys (then the
+    selected subspace is arbitrary in the reference too, e.g. the mu = 0 null
+    cluster when t > p)."""
+    from paper_2412_08264_b200.recycling import _select_indices, _sym, build_candidate_basis, gsvd_pair
+
+    W = build_candidate_basis(seq._prev_basis[b], seq._prev_recycle[b].U).W
+    t = W.shape[1]
+    Ht = _sym(W.T @ Hb.apply_matrix(W))
+    if st.vec_type == "Ritz":
+        key = torch.linalg.eigvalsh(Ht)
+    else:
+        Jt = Jb.apply_adjoint_matrix(W)
+        if Jt.shape[0] < t:
+            Jt = torch.cat([Jt, torch.zeros(t - Jt.shape[0], t, dtype=Jt.dtype, device=Jt.device)])
+        key = gsvd_pair(Jt, Ht, symmetric=True).mu
+    key = key.sort().values
+    s = min(seq.cfg.recycle_dim, t)
+    sel = set(_select_indices(t, s, st.size, "cpu").tolist())
+    scale = float(key.abs().max())
+    for i in range(t - 1):
+        if (i in sel) != (i + 1 in sel) and float(key[i + 1] - key[i]) <= 1e-6 * scale:
+            return False
+    return True
+
+
+def test_declines_small_mu_selections():
+    from paper_2412_08264_b200.batched import supports
+    from paper_2412_08264_b200.recycling import StrategyDescriptor as S
+
+    assert supports(S.parse("RGen-L(R)-NSC")) and supports(S.parse("Ritz-S")) and supports(S.parse("RGen-L(M)"))
+    assert not supports(S.parse("RGen-S(L)")) and not supports(S.parse("RGen-M(R)"))
+    assert not supports(S.parse("inner:RGen-L(R)")) and not supports(S.parse("HRitz-S"))
+
+
+@pytest.mark.parametrize("strategy", ["RGen-L(R)-NSC", "RGen-L(L)", "RGen-L(M)", "Ritz-S", "Ritz-L", "Ritz-M"])
+def test_recycle_update_matches_per_sample(strategy):
+    from paper_2412_08264_b200.batched import recycle_update
+    from paper_2412_08264_b200.recycling import next_recycle
+
+    model, seq, H, J = _setup(strategy)
+    st = seq.cfg.strategy
+    batched = recycle_update(st, seq.cfg.recycle_dim, H, J, seq._prev_basis, seq._prev_recycle)
+    for b in range(model.batch):
+        ref = next_recycle(st, h_current=H.sample(b), jac_current=J.sample(b), prev_basis=seq._prev_basis[b],
+                           prev_recycle=seq._prev_recycle[b], s=seq.cfg.recycle_dim)
+        got = batched[b]
+        assert got is not None
+        assert got.dim == ref.dim
+        if _selection_well_posed(st, H.sample(b), J.sample(b), seq, b):
+            assert torch.dist(_proj(got.C), _proj(ref.C)) <= 1e-8
+            assert torch.dist(_proj(got.U), _proj(ref.U)) <= 1e-8
+        assert torch.allclose(got.C.T @ got.C, torch.eye(got.dim, dtype=torch.float64, device="cuda"), atol=1e-13)
+        HU = H.sample(b).apply_matrix(got.U)
+        assert torch.dist(HU, got.C) <= 1e-10 * torch.linalg.norm(HU)
+        if ref.nsc_data is not None:
+            a, r = got.nsc_data, ref.nsc_data
+            assert torch.allclose(a.values, r.values, rtol=1e-8, atol=1e-12)
+            assert torch.dist(_proj(a.z_block()), _proj(r.z_block())) <= 1e-8
+            # the NSC value of any residual agrees (sign-free)
+            v = torch.randn(model.n, dtype=torch.float64, device="cuda")
+            na = torch.linalg.vector_norm(a.z_block().T @ v)
+            nr = torch.linalg.vector_norm(r.z_block().T @ v)
+            # (mu near zero -- size S -- is only absolutely accurate, as in the reference)
+            floor = 1e-12 * float(torch.linalg.vector_norm(v)) * r.values.numel() ** 0.5
+            assert abs(float(na - nr)) <= 1e-9 * float(nr) + floor
+
+
+def test_sequence_batched_equals_per_sample():
+    """Whole sequences through SequenceSolver: iteration counts and hypergradients agree."""
+    from paper_2412_08264_b200 import HessianSolveConfig, SequenceSolver
+    from paper_2412_08264_b200.bilevel import hypergradients
+    from paper_2412_08264_b200.problems import DeblurConfig, make_batch, synthetic_sequence
+
+    cfg = DeblurConfig(48, 4, 7, 1.2, 0.01, "filters", 4, 5)
+    model = make_batch(cfg)
+    th, xh = synthetic_sequence(cfg, model.x_true.cpu().numpy(), 4)
+    out = {}
+    for batched in (False, True):
+        seq = SequenceSolver(HessianSolveConfig.from_strategy("RGen-L(R)-NSC", recycle_dim=8, delta=1e-8,
+                                                              max_iter=120))
+        seq.batched_update = batched
+        rows = []
+        for i in range(4):
+            hg, res, _ = hypergradients(model, th[i], torch.as_tensor(xh[i], device="cuda"), seq)
+            rows.append((hg.cpu().numpy(), [r.iterations for r in res]))
+        out[batched] = rows
+    # the two paths are equal in exact arithmetic; in floating point both carry the
+    # solve's roundoff amplification, so compare their distances to a tight solve
+    from paper_2412_08264_b200 import ResidualNormRule, SolveOptions, minres
+
+    for i, ((hg0, it0), (hg1, it1)) in enumerate(zip(out[False], out[True])):
+        assert max(abs(a - b) for a, b in zip(it0, it1)) <= 2
+        H, J = model.at(th[i], torch.as_tensor(xh[i], device="cuda"))
+        G = torch.as_tensor(xh[i], device="cuda").reshape(model.batch, -1) - model.x_true
+        res = minres(H, G, SolveOptions(stop_rule=ResidualNormRule(1e-13), max_iter=3000))
+        exact = J.apply_adjoint(torch.stack([r.solution for r in res])).cpu().numpy()
+        e0 = np.abs(hg0 - exact).max()
+        e1 = np.abs(hg1 - exact).max()
+        assert e1 <= 3 * e0 + 1e-9 * np.abs(exact).max(), (i, e0, e1)
+
+
+def test_recycle_update_rank_drop():
+    """Exactly dependent candidates are dropped as in recycling._orth_drop (no fallback)."""
+    from paper_2412_08264_b200 import batched
+    from paper_2412_08264_b200.recycling import next_recycle
+
+    model, seq, H, J = _setup("RGen-L(R)-NSC")
+    st = seq.cfg.strategy
+    bases = list(seq._prev_basis)
+    V0 = bases[0]
+    bases[0] = torch.cat([V0, V0[:, :2], 3.0 * V0[:, 5:6]], dim=1)  # three dependent columns
+    batched.STATS = {}
+    try:
+        got = batched.recycle_update(st, seq.cfg.recycle_dim, H, J, bases, seq._prev_recycle)
+        assert batched.STATS["declined"] == 0, batched.STATS
+    finally:
+        batched.STATS = None
+    ref = next_recycle(st, h_current=H.sample(0), jac_current=J.sample(0), prev_basis=bases[0],
+                       prev_recycle=seq._prev_recycle[0], s=seq.cfg.recycle_dim)
+    assert got[0].nsc_data.w.shape[1] == ref.nsc_data.w.shape[1] == V0.shape[1] + seq._prev_recycle[0].dim
+    assert torch.dist(_proj(got[0].C), _proj(ref.C)) <= 1e-8
+    assert torch.allclose(got[0].nsc_data.values, ref.nsc_data.values, rtol=1e-8)
+
+
+@pytest.mark.parametrize("T", [1, 7, 64, 228])
+def test_chol_inv_kernel_matches_torch(T, monkeypatch):
+    """kr_chol_inv (one CTA per matrix) against the torch.linalg formulation."""
+    from paper_2412_08264_b200 import batched
+
+    g = torch.Generator(device="cuda").manual_seed(T)
+    B = 5
+    dims = torch.tensor([T, max(T - 3, 0), T, 1, T], dtype=torch.int32)
+    X = torch.randn(B, T, 3 * T + 4, generator=g, dtype=torch.float64, device="cuda")
+    X = X * torch.logspace(0, -3, T, dtype=torch.float64, device="cuda").reshape(1, -1, 1)
+    G = X @ X.transpose(1, 2)
+    if T > 2:
+        G[2, 1, :] = G[2, 0, :]  # breakdown at row 1 of sample 2 (rows 0, 1 equal)
+        G[2, :, 1] = G[2, :, 0]
+    shift = torch.tensor([0.0, 1e-3, 0.0, 0.0, 2e-6], dtype=torch.float64, device="cuda")
+    for scale in (True, False):
+        for sh in (None, shift):
+            F, info, st = batched._chol_inv(G, dims, scale, sh)
+            monkeypatch.setattr(batched, "CHOL_TMAX", -1)
+            Ft, infot, stt = batched._chol_inv(G, dims, scale, sh)
+            monkeypatch.setattr(batched, "CHOL_TMAX", 228)
+            assert info.tolist() == infot.tolist()
+            good = info < 0
+            assert torch.allclose(st[good, :3], stt[good, :3], rtol=1e-12, atol=0)
+            assert torch.allclose(F[good], Ft[good], rtol=1e-9, atol=1e-12 * float(Ft[good].abs().max()))
