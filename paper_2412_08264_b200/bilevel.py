@@ -8,6 +8,7 @@ launch per upper step.  ``hypergradient`` is bilevel.py:291-305.
 
 from __future__ import annotations
 
+import os
 import warnings
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
@@ -97,6 +98,9 @@ class SequenceSolver:
         self._prev_solution = None
         self.max_workers = 8
         self.batched_update = True
+        self.groups = int(os.environ.get("KR_RECYCLE_GROUPS", "2"))
+        self._gstreams = None
+        self._gpool = None
         self._streams = None
         self._pool = None
 
@@ -109,6 +113,16 @@ class SequenceSolver:
         if batch <= 1 or self.max_workers <= 1:
             return
         _warm_linalg()
+        ng = max(1, min(self.groups, batch))
+        if self.batched_update and ng > 1:
+            if self._gstreams is None or len(self._gstreams) < ng:
+                self._gstreams = [torch.cuda.Stream() for _ in range(ng)]
+                self._gpool = ThreadPoolExecutor(max_workers=ng)
+            for st in self._gstreams:
+                with torch.cuda.stream(st):
+                    torch.empty(-(-batch // ng) * nbytes // 8, dtype=torch.float64, device="cuda")
+            torch.cuda.synchronize()
+            return
         if self._streams is None or len(self._streams) < batch:
             self._streams = [torch.cuda.Stream() for _ in range(batch)]
             self._pool = ThreadPoolExecutor(max_workers=min(batch, self.max_workers))
@@ -125,6 +139,47 @@ class SequenceSolver:
         if not isinstance(hessian, HessianOperator) or isinstance(hessian, DenseOperator):
             return False
         return st.vec_type == "Ritz" or isinstance(jac, StencilJacobian)
+
+    def _recycle_batched(self, hessian, jac, B):
+        """Whole-batch recycle update in ``groups`` sample groups, each on its own host
+        thread and CUDA stream: a group's latency-bound t x t kernels (one CTA per
+        sample) overlap the other groups' GEMMs and stencils."""
+        cfg = self.cfg
+        ng = max(1, min(self.groups, B))
+        bounds = [(g * B // ng, (g + 1) * B // ng) for g in range(ng)]
+
+        def run(lo, hi):
+            hs = hessian if (lo, hi) == (0, B) else hessian.slice(lo, hi)
+            js = jac if (lo, hi) == (0, B) or jac is None else jac.slice(lo, hi)
+            recs = recycle_update(cfg.strategy, cfg.recycle_dim, hs, js, self._prev_basis[lo:hi],
+                                  self._prev_recycle[lo:hi], cfg.reuse_products)
+            # samples the batched path declined take the per-sample reference path
+            return [r if r is not None else self._recycle_one(hessian, jac, B, lo + i) for i, r in enumerate(recs)]
+
+        if ng == 1:
+            return run(0, B)
+        main = torch.cuda.current_stream()
+        if self._gstreams is None or len(self._gstreams) < ng:
+            _warm_linalg()
+            self._gstreams = [torch.cuda.Stream() for _ in range(ng)]
+            self._gpool = ThreadPoolExecutor(max_workers=ng)
+
+        def work(g):
+            st = self._gstreams[g]
+            st.wait_stream(main)
+            with torch.cuda.stream(st):
+                recs = run(*bounds[g])
+            for rec in recs:
+                for t in (rec.U, rec.C) + ((rec.nsc_data.values, rec.nsc_data.v_h, rec.nsc_data.w,
+                                           rec.nsc_data.z_block()) if rec.nsc_data is not None else ()):
+                    if t is not None:
+                        t.record_stream(main)
+            return recs
+
+        out = [r for recs in self._gpool.map(work, range(ng)) for r in recs]
+        for g in range(ng):
+            main.wait_stream(self._gstreams[g])
+        return out
 
     def _recycle_one(self, hessian, jac, B, b):
         cfg = self.cfg
@@ -144,10 +199,7 @@ class SequenceSolver:
         on its own host thread and CUDA stream (torch releases the GIL inside ops);
         the caller's stream waits for all of them."""
         if self._batched(hessian, jac):
-            recs = recycle_update(self.cfg.strategy, self.cfg.recycle_dim, hessian, jac, self._prev_basis,
-                                  self._prev_recycle, self.cfg.reuse_products)
-            # samples the batched path declined take the per-sample reference path
-            return [r if r is not None else self._recycle_one(hessian, jac, B, b) for b, r in enumerate(recs)]
+            return self._recycle_batched(hessian, jac, B)
         if B == 1 or self.max_workers <= 1:
             return [self._recycle_one(hessian, jac, B, b) for b in range(B)]
         main = torch.cuda.current_stream()

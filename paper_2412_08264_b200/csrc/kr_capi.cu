@@ -1,6 +1,8 @@
 // kr_capi.cu -- ABI version, error state, operator validation, device queries.
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <utility>
 #include <string>
 
 #include "kr_common.cuh"
@@ -66,11 +68,22 @@ int validate_op(const kr_op& op) {
   return KR_OK;
 }
 
+// The opt-in cap only ever grows (per kernel and device): host threads launching
+// the same kernel with different sizes must not lower it under each other.
 int ensure_smem(const void* kernel, size_t bytes) {
   if (bytes > 227 * 1024) return fail(KR_EINVAL, "tile needs more than 227 KB of shared memory");
   if (bytes > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e != cudaSuccess) return fail(KR_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> cap;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& c = cap[{dev, kernel}];
+    if (bytes > c) {
+      cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      if (e != cudaSuccess) return fail(KR_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+      c = bytes;
+    }
   }
   return KR_OK;
 }

@@ -578,6 +578,10 @@ class StencilJacobian(MixedJacobianOperator):
         H = HessianOperator(self.model, self.op, self._keep).sample(b)
         return StencilJacobian(H.model, H.op, self._keep)
 
+    def slice(self, lo: int, hi: int) -> "StencilJacobian":
+        H = HessianOperator(self.model, self.op, self._keep).slice(lo, hi)
+        return StencilJacobian(H.model, H.op, self._keep)
+
     def _apply_cols(self, W: torch.Tensor) -> torch.Tensor:
         B, n, t = W.shape
         p = self.num_params
