@@ -30,6 +30,10 @@ from pathlib import Path
 
 import numpy as np
 
+# load every CUDA module at context creation: a library kernel first used inside
+# the timed region (e.g. the Householder rank-drop path) must not pay module loading there
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
@@ -151,7 +155,7 @@ def run_ours(args):
     t_max = cfg.max_iter + cfg.recycle_dim
     per_sample = 8 * n * t_max * 6  # W, H W, candidates, QR workspaces of one sample's recycle update
     seq = SequenceSolver(solver_cfg)
-    seq.reserve(B, per_sample)
+    seq.reserve(B, per_sample, shape=(n, t_max))
     for i in range(args.warmup):
         step(seq, i, xhats[i])
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
@@ -163,7 +167,14 @@ def run_ours(args):
     evs = []
     iters = []
     with ClockSampler(local) as clk:
+        dbg = os.environ.get("KR_BENCH_DEBUG")
+        if dbg:
+            from paper_2412_08264_b200 import batched as _bt
+            _bt.STATS = {}
         for i in range(args.warmup, steps_total):
+            if dbg:
+                m0 = torch.cuda.memory_stats()
+                s0 = dict(_bt.STATS)
             flush.zero_()  # L2 flush between timed steps (outside the events)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -171,6 +182,14 @@ def run_ours(args):
             e1.record()
             evs.append((e0, e1))
             iters.append([r.iterations for r in res])
+            if dbg:
+                torch.cuda.synchronize()
+                m1 = torch.cuda.memory_stats()
+                ds = {k: _bt.STATS[k] - s0.get(k, 0) for k in _bt.STATS}
+                print(f"step {i}: {e0.elapsed_time(e1):.1f} ms iters {iters[-1]} stats {ds} "
+                      f"mallocs {m1.get('num_device_alloc', 0) - m0.get('num_device_alloc', 0)} "
+                      f"retries {m1.get('num_alloc_retries', 0) - m0.get('num_alloc_retries', 0)}",
+                      file=sys.stderr, flush=True)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -204,7 +223,7 @@ def run_ours(args):
     if not args.no_e2e:
         pinned = [torch.from_numpy(x).pin_memory() for x in xhats_np]
         seq2 = SequenceSolver(solver_cfg)
-        seq2.reserve(B, per_sample)
+        seq2.reserve(B, per_sample, shape=(n, t_max))
         for i in range(args.warmup):
             X = pinned[i].to("cuda", non_blocking=True)
             step(seq2, i, X).__getitem__(0).cpu()
@@ -243,6 +262,7 @@ def run_ours(args):
                        "sequence": "synthetic frozen sequence (problems.synthetic_sequence)",
                        "l2": "flushed (256 MB write) before every timed step",
                        "parallelism": f"sample-sharded dp{world}"},
+            "step_ms": [round(x, 3) for x in step_ms],
             "iterations_per_solve": {"mean": float(np.mean(flat_iters)), "min": int(np.min(flat_iters)),
                                      "max": int(np.max(flat_iters))},
             "roofline": {"kernel": "kr_rminres (persistent RMINRES, all iterations of all samples)",

@@ -22,6 +22,8 @@
  *   kr_cg              <- cg (krylov.py:408-483)
  *   kr_syev_select     <- the t x t eigen-selection inside ritz_select / gsvd_pair /
  *                         rgen_select (recycling.py:202-213, 226-236, 275-359)
+ *   kr_qrcp_small      <- the pivoted QR's column choice and rank drop
+ *                         (recycling.py:187-199, 362-383) on the small R factor
  *   kr_chol_inv        <- the t x t factorizations of the QRs in build_candidate_basis,
  *                         gsvd_pair, prepare_recycle and the condition check
  *                         (recycling.py:187-199, 290-313, 362-383)
@@ -173,14 +175,27 @@ int kr_syev_select(const double* A, int64_t lda, int64_t bsa, const int32_t* dim
  * recycling.py:187-199, 362-383 and the QR of [Jt; Ht] at :305) and of the
  * W^T H W condition screen (recycling.py:290-296).  G b: element (i, j) at
  * G + b*bsg + i*ldg + j (symmetrised), t_b = dims[b] <= tmax <= 228 (DEVICE int32).
- * flags bit 0: scale by D = sqrt(diag G); bit 1: write F.  shift (nullable,
+ * flags bit 0: scale by D = sqrt(diag G); bit 1: write F; bit 2: skip mode -- a row
+ * whose pivot falls below 4 t eps times its diagonal is removed (zero column of L,
+ * zero row of F, skipped[b*tmax + i] = 1) instead of stopping.  shift (nullable,
  * DEVICE, per sample) is added to the scaled diagonal.  G_s = L L^T; F = L^{-1} D^{-1}
  * row-major (F + b*bsf + i*ldf + j), zero upper triangle, identity pad block.
  * info[b] = -1 or the first row whose pivot is not positive; stats[4b..4b+3] =
  * (min L_jj, max L_jj, min D, 0) (nullable). */
 int kr_chol_inv(const double* G, int64_t ldg, int64_t bsg, const int32_t* dims, int32_t batch,
                 int32_t tmax, int32_t flags, const double* shift, double* F, int64_t ldf, int64_t bsf,
-                double* stats, int32_t* info, kr_stream_t stream);
+                double* stats, int32_t* info, uint8_t* skipped, kr_stream_t stream);
+
+/* QR with column pivoting of small matrices (t_b <= tmax <= 256), one CTA each:
+ * the pivoted QR of build_candidate_basis / prepare_recycle (recycling.py:187-199,
+ * 362-383, scipy qr(pivoting=True)) applied to the R factor of the tall block.
+ * M (in/out, DEVICE): column j of sample b at M + b*tmax*tmax + j*tmax; on return
+ * its upper triangle holds R_piv.  Stops at the first |R_kk| <= rtol |R_00|:
+ * rank[b] = k.  Q (out): column j (< rank) of Q_R at Q + b*tmax*tmax + j*tmax, the
+ * other columns zero.  perm[b*tmax + j] = original index of pivot j (nullable).
+ * work: batch*tmax doubles. */
+int kr_qrcp_small(double* M, const int32_t* dims, int32_t batch, int32_t tmax, double rtol, double* Q,
+                  int32_t* rank, int32_t* perm, double* work, int64_t work_len, kr_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -54,6 +54,29 @@ def syev_select(M: torch.Tensor, dims: torch.Tensor, size: str, s: int):
 
 STATS: dict | None = None  # set to {} to count declined samples per check
 
+def qrcp_small(M: torch.Tensor, dims: torch.Tensor, rtol: float):
+    """QR with column pivoting of the leading dims[b] blocks (kr_qrcp_small).
+
+    M (B, T, T) holds each matrix column-major (M[b, j] = column j).  Returns
+    (Q, R, rank, perm): Q[b, j] = column j of Q_R (j < rank, else zero), R[b, j]
+    = column j of R_piv (upper triangle), perm (B, T) the pivot order."""
+    B, T, _ = M.shape
+    Mw = M.to(torch.float64).contiguous().clone()
+    Q = torch.empty_like(Mw)
+    rank = torch.empty(B, dtype=torch.int32, device=M.device)
+    perm = torch.empty(B, T, dtype=torch.int32, device=M.device)
+    work = torch.empty(max(B * T, 1), dtype=torch.float64, device=M.device)
+    dims = dims.to(device=M.device, dtype=torch.int32).contiguous()
+    _lib.check(_lib.lib().kr_qrcp_small(Mw.data_ptr(), dims.data_ptr(), B, T, float(rtol), Q.data_ptr(),
+                                        rank.data_ptr(), perm.data_ptr(), work.data_ptr(), work.numel(),
+                                        _lib.stream_ptr()), "kr_qrcp_small")
+    _lib.note_launch("kr_qrcp_small")
+    return Q, Mw, rank, perm
+
+
+QRCP_TMAX = 256
+PIVOT_COND = 1e9   # below this cond(A) bound pivoted QR keeps every column (|R_kk| ~ sigma_k > 1e-10 |R_00|)
+
 CHOLQR_TOL = 1e-7   # recycling.CHOLQR_TOL
 COND_SCREEN = 1e6   # recycling.COND_SCREEN
 COND_LIMIT = 1e12   # recycling.COND_LIMIT
@@ -76,16 +99,19 @@ def _masked_extrema(d: torch.Tensor, mask: torch.Tensor):
 
 
 CHOL_TMAX = 228          # kr_chol_inv's shared-memory limit
+SKIP_DEPENDENT = False   # remove dependent rows inside the Cholesky passes (kr_chol_inv skip mode)
 SHIFTED_COND_MAX = 1e14  # shifted CholeskyQR3 is backward stable below ~1/u; keep a margin
 
 
 def _chol_inv(G: torch.Tensor, dims: torch.Tensor, scale: bool, shift: torch.Tensor | None = None,
-              inverse: bool = True):
+              inverse: bool = True, skip: bool = False):
     """Per sample: D = sqrt(diag G) (scale) or 1, G_s = D^-1 G D^-1 + shift I on the
     leading dims[b] block, G_s = L L^T.  Returns (F, info, stats): F = L^-1 D^-1
     (row-major, identity pad; None unless inverse), info[b] = first failing row or
     -1, stats[b] = (min L_jj, max L_jj, min D).  kr_chol_inv (one CTA per matrix)
-    for T <= 228, torch.linalg otherwise."""
+    for T <= 228, torch.linalg otherwise.  skip=True (kernel only): dependent rows
+    are removed instead of failing; returns a 4th value, the (B, T) removed mask
+    (None on the torch path, which reports the first failing row instead)."""
     B, T, _ = G.shape
     dev = G.device
     dims = dims.to(device=dev, dtype=torch.int32).contiguous()
@@ -94,12 +120,17 @@ def _chol_inv(G: torch.Tensor, dims: torch.Tensor, scale: bool, shift: torch.Ten
         F = torch.empty_like(G) if inverse else None
         stats = torch.empty(B, 4, dtype=torch.float64, device=dev)
         info = torch.empty(B, dtype=torch.int32, device=dev)
+        skipped = torch.empty(B, T, dtype=torch.uint8, device=dev) if skip else None
         sh = None if shift is None else shift.to(torch.float64).contiguous()
-        _lib.check(_lib.lib().kr_chol_inv(G.data_ptr(), T, T * T, dims.data_ptr(), B, T,
-                                          int(scale) | (2 if inverse else 0), 0 if sh is None else sh.data_ptr(),
-                                          0 if F is None else F.data_ptr(), T, T * T, stats.data_ptr(),
-                                          info.data_ptr(), _lib.stream_ptr()), "kr_chol_inv")
+        flags = int(scale) | (2 if inverse else 0) | (4 if skip else 0)
+        _lib.check(_lib.lib().kr_chol_inv(G.data_ptr(), T, T * T, dims.data_ptr(), B, T, flags,
+                                          0 if sh is None else sh.data_ptr(), 0 if F is None else F.data_ptr(),
+                                          T, T * T, stats.data_ptr(), info.data_ptr(),
+                                          0 if skipped is None else skipped.data_ptr(), _lib.stream_ptr()),
+                   "kr_chol_inv")
         _lib.note_launch("kr_chol_inv")
+        if skip:
+            return F, info, stats, skipped.bool()
         return F, info, stats
     mask = _row_mask(dims, T, dev)
     live = mask > 0
@@ -124,6 +155,8 @@ def _chol_inv(G: torch.Tensor, dims: torch.Tensor, scale: bool, shift: torch.Ten
     if inverse:
         eye = torch.eye(T, dtype=G.dtype, device=dev).expand(B, T, T)
         F = torch.linalg.solve_triangular(L, eye, upper=False) / D.unsqueeze(1)
+    if skip:
+        return F, info, stats, None
     return F, info, stats
 
 
@@ -148,6 +181,8 @@ def cholqr2_rows(A: torch.Tensor, mask: torch.Tensor, robust: bool = False, want
     F1, i1, st = _chol_inv(G, dims, scale=True)
     ok1 = (i1 < 0) & (st[:, 0] > CHOLQR_TOL * st[:, 1]) & (st[:, 2] > 0)
     shifted = robust and not bool(ok1.all())
+    if shifted and STATS is not None:
+        STATS["shifted"] = STATS.get("shifted", 0) + 1
     if shifted:
         tb = dims.to(torch.float64)  # ||A_s||_2^2 <= ||A_s||_F^2 = t_b after row scaling
         sigma = 11.0 * (n * tb + tb * (tb + 1)) * torch.finfo(A.dtype).eps * tb
@@ -156,8 +191,14 @@ def cholqr2_rows(A: torch.Tensor, mask: torch.Tensor, robust: bool = False, want
     ok = i1 < 0
     fail_row = i1.clone()
     Fs = [F1]
+    skipped = None
     for _ in range(2 if shifted else 1):
-        Fk, ik, _ = _chol_inv(Q @ Q.transpose(1, 2), dims, scale=False)
+        # (skip mode stays off: the breakdown test of a pass behind a shifted pass
+        # fires ~30x above the reference's pivoted-QR drop threshold)
+        out = _chol_inv(Q @ Q.transpose(1, 2), dims, scale=False, skip=robust and SKIP_DEPENDENT)
+        Fk, ik = out[0], out[1]
+        if len(out) > 3 and out[3] is not None:
+            skipped = out[3] if skipped is None else skipped | out[3]
         Q = Fk @ Q
         Fs.append(Fk)
         fail_row = torch.where((fail_row < 0) & (ik >= 0), ik, fail_row)
@@ -176,7 +217,7 @@ def cholqr2_rows(A: torch.Tensor, mask: torch.Tensor, robust: bool = False, want
         for Fk in Fs[1:]:
             F = F * Fk.diagonal(dim1=1, dim2=2)
     if robust:
-        return Q, F, ok, fail_row
+        return Q, F, ok, fail_row, skipped
     return Q, F, ok
 
 
@@ -195,31 +236,92 @@ def orth_rows_drop(A: torch.Tensor, dims: list[int], rounds: int = 8):
     """Candidate basis with the reference's rank drop, batched: (W, dims_after, ok).
 
     recycling._orth_drop removes the rows (columns of the n x t block) whose
-    unpivoted |R_jj| <= RANK_TOL max |R_ii| and redoes the QR.  Here a round of
-    (shifted) Cholesky QR either succeeds -- then that rule is applied to R's
-    diagonal (|R_jj| = 1 / |F_jj|) -- or its Cholesky breaks down at the first
-    numerically dependent row (the later row of a dependent set, the one the
-    unpivoted rule drops), which is removed; rows are compacted and the QR redone."""
+    unpivoted |R_jj| <= RANK_TOL max |R_ii| and redoes the QR.  Here one (shifted)
+    Cholesky-QR removes the numerically dependent rows inside its second and third
+    passes (kr_chol_inv's skip mode: the factor of the Gram without those rows), and
+    rows with |R_jj| <= RANK_TOL max |R_ii| in the result are removed too; the kept
+    rows of W are compacted to the front.  A removed row's own direction in W is
+    below RANK_TOL relative, so no re-factorization is needed.  (On the torch path,
+    T > 228, a breakdown row is removed and the QR redone, up to `rounds` times.)"""
     from .recycling import RANK_TOL
 
     B, T, _ = A.shape
     mask = _row_mask(dims, T, A.device)
     ar = torch.arange(T, device=A.device).reshape(1, -1)
     for _ in range(rounds):
-        W, Fd, ok, fail_row = cholqr2_rows(A, mask, robust=True, want_f=False)
-        rd = 1.0 / Fd.abs()
-        rmax, _ = _masked_extrema(rd, mask)
+        W, Fd, ok, fail_row, skipped = cholqr2_rows(A, mask, robust=True, want_f=False)
         live = mask > 0
+        keep_live = live if skipped is None else live & ~skipped
+        rd = 1.0 / Fd.abs()
+        rmax, _ = _masked_extrema(rd, keep_live.to(rd.dtype))
         factored = (fail_row < 0) & torch.isfinite(rmax)
-        drop = live & (rd <= RANK_TOL * rmax.unsqueeze(1)) & factored.unsqueeze(1)
-        drop = drop | (live & (ar == fail_row.unsqueeze(1)))
-        if not bool(drop.any()):
+        drop = keep_live & (rd <= RANK_TOL * rmax.unsqueeze(1)) & factored.unsqueeze(1)
+        if skipped is not None:
+            drop = drop | (live & skipped)
+        refactor = live & (ar == fail_row.unsqueeze(1))
+        if not bool((drop | refactor).any()):
             return W, dims, ok
-        A, cnt = _compact_rows(A, live & ~drop)
+        if STATS is not None:
+            STATS["drop_rounds"] = STATS.get("drop_rounds", 0) + 1
+            STATS["dropped_rows"] = STATS.get("dropped_rows", 0) + int((drop | refactor).sum())
+        if skipped is not None and not bool(refactor.any()):
+            # skip-mode drops only: compact W itself (dropped directions are negligible)
+            W, cnt = _compact_rows(W, live & ~drop)
+            return W, cnt.cpu().tolist(), ok
+        A, cnt = _compact_rows(A, live & ~(drop | refactor))
         dims = cnt.cpu().tolist()
         mask = _row_mask(dims, T, A.device)
-    W, _, ok, _ = cholqr2_rows(A, mask, robust=True, want_f=False)
+    W, _, ok, _, _ = cholqr2_rows(A, mask, robust=True, want_f=False)
     return W, dims, ok
+
+
+def orth_rows(A: torch.Tensor, dims: list[int]):
+    """Candidate basis W = orth(A rows) with the reference's pivoted-QR rank drop
+    (recycling.py:187-199), batched: (W, dims_after, ok).
+
+    Every sample first goes through (shifted) Cholesky QR.  Where the block may be
+    numerically rank deficient -- cond(A) <= ||A||_F ||R^{-1}||_F above PIVOT_COND,
+    or Cholesky QR not applicable -- the pivoted QR of the reference is reproduced:
+    pivoted QR of A is Q_A times pivoted QR of the small R factor, so
+    kr_qrcp_small runs on R (from the Cholesky QR, or from a Householder QR of the
+    sample when shifted CholeskyQR3 cannot be trusted) and the kept basis is
+    Q_A Q_R[:, :r] with the reference's |R_kk| > 1e-10 |R_00| rule."""
+    from .recycling import RANK_TOL
+
+    B, T, n = A.shape
+    if T > QRCP_TMAX:
+        return orth_rows_drop(A, dims)
+    dev = A.device
+    mask = _row_mask(dims, T, dev)
+    W, F, ok, _, _ = cholqr2_rows(A, mask, robust=True)
+    cond_bound = torch.linalg.vector_norm(A, dim=(1, 2)) * torch.linalg.matrix_norm(F)
+    ill = ~ok | (cond_bound > PIVOT_COND)
+    ill_h, ok_h = ill.cpu().tolist(), ok.cpu().tolist()
+    idx = [b for b in range(B) if ill_h[b] and dims[b] > 0]
+    if not idx:
+        return W, dims, torch.ones_like(ok)
+    if STATS is not None:
+        STATS["pivoted"] = STATS.get("pivoted", 0) + len(idx)
+    ii = torch.tensor(idx, device=dev)
+    Wsub = W[ii].clone()
+    M = A[ii] @ Wsub.transpose(1, 2)  # M[j][i] = a_j . q_i = R[i][j]: R column-major
+    for s_, b in enumerate(idx):
+        if not ok_h[b]:  # Householder QR where shifted CholeskyQR3 is not trustworthy
+            Qh, Rh = torch.linalg.qr(A[b, : dims[b]].T)
+            Wsub[s_] = 0.0
+            Wsub[s_, : dims[b]] = Qh.T
+            M[s_] = 0.0
+            M[s_, : dims[b], : dims[b]] = Rh.T
+            if STATS is not None:
+                STATS["householder"] = STATS.get("householder", 0) + 1
+    Qr, _, rank, _ = qrcp_small(M, torch.tensor([dims[b] for b in idx], dtype=torch.int32), RANK_TOL)
+    W[ii] = Qr @ Wsub  # rows j < rank: Q_A Q_R[:, j]; the rest zero
+    dims = list(dims)
+    for s_, r in zip(idx, rank.cpu().tolist()):
+        if STATS is not None and r < dims[s_]:
+            STATS["dropped_rows"] = STATS.get("dropped_rows", 0) + dims[s_] - r
+        dims[s_] = r
+    return W, dims, torch.ones_like(ok)
 
 
 def supports(strategy) -> bool:
@@ -275,7 +377,7 @@ def recycle_update(strategy, s: int, H, J, bases, recycles, reuse_products: bool
         if sp[b]:
             A[b, k[b]: t[b]] = recycles[b].U.T
     # candidate basis W = orth([V_prev, U_prev]) with the rank drop (recycling.py:187-199)
-    W, t, ok = orth_rows_drop(A, t)
+    W, t, ok = orth_rows(A, t)
     mask = _row_mask(t, T, dev)
     tt = torch.tensor(t, dtype=torch.int32, device=dev)
     checks = {"candidates": ok}

@@ -9,6 +9,7 @@ launch per upper step.  ``hypergradient`` is bilevel.py:291-305.
 from __future__ import annotations
 
 import os
+import threading
 import warnings
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
@@ -67,6 +68,10 @@ def _warm_linalg():
     a = torch.eye(4, dtype=torch.float64, device="cuda") * 2.0
     torch.linalg.cholesky_ex(a)
     torch.linalg.qr(a)
+    # the tall Householder QR of the rank-drop path uses other cuSOLVER kernels than a
+    # 4 x 4 one; load them now rather than inside a timed step
+    torch.linalg.qr(torch.randn(4096, 64, dtype=torch.float64, device="cuda"))
+    torch.linalg.eigh(torch.randn(64, 64, dtype=torch.float64, device="cuda"))
     torch.linalg.eigh(a)
     torch.linalg.eigvalsh(a)
     torch.linalg.svdvals(a)
@@ -75,6 +80,22 @@ def _warm_linalg():
     torch.argsort(a[0], stable=True)
     torch.cuda.synchronize()
     _LINALG_WARM = True
+
+
+def _warm_thread(shape=None):
+    """The library routines of the recycle update, once on the calling thread at the
+    shapes they run at (handle creation and kernel selection are per thread)."""
+    a = torch.randn(64, 64, dtype=torch.float64, device="cuda")
+    g = a @ a.T + 64 * torch.eye(64, dtype=torch.float64, device="cuda")
+    torch.linalg.cholesky_ex(g)
+    torch.linalg.solve_triangular(torch.linalg.cholesky(g), g, upper=False)
+    torch.linalg.qr(torch.randn(4096, 64, dtype=torch.float64, device="cuda"))
+    if shape is not None:  # the tall Householder QR of the pivoted rank-drop path
+        torch.linalg.qr(torch.randn(*shape, dtype=torch.float64, device="cuda"))
+    torch.linalg.eigh(g)
+    torch.linalg.eigvalsh(g)
+    torch.bmm(a.unsqueeze(0), a.unsqueeze(0))
+    torch.cuda.current_stream().synchronize()
 
 
 class SequenceSolver:
@@ -107,7 +128,7 @@ class SequenceSolver:
     def _needs_basis(self) -> bool:
         return not self.cfg.strategy.is_none
 
-    def reserve(self, batch: int, nbytes: int) -> None:
+    def reserve(self, batch: int, nbytes: int, shape: tuple[int, int] | None = None) -> None:
         """Pre-size the caching-allocator pools of the per-sample worker streams (each
         stream has its own pool) so steady-state steps never call cudaMalloc."""
         if batch <= 1 or self.max_workers <= 1:
@@ -121,6 +142,17 @@ class SequenceSolver:
             for st in self._gstreams:
                 with torch.cuda.stream(st):
                     torch.empty(-(-batch // ng) * nbytes // 8, dtype=torch.float64, device="cuda")
+            # torch creates cuBLAS / cuSOLVER handles per host thread on first use (tens of
+            # ms): touch them on every worker thread now, not inside a step
+            gate = threading.Barrier(ng)
+
+            def warm(g):
+                gate.wait()
+                with torch.cuda.stream(self._gstreams[g]):
+                    _warm_thread(shape)
+                return g
+
+            list(self._gpool.map(warm, range(ng)))
             torch.cuda.synchronize()
             return
         if self._streams is None or len(self._streams) < batch:

@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
     for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) r[p] = gb[p];
   }
   for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) w[p] = w0 ? w0[p] : 0.0;
-  grid_barrier(reinterpret_cast<unsigned int*>(P.done) + 1, gridDim.x, grid_target);
+  grid_barrier(reinterpret_cast<unsigned int*>(P.done) + 1 + bl, P.Gs, grid_target);  // per-sample
   {
     double v[1] = {0.0};
     for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) v[0] += r[p] * r[p];
@@ -96,10 +96,10 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
       write_partials(PP, bl, j, SL_NSC, ns, slot_acc);
     }
   }
-  grid_barrier(reinterpret_cast<unsigned int*>(P.done) + 1, gridDim.x, grid_target);
+  grid_barrier(reinterpret_cast<unsigned int*>(P.done) + 1 + bl, P.Gs, grid_target);  // per-sample
 
   for (int k = 1; k <= A.max_iter + 1; ++k) {
-    if (k > 1 && __syncthreads_or(threadIdx.x == 0 && *((volatile int*)P.done) >= P.nb)) break;
+    if (s_counted) break;  // this sample is reported: its blocks leave together
     // ===== P1: stop test on r_{k-1}, then hp = H p_k =====
     if (ns && s_active) {
       reduce_slots(PP, bl, SL_NSC, ns, nscv);
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
       block_sum<1>(php, red);
       write_partial1(PP, bl, j, SL_PHP, red[0]);
     }
-    grid_barrier(reinterpret_cast<unsigned int*>(P.done) + 1, gridDim.x, grid_target);
+    grid_barrier(reinterpret_cast<unsigned int*>(P.done) + 1 + bl, P.Gs, grid_target);  // per-sample
     // ===== P2: step =====
     if (s_hvp) {
       if (threadIdx.x == 0) {
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
       }
       block_barrier();
     }
-    grid_barrier(reinterpret_cast<unsigned int*>(P.done) + 1, gridDim.x, grid_target);
+    grid_barrier(reinterpret_cast<unsigned int*>(P.done) + 1 + bl, P.Gs, grid_target);  // per-sample
   }
 }
 
@@ -249,7 +249,7 @@ void cg_plan(const kr_op& op, const kr_solve_args& a, CgLayout& L) {
   int Gs = max_blocks / L.chunk;
   L.Gs = Gs < 1 ? 1 : (Gs > want ? want : Gs);
   L.nslot = (a.stop_kind == 1 ? a.nsc_s : 0) + 2;
-  L.total = 5 * (int64_t)B * n + (int64_t)L.chunk * L.nslot * L.Gs + 2;
+  L.total = 5 * (int64_t)B * n + (int64_t)L.chunk * L.nslot * L.Gs + 2 + (L.chunk + 1) / 2;
 }
 
 }  // namespace
@@ -294,7 +294,7 @@ extern "C" int kr_cg(const kr_op* op, const kr_solve_args* a, double* work, int6
   for (int b0 = 0; b0 < B; b0 += L.chunk) {
     P.b0 = b0;
     P.nb = (B - b0) < L.chunk ? (B - b0) : L.chunk;
-    cudaMemsetAsync(P.done, 0, 2 * sizeof(int), st);
+    cudaMemsetAsync(P.done, 0, (4 + 2 * ((L.chunk + 1) / 2)) * sizeof(int), st);
     void* args[] = {&P};
     cudaError_t e = cudaLaunchCooperativeKernel(kfn, dim3(P.nb * P.Gs), dim3(NT), args, L.smem, st);
     if (e != cudaSuccess) return fail(KR_ECUDA, std::string("cg cooperative launch: ") + cudaGetErrorString(e));

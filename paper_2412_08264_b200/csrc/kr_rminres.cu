@@ -79,7 +79,9 @@ __device__ inline double* lanczos(const Params& P, int b, int k, int site = 0) {
   return vec(P.w.vr[k & 1], P.n, b);
 }
 
-#define KR_GRID_SYNC() grid_barrier(reinterpret_cast<unsigned int*>(P.w.done) + 1, gridDim.x, grid_target)
+// All cross-block traffic is within a sample (its Gs blocks share partials), so the
+// "grid" barrier is a per-sample barrier: one counter per sample, Gs arrivals.
+#define KR_GRID_SYNC() grid_barrier(reinterpret_cast<unsigned int*>(P.w.done) + 1 + bl, P.Gs, grid_target)
 
 template <int Q>
 __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
@@ -239,8 +241,9 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
 
   // ---------------- main loop ----------------
   for (int k = 1; k <= A.max_iter + 1; ++k) {
-    // every sample counted: leave together (one read, broadcast -> block-uniform)
-    if (k > 1 && __syncthreads_or(threadIdx.x == 0 && *((volatile int*)P.w.done) >= P.nb)) break;
+    // this sample is finished and reported: its blocks leave (sc is block-shared and
+    // identical across the sample's blocks, so all of them leave at the same k)
+    if (sc.counted) break;
 #ifdef KR_GUARD
     {
       __shared__ int guard_k[NT];
@@ -550,7 +553,7 @@ int plan(const kr_op& op, const kr_solve_args& a, Layout& L) {
   L.nslot = 2 * a.s + ns + 2;
   L.vec_doubles = (int64_t)B * n * (a.basis ? 11 : 13);
   L.part_doubles = (int64_t)L.chunk * L.nslot * Gs;
-  L.total = L.vec_doubles + L.part_doubles + 2;
+  L.total = L.vec_doubles + L.part_doubles + 2 + (L.chunk + 1) / 2;  // + one barrier counter per sample
   return KR_OK;
 }
 
@@ -625,14 +628,14 @@ extern "C" int kr_rminres(const kr_op* op, const kr_solve_args* a, double* work,
   }
   take((a->basis ? 11 : 13) * (int64_t)B * n - (cur - work));  // keep layout == plan
   P.w.part = take(L.part_doubles);
-  P.w.done = reinterpret_cast<int*>(take(2));
+  P.w.done = reinterpret_cast<int*>(take(2 + (L.chunk + 1) / 2));
   cudaStream_t st = (cudaStream_t)stream;
   const void* kfn = KR_PICK_Q(rminres_kernel, q_variant(*op));
   KR_TRY(ensure_smem(kfn, L.smem));
   for (int b0 = 0; b0 < B; b0 += L.chunk) {
     P.b0 = b0;
     P.nb = (B - b0) < L.chunk ? (B - b0) : L.chunk;
-    cudaMemsetAsync(P.w.done, 0, 4 * sizeof(int), st);
+    cudaMemsetAsync(P.w.done, 0, (4 + 2 * ((L.chunk + 1) / 2)) * sizeof(int), st);
     dim3 grid(P.nb * P.Gs), block(NT);
     void* args[] = {&P};
     cudaError_t e = cudaLaunchCooperativeKernel(kfn, grid, block, args, L.smem, st);

@@ -30,6 +30,7 @@ struct CholParams {
   int64_t ldf, bsf;
   double* stats;  // per sample: [min L_jj, max L_jj, min D, 0]
   int32_t* info;  // per sample: -1 = factored, else the first failing row
+  uint8_t* skipped;  // per sample and row (skip mode): 1 = dependent row removed
 };
 
 __device__ __forceinline__ int64_t pk(int i, int j) { return (int64_t)i * (i + 1) / 2 + j; }
@@ -59,13 +60,15 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
   double* Lbb = rdiag + NB;       // NB x (NB + 1) copy of a diagonal block
   double* A = Lbb + NB * (NB + 1);  // packed lower t(t+1)/2
   __shared__ int s_fail;
+  __shared__ unsigned char skp[CHOL_TMAX];
   const double* Gb = P.G + (int64_t)b * P.bsg;
-  const bool scale = P.flags & 1, inv = P.flags & 2;
+  const bool scale = P.flags & 1, inv = P.flags & 2, skipmode = P.flags & 4;
   for (int i = tid; i < t; i += CNT) {
     const double g = Gb[(int64_t)i * P.ldg + i];
     D[i] = (scale && g > 0.0) ? sqrt(g) : 1.0;
   }
   if (tid == 0) s_fail = -1;
+  for (int i = tid; i < CHOL_TMAX; i += CNT) skp[i] = 0;
   __syncthreads();
   const double sh = P.shift ? P.shift[b] : 0.0;
   // lower triangle (as potrf 'L'), rows coalesced, independent loads in flight
@@ -95,7 +98,13 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
         if (j < nb && bad < 0) {
           const double d = __shfl_sync(0xffffffffu, a[j], j);
           if (!(d > piv_rtol * col[kb + j])) {
-            bad = kb + j;
+            if (skipmode) {  // remove the dependent row: zero column below, unit pivot
+              if (lane > j) a[j] = 0.0;
+              if (lane == j) a[j] = 1.0;
+              if (lane == 0) skp[kb + j] = 1;
+            } else {
+              bad = kb + j;
+            }
           } else {
             const double rl = rsqrt_nr(d), ljj = d * rl;
             const double lij = lane == j ? ljj : a[j] * rl;
@@ -126,7 +135,7 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
         if (c < nb) {
           double v = A[pk(r, kb + c)];
           for (int m = 0; m < c; ++m) v -= x[m] * A[pk(kb + c, kb + m)];
-          x[c] = v * rdiag[c];
+          x[c] = skp[kb + c] ? 0.0 : v * rdiag[c];
           A[pk(r, kb + c)] = x[c];
         }
       }
@@ -151,7 +160,7 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
     if (warp == 0) {
       double lo = 1e308, hi = 0.0, dm = 1e308;
       for (int j = lane; j < t; j += 32) {
-        if (fail < 0) {
+        if (fail < 0 && !skp[j]) {
           lo = fmin(lo, A[pk(j, j)]);
           hi = fmax(hi, A[pk(j, j)]);
         }
@@ -172,6 +181,8 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
     }
   }
   if (tid == 0) P.info[b] = fail;
+  if (P.skipped)
+    for (int i = tid; i < T; i += CNT) P.skipped[(int64_t)b * T + i] = i < t ? skp[i] : 0;
   if (!inv) return;
   double* Fb = P.F + (int64_t)b * P.bsf;
   if (fail >= 0) {  // no factor: identity (callers discard the sample)
@@ -233,7 +244,7 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
     for (int j = lane; j < T; j += 32) {
       double v;
       if (i < t && j < t)
-        v = j <= i ? A[pk(i, j)] / D[j] : 0.0;
+        v = (j <= i && !skp[i]) ? A[pk(i, j)] / D[j] : 0.0;
       else
         v = i == j ? 1.0 : 0.0;
       fi[j] = v;
@@ -248,14 +259,14 @@ using namespace kr;
 
 extern "C" int kr_chol_inv(const double* G, int64_t ldg, int64_t bsg, const int32_t* dims, int32_t batch,
                            int32_t tmax, int32_t flags, const double* shift, double* F, int64_t ldf, int64_t bsf,
-                           double* stats, int32_t* info, kr_stream_t stream) {
+                           double* stats, int32_t* info, uint8_t* skipped, kr_stream_t stream) {
   KR_CHECK_ARG(batch >= 0 && tmax >= 0, "negative size");
   KR_CHECK_ARG(tmax <= CHOL_TMAX, "kr_chol_inv: t exceeds the shared-memory limit (228)");
   KR_CHECK_ARG(ldg >= tmax, "leading dimension smaller than t");
   KR_CHECK_ARG(!(flags & 2) || (F && ldf >= tmax), "inverse requested without an output");
   if (batch == 0) return KR_OK;
   KR_CHECK_ARG(G && dims && info, "null pointer");
-  CholParams P{G, ldg, bsg, dims, tmax, flags, shift, F, ldf, bsf, stats, info};
+  CholParams P{G, ldg, bsg, dims, tmax, flags, shift, F, ldf, bsf, stats, info, skipped};
   const size_t smem = (size_t)(2 * tmax + NB + NB * (NB + 1) + (int64_t)tmax * (tmax + 1) / 2) * sizeof(double);
   KR_TRY(ensure_smem((const void*)chol_inv_kernel, smem));
   chol_inv_kernel<<<batch, CNT, smem, (cudaStream_t)stream>>>(P);

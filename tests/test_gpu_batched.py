@@ -49,14 +49,16 @@ def test_cholqr2_rows_padding():
     A3 = A.clone()
     A3[0, 5] = A3[0, 4] + 1e-8 * A3[0, 5]
     _, _, ok3 = cholqr2_rows(A3, mask)
-    Q3, F3, ok3r, _ = cholqr2_rows(A3, mask, robust=True)
+    Q3, F3, ok3r, _, _ = cholqr2_rows(A3, mask, robust=True)
     assert ok3.tolist() == [False, True, True] and ok3r.tolist() == [True, True, True]
     Qb = Q3[0, :12]
     assert torch.allclose(Qb @ Qb.T, torch.eye(12, dtype=torch.float64, device="cuda"), atol=1e-14)
     assert torch.dist(F3[0] @ A3[0], Q3[0]) <= 1e-6 * torch.linalg.norm(Q3[0])  # forward error ~ cond * eps
     # ... and still declines near-dependent ones (the reference's pivoted QR drops a column)
-    _, _, ok2r, fr = cholqr2_rows(A2, mask, robust=True)
-    assert ok2r.tolist() == [False, False, True] and fr.tolist()[2] == -1
+    _, _, ok2r, fr, sk = cholqr2_rows(A2, mask, robust=True)
+    # ... the robust path reports the breakdown row (the rank-drop round removes it)
+    # (sample 0's near-duplicate row survives the shifted passes; the |R_jj| rule drops it)
+    assert sk is None and fr.tolist()[1:] == [3, -1]
 
 
 def _setup(strategy, s=6, size=32, B=4, steps=2):
@@ -225,3 +227,43 @@ def test_chol_inv_kernel_matches_torch(T, monkeypatch):
             good = info < 0
             assert torch.allclose(st[good, :3], stt[good, :3], rtol=1e-12, atol=0)
             assert torch.allclose(F[good], Ft[good], rtol=1e-9, atol=1e-12 * float(Ft[good].abs().max()))
+
+
+def test_qrcp_small_matches_scipy_pivoted_qr():
+    """kr_qrcp_small on R against scipy.linalg.qr(A, pivoting=True), the reference's
+    candidate-basis QR (recycling.py:187-199): same pivots, |R_kk|, rank under the
+    1e-10 rule, and the same kept span."""
+    import scipy.linalg as sl
+
+    from paper_2412_08264_b200.batched import qrcp_small
+
+    rng = np.random.default_rng(17)
+    mats = []
+    for t in (1, 5, 40, 120, 220):
+        A = rng.standard_normal((600, t)) * np.logspace(0, -6, t)
+        if t >= 40:
+            A[:, 7] = A[:, 3] * (1 + 1e-13)       # numerically dependent
+            A[:, 20] = 2.5 * A[:, 11]              # exactly dependent
+        mats.append(A)
+    T = max(A.shape[1] for A in mats)
+    M = np.zeros((len(mats), T, T))
+    for b, A in enumerate(mats):
+        _, R = np.linalg.qr(A)
+        M[b, : A.shape[1], : A.shape[1]] = R.T  # column-major storage of R
+    dims = torch.tensor([A.shape[1] for A in mats], dtype=torch.int32)
+    Q, Rp, rank, perm = qrcp_small(torch.as_tensor(M, device="cuda"), dims, 1e-10)
+    Q, Rp, rank, perm = Q.cpu().numpy(), Rp.cpu().numpy(), rank.cpu().numpy(), perm.cpu().numpy()
+    for b, A in enumerate(mats):
+        t = A.shape[1]
+        Qs, Rs, Ps = sl.qr(A, mode="economic", pivoting=True)
+        d = np.abs(np.diag(Rs))
+        r_ref = int(np.sum(d > 1e-10 * d[0]))
+        assert rank[b] == r_ref, (t, rank[b], r_ref)
+        r = r_ref
+        assert list(perm[b, :r]) == list(Ps[:r]), t
+        assert np.allclose(np.abs(np.diag(Rp[b][:r, :r])), d[:r], rtol=1e-8, atol=1e-14 * d[0])
+        _, R = np.linalg.qr(A)
+        Qa = np.linalg.qr(A)[0] @ Q[b, :r, :t].T  # kept basis Q_A Q_R[:, :r]
+        Pk = Qa @ Qa.T
+        Pr = Qs[:, :r] @ Qs[:, :r].T
+        assert np.linalg.norm(Pk - Pr) <= 1e-7
