@@ -110,9 +110,16 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def krylov_bytes_per_iter(n, s, nsc, J):
-    """8n(21 + 3s + s_nsc) + HVP bytes 8n(2 + J) per iteration per sample."""
-    return 8 * n * (21 + 3 * s + nsc) + 8 * n * (2 + J)
+def krylov_bytes_per_iter(kernel, n, s, nsc, w):
+    """Algorithmic HBM bytes per iteration per sample.
+    RMINRES: 8n(21 + 3s + s_nsc) + the HVP's 8n(2 + w).
+    Recycled CG: direction p = r + beta p - U mu (read r, p_old, U; write p), the
+    stencil re-forming p on its tiles (r, p_old, U again), hp, the x/r update (read
+    p, hp, x, r; write x, r) and the C^T r / Z^T r dots: 8n(12 + 3s + s_nsc) + 8n w.
+    w = per-pixel weight vectors of the HVP (J filters, 3 for TV)."""
+    if kernel == "kr_cg":
+        return 8 * n * (12 + 3 * s + nsc) + 8 * n * w
+    return 8 * n * (21 + 3 * s + nsc) + 8 * n * (2 + w)
 
 
 # ---------------------------------------------------------------------------
@@ -139,6 +146,7 @@ def run_ours(args):
     thetas, xhats_np = synthetic_sequence(cfg, xt, steps_total, seed=1234 + rank)
     xhats = [torch.as_tensor(x, device="cuda") for x in xhats_np]
     solver_cfg = HessianSolveConfig.from_strategy(args.strategy, recycle_dim=cfg.recycle_dim, delta=args.delta,
+                                                  method=cfg.method,
                                                   max_iter=cfg.max_iter)
 
     from paper_2412_08264_b200.distributed import allgather_sum
@@ -205,16 +213,18 @@ def run_ours(args):
     hg_count = B * args.steps * world
     value = hg_count / (total_ms / 1e3)
 
-    # roofline of the dominant kernel (the persistent RMINRES solve)
+    # roofline of the dominant kernel (the persistent RMINRES / recycled-CG solve)
+    kname = "kr_cg" if cfg.method == "cg" else "kr_rminres"
+    wts = 3 if cfg.reg == "tv" else cfg.num_filters
     k_ms, k_bytes, k_iters = 0.0, 0.0, 0
     for a, b, info in prof:
-        if info["kernel"] != "kr_rminres":
+        if info["kernel"] != kname:
             continue
         ms = a.elapsed_time(b)
         its = int(info["iters"].sum().item())
         k_ms += ms
         k_iters += its
-        k_bytes += its * krylov_bytes_per_iter(info["n"], info["s"], info["nsc"], cfg.num_filters)
+        k_bytes += its * krylov_bytes_per_iter(kname, info["n"], info["s"], info["nsc"], wts)
     peak, peak_src = measured_peak()
     achieved = (k_bytes / 1e9) / (k_ms / 1e3) if k_ms > 0 else 0.0
 
@@ -256,20 +266,25 @@ def run_ours(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: {B} samples x {cfg.size}^2, blur {cfg.blur_size} "
                                    f"sigma {cfg.blur_sigma}, J={cfg.num_filters} q={cfg.kernel_size}, "
-                                   f"s={cfg.recycle_dim}, max {cfg.max_iter} it, {args.strategy} delta={args.delta}",
+                                   f"s={cfg.recycle_dim}, max {cfg.max_iter} it, {args.strategy} delta={args.delta}, "
+                                   f"{'recycled CG' if cfg.method == 'cg' else 'RMINRES'}",
                        "samples_per_gpu": B, "image": cfg.size, "recycle_dim": cfg.recycle_dim,
                        "max_iter": cfg.max_iter, "strategy": args.strategy, "delta": args.delta,
+                       "krylov": cfg.method,
                        "sequence": "synthetic frozen sequence (problems.synthetic_sequence)",
                        "l2": "flushed (256 MB write) before every timed step",
                        "parallelism": f"sample-sharded dp{world}"},
             "step_ms": [round(x, 3) for x in step_ms],
             "iterations_per_solve": {"mean": float(np.mean(flat_iters)), "min": int(np.min(flat_iters)),
                                      "max": int(np.max(flat_iters))},
-            "roofline": {"kernel": "kr_rminres (persistent RMINRES, all iterations of all samples)",
+            "roofline": {"kernel": f"{kname} (persistent {'recycled CG' if kname == 'kr_cg' else 'RMINRES'}, "
+                                   "all iterations of all samples)",
                          "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if peak else None, "traffic": None,
                          "peak_source": peak_src,
-                         "algorithmic_bytes": "SURVEY 8(d): per iteration per sample 8n(21+3s+s_nsc)+8n(2+J)",
+                         "algorithmic_bytes": ("per iteration per sample 8n(12+3s+s_nsc)+8n*w (recycled CG)"
+                                               if kname == "kr_cg" else
+                                               "SURVEY 8(d): per iteration per sample 8n(21+3s+s_nsc)+8n(2+J)"),
                          "kernel_ms_total": k_ms, "kernel_share_of_step": k_ms / total_ms if total_ms else None,
                          "krylov_iterations": k_iters},
             "clocks": clk.summary(),
@@ -295,7 +310,7 @@ def _oracle_solve_sample(payload):
         else im.Regularizer("tv", eps=cfg.eps)
     model = im.Model(data, reg)
     solver = ob.SequenceSolver(ob.SolveConfig.from_strategy(strategy, recycle_dim=cfg.recycle_dim, delta=delta,
-                                                            max_iter=cfg.max_iter))
+                                                            max_iter=cfg.max_iter, method=cfg.method))
     count = 0
     for i in systems:
         H = im.hessian(model, thetas[i], xhats[i])
@@ -334,7 +349,7 @@ def _reference_worker(conn, payload):
         else im.Regularizer("tv", eps=cfg.eps)
     model = im.Model(data, reg)
     solver = ob.SequenceSolver(ob.SolveConfig.from_strategy(strategy, recycle_dim=cfg.recycle_dim, delta=delta,
-                                                            max_iter=cfg.max_iter))
+                                                            max_iter=cfg.max_iter, method=cfg.method))
     while True:
         i = conn.recv()
         if i is None:

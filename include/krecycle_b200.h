@@ -50,7 +50,7 @@ extern "C" {
 
 typedef struct CUstream_st* kr_stream_t; /* == cudaStream_t */
 
-#define KR_ABI_VERSION 1
+#define KR_ABI_VERSION 2
 
 #define KR_OK 0
 #define KR_EINVAL (-1)
@@ -121,7 +121,8 @@ typedef struct kr_solve_args {
   double* res_norms;       /* out [batch][max_iter+1] */
   double* stop_vals;       /* out [batch][max_iter+1] */
   int32_t* iters;          /* out [batch] */
-  int32_t* reasons;        /* out [batch]: 0 tolerance, 1 max_iter, 2 breakdown */
+  int32_t* reasons;        /* out [batch]: 0 tolerance, 1 max_iter, 2 breakdown, 3 non-SPD */
+  const double* Minv;      /* [batch][s][s] (U^T C)^{-1}, row-major: kr_cg deflation (recycled CG); NULL = plain CG */
 } kr_solve_args;
 
 int kr_abi_version(void);
@@ -150,7 +151,10 @@ int64_t kr_rminres_workspace(const kr_op* op, const kr_solve_args* args);
 int kr_rminres(const kr_op* op, const kr_solve_args* args, double* work, int64_t work_len,
                kr_stream_t stream);
 
-/* Plain CG (krylov.py:408-483); NonSPD curvature is reported through reasons[b] = 3. */
+/* CG (krylov.py:408-483); NonSPD curvature is reported through reasons[b] = 3.  With
+ * s > 0 and Minv set: recycled (deflated) CG with deflation space U (Saad, Yeung,
+ * Erhel & Guyomarc'h 2000; the "recycled CG" of the north star), residuals kept
+ * orthogonal to U, directions p = r + beta p - U Minv C^T r. */
 int64_t kr_cg_workspace(const kr_op* op, const kr_solve_args* args);
 int kr_cg(const kr_op* op, const kr_solve_args* args, double* work, int64_t work_len,
           kr_stream_t stream);

@@ -20,7 +20,7 @@ import numpy as np
 from scipy.linalg import cho_factor, cho_solve
 
 from . import cpu_imaging as im
-from .cpu_krylov import Options, ResidualRule, minres, rminres
+from .cpu_krylov import Options, ResidualRule, minres, rcg, rminres
 from .cpu_recycle import (ConfigurationError, NscRule, Recycle, Strategy, TrueHgRule,
                           next_recycle)
 
@@ -118,10 +118,13 @@ class SolveConfig:
     warm_start: bool = False
     inner_tol: float = 1e-13
     dense_limit: int = 2000
+    method: str = "minres"  # "minres" (reference) or "cg" (recycled CG, BASELINE config 1)
 
     def __post_init__(self):
         if self.stop not in ("res", "nsc", "true-hg"):
             raise ValueError(f"unknown stop rule {self.stop!r}")
+        if self.method not in ("minres", "cg"):
+            raise ValueError(f"unknown Krylov method {self.method!r}")
         if self.stop == "nsc" and self.strategy.vec_type not in ("GSVD", "RGen"):
             raise ConfigurationError("the projected stopping criterion needs a GSVD-based strategy")
 
@@ -164,7 +167,7 @@ class SequenceSolver:
             rule = NscRule(cfg.delta, rec.nsc_data) if rec.nsc_data is not None else ResidualRule(cfg.delta)
         opts = Options(max_iter=cfg.max_iter, stop_rule=rule, track_basis=not cfg.strategy.is_none,
                        initial_guess=self.prev_solution if cfg.warm_start else None)
-        res = rminres(H, g, rec, opts)
+        res = (rminres if cfg.method == "minres" else rcg)(H, g, rec, opts)
         self.prev_basis, self.prev_recycle = res.basis, rec
         self.prev_h, self.prev_jac, self.prev_solution = H, jac, res.solution
         return res, rec

@@ -333,3 +333,90 @@ def cg(H, g, opts: Options | None = None) -> Result:
         basis=None if basis is None else (np.column_stack(basis) if basis else np.zeros((n, 0))),
         residual_vector=r.copy(), iterates=iterates,
     )
+
+
+def flops_rcg(k: int, n: int, s: int, h: int) -> int:
+    """Deflated CG: cg's count (krylov.py:119-135 style) plus the deflation work,
+    U^T r, C y, U y once (6ns) and C^T r, U mu per iteration (4ns); the s x s
+    Cholesky solves are not counted (O(s^2), like the reference's omissions)."""
+    _nonneg(k=k, n=n, s=s, h=h)
+    return h + 3 * n + 6 * n * s + k * (h + 10 * n + 4 * n * s)
+
+
+def rcg(H, g, recycle, opts: Options | None = None) -> Result:
+    """Recycled (deflated) CG -- the "recycled CG" of BASELINE config 1; the
+    reference ships only plain cg (krylov.py:408-483), so this restates the
+    published algorithm: Saad, Yeung, Erhel & Guyomarc'h, "A deflated version of
+    the conjugate gradient algorithm", SIAM J. Sci. Comput. 21 (2000), Alg. 2.2,
+    with deflation space W = U of a RecycleSpace (C = H U, so W^T H W = U^T C and
+    H W = C):
+
+        x0 = x + U M^-1 U^T r,  r0 = r - C M^-1 U^T r   (M = U^T C; U^T r0 = 0)
+        p0 = r0 - U M^-1 C^T r0
+        a = r.r / p.Hp,  x += a p,  r -= a Hp
+        p = r + (r_new.r_new / r.r) p - U M^-1 C^T r_new
+
+    Conventions follow cg exactly (r = g - H w even for w = 0, the stop test on
+    the new residual before the direction update, NonSPDError on p^T H p <= 0,
+    basis = normalised residuals, which stay mutually orthogonal and orthogonal
+    to U).  An empty recycle space is plain cg."""
+    if recycle is None or recycle.dim == 0:
+        return cg(H, g, opts)
+    opts = opts or Options()
+    n = H.dim
+    g = np.asarray(g, dtype=float)
+    U, C = np.asarray(recycle.U, dtype=float), np.asarray(recycle.C, dtype=float)
+    s = U.shape[1]
+    M = U.T @ C
+    Lm = np.linalg.cholesky(0.5 * (M + M.T))
+
+    def msolve(y):
+        return np.linalg.solve(Lm.T, np.linalg.solve(Lm, y))
+
+    rule = opts.rule()
+    hc = H.apply_cost
+    w = np.zeros(n) if opts.initial_guess is None else np.array(opts.initial_guess, dtype=float)
+    r = g - H(w)
+    y = msolve(U.T @ r)
+    w = w + U @ y
+    r = r - C @ y
+    rr = float(r @ r)
+    flops = hc + 3 * n + 6 * n * s
+    rn = float(np.sqrt(rr))
+    norms, svals = [rn], [rule.value(rn, r)]
+    basis = [] if opts.track_basis else None
+    iterates = [w.copy()] if opts.collect_iterates else None
+    why, k = "max_iter", 0
+    if rule.done(svals[0]):
+        why = "tolerance"
+    else:
+        p = r - U @ msolve(C.T @ r)
+        for k in range(1, opts.max_iter + 1):
+            if basis is not None and rn > 0:
+                basis.append(r / rn)
+            hp = H(p)
+            php = float(p @ hp)
+            flops += hc + 2 * n
+            if php <= 0:
+                raise NonSPDError(f"curvature p^T H p = {php:g} <= 0 at iteration {k}; operator is not SPD")
+            a = rr / php
+            w = w + a * p
+            r = r - a * hp
+            rr_new = float(r @ r)
+            flops += 8 * n + 4 * n * s
+            rn = float(np.sqrt(rr_new))
+            norms.append(rn)
+            svals.append(rule.value(rn, r))
+            if iterates is not None:
+                iterates.append(w.copy())
+            if rule.done(svals[-1]):
+                why = "tolerance"
+                break
+            p = r + (rr_new / rr) * p - U @ msolve(C.T @ r)
+            rr = rr_new
+    return Result(
+        solution=w, iterations=k, residual_norms=np.asarray(norms), flops=flops,
+        stop_reason=why, stop_values=np.asarray(svals),
+        basis=None if basis is None else (np.column_stack(basis) if basis else np.zeros((n, 0))),
+        residual_vector=r.copy(), iterates=iterates,
+    )

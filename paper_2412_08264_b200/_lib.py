@@ -39,6 +39,9 @@ class KrOp(ctypes.Structure):
     ]
 
 
+ABI_VERSION = 2  # KR_ABI_VERSION of include/krecycle_b200.h
+
+
 class KrSolveArgs(ctypes.Structure):
     """Mirror of ``kr_solve_args``."""
 
@@ -50,6 +53,7 @@ class KrSolveArgs(ctypes.Structure):
         ("track_residual", _c_i32),
         ("w", _c_p), ("r", _c_p), ("basis", _c_p), ("ld_basis", _c_i64), ("bs_basis", _c_i64),
         ("res_norms", _c_p), ("stop_vals", _c_p), ("iters", _c_p), ("reasons", _c_p),
+        ("Minv", _c_p),
     ]
 
 
@@ -118,7 +122,7 @@ def load_library(path: Path | None = None):
             )
         lib = ctypes.CDLL(str(p))
         _declare(lib)
-        if lib.kr_abi_version() != 1:
+        if lib.kr_abi_version() != ABI_VERSION:
             raise ImportError("libkrecycle_b200 ABI version mismatch")
         a, b = _c_i64(), _c_i64()
         lib.kr_struct_sizes(ctypes.byref(a), ctypes.byref(b))

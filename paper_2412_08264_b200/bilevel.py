@@ -17,7 +17,7 @@ from dataclasses import dataclass, field
 import torch
 
 from .batched import recycle_update, supports as batched_supports
-from .krylov import SolveOptions, SolveResult, rminres
+from .krylov import SolveOptions, SolveResult, rcg, rminres
 from .operators import (DenseOperator, FoEParams, HessianOperator, ImageVector, InpaintingProblem, Model,
                         StencilJacobian, as_device, _foe_model)
 from .recycling import RecycleSpace, StrategyDescriptor, next_recycle
@@ -39,10 +39,13 @@ class HessianSolveConfig:
     inner_tol: float = 1e-13
     dense_limit: int = 2000
     reuse_products: bool = True
+    method: str = "minres"  # "minres" (reference RMINRES) or "cg" (recycled CG, BASELINE config 1)
 
     def __post_init__(self):
         if self.stop not in ("res", "nsc", "true-hg"):
             raise ValueError(f"unknown stop rule {self.stop!r}")
+        if self.method not in ("minres", "cg"):
+            raise ValueError(f"unknown Krylov method {self.method!r}")
         if self.stop == "nsc" and self.strategy.vec_type not in ("GSVD", "RGen"):
             raise ConfigurationError("the projected stopping criterion needs a GSVD-based strategy; "
                                      f"got {self.strategy}")
@@ -275,7 +278,8 @@ class SequenceSolver:
         init = self._prev_solution if cfg.warm_start else None
         opts = SolveOptions(max_iter=cfg.max_iter, stop_rule=rules if B > 1 else rules[0],
                             track_basis=self._needs_basis(), initial_guess=init)
-        results = rminres(hessian, g, recycles if B > 1 else recycles[0], opts)
+        solve = rminres if cfg.method == "minres" else rcg
+        results = solve(hessian, g, recycles if B > 1 else recycles[0], opts)
         res_list = [results] if single else results
         self._prev_basis = [r.basis for r in res_list]
         self._prev_recycle = recycles

@@ -2,9 +2,15 @@
 //
 // Algorithm: /root/reference/pkg/src/krecycle/krylov.py:408-483 (plain CG,
 // NonSPDError on p^T H p <= 0, basis columns r_k/||r_k||), with the stop rule
-// evaluated on the explicit residual (stopping.py:93-118).  Two grid barriers
-// per iteration: the direction p_k = r_{k-1} + (rr_{k-1}/rr_{k-2}) p_{k-1} is
-// formed on the fly inside the stencil load, so it needs no barrier of its own.
+// evaluated on the explicit residual (stopping.py:93-118).  Two per-sample
+// barriers per iteration: the direction p_k = r_{k-1} + (rr_{k-1}/rr_{k-2}) p_{k-1}
+// is formed on the fly inside the stencil load, so it needs no barrier of its own.
+//
+// Recycled CG (s > 0, Minv = (U^T C)^{-1}): deflated CG (Saad, Yeung, Erhel &
+// Guyomarc'h, SIAM J. Sci. Comput. 21 (2000), Alg. 2.2; oracle cpu_krylov.rcg):
+// the start is projected, x += U Minv U^T r, r -= C Minv U^T r (one extra barrier),
+// and p_k = r + beta p_{k-1} - U mu with mu = Minv C^T r, the C^T r partials riding
+// with r.r and the U mu term folded into the same on-the-fly stencil load.
 
 #include <string>
 
@@ -38,7 +44,9 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
   Smem sm = carve(g, smem);
   double* slot_acc = smem + g.total;
   double* nscv = slot_acc + MAX_SLOTS;
-  double* red = nscv + MAX_NSC;
+  double* ctr = nscv + MAX_NSC;   // C^T r (or U^T r at the start), MAX_S
+  double* mu = ctr + MAX_S;       // Minv C^T r, MAX_S
+  double* red = mu + MAX_S;
   __shared__ double s_rr, s_rr_old, s_res, s_php, s_coef;
   __shared__ int s_active, s_finished, s_counted, s_iters, s_reason, s_hvp;
 
@@ -46,7 +54,11 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
   const int bl = blockIdx.x / P.Gs, j = blockIdx.x % P.Gs, b = P.b0 + bl;
   const int64_t n = P.n;
   const int ns = (A.stop_kind == 1) ? A.nsc_s : 0;
-  const int SL_NSC = 0, SL_RR = ns, SL_PHP = ns + 1;
+  const int s = A.Minv ? A.s : 0;  // deflation columns (recycled CG)
+  const int SL_NSC = 0, SL_RR = ns, SL_PHP = ns + 1, SL_CR = ns + 2;  // SL_CR .. SL_CR + s: C^T r
+  const double* U = s ? A.U + (int64_t)b * A.bs_uc : nullptr;
+  const double* C = s ? A.C + (int64_t)b * A.bs_uc : nullptr;
+  const double* Mi = s ? A.Minv + (int64_t)b * s * s : nullptr;
   const int64_t lo = n * j / P.Gs, hi = n * (j + 1) / P.Gs;
   const int ntiles = num_tiles(op);
   const bool leader = (j == 0);
@@ -84,6 +96,33 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
   }
   for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) w[p] = w0 ? w0[p] : 0.0;
   grid_barrier(reinterpret_cast<unsigned int*>(P.done) + 1 + bl, P.Gs, grid_target);  // per-sample
+  if (s) {
+    // deflated start: y = Minv U^T r, w += U y, r -= C y  (U^T r = 0 afterwards)
+    for (int i = threadIdx.x; i < s; i += blockDim.x) slot_acc[i] = 0.0;
+    block_barrier();
+    slot_dots(U, A.ld_uc, s, lo, hi, [&](int64_t p) { return r[p]; }, slot_acc, red);
+    write_partials(PP, bl, j, SL_CR, s, slot_acc);
+    grid_barrier(reinterpret_cast<unsigned int*>(P.done) + 1 + bl, P.Gs, grid_target);  // per-sample
+    reduce_slots(PP, bl, SL_CR, s, ctr);
+    block_barrier();
+    for (int i = threadIdx.x; i < s; i += blockDim.x) {
+      double y = 0.0;
+      for (int l = 0; l < s; ++l) y += Mi[(int64_t)i * s + l] * ctr[l];
+      mu[i] = y;
+    }
+    block_barrier();
+    for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+      double du = 0.0, dc = 0.0;
+      for (int i = 0; i < s; ++i) {
+        du += U[(int64_t)i * A.ld_uc + p] * mu[i];
+        dc += C[(int64_t)i * A.ld_uc + p] * mu[i];
+      }
+      w[p] += du;
+      r[p] -= dc;
+    }
+    // all of the sample's SL_CR partials were read before anyone rewrites them below
+    grid_barrier(reinterpret_cast<unsigned int*>(P.done) + 1 + bl, P.Gs, grid_target);  // per-sample
+  }
   {
     double v[1] = {0.0};
     for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) v[0] += r[p] * r[p];
@@ -95,6 +134,12 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
       slot_dots(Z, A.ld_z, ns, lo, hi, [&](int64_t p) { return r[p]; }, slot_acc, red);
       write_partials(PP, bl, j, SL_NSC, ns, slot_acc);
     }
+    if (s) {
+      for (int i = threadIdx.x; i < s; i += blockDim.x) slot_acc[i] = 0.0;
+      block_barrier();
+      slot_dots(C, A.ld_uc, s, lo, hi, [&](int64_t p) { return r[p]; }, slot_acc, red);
+      write_partials(PP, bl, j, SL_CR, s, slot_acc);
+    }
   }
   grid_barrier(reinterpret_cast<unsigned int*>(P.done) + 1 + bl, P.Gs, grid_target);  // per-sample
 
@@ -104,6 +149,15 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
     if (ns && s_active) {
       reduce_slots(PP, bl, SL_NSC, ns, nscv);
       block_barrier();
+    }
+    if (s && s_active) {  // mu = Minv C^T r_{k-1}
+      reduce_slots(PP, bl, SL_CR, s, ctr);
+      block_barrier();
+      for (int i = threadIdx.x; i < s; i += blockDim.x) {
+        double y = 0.0;
+        for (int l = 0; l < s; ++l) y += Mi[(int64_t)i * s + l] * ctr[l];
+        mu[i] = y;
+      }
     }
     if (threadIdx.x == 0) {
       s_hvp = 0;
@@ -139,12 +193,21 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
       const double coef = s_coef, res = s_res;
       double* basis = A.basis ? A.basis + (int64_t)b * A.bs_basis + (int64_t)(k - 1) * A.ld_basis : nullptr;
       for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
-        pk[p] = po ? r[p] + coef * po[p] : r[p];
+        double d = po ? r[p] + coef * po[p] : r[p];
+        for (int i = 0; i < s; ++i) d -= U[(int64_t)i * A.ld_uc + p] * mu[i];
+        pk[p] = d;
         if (basis) basis[p] = (res > 0.0) ? r[p] / res : 0.0;
       }
       double php[1] = {0.0};
       for (int tile = j; tile < ntiles; tile += P.Gs) {
-        tile_hvp_t<Q>(op, g, sm, b, TileIn{r, 1.0, po, coef}, tile);
+        TileIn tin{r, 1.0, po ? po : r, po ? coef : 0.0};
+        if (s) {
+          tin.U = U;
+          tin.ldu = A.ld_uc;
+          tin.s = s;
+          tin.mu = mu;
+        }
+        tile_hvp_t<Q>(op, g, sm, b, tin, tile);
         const int tyc = tiles_x(op);
         for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
           int64_t p = tile_pixel(op, tile, l);
@@ -152,7 +215,7 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
           hp[p] = sm.res[l];
           double pv;
           if (op.data_kind == KR_DATA_DENSE) {
-            pv = po ? r[p] + coef * po[p] : r[p];
+            pv = pk[p];
           } else {
             int ty = l / TW, tx = l - ty * TW;
             pv = sm.S0[(ty + g.H) * g.RW + tx + g.H];
@@ -194,6 +257,12 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
           slot_dots(Z, A.ld_z, ns, lo, hi, [&](int64_t p) { return r[p]; }, slot_acc, red);
           write_partials(PP, bl, j, SL_NSC, ns, slot_acc);
         }
+        if (s) {
+          for (int i = threadIdx.x; i < s; i += blockDim.x) slot_acc[i] = 0.0;
+          block_barrier();
+          slot_dots(C, A.ld_uc, s, lo, hi, [&](int64_t p) { return r[p]; }, slot_acc, red);
+          write_partials(PP, bl, j, SL_CR, s, slot_acc);
+        }
       }
     }
     if (s_finished && !s_counted) {
@@ -233,11 +302,11 @@ struct CgLayout {
 void cg_plan(const kr_op& op, const kr_solve_args& a, CgLayout& L) {
   const int64_t n = op_n(op);
   Geom g = make_geom(op);
-  L.smem = sizeof(double) * ((size_t)g.total + MAX_SLOTS + MAX_NSC + 16 * 33 + 16);
+  L.smem = sizeof(double) * ((size_t)g.total + MAX_SLOTS + MAX_NSC + 2 * MAX_S + 16 * 33 + 16);
   int sms = device_sms(), per_sm = 0;
   if (sms > 0) {
     if (L.smem > 48 * 1024)
-      cudaFuncSetAttribute(KR_PICK_Q(cg_kernel, q_variant(op)), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+      ensure_smem(KR_PICK_Q(cg_kernel, q_variant(op)), L.smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, KR_PICK_Q(cg_kernel, q_variant(op)), NT, L.smem);
   }
   if (per_sm < 1) per_sm = 1;
@@ -248,7 +317,7 @@ void cg_plan(const kr_op& op, const kr_solve_args& a, CgLayout& L) {
   if (want < num_tiles(op)) want = num_tiles(op);
   int Gs = max_blocks / L.chunk;
   L.Gs = Gs < 1 ? 1 : (Gs > want ? want : Gs);
-  L.nslot = (a.stop_kind == 1 ? a.nsc_s : 0) + 2;
+  L.nslot = (a.stop_kind == 1 ? a.nsc_s : 0) + 2 + (a.Minv ? a.s : 0);
   L.total = 5 * (int64_t)B * n + (int64_t)L.chunk * L.nslot * L.Gs + 2 + (L.chunk + 1) / 2;
 }
 
@@ -269,6 +338,8 @@ extern "C" int kr_cg(const kr_op* op, const kr_solve_args* a, double* work, int6
   KR_CHECK_ARG(a->stop_kind == 0 || a->stop_kind == 1, "stop_kind must be 0 or 1");
   KR_CHECK_ARG(a->delta > 0.0, "tolerance must be positive");
   KR_CHECK_ARG(a->stop_kind == 0 || (a->Z && a->nsc_s >= 1 && a->nsc_s <= MAX_NSC), "NSC needs Z");
+  KR_CHECK_ARG(!a->Minv || (a->s >= 1 && a->s <= MAX_S && a->U && a->C && a->ld_uc >= op_n(*op)),
+               "recycled CG needs U, C (s <= 128) with Minv");
   KR_CHECK_ARG(a->g && a->w && a->res_norms && a->stop_vals && a->iters && a->reasons, "missing output buffer");
   CgLayout L;
   cg_plan(*op, *a, L);

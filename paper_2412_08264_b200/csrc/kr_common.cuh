@@ -214,13 +214,23 @@ __device__ inline void load_weights(const kr_op& op, const Geom& g, Smem& sm) {
 }
 
 // Input of a tile stencil: v = a / div, or v = a + coef * b when b != nullptr
-// (CG's direction p = r + (rr_new/rr) p_old, formed on the fly).
+// (CG's direction p = r + (rr_new/rr) p_old, formed on the fly), minus
+// sum_i U_i mu_i when U != nullptr (recycled CG's deflated direction).
 struct TileIn {
   const double* a;
   double div;
   const double* b;
   double coef;
-  __device__ inline double at(int64_t p) const { return b ? a[p] + coef * b[p] : a[p] / div; }
+  const double* U = nullptr;
+  int64_t ldu = 0;
+  int s = 0;
+  const double* mu = nullptr;
+  __device__ inline double at(int64_t p) const {
+    double v = b ? a[p] + coef * b[p] : a[p] / div;
+    if (U)
+      for (int i = 0; i < s; ++i) v -= U[(int64_t)i * ldu + p] * mu[i];
+    return v;
+  }
 };
 
 __device__ inline void load_region(const kr_op& op, const Geom& g, const TileIn& in, int y0, int x0,

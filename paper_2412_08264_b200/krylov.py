@@ -26,7 +26,7 @@ from .operators import as_device, columns, new_columns
 from .stopping import NscRule, ResidualNormRule, StopRule
 
 __all__ = ["BREAKDOWN_RTOL", "NonSPDError", "SolveOptions", "SolveResult", "TridiagState", "cg", "flops_cg",
-           "flops_minres", "flops_rminres", "minres", "rminres"]
+           "flops_minres", "flops_rcg", "flops_rminres", "minres", "rcg", "rminres"]
 
 BREAKDOWN_RTOL = 1e-13
 
@@ -107,6 +107,13 @@ def flops_rminres(k_total: int, n: int, s: int, h_cost: int) -> int:
     return h_cost + 4 * n + 6 * n * s + k_total * (h_cost + 21 * n + 6 * n * s - s)
 
 
+def flops_rcg(k_total: int, n: int, s: int, h_cost: int) -> int:
+    """Deflated CG: flops_cg plus U^T r, C y, U y once and C^T r, U mu per iteration
+    (oracle cpu_krylov.flops_rcg)."""
+    _check_counts(k_total=k_total, n=n, s=s, h_cost=h_cost)
+    return h_cost + 3 * n + 6 * n * s + k_total * (h_cost + 10 * n + 4 * n * s)
+
+
 def flops_cg(k_total: int, n: int, h_cost: int) -> int:
     """krylov.py:131-135"""
     _check_counts(k_total=k_total, n=n, h_cost=h_cost)
@@ -172,7 +179,7 @@ def _buf(tag, *shape, zero=False, dev=None):
 class _Launch:
     """Device buffers + kr_solve_args for one batched solve."""
 
-    def __init__(self, H, G, recycles, rules, opts, want_basis):
+    def __init__(self, H, G, recycles, rules, opts, want_basis, deflate=False):
         B, n = G.shape
         dev = G.device
         self.B, self.n = B, n
@@ -200,6 +207,19 @@ class _Launch:
             self.U, self.C = U, C
             self.keep += [U, C]
             a.U, a.C, a.ld_uc, a.bs_uc = U.data_ptr(), C.data_ptr(), n, s * n
+            if deflate:  # recycled CG: Minv = (U^T C)^{-1}, identity on padded columns
+                live = torch.zeros(B, s, dtype=torch.float64, device=dev)
+                for b, d in enumerate(dims):
+                    live[b, :d] = 1.0
+                M = U @ C.transpose(1, 2)
+                M = 0.5 * (M + M.transpose(1, 2)) * (live.unsqueeze(2) * live.unsqueeze(1))
+                M = M + torch.diag_embed(1.0 - live)
+                L, info = torch.linalg.cholesky_ex(M)
+                if bool((info != 0).any()):
+                    raise ValueError("U^T H U is not positive definite; the recycle space does not fit H")
+                Minv = torch.cholesky_inverse(L).contiguous()
+                self.keep.append(Minv)
+                a.Minv = Minv.data_ptr()
         kinds = {_rule_kind(r) for r in rules}
         if len(kinds) != 1:
             raise ValueError("one launch needs one rule kind; split the batch")
@@ -329,10 +349,15 @@ def _solve(H, g, recycle, opts, kind):
             sub_opts = SolveOptions(**{**opts.__dict__, "initial_guess": w0[idx].contiguous(), "stop_rule": None})
         if kind == "cg":
             if any(r is not None and r.dim for r in rec):
-                raise ValueError("plain CG takes no recycle space")
+                raise ValueError("plain CG takes no recycle space; use rcg")
             launch = _Launch(Hs, Gs, [None] * len(idx), rs, sub_opts, opts.track_basis)
             launch.run(Hs, L.kr_cg_workspace, L.kr_cg)
             res = launch.results(Hs, lambda k, s: flops_cg(k, n, H.apply_cost))
+        elif kind == "rcg":
+            launch = _Launch(Hs, Gs, rec, rs, sub_opts, opts.track_basis, deflate=True)
+            launch.run(Hs, L.kr_cg_workspace, L.kr_cg)
+            res = launch.results(
+                Hs, lambda k, s: flops_rcg(k, n, s, H.apply_cost) if s else flops_cg(k, n, H.apply_cost))
         else:
             launch = _Launch(Hs, Gs, rec, rs, sub_opts, opts.track_basis)
             launch.run(Hs, L.kr_rminres_workspace, L.kr_rminres)
@@ -363,3 +388,13 @@ def rminres(H, g, recycle, opts: SolveOptions | None = None):
 def cg(H, g, opts: SolveOptions | None = None):
     """krylov.py:408-483"""
     return _solve(H, g, None, opts, "cg")
+
+
+def rcg(H, g, recycle, opts: SolveOptions | None = None):
+    """Recycled (deflated) CG with the recycle space (U, C = H U) as deflation
+    space -- BASELINE config 1's "recycled CG"; the reference has plain cg only
+    (krylov.py:408-483), so this follows the published deflated CG (Saad, Yeung,
+    Erhel & Guyomarc'h, SIAM J. Sci. Comput. 21 (2000)), restated in the oracle as
+    cpu_krylov.rcg.  Same options, results and NonSPDError as cg; an empty
+    recycle space is plain cg."""
+    return _solve(H, g, recycle, opts, "rcg")

@@ -41,11 +41,12 @@ class DeblurConfig:
     recycle_dim: int = 10
     max_iter: int = 100
     upper_steps: int = 20
+    method: str = "minres"  # Krylov method of the Hessian solves: "minres" (RMINRES) or "cg" (recycled CG)
 
 
 CONFIGS = {
     # BASELINE.json configs[0..4]
-    "C1": DeblurConfig(64, 1, 9, 1.5, 0.01, "tv", recycle_dim=10, max_iter=100, upper_steps=20),
+    "C1": DeblurConfig(64, 1, 9, 1.5, 0.01, "tv", recycle_dim=10, max_iter=100, upper_steps=20, method="cg"),
     "C2": DeblurConfig(128, 8, 9, 1.5, 0.01, "filters", 8, 5, recycle_dim=20, max_iter=200, upper_steps=30),
     "C3": DeblurConfig(256, 64, 15, 2.5, 0.02, "filters", 8, 5, recycle_dim=30, max_iter=300, upper_steps=30),
     "C4": DeblurConfig(512, 128, 21, 3.5, 0.01, "filters", 24, 7, recycle_dim=40, max_iter=500, upper_steps=20),

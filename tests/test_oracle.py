@@ -241,3 +241,67 @@ def test_product_generator_matches_oracle():
             assert np.array_equal(xt, xo)
             assert np.array_equal(y, m.data.y)
         assert np.array_equal(pr.theta0(c), im.deblur_theta0(oc))
+
+
+def _spd(rng, n, lo=1e-3, hi=1.0):
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    return (Q * np.geomspace(lo, hi, n)) @ Q.T, Q
+
+
+def test_rcg_deflated_cg_properties():
+    """Recycled (deflated) CG restatement: exact solve, U^T r = 0 throughout,
+    mutually orthogonal residuals, empty space == plain cg, deflating the low end
+    of the spectrum cuts iterations, FLOP count."""
+    from oracle.cpu_imaging import dense_op
+
+    rng = np.random.default_rng(4)
+    n = 80
+    M, Q = _spd(rng, n)
+    g = rng.standard_normal(n)
+    H = dense_op(M)
+    Ut = Q[:, :6] + 1e-3 * rng.standard_normal((n, 6))  # near the 6 smallest eigenvectors
+    C, R = np.linalg.qr(M @ Ut)
+    U = Ut @ np.linalg.inv(R)
+    rec = orc.Recycle(U, C)
+    opts = ok.Options(stop_rule=ok.ResidualRule(1e-10), max_iter=500, track_basis=True)
+    r = ok.rcg(H, g, rec, opts)
+    assert r.stop_reason == "tolerance"
+    assert np.linalg.norm(r.solution - np.linalg.solve(M, g)) <= 1e-6 * np.linalg.norm(np.linalg.solve(M, g))
+    assert np.linalg.norm(U.T @ r.residual_vector) <= 1e-10 * np.linalg.norm(g) * np.linalg.norm(U)
+    V = r.basis[:, :12]  # before finite-precision loss of orthogonality
+    assert np.max(np.abs(V.T @ V - np.eye(V.shape[1]))) <= 1e-8
+    assert np.abs(U.T @ V).max() <= 1e-8 * np.linalg.norm(U)
+    plain = ok.cg(H, g, opts)
+    assert r.iterations < plain.iterations
+    assert r.flops == ok.flops_rcg(r.iterations, n, 6, H.apply_cost)
+    e = ok.rcg(H, g, orc.Recycle.empty(n), opts)
+    assert e.iterations == plain.iterations and np.array_equal(e.solution, plain.solution)
+    with pytest.raises(ok.NonSPDError):
+        ok.rcg(dense_op(-M), g, rec, opts)
+
+
+def test_rcg_sequence_tv():
+    """SequenceSolver with method="cg" (BASELINE config 1's recycled CG) on a small
+    smoothed-TV deblurring sequence: recycled solves reach the tolerance and the
+    hypergradients match an exact solve."""
+    cfg = im.DeblurConfig(16, 1, 5, 1.0, 0.01, "tv", 1, 1)
+    model, xt = im.deblur_sample(cfg, 0)
+    th0 = im.deblur_theta0(cfg)
+    rng = np.random.default_rng(0)
+    seq = ob.SequenceSolver(ob.SolveConfig.from_strategy("RGen-L(R)", recycle_dim=4, delta=1e-9, max_iter=300,
+                                                         method="cg"))
+    for step in range(3):
+        th = th0 + 0.05 * step
+        xh = xt + 0.02 * rng.standard_normal(xt.size)
+        H, J = im.hessian(model, th, xh), im.jacobian(model, th, xh)
+        res, rec = seq.solve(H, xh - xt, J)
+        assert res.stop_reason == "tolerance"
+        if step:
+            assert rec.dim == 4
+        exact = np.linalg.solve(_dense(H), xh - xt)
+        hg, hge = J.apply_adjoint(res.solution), J.apply_adjoint(exact)
+        assert np.linalg.norm(hg - hge) <= 1e-6 * np.linalg.norm(hge)
+
+
+def _dense(H):
+    return np.column_stack([H(e) for e in np.eye(H.dim)])
