@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
   double* red = mu + MAX_S;
   __shared__ double s_rr, s_rr_old, s_res, s_php, s_coef;
   __shared__ int s_active, s_finished, s_counted, s_iters, s_reason, s_hvp;
+  __shared__ double red1[4];  // single-slot reductions
 
   const Partials PP{P.part, P.nslot, P.Gs};
   const int bl = blockIdx.x / P.Gs, j = blockIdx.x % P.Gs, b = P.b0 + bl;
@@ -150,6 +151,10 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
       reduce_slots(PP, bl, SL_NSC, ns, nscv);
       block_barrier();
     }
+    if (s_active) {
+      reduce_slots(PP, bl, SL_RR, 1, red1);
+      block_barrier();
+    }
     if (s && s_active) {  // mu = Minv C^T r_{k-1}
       reduce_slots(PP, bl, SL_CR, s, ctr);
       block_barrier();
@@ -162,7 +167,7 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
     if (threadIdx.x == 0) {
       s_hvp = 0;
       if (s_active) {
-        double rr = reduce_slot1(PP, bl, SL_RR);
+        double rr = red1[0];
         double res = sqrt(rr);
         double val = res;
         if (ns) {
@@ -231,8 +236,10 @@ __global__ void __launch_bounds__(NT, 2) cg_kernel(CgParams P) {
     grid_barrier(reinterpret_cast<unsigned int*>(P.done) + 1 + bl, P.Gs, grid_target);  // per-sample
     // ===== P2: step =====
     if (s_hvp) {
+      reduce_slots(PP, bl, SL_PHP, 1, red1 + 1);
+      block_barrier();
       if (threadIdx.x == 0) {
-        double php = reduce_slot1(PP, bl, SL_PHP);
+        double php = red1[1];
         s_php = php;
         if (php <= 0.0) {
           s_active = 0; s_finished = 1; s_iters = k; s_reason = R_NONSPD;

@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
 #else
   __shared__ Scalars sc;
 #endif
+  __shared__ double red1[4];  // single-slot reductions
 
   const int bl = blockIdx.x / P.Gs;      // local sample index
   const int j = blockIdx.x % P.Gs;       // rank within the sample
@@ -230,10 +231,10 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
     if (threadIdx.x == 0) P.w.part[((int64_t)bl * P.nslot + SL_ALPHA) * P.Gs + j] = red[0];
   }
   KR_GRID_SYNC();
+  reduce_slots(PP, bl, SL_ALPHA, 1, red1);
+  block_barrier();
   if (threadIdx.x == 0) {
-    double gg = 0.0;
-    const double* src = P.w.part + ((int64_t)bl * P.nslot + SL_ALPHA) * P.Gs;
-    for (int jj = 0; jj < P.Gs; ++jj) gg += src[jj];
+    double gg = red1[0];
     double gn = sqrt(gg);
     sc.tol_bd = BREAKDOWN_RTOL * (gn > 1e-300 ? gn : 1e-300);
   }
@@ -255,13 +256,15 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
     }
 #endif
     // ===== P1 =====
+    if (sc.active) {
+      reduce_slots(PP, bl, SL_BETA2, 1, red1);
+      block_barrier();
+    }
     if (threadIdx.x == 0) {
       sc.do_update = 0;
       sc.do_hvp = 0;
       if (sc.active) {
-        const double* src = P.w.part + ((int64_t)bl * P.nslot + SL_BETA2) * P.Gs;
-        double bb = 0.0;
-        for (int jj = 0; jj < P.Gs; ++jj) bb += src[jj];
+        double bb = red1[0];
         double beta_k = sqrt(bb);
         bool broke = beta_k <= sc.tol_bd;
         if (k == 1) {
@@ -423,17 +426,25 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
     if (sc.pending) {
       reduce_slots(PP, bl, SL_NSC, ns, nscv);
       block_barrier();
+      // (Z^T r)_i = (Z^T r_v)_i + (Z^T C Omega)_i, squared, one thread per column
+      for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+        double z = nscv[i];
+        if (ZtC) {
+          double c0 = 0.0, c1 = 0.0;
+          int l = 0;
+          for (; l + 1 < s; l += 2) {
+            c0 += ZtC[(int64_t)i * s + l] * omega[l];
+            c1 += ZtC[(int64_t)i * s + l + 1] * omega[l + 1];
+          }
+          if (l < s) c0 += ZtC[(int64_t)i * s + l] * omega[l];
+          z += c0 + c1;
+        }
+        nscv[i] = z * z;
+      }
+      block_barrier();
       if (threadIdx.x == 0) {
         double ss = 0.0;
-        for (int i = 0; i < ns; ++i) {
-          double z = nscv[i];
-          if (ZtC) {
-            double corr = 0.0;
-            for (int l = 0; l < s; ++l) corr += ZtC[(int64_t)i * s + l] * omega[l];
-            z += corr;
-          }
-          ss += z * z;
-        }
+        for (int i = 0; i < ns; ++i) ss += nscv[i];
         double val = sqrt(ss);
         const int kk = sc.pend_k;
         if (leader) stop_vals[kk] = val;
@@ -465,9 +476,10 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
     if (sc.do_hvp) {
       // chv = C^T hv, cv = C^T v, alpha = v.hv - cv.chv  (== v.(hv - C chv), krylov.py:269-283)
       reduce_slots(PP, bl, SL_CHV, 2 * s, chv);  // chv[0..s) and cv at chv[s..2s) (MAX_S >= 2s is checked)
+      reduce_slots(PP, bl, SL_ALPHA, 1, red1);
       block_barrier();
       if (threadIdx.x == 0) {
-        double a = reduce_slot1(PP, bl, SL_ALPHA);
+        double a = red1[0];
         double corr = 0.0;
         for (int i = 0; i < s; ++i) corr += chv[s + i] * chv[i];
         sc.alpha = a - corr;

@@ -60,21 +60,31 @@ __device__ inline void write_partial1(const Partials& P, int bl, int j, int slot
   if (threadIdx.x == 0) P.at(bl, slot)[j] = v;
 }
 
-// out[i] = sum over the sample's blocks, rank order (deterministic).
+// out[i] = sum over the sample's Gs blocks.  A warp per slot: lanes read the
+// Gs partials coalesced (4 slots in flight per warp), then a fixed shuffle tree
+// -- deterministic (the same order every run and for every block).  Callers
+// synchronise the block before reading out[].
 __device__ inline void reduce_slots(const Partials& P, int bl, int slot0, int S, double* out) {
-  for (int i = threadIdx.x; i < S; i += blockDim.x) {
-    const double* src = P.at(bl, slot0 + i);
-    double acc = 0.0;
-    for (int jj = 0; jj < P.Gs; ++jj) acc += src[jj];
-    out[i] = acc;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i0 = warp; i0 < S; i0 += 4 * nw) {
+    double acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * nw;
+      double a = 0.0;
+      if (i < S) {
+        const double* src = P.at(bl, slot0 + i);
+        for (int jj = lane; jj < P.Gs; jj += 32) a += src[jj];
+      }
+      acc[u] = a;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double v = warp_sum(acc[u]);
+      const int i = i0 + u * nw;
+      if (lane == 0 && i < S) out[i] = v;
+    }
   }
-}
-
-__device__ inline double reduce_slot1(const Partials& P, int bl, int slot) {
-  const double* src = P.at(bl, slot);
-  double acc = 0.0;
-  for (int jj = 0; jj < P.Gs; ++jj) acc += src[jj];
-  return acc;
 }
 
 // Grid-wide barrier for a cooperative launch.  Thread 0 of every block arrives
