@@ -194,7 +194,7 @@ int kr_chol_inv(const double* G, int64_t ldg, int64_t bsg, const int32_t* dims, 
  * the pivoted QR of build_candidate_basis / prepare_recycle (recycling.py:187-199,
  * 362-383, scipy qr(pivoting=True)) applied to the R factor of the tall block.
  * M (in/out, DEVICE): column j of sample b at M + b*tmax*tmax + j*tmax; on return
- * its upper triangle holds R_piv.  Stops at the first |R_kk| <= rtol |R_00|:
+ * column perm[j] (the physical column of pivot j) holds column j of R_piv.  Stops at the first |R_kk| <= rtol |R_00|:
  * rank[b] = k.  Q (out): column j (< rank) of Q_R at Q + b*tmax*tmax + j*tmax, the
  * other columns zero.  perm[b*tmax + j] = original index of pivot j (nullable).
  * work: batch*tmax doubles. */

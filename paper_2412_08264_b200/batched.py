@@ -59,7 +59,8 @@ def qrcp_small(M: torch.Tensor, dims: torch.Tensor, rtol: float):
 
     M (B, T, T) holds each matrix column-major (M[b, j] = column j).  Returns
     (Q, R, rank, perm): Q[b, j] = column j of Q_R (j < rank, else zero), R[b, j]
-    = column j of R_piv (upper triangle), perm (B, T) the pivot order."""
+    = column j of R_piv (upper triangle, gathered from the kernel's physical
+    columns), perm (B, T) the pivot order."""
     B, T, _ = M.shape
     Mw = M.to(torch.float64).contiguous().clone()
     Q = torch.empty_like(Mw)
@@ -71,7 +72,9 @@ def qrcp_small(M: torch.Tensor, dims: torch.Tensor, rtol: float):
                                         rank.data_ptr(), perm.data_ptr(), work.data_ptr(), work.numel(),
                                         _lib.stream_ptr()), "kr_qrcp_small")
     _lib.note_launch("kr_qrcp_small")
-    return Q, Mw, rank, perm
+    idx = perm.clamp_min(0).long()
+    R = torch.gather(Mw, 1, idx.unsqueeze(2).expand(B, T, T))
+    return Q, R, rank, perm
 
 
 QRCP_TMAX = 256
@@ -392,8 +395,12 @@ def recycle_update(strategy, s: int, H, J, bases, recycles, reuse_products: bool
         Jt = J.apply_adjoint_matrix(W.transpose(1, 2)).transpose(1, 2)  # (B, T, p): row j = J w_j
         p = Jt.shape[2]
         # _hessian_condition: Cholesky-pivot screen, exact extreme eigenvalues where it fails
-        _, ih, hst = _chol_inv(Ht, tt, scale=False, inverse=False)
-        screen = (ih < 0) & (hst[:, 0] > 0) & ((hst[:, 1] / hst[:, 0]) ** 2 < COND_SCREEN)
+        # Ht = L L^T: (max L_jj / min L_jj)^2 <= cond(Ht) <= ||Ht||_F ||L^-1||_F^2 brackets the
+        # condition number; the exact extreme eigenvalues are needed only when the
+        # reference's limit falls inside the bracket
+        Fh, ih, hst = _chol_inv(Ht, tt, scale=False, inverse=True)
+        cond_ub = torch.linalg.matrix_norm(Ht) * torch.linalg.matrix_norm(Fh) ** 2
+        screen = (ih < 0) & (hst[:, 0] > 0) & (cond_ub < COND_LIMIT)
         if not bool(screen.all()):
             ext, _, _ = syev_select(Ht, tt, "M", 2)
             lo_, hi_ = ext[:, 0], ext[:, -1]

@@ -11,7 +11,9 @@
 // Q_A Q_R[:, :r] (a GEMM), with the reference's drop decisions.
 //
 // The matrix (column-major, T x T per sample) is worked on in place in global
-// memory (L2-resident); a warp per column for the Householder application.
+// memory (L2-resident).  Each reflector is applied with the trailing columns held
+// in registers, QC columns per warp in flight, and the same pass returns their
+// exact trailing norms for the next pivot choice.
 
 #include <cfloat>
 
@@ -21,7 +23,7 @@
 namespace kr {
 namespace {
 
-constexpr int QNT = 512;
+constexpr int QNT = 256;
 constexpr int QW = QNT / 32;
 
 struct QrcpParams {
@@ -35,11 +37,66 @@ struct QrcpParams {
   double* tau;    // work: T per sample
 };
 
+constexpr int QR = 8;   // rows per lane (t <= 256)
+constexpr int QC = 4;   // columns per warp per round (independent loads in flight)
+
+// Apply H = I - tau v v^T (v = vs[k..t), vs[k] = 1) to columns [j0, t) of M from
+// row k, QC columns per warp at a time held in registers; optionally return the
+// exact norms^2 of rows (k, t) of the updated columns in cn[].
+__device__ void apply_reflector(double* M, int T, int t, int k, int j0, int jend, double tau, const double* vs,
+                                double* cn, const int* col = nullptr) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int jb = j0 + warp * QC; jb < jend; jb += QW * QC) {
+    double c[QC][QR];
+#pragma unroll
+    for (int u = 0; u < QC; ++u) {
+      const int jj = jb + u < jend ? (col ? col[jb + u] : jb + u) : 0;
+      const double* cj = M + (int64_t)jj * T;
+#pragma unroll
+      for (int r = 0; r < QR; ++r) {
+        const int i = k + lane + 32 * r;
+        c[u][r] = (jb + u < jend && i < t) ? cj[i] : 0.0;
+      }
+    }
+    double d[QC];
+#pragma unroll
+    for (int u = 0; u < QC; ++u) {
+      double s = 0.0;
+#pragma unroll
+      for (int r = 0; r < QR; ++r) {
+        const int i = k + lane + 32 * r;
+        if (i < t) s += vs[i] * c[u][r];
+      }
+      d[u] = s;
+    }
+#pragma unroll
+    for (int u = 0; u < QC; ++u) d[u] = tau * warp_sum(d[u]);
+#pragma unroll
+    for (int u = 0; u < QC; ++u) {
+      double nn = 0.0;
+      const int jj = jb + u < jend ? (col ? col[jb + u] : jb + u) : 0;
+      double* cj = M + (int64_t)jj * T;
+#pragma unroll
+      for (int r = 0; r < QR; ++r) {
+        const int i = k + lane + 32 * r;
+        if (i < t) {
+          c[u][r] -= d[u] * vs[i];
+          if (jb + u < jend) cj[i] = c[u][r];
+          if (i > k) nn += c[u][r] * c[u][r];
+        }
+      }
+      if (cn) {
+        nn = warp_sum(nn);
+        if (lane == 0 && jb + u < jend) cn[jb + u] = nn;
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(QNT, 1) qrcp_kernel(QrcpParams P) {
-  __shared__ double cn[256];   // column norms^2 (t <= 256)
+  __shared__ double cn[256];   // norms^2 of the trailing parts of the columns (exact)
+  __shared__ double vs[256];   // current Householder vector
   __shared__ int pv[256];
-  __shared__ double red_v[QW];
-  __shared__ int red_i[QW];
   __shared__ double s_beta, s_tau, s_r00;
   __shared__ int s_piv, s_rank;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -47,20 +104,17 @@ __global__ void __launch_bounds__(QNT, 1) qrcp_kernel(QrcpParams P) {
   double* M = P.M + (int64_t)b * T * T;
   double* tau = P.tau + (int64_t)b * T;
   for (int j = tid; j < t; j += QNT) pv[j] = j;
+  for (int j = warp; j < t; j += QW) {  // initial column norms
+    const double* cj = M + (int64_t)j * T;
+    double s = 0.0;
+    for (int i = lane; i < t; i += 32) s += cj[i] * cj[i];
+    s = warp_sum(s);
+    if (lane == 0) cn[j] = s;
+  }
   if (tid == 0) s_rank = t;
   __syncthreads();
-  int k = 0;
-  for (; k < t; ++k) {
-    // exact norms of the trailing parts of the remaining columns (warp per column)
-    for (int j = k + warp; j < t; j += QW) {
-      const double* cj = M + (int64_t)j * T;
-      double s = 0.0;
-      for (int i = k + lane; i < t; i += 32) s += cj[i] * cj[i];
-      s = warp_sum(s);
-      if (lane == 0) cn[j] = s;
-    }
-    __syncthreads();
-    // pivot: the largest norm, lowest index on ties (warp 0)
+  for (int k = 0; k < t; ++k) {
+    // pivot: the largest remaining norm, lowest index on ties (warp 0)
     if (warp == 0) {
       double best = -1.0;
       int bi = k;
@@ -81,38 +135,52 @@ __global__ void __launch_bounds__(QNT, 1) qrcp_kernel(QrcpParams P) {
       if (lane == 0) s_piv = bi;
     }
     __syncthreads();
-    const int p = s_piv;
-    if (p != k) {  // swap columns k and p
-      double* ck = M + (int64_t)k * T;
-      double* cp = M + (int64_t)p * T;
-      for (int i = tid; i < t; i += QNT) {
-        const double a = ck[i];
-        ck[i] = cp[i];
-        cp[i] = a;
-      }
-      if (tid == 0) {
-        const int a = pv[k];
-        pv[k] = pv[p];
-        pv[p] = a;
-      }
+    // pivot swap through the index: column j of the pivoted matrix is physical column pv[j]
+    if (tid == 0) {
+      const int p = s_piv;
+      const int a = pv[k];
+      pv[k] = pv[p];
+      pv[p] = a;
+      const double c = cn[k];
+      cn[k] = cn[p];
+      cn[p] = c;
     }
     __syncthreads();
-    // Householder of column k below the diagonal (larfg)
-    double* ck = M + (int64_t)k * T;
+    // Householder of column k (larfg), v staged in shared memory
+    double* ck = M + (int64_t)pv[k] * T;
     if (warp == 0) {
+      double x[QR];
       double s = 0.0;
-      for (int i = k + 1 + lane; i < t; i += 32) s += ck[i] * ck[i];
+#pragma unroll
+      for (int r = 0; r < QR; ++r) {
+        const int i = k + 1 + lane + 32 * r;
+        x[r] = i < t ? ck[i] : 0.0;
+        s += x[r] * x[r];
+      }
       s = warp_sum(s);
-      if (lane == 0) {
-        const double alpha = ck[k];
-        double beta = alpha, tk = 0.0;
-        if (s > 0.0) {
-          beta = -copysign(sqrt(alpha * alpha + s), alpha);
-          tk = (beta - alpha) / beta;
+      const double alpha = ck[k];
+      double beta = alpha, tk = 0.0;
+      if (s > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + s), alpha);
+        tk = (beta - alpha) / beta;
+      }
+      const double scal = tk != 0.0 ? 1.0 / (alpha - beta) : 0.0;
+#pragma unroll
+      for (int r = 0; r < QR; ++r) {
+        const int i = k + 1 + lane + 32 * r;
+        if (i < t) {
+          const double v = x[r] * scal;
+          vs[i] = v;
+          ck[i] = v;
         }
+      }
+      if (lane == 0) {
+        vs[k] = 1.0;
         s_beta = beta;
         s_tau = tk;
         if (k == 0) s_r00 = fabs(beta);
+        ck[k] = beta;
+        tau[k] = tk;
       }
     }
     __syncthreads();
@@ -122,24 +190,16 @@ __global__ void __launch_bounds__(QNT, 1) qrcp_kernel(QrcpParams P) {
       break;
     }
     if (tk != 0.0) {
-      const double scal = 1.0 / (ck[k] - beta);
-      for (int i = k + 1 + tid; i < t; i += QNT) ck[i] *= scal;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      ck[k] = beta;
-      tau[k] = tk;
-    }
-    // apply H_k = I - tau v v^T (v = [1; ck[k+1:]]) to the trailing columns
-    if (tk != 0.0)
-      for (int j = k + 1 + warp; j < t; j += QW) {
-        double* cj = M + (int64_t)j * T;
-        double d = (lane == 0) ? cj[k] : 0.0;
-        for (int i = k + 1 + lane; i < t; i += 32) d += ck[i] * cj[i];
-        d = tk * warp_sum(d);
-        if (lane == 0) cj[k] -= d;
-        for (int i = k + 1 + lane; i < t; i += 32) cj[i] -= d * ck[i];
+      apply_reflector(M, T, t, k, k + 1, t, tk, vs, cn, pv);
+    } else {
+      for (int j = k + 1 + warp; j < t; j += QW) {  // norms still drop row k
+        const double* cj = M + (int64_t)pv[j] * T;
+        double s = 0.0;
+        for (int i = k + 1 + lane; i < t; i += 32) s += cj[i] * cj[i];
+        s = warp_sum(s);
+        if (lane == 0) cn[j] = s;
       }
+    }
     __syncthreads();
   }
   __syncthreads();
@@ -147,23 +207,20 @@ __global__ void __launch_bounds__(QNT, 1) qrcp_kernel(QrcpParams P) {
   if (tid == 0) P.rank[b] = r;
   if (P.perm)
     for (int j = tid; j < T; j += QNT) P.perm[(int64_t)b * T + j] = j < t ? pv[j] : -1;
-  // Q_R[:, :r] = H_0 ... H_{r-1} [I_r; 0]  (orgqr, backward accumulation), column per warp
+  // Q_R[:, :r] = H_0 ... H_{r-1} [I_r; 0]  (orgqr, backward accumulation)
   double* Qb = P.Q + (int64_t)b * T * T;
   for (int j = warp; j < T; j += QW)
     for (int i = lane; i < T; i += 32) Qb[(int64_t)j * T + i] = (j < r && i == j) ? 1.0 : 0.0;
   __syncthreads();
   for (int kk = r - 1; kk >= 0; --kk) {
     const double tk = tau[kk];
-    const double* vk = M + (int64_t)kk * T;  // v = [1; vk[kk+1:]]
-    if (tk != 0.0)
-      for (int j = kk + warp; j < r; j += QW) {
-        double* qj = Qb + (int64_t)j * T;
-        double d = (lane == 0) ? qj[kk] : 0.0;
-        for (int i = kk + 1 + lane; i < t; i += 32) d += vk[i] * qj[i];
-        d = tk * warp_sum(d);
-        if (lane == 0) qj[kk] -= d;
-        for (int i = kk + 1 + lane; i < t; i += 32) qj[i] -= d * vk[i];
-      }
+    if (tk != 0.0) {
+      const double* vk = M + (int64_t)pv[kk] * T;
+      for (int i = kk + 1 + tid; i < t; i += QNT) vs[i] = vk[i];
+      if (tid == 0) vs[kk] = 1.0;
+      __syncthreads();
+      apply_reflector(Qb, T, t, kk, kk, r, tk, vs, nullptr);
+    }
     __syncthreads();
   }
 }

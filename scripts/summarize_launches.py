@@ -1,32 +1,26 @@
-"""Summarise an `ncu --metrics gpu__time_duration.sum --csv` launch list: share per kernel.
-
-    python scripts/summarize_launches.py gpurun_out/launches.csv "title" > profiles/rN_launches.txt
-"""
-
-import collections
+"""Summarise an ncu --metrics gpu__time_duration.sum launch list (csv) by kernel:
+launches, total ms and share (cold-cache, serialised: compare SHARES, not absolutes)."""
 import csv
 import sys
+from collections import defaultdict
 
-UNIT = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "s": 1e3, "second": 1e3}
-
-
-def main(path, title=""):
-    lines = [l for l in open(path) if l.startswith('"')]
-    agg = collections.defaultdict(lambda: [0, 0.0])
-    for row in csv.DictReader(lines):
-        if row.get("Metric Name") != "gpu__time_duration.sum":
-            continue
-        ms = float(row["Metric Value"].replace(",", "")) * UNIT[row["Metric Unit"]]
-        name = row["Kernel Name"].split("(")[0][:80]
-        agg[name][0] += 1
-        agg[name][1] += ms
-    tot = sum(v[1] for v in agg.values())
-    print(title)
-    print("(ncu --metrics gpu__time_duration.sum --clock-control none; cold-cache, serialised: compare SHARES)")
-    print(f"launches: {sum(v[0] for v in agg.values())}, total {tot:.2f} ms")
-    for name, (cnt, ms) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:40]:
-        print(f"{100 * ms / tot:6.2f}%  {ms:9.3f} ms  {cnt:6d}x  {name}")
-
-
-if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "")
+rows = [r for r in csv.reader(open(sys.argv[1])) if r]
+hdr_i = next(i for i, r in enumerate(rows) if "Kernel Name" in r and "Metric Value" in r)
+hdr = rows[hdr_i]
+tot = defaultdict(float)
+cnt = defaultdict(int)
+for r in rows[hdr_i + 1:]:
+    d = dict(zip(hdr, r))
+    if d.get("Metric Name") != "gpu__time_duration.sum":
+        continue
+    name = d["Kernel Name"]
+    short = name.split("(")[0].replace("void ", "")[:90]
+    val = float(d["Metric Value"].replace(",", ""))
+    unit = d.get("Metric Unit", "ns")
+    ms = val / 1e6 if unit == "ns" else (val / 1e3 if unit in ("us", "usecond") else val)
+    tot[short] += ms
+    cnt[short] += 1
+T = sum(tot.values())
+print(f"launches: {sum(cnt.values())}, total {T:.2f} ms")
+for k, v in sorted(tot.items(), key=lambda kv: -kv[1])[:30]:
+    print(f"{100 * v / T:6.2f}%  {v:9.3f} ms  {cnt[k]:6d}x  {k}")

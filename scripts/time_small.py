@@ -31,4 +31,6 @@ tm("chol_inv factor only", lambda: batched._chol_inv(G, dims, True, inverse=Fals
 tm("syev_select L 20", lambda: batched.syev_select(G / T, dims, "L", 20))
 tm("syev_select M 2", lambda: batched.syev_select(G / T, dims, "M", 2))
 tm("torch cholesky_ex", lambda: torch.linalg.cholesky_ex(G))
+R = torch.linalg.cholesky(G).transpose(1, 2).contiguous()  # upper triangular, stored so rows = columns of R^T
+tm("qrcp_small", lambda: batched.qrcp_small(R, dims, 1e-10))
 tm("gram (B,T,16384)", lambda: torch.randn(1, device="cuda") if False else None)
