@@ -110,6 +110,18 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def measured_traffic(config: str, kernel: str):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture
+    (profiles/r1_traffic.json), or None when this config/kernel was not captured."""
+    p = Path(__file__).resolve().parent / "profiles" / "r1_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text()).get(config)
+    if not d or d.get("kernel") != kernel:
+        return None
+    return int(d["dram_bytes_per_launch"]), d.get("source")
+
+
 def krylov_bytes_per_iter(kernel, n, s, nsc, w):
     """Algorithmic HBM bytes per iteration per sample.
     RMINRES: 8n(21 + 3s + s_nsc) + the HVP's 8n(2 + w).
@@ -227,6 +239,7 @@ def run_ours(args):
         k_bytes += its * krylov_bytes_per_iter(kname, info["n"], info["s"], info["nsc"], wts)
     peak, peak_src = measured_peak()
     achieved = (k_bytes / 1e9) / (k_ms / 1e3) if k_ms > 0 else 0.0
+    traffic = measured_traffic(args.config, kname)
 
     # ---- e2e through the public API with host buffers ----
     e2e = None
@@ -280,7 +293,12 @@ def run_ours(args):
             "roofline": {"kernel": f"{kname} (persistent {'recycled CG' if kname == 'kr_cg' else 'RMINRES'}, "
                                    "all iterations of all samples)",
                          "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak if peak else None, "traffic": None,
+                         "frac": achieved / peak if peak else None,
+                         "traffic": None if traffic is None else traffic[0],
+                         "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
+                         "traffic_source": None if traffic is None else traffic[1],
+                         "algorithmic_bytes_per_launch": (k_bytes / max(len([1 for _, _, i in prof
+                                                                            if i["kernel"] == kname]), 1)),
                          "peak_source": peak_src,
                          "algorithmic_bytes": ("per iteration per sample 8n(12+3s+s_nsc)+8n*w (recycled CG)"
                                                if kname == "kr_cg" else
