@@ -201,6 +201,15 @@ int kr_chol_inv(const double* G, int64_t ldg, int64_t bsg, const int32_t* dims, 
 int kr_qrcp_small(double* M, const int32_t* dims, int32_t batch, int32_t tmax, double rtol, double* Q,
                   int32_t* rank, int32_t* perm, double* work, int64_t work_len, kr_stream_t stream);
 
+/* Batched Gram of row blocks: G_b[i][j] = a_i . b_j (row-major G, ldg, bsg) for
+ * A_b, B_b given as `rows` rows of length n (row stride ld, batch stride bs) -- the
+ * (B, t, n) Grams of the recycle update's QRs and W^T H W (recycling.py:194, 250,
+ * 333).  Split-K over the pixel dimension (pointer-array batched cuBLAS DGEMM),
+ * partials summed in fixed order.  work: kr_gram_workspace doubles. */
+int64_t kr_gram_workspace(int32_t batch, int32_t rows, int64_t n);
+int kr_gram(const double* A, const double* B, int64_t ld, int64_t bs, int32_t batch, int32_t rows, int64_t n,
+            double* G, int64_t ldg, int64_t bsg, double* work, int64_t work_len, kr_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -77,6 +77,25 @@ def qrcp_small(M: torch.Tensor, dims: torch.Tensor, rtol: float):
     return Q, R, rank, perm
 
 
+def gram(A: torch.Tensor, Bm: torch.Tensor | None = None) -> torch.Tensor:
+    """(B, T, T) with G[b, i, j] = A[b, i] . Bm[b, j] for row blocks (B, T, n):
+    kr_gram (split-K over n, fixed-order partial sums) for long rows, bmm else."""
+    Bm = A if Bm is None else Bm
+    B, T, n = A.shape
+    if n < 4096 or B == 0 or T == 0:
+        return A @ Bm.transpose(1, 2)
+    A = A.contiguous()
+    Bm = Bm.contiguous()
+    G = torch.empty(B, T, T, dtype=torch.float64, device=A.device)
+    L = _lib.lib()
+    wl = int(L.kr_gram_workspace(B, T, n))
+    ws = torch.empty(max(wl, 1), dtype=torch.float64, device=A.device)
+    _lib.check(L.kr_gram(A.data_ptr(), Bm.data_ptr(), n, T * n, B, T, n, G.data_ptr(), T, T * T, ws.data_ptr(), wl,
+                         _lib.stream_ptr()), "kr_gram")
+    _lib.note_launch("kr_gram", 3)
+    return G
+
+
 QRCP_TMAX = 256
 PIVOT_COND = 1e9   # below this cond(A) bound pivoted QR keeps every column (|R_kk| ~ sigma_k > 1e-10 |R_00|)
 
@@ -180,7 +199,7 @@ def cholqr2_rows(A: torch.Tensor, mask: torch.Tensor, robust: bool = False, want
     first row where a Cholesky broke down (-1 if none)."""
     B, T, n = A.shape
     dims = mask.sum(1).to(torch.int32)
-    G = A @ A.transpose(1, 2)
+    G = gram(A)
     F1, i1, st = _chol_inv(G, dims, scale=True)
     ok1 = (i1 < 0) & (st[:, 0] > CHOLQR_TOL * st[:, 1]) & (st[:, 2] > 0)
     shifted = robust and not bool(ok1.all())
@@ -198,7 +217,7 @@ def cholqr2_rows(A: torch.Tensor, mask: torch.Tensor, robust: bool = False, want
     for _ in range(2 if shifted else 1):
         # (skip mode stays off: the breakdown test of a pass behind a shifted pass
         # fires ~30x above the reference's pivoted-QR drop threshold)
-        out = _chol_inv(Q @ Q.transpose(1, 2), dims, scale=False, skip=robust and SKIP_DEPENDENT)
+        out = _chol_inv(gram(Q), dims, scale=False, skip=robust and SKIP_DEPENDENT)
         Fk, ik = out[0], out[1]
         if len(out) > 3 and out[3] is not None:
             skipped = out[3] if skipped is None else skipped | out[3]
@@ -307,7 +326,7 @@ def orth_rows(A: torch.Tensor, dims: list[int]):
         STATS["pivoted"] = STATS.get("pivoted", 0) + len(idx)
     ii = torch.tensor(idx, device=dev)
     Wsub = W[ii].clone()
-    M = A[ii] @ Wsub.transpose(1, 2)  # M[j][i] = a_j . q_i = R[i][j]: R column-major
+    M = gram(A[ii], Wsub)  # M[j][i] = a_j . q_i = R[i][j]: R column-major
     for s_, b in enumerate(idx):
         if not ok_h[b]:  # Householder QR where shifted CholeskyQR3 is not trustworthy
             Qh, Rh = torch.linalg.qr(A[b, : dims[b]].T)
@@ -385,7 +404,7 @@ def recycle_update(strategy, s: int, H, J, bases, recycles, reuse_products: bool
     tt = torch.tensor(t, dtype=torch.int32, device=dev)
     checks = {"candidates": ok}
     HW = H.apply_matrix(W.transpose(1, 2)).transpose(1, 2)          # (B, T, n)
-    Ht = W @ HW.transpose(1, 2)
+    Ht = gram(W, HW)
     Ht = 0.5 * (Ht + Ht.transpose(1, 2))                            # _sym(W^T H W)
     mu = VH = None
     if strategy.vec_type == "Ritz":

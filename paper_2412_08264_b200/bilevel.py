@@ -258,28 +258,34 @@ class SequenceSolver:
             main.wait_stream(self._streams[b])
         return recs
 
-    def solve(self, hessian, g, jac):
+    def _options(self, recycles, init):
+        """Stop rules per sample (bilevel.py:264-276) and the solve options."""
         cfg = self.cfg
-        g = as_device(g)
-        single = g.dim() == 1
-        B = 1 if single else g.shape[0]
-        n = hessian.dim
-        if cfg.strategy.is_none or self._first:
-            recycles = [RecycleSpace.empty(n) for _ in range(B)]
-        else:
-            recycles = self._recycle_all(hessian, jac, B)
-        self._first = False
         rules = []
         for rec in recycles:
             if cfg.stop == "nsc" and rec.nsc_data is not None:
                 rules.append(NscRule(cfg.delta, rec.nsc_data))
             else:  # res, or nsc on the first system (bilevel.py:269-273)
                 rules.append(ResidualNormRule(cfg.delta))
-        init = self._prev_solution if cfg.warm_start else None
-        opts = SolveOptions(max_iter=cfg.max_iter, stop_rule=rules if B > 1 else rules[0],
+        return SolveOptions(max_iter=cfg.max_iter, stop_rule=rules if len(rules) > 1 else rules[0],
                             track_basis=self._needs_basis(), initial_guess=init)
+
+    def solve(self, hessian, g, jac):
+        cfg = self.cfg
+        g = as_device(g)
+        single = g.dim() == 1
+        B = 1 if single else g.shape[0]
+        n = hessian.dim
+        # one batched solve for all samples: the persistent kernel is latency bound per
+        # iteration, so a launch over 8 samples costs what one over 4 does
+        if cfg.strategy.is_none or self._first:
+            recycles = [RecycleSpace.empty(n) for _ in range(B)]
+        else:
+            recycles = self._recycle_all(hessian, jac, B)
+        self._first = False
+        init = self._prev_solution if cfg.warm_start else None
         solve = rminres if cfg.method == "minres" else rcg
-        results = solve(hessian, g, recycles if B > 1 else recycles[0], opts)
+        results = solve(hessian, g, recycles if B > 1 else recycles[0], self._options(recycles, init))
         res_list = [results] if single else results
         self._prev_basis = [r.basis for r in res_list]
         self._prev_recycle = recycles

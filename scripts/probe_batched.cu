@@ -50,6 +50,36 @@ int main(int argc, char** argv) {
     CK(cublasDgemmStridedBatched(hb, CUBLAS_OP_T, CUBLAS_OP_N, T, T, n, &one, A, n, (long long)n * T, A, n,
                                  (long long)n * T, &zero, G, T, (long long)T * T, B));
   });
+  double* Gp;
+  CK(cudaMalloc(&Gp, (size_t)T * T * B * 16 * 8));
+  for (int S : {2, 4, 8, 16}) {
+    char nm[96];
+    snprintf(nm, sizeof nm, "gram split-K S=%d (per-sample strided batch)", S);
+    const int c = n / S;
+    timeit(nm, [&] {
+      for (int b = 0; b < B; ++b)
+        CK(cublasDgemmStridedBatched(hb, CUBLAS_OP_T, CUBLAS_OP_N, T, T, c, &one, A + (size_t)b * n * T, n, c,
+                                     A + (size_t)b * n * T, n, c, &zero, Gp + (size_t)b * S * T * T, T,
+                                     (long long)T * T, S));
+    });
+    std::vector<const double*> pa(B * S), pb(B * S);
+    std::vector<double*> pc(B * S);
+    for (int b = 0; b < B; ++b)
+      for (int s = 0; s < S; ++s) {
+        pa[b * S + s] = A + (size_t)b * n * T + (size_t)s * c;
+        pc[b * S + s] = Gp + ((size_t)b * S + s) * T * T;
+      }
+    const double** dpa;
+    double** dpc;
+    CK(cudaMalloc(&dpa, B * S * 8));
+    CK(cudaMalloc(&dpc, B * S * 8));
+    CK(cudaMemcpy(dpa, pa.data(), B * S * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dpc, pc.data(), B * S * 8, cudaMemcpyHostToDevice));
+    snprintf(nm, sizeof nm, "gram split-K S=%d (pointer-array batch %d)", S, B * S);
+    timeit(nm, [&] {
+      CK(cublasDgemmBatched(hb, CUBLAS_OP_T, CUBLAS_OP_N, T, T, c, &one, dpa, n, dpa, n, &zero, dpc, T, B * S));
+    });
+  }
   timeit("gram dsyrk loop (8 calls)", [&] {
     for (int b = 0; b < B; ++b)
       CK(cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, T, n, &one, A + (size_t)b * n * T, n, &zero,

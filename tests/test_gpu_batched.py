@@ -267,3 +267,16 @@ def test_qrcp_small_matches_scipy_pivoted_qr():
         Pk = Qa @ Qa.T
         Pr = Qs[:, :r] @ Qs[:, :r].T
         assert np.linalg.norm(Pk - Pr) <= 1e-7
+
+
+@pytest.mark.parametrize("B,T,n", [(1, 7, 5000), (4, 220, 16384), (3, 33, 12288 + 7)])
+def test_gram_split_k(B, T, n):
+    from paper_2412_08264_b200.batched import gram
+
+    g = torch.Generator(device="cuda").manual_seed(B + T)
+    A = torch.randn(B, T, n, generator=g, dtype=torch.float64, device="cuda")
+    Bm = torch.randn(B, T, n, generator=g, dtype=torch.float64, device="cuda")
+    ref = A @ Bm.transpose(1, 2)
+    got = gram(A, Bm)
+    assert torch.allclose(got, ref, rtol=0, atol=1e-11 * float(ref.abs().max()))
+    assert torch.equal(gram(A, Bm), got)  # deterministic
