@@ -443,10 +443,12 @@ constexpr int JW_CHUNK = 256;  // columns per pass (bounds the workspace)
 template <int Q>
 __global__ void __launch_bounds__(NT) jw_conv_kernel(kr_op op, int b, const double* __restrict__ W, int64_t ldw,
                                                     double* __restrict__ Y, double* __restrict__ hpart) {
+  // one block per (tile, column): the input region is staged once and reused by
+  // all J filters (the J filter loop was a grid dimension -- J region loads)
   constexpr int R = Q / 2, RW = TW + 2 * R, RH = TH + 2 * R, RB = TPX / NT;
   __shared__ double sw[RH * RW];
-  __shared__ double red[1 * 33 + 1];
-  const int tile = blockIdx.x, c = blockIdx.y, j = blockIdx.z, nc = gridDim.y, ntiles = gridDim.x;
+  __shared__ double red[8 * 33 + 8];
+  const int tile = blockIdx.x, c = blockIdx.y, nc = gridDim.y, ntiles = gridDim.x;
   const int J = op.num_filters;
   const int tyc = tiles_x(op);
   const int y0 = (tile / tyc) * TH, x0 = (tile % tyc) * TW;
@@ -457,48 +459,61 @@ __global__ void __launch_bounds__(NT) jw_conv_kernel(kr_op op, int b, const doub
     int y = y0 - R + rr, x = x0 - R + cc;
     sw[i] = (y >= 0 && y < op.rows && x >= 0 && x < op.cols) ? w[(int64_t)y * op.cols + x] : 0.0;
   }
-  double k[Q][Q];
-  const double* kj = op.kernels + j * Q * Q;
-#pragma unroll
-  for (int a = 0; a < Q; ++a)
-#pragma unroll
-    for (int bb = 0; bb < Q; ++bb) k[a][bb] = kj[a * Q + bb];
   block_barrier();
   const int tx = threadIdx.x % TW, r0 = (threadIdx.x / TW) * RB;
-  double acc[RB];
-#pragma unroll
-  for (int i = 0; i < RB; ++i) acc[i] = 0.0;
-#pragma unroll
-  for (int sr = 0; sr < RB + Q - 1; ++sr) {
-    const double* src = sw + (r0 + sr) * RW + tx + 2 * R;
-    double v[Q];
-#pragma unroll
-    for (int bb = 0; bb < Q; ++bb) v[bb] = src[-bb];
-#pragma unroll
-    for (int i = 0; i < RB; ++i) {
-      const int a = i + Q - 1 - sr;  // output row r0+i reads region row r0+i+2R-a
-      if (a >= 0 && a < Q) {
-#pragma unroll
-        for (int bb = 0; bb < Q; ++bb) acc[i] = fma(k[a][bb], v[bb], acc[i]);
-      }
-    }
-  }
   const bool quad = op.potential == KR_POT_QUADRATIC;
-  const double* sl = op.slope + ((int64_t)b * J + j) * n;
-  const double* cv = quad ? nullptr : op.curv + ((int64_t)b * J + j) * n;
-  double* yo = Y + ((int64_t)j * nc + c) * n;
-  double head[1] = {0.0};
+  for (int j0 = 0; j0 < J; j0 += 8) {
+    double head[8];
 #pragma unroll
-  for (int i = 0; i < RB; ++i) {
-    int y = y0 + r0 + i, x = x0 + tx;
-    if (y < op.rows && x < op.cols) {
-      int64_t p = (int64_t)y * op.cols + x;
-      head[0] = fma(sl[p], acc[i], head[0]);
-      yo[p] = (quad ? 2.0 : cv[p]) * acc[i];
+    for (int jj = 0; jj < 8; ++jj) head[jj] = 0.0;
+    for (int jj = 0; jj < 8 && j0 + jj < J; ++jj) {
+      const int j = j0 + jj;
+      double k[Q][Q];
+      const double* kj = op.kernels + j * Q * Q;
+#pragma unroll
+      for (int a = 0; a < Q; ++a)
+#pragma unroll
+        for (int bb = 0; bb < Q; ++bb) k[a][bb] = kj[a * Q + bb];
+      double acc[RB];
+#pragma unroll
+      for (int i = 0; i < RB; ++i) acc[i] = 0.0;
+#pragma unroll
+      for (int sr = 0; sr < RB + Q - 1; ++sr) {
+        const double* src = sw + (r0 + sr) * RW + tx + 2 * R;
+        double v[Q];
+#pragma unroll
+        for (int bb = 0; bb < Q; ++bb) v[bb] = src[-bb];
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+          const int a = i + Q - 1 - sr;  // output row r0+i reads region row r0+i+2R-a
+          if (a >= 0 && a < Q) {
+#pragma unroll
+            for (int bb = 0; bb < Q; ++bb) acc[i] = fma(k[a][bb], v[bb], acc[i]);
+          }
+        }
+      }
+      const double* sl = op.slope + ((int64_t)b * J + j) * n;
+      const double* cv = quad ? nullptr : op.curv + ((int64_t)b * J + j) * n;
+      double* yo = Y + ((int64_t)j * nc + c) * n;
+      double h = 0.0;
+#pragma unroll
+      for (int i = 0; i < RB; ++i) {
+        int y = y0 + r0 + i, x = x0 + tx;
+        if (y < op.rows && x < op.cols) {
+          int64_t p = (int64_t)y * op.cols + x;
+          h = fma(sl[p], acc[i], h);
+          yo[p] = (quad ? 2.0 : cv[p]) * acc[i];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q == jj) head[q] = h;
     }
+    block_sum<8>(head, red);
+    if (threadIdx.x < 8 && j0 + threadIdx.x < J)
+      hpart[((int64_t)(j0 + threadIdx.x) * nc + c) * ntiles + tile] = red[threadIdx.x];
+    block_barrier();
   }
-  block_sum<1>(head, red);
-  if (threadIdx.x == 0) hpart[((int64_t)j * nc + c) * ntiles + tile] = red[0];
 }
 
 // Phi[j][d][p] = phi'_j(p + delta_d) (j < J), Xs[d][p] = xhat(p - delta_d) (j == J); zero outside.
@@ -597,7 +612,7 @@ static int jadj_gemm(const kr_op& op, const double* W, int64_t ldw, int64_t bsw,
       kr_op opv = op;
       int bb = b;
       void* args[] = {&opv, &bb, (void*)&Wc, &ldw, &Y, &hpart};
-      cudaError_t e = cudaLaunchKernel(conv, dim3(ntiles, nc, J), dim3(NT), args, 0, st);
+      cudaError_t e = cudaLaunchKernel(conv, dim3(ntiles, nc), dim3(NT), args, 0, st);
       if (e != cudaSuccess) return fail(KR_ECUDA, std::string("jw_conv launch: ") + cudaGetErrorString(e));
       // split-K over pixel chunks: G1[kc] = Phi[kc rows]^T W[kc rows]  ((J q2) x nc)
       //                            G2[kc] = Xs[kc rows]^T Y[kc rows]   (q2 x (J nc))
