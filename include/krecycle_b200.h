@@ -200,6 +200,10 @@ int kr_chol_inv(const double* G, int64_t ldg, int64_t bsg, const int32_t* dims, 
  * work: batch*tmax doubles. */
 int kr_qrcp_small(double* M, const int32_t* dims, int32_t batch, int32_t tmax, double rtol, double* Q,
                   int32_t* rank, int32_t* perm, double* work, int64_t work_len, kr_stream_t stream);
+/* Same contract, one 4-CTA thread-block cluster per matrix: the columns stay in the
+ * CTAs' shared memory and the pivot / reflector exchange goes over DSMEM. */
+int kr_qrcp_small_cluster(double* M, const int32_t* dims, int32_t batch, int32_t tmax, double rtol, double* Q,
+                          int32_t* rank, int32_t* perm, double* work, int64_t work_len, kr_stream_t stream);
 
 /* Batched Gram of row blocks: G_b[i][j] = a_i . b_j (row-major G, ldg, bsg) for
  * A_b, B_b given as `rows` rows of length n (row stride ld, batch stride bs) -- the

@@ -93,6 +93,8 @@ def _declare(lib):
                                  _c_p, _c_p, _c_p, _c_p]),
         "kr_qrcp_small": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, ctypes.c_double, _c_p, _c_p, _c_p, _c_p, _c_i64,
                                    _c_p]),
+        "kr_qrcp_small_cluster": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, ctypes.c_double, _c_p, _c_p, _c_p, _c_p,
+                                           _c_i64, _c_p]),
         "kr_gram_workspace": (_c_i64, [_c_i32, _c_i32, _c_i64]),
         "kr_gram": (_c_i32, [_c_p, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_i64,
                              _c_p]),
@@ -108,7 +110,8 @@ EXPORTED = (
     "kr_abi_version", "kr_last_error", "kr_device_info", "kr_struct_sizes", "kr_op_prepare",
     "kr_hvp", "kr_jadj_workspace", "kr_jadj", "kr_lower_workspace", "kr_lower_eval",
     "kr_rminres_workspace", "kr_rminres", "kr_cg_workspace", "kr_cg",
-    "kr_syev_select_workspace", "kr_syev_select", "kr_chol_inv", "kr_qrcp_small", "kr_gram_workspace", "kr_gram",
+    "kr_syev_select_workspace", "kr_syev_select", "kr_chol_inv", "kr_qrcp_small", "kr_qrcp_small_cluster",
+    "kr_gram_workspace", "kr_gram",
 )
 
 

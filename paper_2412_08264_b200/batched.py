@@ -54,6 +54,9 @@ def syev_select(M: torch.Tensor, dims: torch.Tensor, size: str, s: int):
 
 STATS: dict | None = None  # set to {} to count declined samples per check
 
+QRCP_CLUSTER = True  # kr_qrcp_small_cluster (4 CTAs per matrix, columns in shared memory)
+
+
 def qrcp_small(M: torch.Tensor, dims: torch.Tensor, rtol: float):
     """QR with column pivoting of the leading dims[b] blocks (kr_qrcp_small).
 
@@ -68,9 +71,9 @@ def qrcp_small(M: torch.Tensor, dims: torch.Tensor, rtol: float):
     perm = torch.empty(B, T, dtype=torch.int32, device=M.device)
     work = torch.empty(max(B * T, 1), dtype=torch.float64, device=M.device)
     dims = dims.to(device=M.device, dtype=torch.int32).contiguous()
-    _lib.check(_lib.lib().kr_qrcp_small(Mw.data_ptr(), dims.data_ptr(), B, T, float(rtol), Q.data_ptr(),
-                                        rank.data_ptr(), perm.data_ptr(), work.data_ptr(), work.numel(),
-                                        _lib.stream_ptr()), "kr_qrcp_small")
+    fn = _lib.lib().kr_qrcp_small_cluster if QRCP_CLUSTER else _lib.lib().kr_qrcp_small
+    _lib.check(fn(Mw.data_ptr(), dims.data_ptr(), B, T, float(rtol), Q.data_ptr(), rank.data_ptr(), perm.data_ptr(),
+                  work.data_ptr(), work.numel(), _lib.stream_ptr()), "kr_qrcp_small")
     _lib.note_launch("kr_qrcp_small")
     idx = perm.clamp_min(0).long()
     R = torch.gather(Mw, 1, idx.unsqueeze(2).expand(B, T, T))

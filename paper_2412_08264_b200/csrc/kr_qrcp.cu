@@ -240,3 +240,280 @@ extern "C" int kr_qrcp_small(double* M, const int32_t* dims, int32_t batch, int3
   qrcp_kernel<<<batch, QNT, 0, (cudaStream_t)stream>>>(P);
   return check_launch("qrcp_kernel");
 }
+
+// ---------------------------------------------------------------------------
+// Cluster version: QNC CTAs per matrix, column g owned by CTA g % QNC (slot
+// g / QNC) and resident in that CTA's shared memory for the whole factorization.
+// Per pivot step: each CTA's best remaining column -> exchanged over DSMEM ->
+// the same pivot everywhere (largest norm, lowest current position on ties);
+// the owner forms the Householder vector; every CTA reads it over DSMEM and
+// updates its own resident columns (exact trailing norms from the same pass).
+// Two cluster barriers per step and no global-memory traffic.  Q_R is then
+// accumulated with its columns distributed the same way (reflectors from L2).
+
+#include <cooperative_groups.h>
+
+namespace kr {
+namespace {
+
+namespace cgc = cooperative_groups;
+constexpr int QNC = 4;                    // CTAs per matrix
+constexpr int QCN = 256;                  // threads per CTA
+constexpr int QCW = QCN / 32;
+constexpr int QCOLS = (256 + QNC - 1) / QNC;  // resident columns per CTA (t <= 256)
+
+struct QcShared {
+  double cand_v;   // this CTA's best remaining norm^2
+  int cand_g;      // its global column (-1: none)
+  int cand_pos;    // its current position
+  double beta, tau;
+  int rank;
+};
+
+__global__ void __cluster_dims__(QNC, 1, 1) __launch_bounds__(QCN, 1) qrcp_cluster_kernel(QrcpParams P) {
+  extern __shared__ double csm[];
+  cgc::cluster_group cluster = cgc::this_cluster();
+  const int cr = (int)cluster.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.x / QNC, t = P.dims[b], T = P.T;
+  double* cols = csm;                       // [QCOLS][T] resident columns
+  double* vb = cols + (int64_t)QCOLS * T;   // [T] Householder vector of the current step (owner's copy)
+  double* vl = vb + T;                      // [T] local copy
+  __shared__ double cn[QCOLS];              // trailing norms^2 of the resident columns
+  __shared__ int done[QCOLS];               // already pivoted
+  __shared__ int pos[256];                  // current position of every global column (replicated)
+  __shared__ int at[256];                   // global column at every position (replicated)
+  __shared__ QcShared sh;
+  double* M = P.M + (int64_t)b * T * T;
+  const int nloc = (t - cr + QNC - 1) / QNC;  // columns g = cr + QNC * l, l < nloc
+  for (int l = warp; l < nloc; l += QCW) {
+    const int g = cr + QNC * l;
+    const double* src = M + (int64_t)g * T;
+    double s = 0.0;
+    for (int i = lane; i < t; i += 32) {
+      const double x = src[i];
+      cols[(int64_t)l * T + i] = x;
+      s += x * x;
+    }
+    s = warp_sum(s);
+    if (lane == 0) {
+      cn[l] = s;
+      done[l] = 0;
+    }
+  }
+  for (int g = tid; g < t; g += QCN) {
+    pos[g] = g;
+    at[g] = g;
+  }
+  if (tid == 0) sh.rank = t;
+  __syncthreads();
+  cluster.sync();
+  double r00 = 0.0;
+  int rank = t;
+  for (int k = 0; k < t; ++k) {
+    // 1. this CTA's candidate (warp 0)
+    if (warp == 0) {
+      double best = -1.0;
+      int bg = -1, bp = 1 << 30;
+      for (int l = lane; l < nloc; l += 32) {
+        if (done[l]) continue;
+        const int g = cr + QNC * l, p = pos[g];
+        if (cn[l] > best || (cn[l] == best && p < bp)) {
+          best = cn[l];
+          bg = g;
+          bp = p;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int og = __shfl_xor_sync(0xffffffffu, bg, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+        if (ob > best || (ob == best && op < bp)) {
+          best = ob;
+          bg = og;
+          bp = op;
+        }
+      }
+      if (lane == 0) {
+        sh.cand_v = best;
+        sh.cand_g = bg;
+        sh.cand_pos = bp;
+      }
+    }
+    __syncwarp();
+    cluster.sync();
+    // 2. the cluster's pivot, decided identically in every CTA
+    double best = -1.0;
+    int pg = -1, pp = 1 << 30;
+    for (int r = 0; r < QNC; ++r) {
+      const QcShared* o = cluster.map_shared_rank(&sh, r);
+      const double v = o->cand_v;
+      const int g = o->cand_g, p = o->cand_pos;
+      if (g >= 0 && (v > best || (v == best && p < pp))) {
+        best = v;
+        pg = g;
+        pp = p;
+      }
+    }
+    // position bookkeeping (LAPACK's swap of positions k and pp)
+    __syncthreads();
+    if (tid == 0) {
+      const int gk = at[k];
+      at[pp] = gk;
+      pos[gk] = pp;
+      at[k] = pg;
+      pos[pg] = k;
+    }
+    const int owner = pg % QNC, lslot = pg / QNC;
+    // 3. the owner forms the Householder vector of its column pg (rows k..t)
+    if (cr == owner && warp == 0) {
+      double* cp = cols + (int64_t)lslot * T;
+      double x[QR];
+      double s = 0.0;
+#pragma unroll
+      for (int r = 0; r < QR; ++r) {
+        const int i = k + 1 + lane + 32 * r;
+        x[r] = i < t ? cp[i] : 0.0;
+        s += x[r] * x[r];
+      }
+      s = warp_sum(s);
+      const double alpha = cp[k];
+      double beta = alpha, tk = 0.0;
+      if (s > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + s), alpha);
+        tk = (beta - alpha) / beta;
+      }
+      const double scal = tk != 0.0 ? 1.0 / (alpha - beta) : 0.0;
+#pragma unroll
+      for (int r = 0; r < QR; ++r) {
+        const int i = k + 1 + lane + 32 * r;
+        if (i < t) {
+          const double v = x[r] * scal;
+          vb[i] = v;
+          cp[i] = v;
+        }
+      }
+      if (lane == 0) {
+        vb[k] = 1.0;
+        cp[k] = beta;
+        sh.beta = beta;
+        sh.tau = tk;
+        done[lslot] = 1;
+        P.tau[(int64_t)b * T + k] = tk;
+      }
+    }
+    __syncwarp();
+    cluster.sync();
+    // 4. everyone: beta/tau and v from the owner over DSMEM
+    const QcShared* os = cluster.map_shared_rank(&sh, owner);
+    const double beta = os->beta, tk = os->tau;
+    if (k == 0) r00 = fabs(beta);
+    if (fabs(beta) <= P.rtol * r00 || (k == 0 && r00 == 0.0)) {  // recycling.py:194 keep rule
+      rank = k;
+      break;
+    }
+    const double* ovb = cluster.map_shared_rank(vb, owner);
+    for (int i = k + tid; i < t; i += QCN) vl[i] = ovb[i];
+    __syncthreads();
+    // 5. apply H_k to the resident unpivoted columns; exact trailing norms
+    if (tk != 0.0) {
+      for (int l = warp; l < nloc; l += QCW) {
+        if (done[l]) continue;
+        double* cj = cols + (int64_t)l * T;
+        double c[QR];
+        double d = 0.0;
+#pragma unroll
+        for (int r = 0; r < QR; ++r) {
+          const int i = k + lane + 32 * r;
+          c[r] = i < t ? cj[i] : 0.0;
+          if (i < t) d += vl[i] * c[r];
+        }
+        d = tk * warp_sum(d);
+        double nn = 0.0;
+#pragma unroll
+        for (int r = 0; r < QR; ++r) {
+          const int i = k + lane + 32 * r;
+          if (i < t) {
+            c[r] -= d * vl[i];
+            cj[i] = c[r];
+            if (i > k) nn += c[r] * c[r];
+          }
+        }
+        nn = warp_sum(nn);
+        if (lane == 0) cn[l] = nn;
+      }
+    } else {
+      for (int l = warp; l < nloc; l += QCW) {
+        if (done[l]) continue;
+        const double* cj = cols + (int64_t)l * T;
+        double nn = 0.0;
+        for (int i = k + 1 + lane; i < t; i += 32) nn += cj[i] * cj[i];
+        nn = warp_sum(nn);
+        if (lane == 0) cn[l] = nn;
+      }
+    }
+    __syncthreads();
+  }
+  // write back the resident columns (R_piv above the diagonal, reflectors below)
+  for (int l = warp; l < nloc; l += QCW) {
+    const int g = cr + QNC * l;
+    double* dst = M + (int64_t)g * T;
+    for (int i = lane; i < t; i += 32) dst[i] = cols[(int64_t)l * T + i];
+  }
+  if (cr == 0) {
+    if (tid == 0) P.rank[b] = rank;
+    if (P.perm)
+      for (int j = tid; j < T; j += QCN) P.perm[(int64_t)b * T + j] = j < t ? at[j] : -1;
+  }
+  __syncthreads();
+  cluster.sync();  // every CTA's columns and tau are in global memory (cluster-scope release/acquire)
+  // Q_R[:, :r]: logical column j held by CTA j % QNC in the columns area
+  const int r = rank;
+  double* Qb = P.Q + (int64_t)b * T * T;
+  const int qloc = (r - cr + QNC - 1) / QNC;  // Q columns j = cr + QNC * l, l < qloc
+  for (int l = warp; l < QCOLS; l += QCW)
+    for (int i = lane; i < T; i += 32) cols[(int64_t)l * T + i] = (l < qloc && i == cr + QNC * l) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int kk = r - 1; kk >= 0; --kk) {
+    const double tk = P.tau[(int64_t)b * T + kk];
+    if (tk == 0.0) continue;
+    const double* vk = M + (int64_t)at[kk] * T;  // reflector kk below the diagonal of pivot column kk
+    for (int i = kk + 1 + tid; i < t; i += QCN) vl[i] = vk[i];
+    if (tid == 0) vl[kk] = 1.0;
+    __syncthreads();
+    for (int l = warp; l < qloc; l += QCW) {
+      const int j = cr + QNC * l;
+      if (j < kk) continue;
+      double* qj = cols + (int64_t)l * T;
+      double d = 0.0;
+      for (int i = kk + lane; i < t; i += 32) d += vl[i] * qj[i];
+      d = tk * warp_sum(d);
+      for (int i = kk + lane; i < t; i += 32) qj[i] -= d * vl[i];
+    }
+    __syncthreads();
+  }
+  for (int j = cr; j < T; j += QNC) {
+    const int l = (j - cr) / QNC;
+    double* dst = Qb + (int64_t)j * T;
+    for (int i = tid; i < T; i += QCN) dst[i] = (j < r) ? cols[(int64_t)l * T + i] : 0.0;
+  }
+}
+
+}  // namespace
+}  // namespace kr
+
+extern "C" int kr_qrcp_small_cluster(double* M, const int32_t* dims, int32_t batch, int32_t tmax, double rtol,
+                                     double* Q, int32_t* rank, int32_t* perm, double* work, int64_t work_len,
+                                     kr_stream_t stream) {
+  using namespace kr;
+  KR_CHECK_ARG(batch >= 0 && tmax >= 0 && tmax <= 256, "kr_qrcp_small: t must be in [0, 256]");
+  KR_CHECK_ARG(work_len >= (int64_t)batch * tmax, "workspace too small");
+  if (batch == 0) return KR_OK;
+  KR_CHECK_ARG(M && dims && Q && rank && work, "null pointer");
+  QrcpParams P{M, dims, tmax, rtol, Q, rank, perm, work};
+  const size_t smem = ((size_t)QCOLS * tmax + 2 * (size_t)tmax) * sizeof(double);
+  KR_TRY(ensure_smem((const void*)qrcp_cluster_kernel, smem));
+  qrcp_cluster_kernel<<<batch * QNC, QCN, smem, (cudaStream_t)stream>>>(P);
+  return check_launch("qrcp_cluster_kernel");
+}

@@ -229,14 +229,17 @@ def test_chol_inv_kernel_matches_torch(T, monkeypatch):
             assert torch.allclose(F[good], Ft[good], rtol=1e-9, atol=1e-12 * float(Ft[good].abs().max()))
 
 
-def test_qrcp_small_matches_scipy_pivoted_qr():
+@pytest.mark.parametrize("cluster", [True, False])
+def test_qrcp_small_matches_scipy_pivoted_qr(cluster, monkeypatch):
     """kr_qrcp_small on R against scipy.linalg.qr(A, pivoting=True), the reference's
     candidate-basis QR (recycling.py:187-199): same pivots, |R_kk|, rank under the
     1e-10 rule, and the same kept span."""
     import scipy.linalg as sl
 
+    from paper_2412_08264_b200 import batched
     from paper_2412_08264_b200.batched import qrcp_small
 
+    monkeypatch.setattr(batched, "QRCP_CLUSTER", cluster)
     rng = np.random.default_rng(17)
     mats = []
     for t in (1, 5, 40, 120, 220):
