@@ -309,7 +309,7 @@ struct CgLayout {
 void cg_plan(const kr_op& op, const kr_solve_args& a, CgLayout& L) {
   const int64_t n = op_n(op);
   Geom g = make_geom(op);
-  L.smem = sizeof(double) * ((size_t)g.total + MAX_SLOTS + MAX_NSC + 2 * MAX_S + 16 * 33 + 16);
+  L.smem = sizeof(double) * ((size_t)g.total + MAX_SLOTS + MAX_NSC + 2 * MAX_S + RED_DOUBLES);
   int sms = device_sms(), per_sm = 0;
   if (sms > 0) {
     if (L.smem > 48 * 1024)

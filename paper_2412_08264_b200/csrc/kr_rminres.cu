@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
   double* btc2 = btc1 + MAX_S;
   double* omega = btc2 + MAX_S;
   double* nscv = omega + MAX_S;          // MAX_NSC
-  double* red = nscv + MAX_NSC;          // 8*33+8
+  double* red = nscv + MAX_NSC;          // RED_DOUBLES
 #ifdef KR_VOLATILE_SC
   __shared__ volatile Scalars sc;
 #else
@@ -377,13 +377,21 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
       for (int i = threadIdx.x; i < 2 * s + 1; i += blockDim.x) slot_acc[i] = 0.0;
       block_barrier();
       double* hvk = vec(P.w.hv[k & 1], n, b);
+      const int npass = s > 0 ? (s + 7) / 8 : 1;
+      const bool deferred = npass <= DEF_PASSES;
+      if (deferred) {  // warp sums accumulate in red over passes and tiles
+        for (int i = threadIdx.x; i < npass * 17 * DEF_STRIDE; i += blockDim.x) red[i] = 0.0;
+        block_barrier();
+      }
       for (int tile = j; tile < ntiles; tile += P.Gs) {
         tile_hvp_t<Q>(op, g, sm, b, TileIn{tmp, beta_k, nullptr, 0.0}, tile);
         for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
           int64_t p = tile_pixel(op, tile, l);
           if (p >= 0) hvk[p] = sm.res[l];
         }
-        // partials over this tile: C^T hv, C^T v and v . hv (alpha = v.hv - (C^T v).(C^T hv))
+        // partials over this tile: C^T hv, C^T v and v . hv (alpha = v.hv - (C^T v).(C^T hv)),
+        // 8 columns per pass; with <= DEF_PASSES passes the warp sums stay in registers
+        // (accumulated over the block's tiles) and are combined once after the tile loop
         for (int base = 0; base < (s > 0 ? s : 1); base += 8) {
           double v16[17];
 #pragma unroll
@@ -408,6 +416,10 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
                 v16[8 + i] += c * v;
               }
           }
+          if (deferred) {
+            def_add<17>(MultiSum<17>::reduce(v16, threadIdx.x & 31), base / 8, red);
+            continue;
+          }
           block_sum<17>(v16, red);
           if (threadIdx.x < 8 && base + threadIdx.x < s) {
             slot_acc[base + threadIdx.x] += red[threadIdx.x];
@@ -416,6 +428,15 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
           if (threadIdx.x == 0 && base == 0) slot_acc[2 * s] += red[16];
           block_barrier();
         }
+        block_barrier();
+      }
+      if (deferred) {
+        // value (pass q, i): i < 8 -> C^T hv column 8q+i, 8..15 -> C^T v column 8q+i-8, 16 (q = 0) -> v.hv
+        for (int c = threadIdx.x; c < s; c += blockDim.x) {
+          slot_acc[c] = def_sum(red, (c / 8) * 17 + c % 8);
+          slot_acc[s + c] = def_sum(red, (c / 8) * 17 + 8 + c % 8);
+        }
+        if (threadIdx.x == 0) slot_acc[2 * s] = def_sum(red, 16);
         block_barrier();
       }
       write_partials(PP, bl, j, SL_CHV, 2 * s, slot_acc);
@@ -540,7 +561,7 @@ struct Layout {
 int plan(const kr_op& op, const kr_solve_args& a, Layout& L) {
   const int64_t n = op_n(op);
   Geom g = make_geom(op);
-  L.smem = sizeof(double) * ((size_t)g.total + MAX_SLOTS + 5 * MAX_S + MAX_NSC + 17 * 33 + 17);
+  L.smem = sizeof(double) * ((size_t)g.total + MAX_SLOTS + 5 * MAX_S + MAX_NSC + RED_DOUBLES);
   int sms = device_sms();
   int per_sm = 0;
   if (sms > 0) {

@@ -31,10 +31,58 @@ struct Partials {
   }
 };
 
+// Deferred cross-warp reductions.  A pass reduces NV per-thread values inside each
+// warp (MultiSum, no block barrier) and keeps the lane-owned warp sum in a register;
+// after all passes the warp sums go to smem (stride DEF_STRIDE per value) and ONE
+// barrier later each value is summed over the warps in warp order -- the same
+// order as block_sum, without a block barrier per pass.
+constexpr int DEF_PASSES = 4;   // passes kept in registers
+constexpr int DEF_STRIDE = 9;   // >= warps per block (8) + 1, odd: conflict-free
+constexpr int RED_DOUBLES = 640;  // reduction scratch: max(17 * 33 + 17, 17 * DEF_PASSES * DEF_STRIDE)
+
+template <int NV>
+__device__ inline void def_add(double r, int pass, double* red) {  // r: this lane's MultiSum<NV> result
+  using M = MultiSum<NV>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int idx = M::owner(lane);
+  if (idx < NV && (lane & ((32 / M::P) - 1)) == 0) red[(pass * NV + idx) * DEF_STRIDE + warp] += r;
+}
+
+__device__ inline double def_sum(const double* red, int v) {
+  const int nw = blockDim.x >> 5;
+  double acc = 0.0;
+  for (int w = 0; w < nw; ++w) acc += red[v * DEF_STRIDE + w];
+  return acc;
+}
+
 // acc_out[i] += sum_{p in [lo,hi)} A_i[p] * x(p), i < S; A_i = A + i*lda (16 columns per pass).
+// red needs 16 * DEF_PASSES * DEF_STRIDE doubles for the deferred path (S <= 64).
 template <typename XF>
 __device__ inline void slot_dots(const double* __restrict__ A, int64_t lda, int S, int64_t lo, int64_t hi,
                                  XF xf, double* acc_out, double* red) {
+  const int npass = (S + 15) / 16;
+  if (npass <= DEF_PASSES) {
+    block_barrier();  // red may still be read by an earlier reduction
+    for (int i = threadIdx.x; i < npass * 16 * DEF_STRIDE; i += blockDim.x) red[i] = 0.0;
+    block_barrier();
+    for (int pass = 0; pass < npass; ++pass) {
+      const int base = pass * 16;
+      double v16[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v16[i] = 0.0;
+      for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+        double x = xf(p);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (base + i < S) v16[i] += A[(int64_t)(base + i) * lda + p] * x;
+      }
+      def_add<16>(MultiSum<16>::reduce(v16, threadIdx.x & 31), pass, red);
+    }
+    block_barrier();
+    for (int i = threadIdx.x; i < S; i += blockDim.x) acc_out[i] += def_sum(red, i);
+    block_barrier();
+    return;
+  }
   for (int base = 0; base < S; base += 16) {
     double v16[16];
 #pragma unroll
