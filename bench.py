@@ -20,6 +20,7 @@ Multi-GPU (torchrun): weak scaling, each rank owns its own 8 samples
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -60,7 +61,9 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region through NVML
+    (in-process: no nvidia-smi fork of this large multi-threaded process, which
+    stalled the host threads that drive the GPU); nvidia-smi only if NVML is absent."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -70,18 +73,39 @@ class ClockSampler:
         self.rows = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._nv = self._h = None
+        try:  # import and initialise before the timed region, not inside it
+            import pynvml as nv
+
+            nv.nvmlInit()
+            self._h = nv.nvmlDeviceGetHandleByIndex(index)
+            self._nv = nv
+        except Exception:
+            self._nv = None
+
+    def _sample_nvml(self, nv, h):
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        flags = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                 nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        return [str(sm), str(mx)] + ["Active" if r & f else "Not Active" for f in flags]
 
     def _run(self):
+        nv, h = self._nv, self._h
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                parts = [p.strip() for p in out.stdout.strip().split(",")]
-                if len(parts) == 6:
-                    self.rows.append(parts)
+                if nv is not None:
+                    self.rows.append(self._sample_nvml(nv, h))
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                    parts = [p.strip() for p in out.stdout.strip().split(",")]
+                    if len(parts) == 6:
+                        self.rows.append(parts)
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t.start()
@@ -186,7 +210,11 @@ def run_ours(args):
     _lib.PROFILE = []
     evs = []
     iters = []
-    with ClockSampler(local) as clk:
+    # no cyclic-GC pauses inside timed regions (collect now, re-enable afterwards)
+    gc.collect()
+    gc.disable()
+    clk = ClockSampler(local)
+    with clk:
         dbg = os.environ.get("KR_BENCH_DEBUG")
         if dbg:
             from paper_2412_08264_b200 import batched as _bt
@@ -213,6 +241,7 @@ def run_ours(args):
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    gc.enable()
     launches = _lib.total_launches()
     prof = _lib.PROFILE
     _lib.PROFILE = None
@@ -253,6 +282,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        gc.collect()
+        gc.disable()
         t0 = time.perf_counter()
         for i in range(args.warmup, steps_total):
             X = pinned[i].to("cuda", non_blocking=True)
@@ -260,6 +291,7 @@ def run_ours(args):
             d.cpu()
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
+        gc.enable()
         if world > 1:
             t = torch.tensor([wall], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -481,5 +481,5 @@ def recycle_update(strategy, s: int, H, J, bases, recycles, reuse_products: bool
         nsc = None
         if mu is not None:
             nsc = NscData(values=mu[b, :sb], v_h=VH[b, :sb, : t[b]].T, w=W[b, : t[b]].T, z=Znsc[b, :sb].T)
-        out.append(RecycleSpace(U=U[b, :sb].T, C=C[b, :sb].T, nsc_data=nsc))
+        out.append(RecycleSpace(U=U[b, :sb].T, C=C[b, :sb].T, nsc_data=nsc, orthonormal=True))
     return out
