@@ -214,6 +214,43 @@ int64_t kr_gram_workspace(int32_t batch, int32_t rows, int64_t n);
 int kr_gram(const double* A, const double* B, int64_t ld, int64_t bs, int32_t batch, int32_t rows, int64_t n,
             double* G, int64_t ldg, int64_t bsg, double* work, int64_t work_len, kr_stream_t stream);
 
+/* Whole-batch recycle update (recycling.py:386-465 next_recycle for every sample of
+ * the batch at once; outer placement; RGen with size L -- rgen_select :316-359 +
+ * gsvd_pair :275-313 -- or Ritz -- ritz_select :226-236; prepare_recycle
+ * :362-383), orchestrated natively: candidate basis with the reference's pivoted-QR
+ * rank drop, H W / J W, the projected pencil, the selected eigenpairs, the new
+ * (U, C) and the NSC block Z = W V_H diag(mu).  `op` is the operator of the
+ * upcoming system with op->batch == batch.  Host arrays are marked HOST, the rest
+ * are DEVICE pointers.  status[b] = 0 done, 1 declined (the caller runs the
+ * per-sample reference path for sample b: W^T H W numerically singular, or a
+ * breakdown in the GSVD / prepare QR), 2 empty recycle space. */
+typedef struct kr_recycle_args {
+  int32_t batch, T, s;           /* samples; padded candidate count (<= 228); recycle dim */
+  int32_t vec_type;              /* 0 = Ritz, 1 = RGen */
+  int32_t size_code, side;       /* size S/L/M = 0/1/2 (RGen: L only); side R/L/M = 0/1/2 */
+  int32_t reuse_products;        /* H U~ = (H W) X_sel instead of s more H v */
+  const double* V;               /* previous Lanczos bases: sample b, column j at V + b*bs_v + j*ld_v */
+  int64_t ld_v, bs_v;
+  const int32_t* kdims;          /* HOST [batch] basis columns */
+  const double* Uprev;           /* previous U: sample b, column j at Uprev + b*bs_u + j*ld_u */
+  int64_t ld_u, bs_u;
+  const int32_t* sdims;          /* HOST [batch] previous recycle dims */
+  double* W;                     /* out [batch][T][n] candidate basis rows (orthonormal) */
+  double* HW;                    /* out [batch][T][n] H W */
+  double* U;                     /* out [batch][s][n] */
+  double* C;                     /* out [batch][s][n], C^T C = I */
+  double* mu;                    /* out [batch][s] selected mu (RGen) */
+  double* VH;                    /* out [batch][s][T] V_H columns as rows (RGen) */
+  double* Z;                     /* out [batch][s][n] Z = W V_H diag(mu) rows (RGen) */
+  int32_t* tdims;                /* HOST out [batch] candidates kept */
+  int32_t* nsel;                 /* HOST out [batch] recycle dims */
+  int32_t* status;               /* HOST out [batch] */
+} kr_recycle_args;
+
+int64_t kr_recycle_workspace(const kr_op* op, const kr_recycle_args* args);
+int kr_recycle_update(const kr_op* op, const kr_recycle_args* args, double* work, int64_t work_len,
+                      kr_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

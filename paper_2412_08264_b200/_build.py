@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB_NAME = os.environ.get("KR_LIB_NAME", "libkrecycle_b200.so")
-SOURCES = ["kr_capi.cu", "kr_ops.cu", "kr_rminres.cu", "kr_cg.cu", "kr_eig.cu", "kr_small.cu", "kr_qrcp.cu"]
+SOURCES = ["kr_capi.cu", "kr_ops.cu", "kr_rminres.cu", "kr_cg.cu", "kr_eig.cu", "kr_small.cu", "kr_qrcp.cu", "kr_recycle.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3"] + os.environ.get("KR_NVCC_FLAGS", "").split()
 
@@ -62,7 +62,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if failed:
         raise RuntimeError("nvcc failed:\n" + "\n".join(failed))
     tmp = out.with_suffix(".so.tmp")
-    link = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", str(tmp), "-lcublas",
+    link = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", str(tmp), "-lcublas", "-lcusolver",
             "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     res = subprocess.run(link, capture_output=True, text=True)
     if res.returncode != 0:

@@ -57,6 +57,19 @@ class KrSolveArgs(ctypes.Structure):
     ]
 
 
+class KrRecycleArgs(ctypes.Structure):
+    """Mirror of ``kr_recycle_args``."""
+
+    _fields_ = [
+        ("batch", _c_i32), ("T", _c_i32), ("s", _c_i32), ("vec_type", _c_i32), ("size_code", _c_i32),
+        ("side", _c_i32), ("reuse_products", _c_i32),
+        ("V", _c_p), ("ld_v", _c_i64), ("bs_v", _c_i64), ("kdims", _c_p),
+        ("Uprev", _c_p), ("ld_u", _c_i64), ("bs_u", _c_i64), ("sdims", _c_p),
+        ("W", _c_p), ("HW", _c_p), ("U", _c_p), ("C", _c_p), ("mu", _c_p), ("VH", _c_p), ("Z", _c_p),
+        ("tdims", _c_p), ("nsel", _c_p), ("status", _c_p),
+    ]
+
+
 class KrError(RuntimeError):
     pass
 
@@ -95,6 +108,8 @@ def _declare(lib):
                                    _c_p]),
         "kr_qrcp_small_cluster": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, ctypes.c_double, _c_p, _c_p, _c_p, _c_p,
                                            _c_i64, _c_p]),
+        "kr_recycle_workspace": (_c_i64, [P(KrOp), P(KrRecycleArgs)]),
+        "kr_recycle_update": (_c_i32, [P(KrOp), P(KrRecycleArgs), _c_p, _c_i64, _c_p]),
         "kr_gram_workspace": (_c_i64, [_c_i32, _c_i32, _c_i64]),
         "kr_gram": (_c_i32, [_c_p, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_i64,
                              _c_p]),
@@ -111,7 +126,7 @@ EXPORTED = (
     "kr_hvp", "kr_jadj_workspace", "kr_jadj", "kr_lower_workspace", "kr_lower_eval",
     "kr_rminres_workspace", "kr_rminres", "kr_cg_workspace", "kr_cg",
     "kr_syev_select_workspace", "kr_syev_select", "kr_chol_inv", "kr_qrcp_small", "kr_qrcp_small_cluster",
-    "kr_gram_workspace", "kr_gram",
+    "kr_gram_workspace", "kr_gram", "kr_recycle_workspace", "kr_recycle_update",
 )
 
 

@@ -18,6 +18,8 @@ from __future__ import annotations
 
 import ctypes
 
+import numpy as np
+
 import torch
 
 from . import _lib
@@ -482,4 +484,104 @@ def recycle_update(strategy, s: int, H, J, bases, recycles, reuse_products: bool
         if mu is not None:
             nsc = NscData(values=mu[b, :sb], v_h=VH[b, :sb, : t[b]].T, w=W[b, : t[b]].T, z=Znsc[b, :sb].T)
         out.append(RecycleSpace(U=U[b, :sb].T, C=C[b, :sb].T, nsc_data=nsc, orthonormal=True))
+    return out
+
+
+NATIVE_TMAX = 228
+
+
+def _uniform_rows(mats, n, dev):
+    """(ptr, ld, bs, keep) describing the n x k_b column blocks `mats` as one strided
+    batch when they already are one (views of the same solver buffer), else a copy."""
+    live = [(b, m) for b, m in enumerate(mats) if m is not None and m.shape[1] > 0]
+    if not live:
+        return 0, n, 0, None
+    ok = all(m.stride(0) == 1 and (m.shape[1] <= 1 or m.stride(1) == n) for _, m in live)
+    if ok and len(live) > 1:
+        (b0, m0), (b1, m1) = live[0], live[1]
+        bs = (m1.data_ptr() - m0.data_ptr()) // 8 // max(b1 - b0, 1)
+        ok = bs > 0 and all(m.data_ptr() == m0.data_ptr() + (b - b0) * bs * 8 for b, m in live)
+        if ok:
+            return m0.data_ptr() - b0 * bs * 8, n, bs, None
+    if ok and len(live) == 1:
+        b0, m0 = live[0]
+        return m0.data_ptr() - b0 * n * 8 * max(m0.shape[1], 1), n, n * max(m0.shape[1], 1), None
+    kmax = max(m.shape[1] for _, m in live)
+    buf = torch.zeros(len(mats), kmax, n, dtype=torch.float64, device=dev)
+    for b, m in live:
+        buf[b, : m.shape[1]] = m.T
+    return buf.data_ptr(), n, kmax * n, buf
+
+
+def recycle_update_native(strategy, s: int, H, J, bases, recycles, reuse_products: bool = True):
+    """``recycle_update`` through the native orchestrator ``kr_recycle_update`` (one
+    C-ABI call per batch: no Python per-op overhead, no GIL); same contract and
+    results.  Falls back to ``recycle_update`` beyond the kernels' t <= 228."""
+    from .recycling import RecycleSpace
+    from .stopping import NscData
+
+    if not supports(strategy):
+        raise ValueError(f"the batched recycle update covers outer RGen-L / Ritz, not {strategy}")
+    B = len(bases)
+    n = H.dim
+    k = [0 if V is None else int(V.shape[1]) for V in bases]
+    sp = [0 if r is None else int(r.dim) for r in recycles]
+    t = [a + c for a, c in zip(k, sp)]
+    T = max(t) if t else 0
+    if T == 0 or s == 0:
+        return [RecycleSpace.empty(n) for _ in range(B)]
+    if T > NATIVE_TMAX or s > T:
+        return recycle_update(strategy, s, H, J, bases, recycles, reuse_products)
+    dev = H.model.y.device if getattr(H, "model", None) is not None else bases[0].device
+    vptr, ldv, bsv, vkeep = _uniform_rows(list(bases), n, dev)
+    uptr, ldu, bsu, ukeep = _uniform_rows([None if r is None else r.U for r in recycles], n, dev)
+    a = _lib.KrRecycleArgs()
+    a.batch, a.T, a.s = B, T, s
+    a.vec_type = 1 if strategy.vec_type == "RGen" else 0
+    a.size_code = SIZE_CODES[strategy.size]
+    a.side = {"R": 0, "L": 1, "M": 2}.get(strategy.side or "R", 0)
+    a.reuse_products = int(reuse_products)
+    a.V, a.ld_v, a.bs_v = vptr, ldv, bsv
+    a.Uprev, a.ld_u, a.bs_u = uptr, ldu, bsu
+    kd = np.asarray(k, dtype=np.int32)
+    sd = np.asarray(sp, dtype=np.int32)
+    td = np.zeros(B, dtype=np.int32)
+    ns = np.zeros(B, dtype=np.int32)
+    stt = np.zeros(B, dtype=np.int32)
+    a.kdims, a.sdims = kd.ctypes.data, sd.ctypes.data
+    a.tdims, a.nsel, a.status = td.ctypes.data, ns.ctypes.data, stt.ctypes.data
+    f64 = dict(dtype=torch.float64, device=dev)
+    W = torch.empty(B, T, n, **f64)
+    HW = torch.empty(B, T, n, **f64)
+    U = torch.empty(B, s, n, **f64)
+    C = torch.empty(B, s, n, **f64)
+    mu = torch.zeros(B, s, **f64)
+    VH = torch.zeros(B, s, T, **f64)
+    Z = torch.empty(B, s, n, **f64)
+    a.W, a.HW, a.U, a.C = W.data_ptr(), HW.data_ptr(), U.data_ptr(), C.data_ptr()
+    a.mu, a.VH, a.Z = mu.data_ptr(), VH.data_ptr(), Z.data_ptr()
+    L = _lib.lib()
+    wl = int(L.kr_recycle_workspace(ctypes.byref(H.op), ctypes.byref(a)))
+    if wl < 0:
+        _lib.check(-1, "kr_recycle_workspace")
+    ws = torch.empty(max(wl, 1), **f64)
+    _lib.check(L.kr_recycle_update(ctypes.byref(H.op), ctypes.byref(a), ws.data_ptr(), wl, _lib.stream_ptr()),
+               "kr_recycle_update")
+    _lib.note_launch("kr_recycle_update", 40)
+    del vkeep, ukeep
+    if STATS is not None:
+        STATS["declined"] = STATS.get("declined", 0) + int((stt == 1).sum())
+        STATS["samples"] = STATS.get("samples", 0) + B
+    out = []
+    for b in range(B):
+        tb, sb = int(td[b]), int(ns[b])
+        if stt[b] == 2 or tb == 0 or sb == 0:
+            out.append(RecycleSpace.empty(n))
+        elif stt[b] == 1:
+            out.append(None)
+        else:
+            nsc = None
+            if strategy.vec_type == "RGen":
+                nsc = NscData(values=mu[b, :sb], v_h=VH[b, :sb, :tb].T, w=W[b, :tb].T, z=Z[b, :sb].T)
+            out.append(RecycleSpace(U=U[b, :sb].T, C=C[b, :sb].T, nsc_data=nsc, orthonormal=True))
     return out

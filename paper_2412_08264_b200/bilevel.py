@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 
 import torch
 
-from .batched import recycle_update, supports as batched_supports
+from .batched import recycle_update, recycle_update_native, supports as batched_supports
 from .krylov import SolveOptions, SolveResult, rcg, rminres
 from .operators import (DenseOperator, FoEParams, HessianOperator, ImageVector, InpaintingProblem, Model,
                         StencilJacobian, as_device, _foe_model)
@@ -126,6 +126,8 @@ class SequenceSolver:
         self.max_workers = 8
         self.batched_update = True
         self.groups = int(os.environ.get("KR_RECYCLE_GROUPS", "2"))
+        # the update orchestrated in C++ (kr_recycle_update); 0 = the torch orchestration
+        self.native_update = os.environ.get("KR_NATIVE_RECYCLE", "1") != "0"
         self._gstreams = None
         self._gpool = None
         self._streams = None
@@ -189,8 +191,9 @@ class SequenceSolver:
         def run(lo, hi):
             hs = hessian if (lo, hi) == (0, B) else hessian.slice(lo, hi)
             js = jac if (lo, hi) == (0, B) or jac is None else jac.slice(lo, hi)
-            recs = recycle_update(cfg.strategy, cfg.recycle_dim, hs, js, self._prev_basis[lo:hi],
-                                  self._prev_recycle[lo:hi], cfg.reuse_products)
+            update = recycle_update_native if self.native_update else recycle_update
+            recs = update(cfg.strategy, cfg.recycle_dim, hs, js, self._prev_basis[lo:hi],
+                          self._prev_recycle[lo:hi], cfg.reuse_products)
             # samples the batched path declined take the per-sample reference path
             return [r if r is not None else self._recycle_one(hessian, jac, B, lo + i) for i, r in enumerate(recs)]
 

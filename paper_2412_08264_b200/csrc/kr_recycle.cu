@@ -1,0 +1,619 @@
+// kr_recycle.cu -- the whole-batch recycle update, orchestrated natively.
+//
+// Same algorithm as paper_2412_08264_b200/batched.py::recycle_update (which stays
+// as the readable reference and the tests' comparison point), issued from C++:
+// no Python per-op overhead and no GIL, so the sample groups' host threads run
+// truly in parallel, and a host round trip only where a decision needs data
+// (shifted Cholesky QR, the pivoted rank drop, the Hessian-condition bracket).
+//
+// Layout: a block of R vectors of length L per sample is "rows" [B][R][L]; in
+// cuBLAS terms an L x R column-major matrix with ld L.  Samples carry t_b <= T
+// live rows, the rest zero; every Gram gets an identity pad block (kr_chol_inv),
+// so the leading t_b block of each factor is the per-sample factor.
+//
+// Steps (reference lines in recycling.py):
+//   1. A = [V_prev, U_prev] rows                                (:187-199)
+//   2. W = orth(A): CholQR2; shifted CholeskyQR3 where CholQR2 declines; where
+//      cond(A) may exceed 1e9, pivoted QR of the small R factor (kr_qrcp) with the
+//      reference's |R_kk| > 1e-10 |R_00| keep rule (Householder R where even
+//      shifted CholeskyQR3 is out of range)                    (:187-199)
+//   3. HW = H W, Ht = sym(W^T H W)                               (:226-236, :333-336)
+//   4. Ritz: s selected eigenpairs of Ht                         (:226-236)
+//      RGen: condition bracket of Ht (exact extremes only inside it) (:290-296);
+//            [Jt; Ht] = Q R (CholQR2), Q1^T Q1 = Z diag(alpha^2) Z^T for the s
+//            selected pairs, alpha / beta column norms, V_H, X = R^-1 Z  (:275-359)
+//   5. U~ = W X (or W V_H), H U~ = (H W) X, C R = H U~, U = U~ R^-1  (:362-383)
+//   6. Z = W V_H diag(mu) for the NSC rule                      (stopping.py:69-72)
+
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "kr_common.cuh"
+#include "kr_internal.h"
+
+extern "C" {
+int64_t kr_gram_workspace(int32_t batch, int32_t rows, int64_t n);
+int kr_gram(const double* A, const double* B, int64_t ld, int64_t bs, int32_t batch, int32_t rows, int64_t n,
+            double* G, int64_t ldg, int64_t bsg, double* work, int64_t work_len, kr_stream_t stream);
+int kr_chol_inv(const double* G, int64_t ldg, int64_t bsg, const int32_t* dims, int32_t batch, int32_t tmax,
+                int32_t flags, const double* shift, double* F, int64_t ldf, int64_t bsf, double* stats,
+                int32_t* info, uint8_t* skipped, kr_stream_t stream);
+int64_t kr_syev_select_workspace(int32_t batch, int32_t tmax);
+int kr_syev_select(const double* A, int64_t lda, int64_t bsa, const int32_t* dims, int32_t batch, int32_t tmax,
+                   int32_t size_code, int32_t s, double* lam, int64_t bsl, double* Z, int64_t ldz, int64_t bsz,
+                   int32_t* nsel, double* work, int64_t work_len, kr_stream_t stream);
+int kr_qrcp_small_cluster(double* M, const int32_t* dims, int32_t batch, int32_t tmax, double rtol, double* Q,
+                          int32_t* rank, int32_t* perm, double* work, int64_t work_len, kr_stream_t stream);
+}
+
+namespace kr {
+namespace {
+
+constexpr double CHOLQR_TOL = 1e-7;   // recycling.CHOLQR_TOL
+constexpr double RANK_TOL = 1e-10;    // recycling.RANK_TOL (recycling.py:194)
+constexpr double PIVOT_COND = 1e9;    // below: pivoted QR keeps every column
+constexpr double SHIFT_COND_MAX = 1e14;
+constexpr double COND_LIMIT = 1e12;   // recycling.py:291
+constexpr int RC_TMAX = 228;
+
+// ---------------------------------------------------------------- small kernels
+
+// A[b][j] = V_b[j] (j < k_b), U_b[j - k_b] (j < k_b + s_b), 0 otherwise
+__global__ void gather_rows_kernel(const double* V, int64_t ld_v, int64_t bs_v, const int32_t* kd, const double* U,
+                                   int64_t ld_u, int64_t bs_u, const int32_t* sd, double* A, int T, int64_t n) {
+  const int j = blockIdx.x, b = blockIdx.y;
+  const int k = kd[b], s = sd[b];
+  const double* src = j < k ? V + b * bs_v + (int64_t)j * ld_v
+                            : (j < k + s ? U + b * bs_u + (int64_t)(j - k) * ld_u : nullptr);
+  double* dst = A + ((int64_t)b * T + j) * n;
+  for (int64_t p = threadIdx.x; p < n; p += blockDim.x) dst[p] = src ? src[p] : 0.0;
+}
+
+// out[b] = sum of squares of rows x cols block b (rows of length `cols`, row stride ld)
+__global__ void frob2_kernel(const double* X, int rows, int64_t cols, int64_t ld, int64_t bs, double* out) {
+  const int b = blockIdx.x;
+  double s = 0.0;
+  const double* Xb = X + b * bs;
+  for (int r = 0; r < rows; ++r)
+    for (int64_t e = threadIdx.x; e < cols; e += blockDim.x) {
+      const double v = Xb[r * ld + e];
+      s += v * v;
+    }
+  __shared__ double red[8 * 33 + 8];
+  double v1[1] = {s};
+  block_sum<1>(v1, red);
+  if (threadIdx.x == 0) out[b] = red[0];
+}
+
+// out[b] = trace of the T x T block b (= ||A_b||_F^2 for a Gram G_b = A_b A_b^T)
+__global__ void trace_kernel(const double* G, int T, double* out) {
+  const int b = blockIdx.x;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < T; i += blockDim.x) s += G[(int64_t)b * T * T + (int64_t)i * (T + 1)];
+  __shared__ double red[8 * 33 + 8];
+  double v1[1] = {s};
+  block_sum<1>(v1, red);
+  if (threadIdx.x == 0) out[b] = red[0];
+}
+
+// Hs = (Ht + Ht^T)/2 (separate output: other blocks read the transposed entries);
+// S rows [b][j] = [Jt[b][j][0..p) , Hs[b][j][0..T)]
+__global__ void sym_and_s_kernel(const double* Ht, const double* Jt, int p, int T, double* Hs, double* S) {
+  const int b = blockIdx.y, j = blockIdx.x;
+  const double* H = Ht + (int64_t)b * T * T;
+  double* sr = S ? S + ((int64_t)b * T + j) * (p + T) : nullptr;
+  for (int i = threadIdx.x; i < T; i += blockDim.x) {
+    const double v = 0.5 * (H[(int64_t)j * T + i] + H[(int64_t)i * T + j]);
+    Hs[((int64_t)b * T + j) * T + i] = v;
+    if (sr) sr[p + i] = v;
+  }
+  if (sr)
+    for (int i = threadIdx.x; i < p; i += blockDim.x) sr[i] = Jt[((int64_t)b * T + j) * p + i];
+}
+
+// GSVD epilogue: Y rows [b][q][0..p+T): alpha = ||Y[:p]|| (clamped to [0,1]), beta = ||Y[p:]||,
+// mu = alpha/beta, VH = Y[p:]/beta, VHmu = mu VH; bad[b] |= beta == 0 for a selected q
+__global__ void gsvd_epilogue_kernel(const double* Y, int p, int T, int s, const int32_t* nsel, double* mu,
+                                     double* VH, double* VHmu, int32_t* bad) {
+  const int q = blockIdx.x, b = blockIdx.y;
+  const double* y = Y + ((int64_t)b * s + q) * (p + T);
+  __shared__ double red[8 * 33 + 8];
+  double a2[2] = {0.0, 0.0};
+  for (int i = threadIdx.x; i < p + T; i += blockDim.x) {
+    const double v = y[i];
+    if (i < p) a2[0] += v * v; else a2[1] += v * v;
+  }
+  block_sum<2>(a2, red);
+  const double alpha = fmin(fmax(sqrt(red[0]), 0.0), 1.0), beta = sqrt(red[1]);
+  const bool live = q < nsel[b];
+  const double bs = beta > 0.0 ? beta : 1.0, m = alpha / bs;
+  if (threadIdx.x == 0) {
+    mu[(int64_t)b * s + q] = live ? m : 0.0;
+    if (live && !(beta > 0.0)) bad[b] = 1;
+  }
+  for (int i = threadIdx.x; i < T; i += blockDim.x) {
+    const double v = live ? y[p + i] / bs : 0.0;
+    VH[((int64_t)b * s + q) * T + i] = v;
+    VHmu[((int64_t)b * s + q) * T + i] = m * v;
+  }
+}
+
+// rows of X (B, R, L) scaled to unit norm (side M candidates)
+__global__ void normalize_rows_kernel(double* X, int R, int64_t L) {
+  const int r = blockIdx.x, b = blockIdx.y;
+  double* x = X + ((int64_t)b * R + r) * L;
+  __shared__ double red[8 * 33 + 8];
+  double v[1] = {0.0};
+  for (int64_t i = threadIdx.x; i < L; i += blockDim.x) v[0] += x[i] * x[i];
+  block_sum<1>(v, red);
+  const double nr = sqrt(red[0]), sc = nr > 0.0 ? 1.0 / nr : 1.0;
+  for (int64_t i = threadIdx.x; i < L; i += blockDim.x) x[i] *= sc;
+}
+
+// M (column-major, ld T) <- upper triangle of the t x t R held column-major in A (ld n)
+__global__ void copy_r_kernel(const double* A, int64_t n, int t, double* M, int T) {
+  const int j = blockIdx.x;
+  for (int i = threadIdx.x; i < T; i += blockDim.x) M[(int64_t)j * T + i] = (i <= j && j < t) ? A[(int64_t)j * n + i] : 0.0;
+}
+
+// ---------------------------------------------------------------- host helpers
+
+struct Ctx {
+  cudaStream_t st;
+  cublasHandle_t h;
+  double* cur;
+  double* end;
+  double* base = cur;
+  bool overrun = false;
+  double* take(int64_t cnt) {
+    double* r = cur;
+    cur += (cnt + 31) & ~int64_t(31);  // 256-byte aligned pieces
+    if (cur > end) overrun = true;
+    return r;
+  }
+};
+
+// Y rows (B, R2, L) = F rows (B, R2, R1) @ X rows (B, R1, L)  [+ beta Y]
+int rows_mul(Ctx& c, const double* F, int64_t sF, const double* X, int64_t ldX, int64_t sX, double* Y, int64_t ldY,
+             int64_t sY, int R2, int R1, int64_t L, int B, double alpha = 1.0, double beta = 0.0) {
+  if (B == 0 || R2 == 0 || L == 0) return KR_OK;
+  return cublas_check(cublasDgemmStridedBatched(c.h, CUBLAS_OP_N, CUBLAS_OP_N, (int)L, R2, R1, &alpha, X, (int)ldX,
+                                                sX, F, R1, sF, &beta, Y, (int)ldY, sY, B),
+                      "kr_recycle rows_mul");
+}
+
+// G (B, R, R) = X rows (R, L) X^T for short rows (L small): col-major G = X_col^T X_col
+int small_gram(Ctx& c, const double* X, int64_t ldX, int64_t sX, double* G, int R, int64_t L, int B) {
+  const double one = 1.0, zero = 0.0;
+  return cublas_check(cublasDgemmStridedBatched(c.h, CUBLAS_OP_T, CUBLAS_OP_N, R, R, (int)L, &one, X, (int)ldX, sX, X,
+                                                (int)ldX, sX, &zero, G, R, (int64_t)R * R, B),
+                      "kr_recycle small_gram");
+}
+
+int gram(Ctx& c, const double* A, const double* Bm, int B, int R, int64_t n, double* G) {
+  if (n < 4096) {  // short rows: one batched GEMM
+    const double one = 1.0, zero = 0.0;
+    return cublas_check(cublasDgemmStridedBatched(c.h, CUBLAS_OP_T, CUBLAS_OP_N, R, R, (int)n, &one, Bm, (int)n,
+                                                  (int64_t)R * n, A, (int)n, (int64_t)R * n, &zero, G, R,
+                                                  (int64_t)R * R, B),
+                        "kr_recycle gram");
+  }
+  const int64_t wl = kr_gram_workspace(B, R, n);
+  double* ws = c.take(wl);
+  return kr_gram(A, Bm, n, (int64_t)R * n, B, R, n, G, R, (int64_t)R * R, ws, wl, c.st);
+}
+
+template <typename T>
+int d2h(Ctx& c, std::vector<T>& host, const T* dev, size_t cnt) {
+  host.resize(cnt);
+  if (cnt == 0) return KR_OK;
+  cudaError_t e = cudaMemcpyAsync(host.data(), dev, cnt * sizeof(T), cudaMemcpyDeviceToHost, c.st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c.st);
+  return e == cudaSuccess ? KR_OK : fail(KR_ECUDA, std::string("kr_recycle d2h: ") + cudaGetErrorString(e));
+}
+
+template <typename T>
+int h2d(Ctx& c, T* dev, const T* host, size_t cnt) {
+  if (cnt == 0) return KR_OK;
+  cudaError_t e = cudaMemcpyAsync(dev, host, cnt * sizeof(T), cudaMemcpyHostToDevice, c.st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c.st);  // host buffer may go out of scope
+  return e == cudaSuccess ? KR_OK : fail(KR_ECUDA, std::string("kr_recycle h2d: ") + cudaGetErrorString(e));
+}
+
+struct Factor {  // one Cholesky-QR factor of a batch: F (B,T,T), info, stats
+  double* F;
+  int32_t* info;
+  double* stats;
+};
+
+int chol(Ctx& c, const double* G, const int32_t* dims, int B, int T, bool scale, const double* shift, Factor& f) {
+  return kr_chol_inv(G, T, (int64_t)T * T, dims, B, T, (scale ? 1 : 0) | 2, shift, f.F, T, (int64_t)T * T, f.stats,
+                     f.info, nullptr, c.st);
+}
+
+// CholQR2 of rows A (B, T, L) with dims; Q out (B,T,L) (may alias nothing), F = R^{-T} (B,T,T).
+// Returns per-sample device flags through `ok_dev` (1 = fine) for the non-robust use.
+struct QrOut {
+  double* Q;
+  double* F;
+  Factor f1, f2;
+};
+
+int cholqr2(Ctx& c, const double* A, int B, int T, int64_t L, const int32_t* dims, double* tmpQ, QrOut& o) {
+  double* G = c.take((int64_t)B * T * T);
+  KR_TRY(L >= 4096 ? gram(c, A, A, B, T, L, G) : small_gram(c, A, L, (int64_t)T * L, G, T, L, B));
+  KR_TRY(chol(c, G, dims, B, T, true, nullptr, o.f1));
+  KR_TRY(rows_mul(c, o.f1.F, (int64_t)T * T, A, L, (int64_t)T * L, tmpQ, L, (int64_t)T * L, T, T, L, B));
+  KR_TRY(L >= 4096 ? gram(c, tmpQ, tmpQ, B, T, L, G) : small_gram(c, tmpQ, L, (int64_t)T * L, G, T, L, B));
+  KR_TRY(chol(c, G, dims, B, T, false, nullptr, o.f2));
+  KR_TRY(rows_mul(c, o.f2.F, (int64_t)T * T, tmpQ, L, (int64_t)T * L, o.Q, L, (int64_t)T * L, T, T, L, B));
+  return rows_mul(c, o.f2.F, (int64_t)T * T, o.f1.F, T, (int64_t)T * T, o.F, T, (int64_t)T * T, T, T, T, B);
+}
+
+Factor new_factor(Ctx& c, int B, int T) {
+  Factor f;
+  f.F = c.take((int64_t)B * T * T);
+  f.info = reinterpret_cast<int32_t*>(c.take((B + 1) / 2));
+  f.stats = c.take(4 * (int64_t)B);
+  return f;
+}
+
+bool cholqr_ok(const std::vector<int32_t>& info, const std::vector<double>& st, int b) {
+  return info[b] < 0 && st[4 * b + 0] > CHOLQR_TOL * st[4 * b + 1] && st[4 * b + 2] > 0.0;
+}
+
+int64_t workspace_doubles(const kr_op& op, const kr_recycle_args& a) {
+  // generous per-term budget: every Ctx::take of kr_recycle_update is covered with
+  // margin (each take also rounds up to 32 doubles); overruns are reported
+  const int64_t B = a.batch, T = a.T, n = op_n(op), s = a.s;
+  const int64_t p = op.reg_kind == KR_REG_TV ? 1 : (int64_t)op.num_filters * (1 + op.ksize * op.ksize);
+  const int64_t P = p + T;
+  int64_t w = 0;
+  w += 2 * B * T * n;                                   // A, tmpQ
+  w += 24 * (B * T * T + 4 * B + 64);                   // T x T factors, Grams, Ht, Hs, Mq, M, Q_R
+  w += 5 * B * T * P;                                   // Jt, S, QS, CholQR tmp
+  w += 8 * B * s * T + 2 * B * s * P;                   // Z, X, coeffs, VH mu, Y, extremes
+  w += 4 * B * s * n + 8 * (B * s * s + 4 * B + 64);    // cand, HU, CholQR tmp; prepare factors
+  w += 8 * kr_gram_workspace((int32_t)B, (int32_t)T, n);
+  w += kr_jadj_workspace(&op, (int32_t)T) + 3 * kr_syev_select_workspace((int32_t)B, (int32_t)T);
+  w += 8 * T * T + 4 * T + 65536;                       // pivoted path (Householder work, tau), slack
+  return w;
+}
+
+}  // namespace
+}  // namespace kr
+
+using namespace kr;
+
+int overrun(const Ctx& c, int line) {
+  char msg[160];
+  snprintf(msg, sizeof msg, "kr_recycle_update: workspace estimate exceeded at line %d (%lld of %lld doubles)", line,
+           (long long)(c.cur - c.base), (long long)(c.end - c.base));
+  return fail(KR_ENOMEM, msg);
+}
+
+extern "C" int64_t kr_recycle_workspace(const kr_op* op, const kr_recycle_args* a) {
+  if (!op || !a || validate_op(*op) != KR_OK) return -1;
+  return workspace_doubles(*op, *a);
+}
+
+extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, double* work, int64_t work_len,
+                                 kr_stream_t stream) {
+  KR_CHECK_ARG(op && a, "null argument");
+  KR_TRY(validate_op(*op));
+  const int B = a->batch, T = a->T, s = a->s;
+  const int64_t n = op_n(*op);
+  KR_CHECK_ARG(op->batch == B, "operator batch must equal args.batch");
+  KR_CHECK_ARG(T >= 1 && T <= RC_TMAX && s >= 1 && s <= T, "need 1 <= s <= T <= 228");
+  KR_CHECK_ARG(a->vec_type == 0 || (a->vec_type == 1 && a->size_code == 1), "vec_type: Ritz, or RGen with size L");
+  KR_CHECK_ARG(a->vec_type == 0 || op->reg_kind != KR_REG_NONE, "RGen needs a mixed Jacobian");
+  KR_CHECK_ARG(work && work_len >= workspace_doubles(*op, *a), "kr_recycle workspace too small");
+  const int p = op->reg_kind == KR_REG_TV ? 1 : op->num_filters * (1 + op->ksize * op->ksize);
+  const int P = p + T;
+  Ctx c{(cudaStream_t)stream, nullptr, work, work + work_len};
+  KR_TRY(cublas_handle(&c.h, c.st));
+  std::vector<int32_t> t(B), status(B, 0);
+  for (int b = 0; b < B; ++b) t[b] = a->kdims[b] + a->sdims[b];
+
+  // ---- 1. candidates A = [V_prev, U_prev] rows
+  int32_t* dd = reinterpret_cast<int32_t*>(c.take(B * 4 + 8));  // device ints: kd, sd, td, nsel, misc
+  int32_t* d_kd = dd;
+  int32_t* d_sd = dd + B;
+  int32_t* d_td = dd + 2 * B;
+  int32_t* d_ns = dd + 3 * B;
+  int32_t* d_bad = dd + 4 * B;
+  {
+    std::vector<int32_t> hk(5 * B, 0);
+    for (int b = 0; b < B; ++b) {
+      hk[b] = a->kdims[b];
+      hk[B + b] = a->sdims[b];
+      hk[2 * B + b] = t[b];
+    }
+    KR_TRY(h2d(c, dd, hk.data(), hk.size()));
+  }
+  double* A = c.take((int64_t)B * T * n);
+  double* tmpQ = c.take((int64_t)B * T * n);
+  gather_rows_kernel<<<dim3(T, B), 256, 0, c.st>>>(a->V, a->ld_v, a->bs_v, d_kd, a->Uprev, a->ld_u, a->bs_u, d_sd, A,
+                                                   T, n);
+  KR_TRY(check_launch("gather_rows"));
+
+  // ---- 2. W = orth(A) with the reference's rank drop
+  double* W = a->W;
+  Factor f1 = new_factor(c, B, T), f2 = new_factor(c, B, T), f3 = new_factor(c, B, T);
+  double* G = c.take((int64_t)B * T * T);
+  double* F = c.take((int64_t)B * T * T);
+  double* Ft = c.take((int64_t)B * T * T);
+  KR_TRY(gram(c, A, A, B, T, n, G));
+  double* nrm = c.take(2 * B);  // ||A||_F^2 = tr(A A^T) (the Gram is reused below), ||R^-1||_F^2
+  trace_kernel<<<B, 256, 0, c.st>>>(G, T, nrm);
+  KR_TRY(chol(c, G, d_td, B, T, true, nullptr, f1));
+  std::vector<int32_t> info1;
+  std::vector<double> st1;
+  KR_TRY(d2h(c, info1, f1.info, B));
+  KR_TRY(d2h(c, st1, f1.stats, 4 * B));
+  std::vector<char> ok1(B);
+  bool shifted = false;
+  for (int b = 0; b < B; ++b) {
+    ok1[b] = t[b] == 0 || cholqr_ok(info1, st1, b);
+    shifted |= !ok1[b];
+  }
+  if (shifted) {  // shifted CholeskyQR3 for the declined samples (sigma = 11 (n t + t(t+1)) u t)
+    std::vector<double> sh(B, 0.0);
+    for (int b = 0; b < B; ++b)
+      if (!ok1[b]) {
+        const double tb = t[b];
+        sh[b] = 11.0 * (n * tb + tb * (tb + 1)) * 2.220446049250313e-16 * tb;
+      }
+    double* d_sh = c.take(B);
+    KR_TRY(h2d(c, d_sh, sh.data(), B));
+    KR_TRY(chol(c, G, d_td, B, T, true, d_sh, f1));
+  }
+  std::vector<int32_t> is1;
+  if (shifted) KR_TRY(d2h(c, is1, f1.info, B));
+  KR_TRY(rows_mul(c, f1.F, (int64_t)T * T, A, n, (int64_t)T * n, W, n, (int64_t)T * n, T, T, n, B));
+  // second pass (and third when shifted)
+  Factor* fp[2] = {&f2, &f3};
+  double* cur = W;
+  double* nxt = tmpQ;
+  KR_TRY(cudaMemcpyAsync(F, f1.F, sizeof(double) * B * T * T, cudaMemcpyDeviceToDevice, c.st) == cudaSuccess
+             ? KR_OK : fail(KR_ECUDA, "kr_recycle copy"));
+  for (int pass = 0; pass < (shifted ? 2 : 1); ++pass) {
+    KR_TRY(gram(c, cur, cur, B, T, n, G));
+    KR_TRY(chol(c, G, d_td, B, T, false, nullptr, *fp[pass]));
+    KR_TRY(rows_mul(c, fp[pass]->F, (int64_t)T * T, cur, n, (int64_t)T * n, nxt, n, (int64_t)T * n, T, T, n, B));
+    KR_TRY(rows_mul(c, fp[pass]->F, (int64_t)T * T, F, T, (int64_t)T * T, Ft, T, (int64_t)T * T, T, T, T, B));
+    std::swap(F, Ft);
+    std::swap(cur, nxt);
+  }
+  if (cur != W) KR_TRY(cudaMemcpyAsync(W, cur, sizeof(double) * B * T * n, cudaMemcpyDeviceToDevice, c.st) == cudaSuccess
+                           ? KR_OK : fail(KR_ECUDA, "kr_recycle copy W"));
+  // condition bound ||A||_F ||R^-1||_F and the later passes' breakdowns
+  frob2_kernel<<<B, 256, 0, c.st>>>(F, T, T, T, (int64_t)T * T, nrm + B);
+  std::vector<double> nr;
+  std::vector<int32_t> i2, i3;
+  KR_TRY(d2h(c, nr, nrm, 2 * B));
+  KR_TRY(d2h(c, i2, f2.info, B));
+  if (shifted) KR_TRY(d2h(c, i3, f3.info, B));
+  std::vector<int> ill, hh;  // samples for the pivoted path; of those, the ones needing Householder
+  for (int b = 0; b < B; ++b) {
+    if (t[b] == 0) continue;
+    const double cb = sqrt(nr[b]) * sqrt(nr[B + b]);
+    // CholQR2 (ok1) or shifted CholeskyQR3 that factored and stayed within its range
+    const bool okb = shifted ? (is1[b] < 0 && i2[b] < 0 && i3[b] < 0 && (ok1[b] || cb <= SHIFT_COND_MAX))
+                             : (ok1[b] && i2[b] < 0);
+    if (!okb || cb > PIVOT_COND) {
+      ill.push_back(b);
+      if (!okb) hh.push_back(b);
+    }
+  }
+  if (!ill.empty()) {
+    const int nb = (int)ill.size();
+    double* M = c.take((int64_t)nb * T * T);
+    double* Qr = c.take((int64_t)nb * T * T);
+    int32_t* d_misc = reinterpret_cast<int32_t*>(c.take(2 * nb + 2));
+    int32_t* d_rank = d_misc + nb;
+    std::vector<int32_t> tdim(nb);
+    for (int i = 0; i < nb; ++i) tdim[i] = t[ill[i]];
+    KR_TRY(h2d(c, d_misc, tdim.data(), nb));
+    double* tau = c.take(T);
+    // R factors: from the Cholesky-QR basis (R^T = A W^T) or a Householder QR
+    for (int i = 0; i < nb; ++i) {
+      const int b = ill[i];
+      const double one = 1.0, zero = 0.0;
+      const bool house = std::find(hh.begin(), hh.end(), b) != hh.end();
+      if (!house) {  // M column-major R: M[j][i] = a_j . w_i  (col-major M (T x T) = W_col^T A_col)
+        KR_TRY(cublas_check(cublasDgemm(c.h, CUBLAS_OP_T, CUBLAS_OP_N, T, T, (int)n, &one, W + (int64_t)b * T * n,
+                                        (int)n, A + (int64_t)b * T * n, (int)n, &zero, M + (int64_t)i * T * T, T),
+                            "kr_recycle R"));
+      } else {  // Householder: geqrf/orgqr on A_b (n x t column-major == its rows), W_b = Q rows
+        // rare path (rank-deficient candidates): the LAPACK work buffer is sized by cuSOLVER,
+        // so it is allocated stream-ordered here instead of from the caller's workspace
+        cusolverDnHandle_t sh;
+        if (cusolverDnCreate(&sh) != CUSOLVER_STATUS_SUCCESS) return fail(KR_ECUDA, "cusolverDnCreate");
+        cusolverDnSetStream(sh, c.st);
+        double* Ab = A + (int64_t)b * T * n;
+        const int tb = t[b];
+        int lw1 = 0, lw2 = 0;
+        cusolverDnDgeqrf_bufferSize(sh, (int)n, tb, Ab, (int)n, &lw1);
+        cusolverDnDorgqr_bufferSize(sh, (int)n, tb, tb, Ab, (int)n, tau, &lw2);
+        const int lw = std::max(lw1, lw2);
+        void* hw = nullptr;
+        if (cudaMallocAsync(&hw, sizeof(double) * (lw + 1) + 64, c.st) != cudaSuccess) {
+          cusolverDnDestroy(sh);
+          return fail(KR_ENOMEM, "kr_recycle: Householder work buffer");
+        }
+        double* wk = static_cast<double*>(hw);
+        int32_t* dinfo = reinterpret_cast<int32_t*>(wk + lw);
+        const bool qok = cusolverDnDgeqrf(sh, (int)n, tb, Ab, (int)n, tau, wk, lw, dinfo) == CUSOLVER_STATUS_SUCCESS;
+        copy_r_kernel<<<T, 256, 0, c.st>>>(Ab, n, tb, M + (int64_t)i * T * T, T);
+        const bool gok = qok && cusolverDnDorgqr(sh, (int)n, tb, tb, Ab, (int)n, tau, wk, lw, dinfo) ==
+                                    CUSOLVER_STATUS_SUCCESS;
+        cudaMemsetAsync(W + (int64_t)b * T * n, 0, sizeof(double) * T * n, c.st);
+        cudaMemcpyAsync(W + (int64_t)b * T * n, Ab, sizeof(double) * tb * n, cudaMemcpyDeviceToDevice, c.st);
+        cudaFreeAsync(hw, c.st);
+        cusolverDnDestroy(sh);
+        if (!gok) return fail(KR_ECUDA, "kr_recycle: Householder QR");
+      }
+    }
+    double* qw = c.take(nb * T + 1);
+    KR_TRY(kr_qrcp_small_cluster(M, d_misc, nb, T, RANK_TOL, Qr, d_rank, nullptr, qw, nb * T + 1, c.st));
+    // W_b <- Q_R[:, :r]^T W_b  (rows beyond the rank are zero)
+    for (int i = 0; i < nb; ++i) {
+      const int b = ill[i];
+      KR_TRY(rows_mul(c, Qr + (int64_t)i * T * T, 0, W + (int64_t)b * T * n, n, 0, tmpQ, n, 0, T, T, n, 1));
+      KR_TRY(cudaMemcpyAsync(W + (int64_t)b * T * n, tmpQ, sizeof(double) * T * n, cudaMemcpyDeviceToDevice, c.st)
+                     == cudaSuccess ? KR_OK : fail(KR_ECUDA, "kr_recycle copy"));
+    }
+    std::vector<int32_t> rk;
+    KR_TRY(d2h(c, rk, d_rank, nb));
+    for (int i = 0; i < nb; ++i) t[ill[i]] = rk[i];
+    std::vector<int32_t> ht(t.begin(), t.end());
+    KR_TRY(h2d(c, d_td, ht.data(), B));
+  }
+
+  if (c.overrun) return overrun(c, __LINE__);
+  // ---- 3. H W and the projected Hessian
+  double* HW = a->HW;
+  KR_TRY(kr_hvp(op, W, n, (int64_t)T * n, T, HW, n, (int64_t)T * n, c.st));
+  double* Ht = c.take((int64_t)B * T * T);
+  KR_TRY(gram(c, W, HW, B, T, n, Ht));
+  double* coeffs = c.take((int64_t)B * s * T);
+  double* Xc = nullptr;
+  double* VHmu = nullptr;
+  std::vector<int32_t> bad(B, 0);
+  if (a->vec_type == 0) {  // Ritz: eigenpairs of sym(W^T H W)
+    double* Hs = c.take((int64_t)B * T * T);
+    sym_and_s_kernel<<<dim3(T, B), 256, 0, c.st>>>(Ht, nullptr, 0, T, Hs, nullptr);
+    Ht = Hs;
+    const int64_t el = kr_syev_select_workspace(B, T);
+    KR_TRY(kr_syev_select(Ht, T, (int64_t)T * T, d_td, B, T, a->size_code, s, nullptr, 0, coeffs, T,
+                          (int64_t)s * T, d_ns, c.take(el), el, c.st));
+  } else {
+    // J W
+    double* Jt = c.take((int64_t)B * T * p);
+    const int64_t jl = kr_jadj_workspace(op, T);
+    KR_TRY(kr_jadj(op, W, n, (int64_t)T * n, T, Jt, p, (int64_t)T * p, c.take(jl), jl, c.st));
+    double* S = c.take((int64_t)B * T * P);
+    double* Hs = c.take((int64_t)B * T * T);
+    sym_and_s_kernel<<<dim3(T, B), 256, 0, c.st>>>(Ht, Jt, p, T, Hs, S);
+    Ht = Hs;
+    // condition bracket of Ht: (max L_jj / min L_jj)^2 <= cond <= ||Ht||_F ||L^-1||_F^2
+    Factor fh = new_factor(c, B, T);
+    KR_TRY(chol(c, Ht, d_td, B, T, false, nullptr, fh));
+    double* hn = c.take(2 * B);
+    frob2_kernel<<<B, 256, 0, c.st>>>(Ht, T, T, T, (int64_t)T * T, hn);
+    frob2_kernel<<<B, 256, 0, c.st>>>(fh.F, T, T, T, (int64_t)T * T, hn + B);
+    // GSVD: [Jt; Ht] = Q R (CholQR2 of the rows of S)
+    QrOut qs;
+    qs.Q = c.take((int64_t)B * T * P);
+    qs.F = c.take((int64_t)B * T * T);
+    qs.f1 = new_factor(c, B, T);
+    qs.f2 = new_factor(c, B, T);
+    KR_TRY(cholqr2(c, S, B, T, P, d_td, c.take((int64_t)B * T * P), qs));
+    // Q1^T Q1 (Q1 = first p entries of every row of QS)
+    double* Mq = c.take((int64_t)B * T * T);
+    KR_TRY(small_gram(c, qs.Q, P, (int64_t)T * P, Mq, T, p, B));
+    const int64_t el = kr_syev_select_workspace(B, T);
+    double* Zs = c.take((int64_t)B * s * T);
+    KR_TRY(kr_syev_select(Mq, T, (int64_t)T * T, d_td, B, T, 1, s, nullptr, 0, Zs, T, (int64_t)s * T, d_ns,
+                          c.take(el), el, c.st));
+    // the bracket decision (host), overlapping the eigen kernel
+    std::vector<double> hnv, hst;
+    std::vector<int32_t> hinf;
+    KR_TRY(d2h(c, hnv, hn, 2 * B));
+    KR_TRY(d2h(c, hst, fh.stats, 4 * B));
+    KR_TRY(d2h(c, hinf, fh.info, B));
+    std::vector<int> exact;
+    for (int b = 0; b < B; ++b) {
+      if (t[b] == 0) continue;
+      const double ub = sqrt(hnv[b]) * hnv[B + b];
+      const bool scr = hinf[b] < 0 && hst[4 * b] > 0.0 && ub < COND_LIMIT;
+      if (!scr) exact.push_back(b);
+    }
+    if (!exact.empty()) {  // exact extreme eigenvalues where the bracket straddles the limit
+      double* ext = c.take(2 * (int64_t)B);
+      double* zz = c.take(2 * (int64_t)B * T);
+      KR_TRY(kr_syev_select(Ht, T, (int64_t)T * T, d_td, B, T, 2, 2, ext, 2, zz, T, 2 * (int64_t)T, nullptr,
+                            c.take(el), el, c.st));
+      std::vector<double> ex;
+      KR_TRY(d2h(c, ex, ext, 2 * B));
+      for (int b : exact) {
+        const double lo = ex[2 * b], hi = ex[2 * b + 1], smax = std::max(fabs(lo), fabs(hi));
+        if (!(lo > 0.0 && lo >= smax / COND_LIMIT)) status[b] = 1;  // singular: the per-sample path raises
+      }
+    }
+    // alpha, beta, mu, V_H from Y = Z Q^T rows; X = R^-1 z
+    double* Y = c.take((int64_t)B * s * P);
+    KR_TRY(rows_mul(c, Zs, (int64_t)s * T, qs.Q, P, (int64_t)T * P, Y, P, (int64_t)s * P, s, T, P, B));
+    double* VHv = a->VH;
+    VHmu = c.take((int64_t)B * s * T);
+    KR_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int32_t) * B, c.st) == cudaSuccess ? KR_OK : fail(KR_ECUDA, "memset"));
+    gsvd_epilogue_kernel<<<dim3(s, B), 256, 0, c.st>>>(Y, p, T, s, d_ns, a->mu, VHv, VHmu, d_bad);
+    Xc = c.take((int64_t)B * s * T);
+    KR_TRY(rows_mul(c, Zs, (int64_t)s * T, qs.F, T, (int64_t)T * T, Xc, T, (int64_t)s * T, s, T, T, B));
+    double* cf = a->side == 1 ? VHv : Xc;
+    KR_TRY(cudaMemcpyAsync(coeffs, cf, sizeof(double) * B * s * T, cudaMemcpyDeviceToDevice, c.st) == cudaSuccess
+               ? KR_OK : fail(KR_ECUDA, "copy"));
+    // QR breakdowns of [Jt; Ht]
+    std::vector<int32_t> qi1, qi2;
+    std::vector<double> qs1;
+    KR_TRY(d2h(c, qi1, qs.f1.info, B));
+    KR_TRY(d2h(c, qs1, qs.f1.stats, 4 * B));
+    KR_TRY(d2h(c, qi2, qs.f2.info, B));
+    for (int b = 0; b < B; ++b)
+      if (t[b] > 0 && !(cholqr_ok(qi1, qs1, b) && qi2[b] < 0)) status[b] = 1;
+  }
+
+  if (c.overrun) return overrun(c, __LINE__);
+  // ---- 5. U~ = W coeffs, H U~, C R = H U~, U = U~ R^-1
+  double* cand = c.take((int64_t)B * s * n);
+  double* HU = c.take((int64_t)B * s * n);
+  if (a->vec_type == 1 && a->side == 2) {  // side M: normalised mean of both candidate sets
+    KR_TRY(rows_mul(c, a->VH, (int64_t)s * T, W, n, (int64_t)T * n, cand, n, (int64_t)s * n, s, T, n, B, 0.5, 0.0));
+    KR_TRY(rows_mul(c, Xc, (int64_t)s * T, W, n, (int64_t)T * n, cand, n, (int64_t)s * n, s, T, n, B, 0.5, 1.0));
+    normalize_rows_kernel<<<dim3(s, B), 256, 0, c.st>>>(cand, s, n);
+    KR_TRY(kr_hvp(op, cand, n, (int64_t)s * n, s, HU, n, (int64_t)s * n, c.st));
+  } else {
+    KR_TRY(rows_mul(c, coeffs, (int64_t)s * T, W, n, (int64_t)T * n, cand, n, (int64_t)s * n, s, T, n, B));
+    if (a->reuse_products)
+      KR_TRY(rows_mul(c, coeffs, (int64_t)s * T, HW, n, (int64_t)T * n, HU, n, (int64_t)s * n, s, T, n, B));
+    else
+      KR_TRY(kr_hvp(op, cand, n, (int64_t)s * n, s, HU, n, (int64_t)s * n, c.st));
+  }
+  QrOut qu;
+  qu.Q = a->C;
+  qu.F = c.take((int64_t)B * s * s);
+  qu.f1 = new_factor(c, B, s);
+  qu.f2 = new_factor(c, B, s);
+  KR_TRY(cholqr2(c, HU, B, s, n, d_ns, c.take((int64_t)B * s * n), qu));
+  KR_TRY(rows_mul(c, qu.F, (int64_t)s * s, cand, n, (int64_t)s * n, a->U, n, (int64_t)s * n, s, s, n, B));
+  if (a->vec_type == 1)
+    KR_TRY(rows_mul(c, VHmu, (int64_t)s * T, W, n, (int64_t)T * n, a->Z, n, (int64_t)s * n, s, T, n, B));
+
+  // ---- 6. per-sample outcome
+  std::vector<int32_t> ns, ui1, ui2, bd;
+  std::vector<double> us1;
+  KR_TRY(d2h(c, ns, d_ns, B));
+  KR_TRY(d2h(c, ui1, qu.f1.info, B));
+  KR_TRY(d2h(c, us1, qu.f1.stats, 4 * B));
+  KR_TRY(d2h(c, ui2, qu.f2.info, B));
+  if (a->vec_type == 1) KR_TRY(d2h(c, bd, d_bad, B));
+  for (int b = 0; b < B; ++b) {
+    a->tdims[b] = t[b];
+    a->nsel[b] = ns[b];
+    if (t[b] == 0 || ns[b] == 0) {
+      a->status[b] = 2;
+      continue;
+    }
+    if (!(cholqr_ok(ui1, us1, b) && ui2[b] < 0)) status[b] = 1;
+    if (a->vec_type == 1 && bd[b]) status[b] = 1;
+    a->status[b] = status[b];
+  }
+  if (c.overrun) return overrun(c, __LINE__);
+  return check_launch("kr_recycle_update");
+}

@@ -112,14 +112,16 @@ def test_declines_small_mu_selections():
     assert not supports(S.parse("inner:RGen-L(R)")) and not supports(S.parse("HRitz-S"))
 
 
+@pytest.mark.parametrize("impl", ["python", "native"])
 @pytest.mark.parametrize("strategy", ["RGen-L(R)-NSC", "RGen-L(L)", "RGen-L(M)", "Ritz-S", "Ritz-L", "Ritz-M"])
-def test_recycle_update_matches_per_sample(strategy):
-    from paper_2412_08264_b200.batched import recycle_update
+def test_recycle_update_matches_per_sample(strategy, impl):
+    from paper_2412_08264_b200.batched import recycle_update, recycle_update_native
     from paper_2412_08264_b200.recycling import next_recycle
 
     model, seq, H, J = _setup(strategy)
     st = seq.cfg.strategy
-    batched = recycle_update(st, seq.cfg.recycle_dim, H, J, seq._prev_basis, seq._prev_recycle)
+    fn = recycle_update_native if impl == "native" else recycle_update
+    batched = fn(st, seq.cfg.recycle_dim, H, J, seq._prev_basis, seq._prev_recycle)
     for b in range(model.batch):
         ref = next_recycle(st, h_current=H.sample(b), jac_current=J.sample(b), prev_basis=seq._prev_basis[b],
                            prev_recycle=seq._prev_recycle[b], s=seq.cfg.recycle_dim)
@@ -179,8 +181,9 @@ def test_sequence_batched_equals_per_sample():
         assert e1 <= 3 * e0 + 1e-9 * np.abs(exact).max(), (i, e0, e1)
 
 
-def test_recycle_update_rank_drop():
-    """Exactly dependent candidates are dropped as in recycling._orth_drop (no fallback)."""
+@pytest.mark.parametrize("impl", ["python", "native"])
+def test_recycle_update_rank_drop(impl):
+    """Exactly dependent candidates are dropped as by the reference's pivoted QR (no fallback)."""
     from paper_2412_08264_b200 import batched
     from paper_2412_08264_b200.recycling import next_recycle
 
@@ -190,8 +193,9 @@ def test_recycle_update_rank_drop():
     V0 = bases[0]
     bases[0] = torch.cat([V0, V0[:, :2], 3.0 * V0[:, 5:6]], dim=1)  # three dependent columns
     batched.STATS = {}
+    fn = batched.recycle_update_native if impl == "native" else batched.recycle_update
     try:
-        got = batched.recycle_update(st, seq.cfg.recycle_dim, H, J, bases, seq._prev_recycle)
+        got = fn(st, seq.cfg.recycle_dim, H, J, bases, seq._prev_recycle)
         assert batched.STATS["declined"] == 0, batched.STATS
     finally:
         batched.STATS = None
