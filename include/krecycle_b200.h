@@ -247,6 +247,11 @@ typedef struct kr_recycle_args {
   int32_t* status;               /* HOST out [batch] */
 } kr_recycle_args;
 
+/* Creates this host thread's cuBLAS / cuSOLVER handles on the current device (both are
+ * per thread and expensive on first use); optional, for callers that pin update work
+ * to long-lived threads.  Host-side setup only, no reference counterpart. */
+int kr_thread_warmup(void);
+
 int64_t kr_recycle_workspace(const kr_op* op, const kr_recycle_args* args);
 int kr_recycle_update(const kr_op* op, const kr_recycle_args* args, double* work, int64_t work_len,
                       kr_stream_t stream);

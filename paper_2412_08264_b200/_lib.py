@@ -109,6 +109,7 @@ def _declare(lib):
         "kr_qrcp_small_cluster": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, ctypes.c_double, _c_p, _c_p, _c_p, _c_p,
                                            _c_i64, _c_p]),
         "kr_recycle_workspace": (_c_i64, [P(KrOp), P(KrRecycleArgs)]),
+        "kr_thread_warmup": (ctypes.c_int, []),
         "kr_recycle_update": (_c_i32, [P(KrOp), P(KrRecycleArgs), _c_p, _c_i64, _c_p]),
         "kr_gram_workspace": (_c_i64, [_c_i32, _c_i32, _c_i64]),
         "kr_gram": (_c_i32, [_c_p, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_i64,
@@ -126,7 +127,7 @@ EXPORTED = (
     "kr_hvp", "kr_jadj_workspace", "kr_jadj", "kr_lower_workspace", "kr_lower_eval",
     "kr_rminres_workspace", "kr_rminres", "kr_cg_workspace", "kr_cg",
     "kr_syev_select_workspace", "kr_syev_select", "kr_chol_inv", "kr_qrcp_small", "kr_qrcp_small_cluster",
-    "kr_gram_workspace", "kr_gram", "kr_recycle_workspace", "kr_recycle_update",
+    "kr_gram_workspace", "kr_gram", "kr_recycle_workspace", "kr_recycle_update", "kr_thread_warmup",
 )
 
 

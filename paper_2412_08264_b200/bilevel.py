@@ -99,8 +99,10 @@ def _warm_thread(shape=None):
     torch.linalg.eigvalsh(g)
     torch.bmm(a.unsqueeze(0), a.unsqueeze(0))
     # the library's own cuBLAS handle is per host thread as well (kr_gram, kr_jadj)
+    from . import _lib
     from .batched import gram
     gram(torch.zeros(1, 2, 4096, dtype=torch.float64, device="cuda"))
+    _lib.check(_lib.lib().kr_thread_warmup(), "kr_thread_warmup")
     torch.cuda.current_stream().synchronize()
 
 

@@ -138,6 +138,19 @@ int cublas_handle(cublasHandle_t* out, cudaStream_t st) {
   return KR_OK;
 }
 
+int cusolver_handle(cusolverDnHandle_t* out, cudaStream_t st) {
+  static thread_local cusolverDnHandle_t handles[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return fail(KR_ECUDA, "device index out of range");
+  if (!handles[dev] && cusolverDnCreate(&handles[dev]) != CUSOLVER_STATUS_SUCCESS)
+    return fail(KR_ECUDA, "cusolverDnCreate failed");
+  if (cusolverDnSetStream(handles[dev], st) != CUSOLVER_STATUS_SUCCESS)
+    return fail(KR_ECUDA, "cusolverDnSetStream failed");
+  *out = handles[dev];
+  return KR_OK;
+}
+
 int cublas_check(cublasStatus_t s, const char* what) {
   if (s == CUBLAS_STATUS_SUCCESS) return KR_OK;
   return fail(KR_ECUDA, std::string(what) + ": cuBLAS status " + std::to_string((int)s));

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cublas_v2.h>
+#include <cusolverDn.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -18,6 +19,7 @@ int validate_op(const kr_op& op);
 int ensure_smem(const void* kernel, size_t bytes);
 int device_sms();
 int cublas_handle(cublasHandle_t* out, cudaStream_t st);
+int cusolver_handle(cusolverDnHandle_t* out, cudaStream_t st);
 int cublas_check(cublasStatus_t s, const char* what);
 
 }  // namespace kr

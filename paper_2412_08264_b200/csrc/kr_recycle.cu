@@ -28,6 +28,8 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <string>
@@ -297,6 +299,13 @@ int overrun(const Ctx& c, int line) {
   return fail(KR_ENOMEM, msg);
 }
 
+extern "C" int kr_thread_warmup(void) {
+  cublasHandle_t h;
+  cusolverDnHandle_t sh;
+  KR_TRY(cublas_handle(&h, nullptr));
+  return cusolver_handle(&sh, nullptr);
+}
+
 extern "C" int64_t kr_recycle_workspace(const kr_op* op, const kr_recycle_args* a) {
   if (!op || !a || validate_op(*op) != KR_OK) return -1;
   return workspace_doubles(*op, *a);
@@ -316,6 +325,11 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
   const int p = op->reg_kind == KR_REG_TV ? 1 : op->num_filters * (1 + op->ksize * op->ksize);
   const int P = p + T;
   Ctx c{(cudaStream_t)stream, nullptr, work, work + work_len};
+  static const bool debug = getenv("KR_RECYCLE_DEBUG") != nullptr;
+  const auto t_start = std::chrono::steady_clock::now();
+  int n_ill = 0, n_house = 0, n_exact = 0;
+  double house_ms = 0.0;
+  bool was_shifted = false;
   KR_TRY(cublas_handle(&c.h, c.st));
   std::vector<int32_t> t(B), status(B, 0);
   for (int b = 0; b < B; ++b) t[b] = a->kdims[b] + a->sdims[b];
@@ -411,6 +425,9 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
       if (!okb) hh.push_back(b);
     }
   }
+  n_ill = (int)ill.size();
+  n_house = (int)hh.size();
+  was_shifted = shifted;
   if (!ill.empty()) {
     const int nb = (int)ill.size();
     double* M = c.take((int64_t)nb * T * T);
@@ -433,9 +450,10 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
       } else {  // Householder: geqrf/orgqr on A_b (n x t column-major == its rows), W_b = Q rows
         // rare path (rank-deficient candidates): the LAPACK work buffer is sized by cuSOLVER,
         // so it is allocated stream-ordered here instead of from the caller's workspace
+        if (debug) cudaStreamSynchronize(c.st);
+        const auto th0 = std::chrono::steady_clock::now();
         cusolverDnHandle_t sh;
-        if (cusolverDnCreate(&sh) != CUSOLVER_STATUS_SUCCESS) return fail(KR_ECUDA, "cusolverDnCreate");
-        cusolverDnSetStream(sh, c.st);
+        KR_TRY(cusolver_handle(&sh, c.st));
         double* Ab = A + (int64_t)b * T * n;
         const int tb = t[b];
         int lw1 = 0, lw2 = 0;
@@ -443,10 +461,8 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
         cusolverDnDorgqr_bufferSize(sh, (int)n, tb, tb, Ab, (int)n, tau, &lw2);
         const int lw = std::max(lw1, lw2);
         void* hw = nullptr;
-        if (cudaMallocAsync(&hw, sizeof(double) * (lw + 1) + 64, c.st) != cudaSuccess) {
-          cusolverDnDestroy(sh);
+        if (cudaMallocAsync(&hw, sizeof(double) * (lw + 1) + 64, c.st) != cudaSuccess)
           return fail(KR_ENOMEM, "kr_recycle: Householder work buffer");
-        }
         double* wk = static_cast<double*>(hw);
         int32_t* dinfo = reinterpret_cast<int32_t*>(wk + lw);
         const bool qok = cusolverDnDgeqrf(sh, (int)n, tb, Ab, (int)n, tau, wk, lw, dinfo) == CUSOLVER_STATUS_SUCCESS;
@@ -456,7 +472,10 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
         cudaMemsetAsync(W + (int64_t)b * T * n, 0, sizeof(double) * T * n, c.st);
         cudaMemcpyAsync(W + (int64_t)b * T * n, Ab, sizeof(double) * tb * n, cudaMemcpyDeviceToDevice, c.st);
         cudaFreeAsync(hw, c.st);
-        cusolverDnDestroy(sh);
+        if (debug) {
+          cudaStreamSynchronize(c.st);
+          house_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
+        }
         if (!gok) return fail(KR_ECUDA, "kr_recycle: Householder QR");
       }
     }
@@ -535,6 +554,7 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
       const bool scr = hinf[b] < 0 && hst[4 * b] > 0.0 && ub < COND_LIMIT;
       if (!scr) exact.push_back(b);
     }
+    n_exact = (int)exact.size();
     if (!exact.empty()) {  // exact extreme eigenvalues where the bracket straddles the limit
       double* ext = c.take(2 * (int64_t)B);
       double* zz = c.take(2 * (int64_t)B * T);
@@ -615,5 +635,9 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
     a->status[b] = status[b];
   }
   if (c.overrun) return overrun(c, __LINE__);
+  if (debug)
+    fprintf(stderr, "kr_recycle_update: B=%d T=%d shifted=%d ill=%d householder=%d exact=%d host %.2f ms (householder %.2f)\n",
+            B, T, (int)was_shifted, n_ill, n_house, n_exact,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count(), house_ms);
   return check_launch("kr_recycle_update");
 }
