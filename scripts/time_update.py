@@ -25,9 +25,16 @@ torch.cuda.synchronize()
 H, J = model.at(thetas[4], X[4])
 B = model.batch
 print("kdims", [int(v.shape[1]) for v in seq._prev_basis])
+import os
+grp = [int(x) for x in os.environ.get("UPD_GROUPS", "1,2").split(",")]
 for native in (False, True):
-    for groups in (1, 2):
+    for groups in grp:
+        if not native and groups > 2:
+            continue
         seq.native_update, seq.groups = native, groups
+        if seq._gstreams is not None and len(seq._gstreams) < groups:
+            seq._gstreams = None
+            seq.reserve(cfg.batch, 8 * model.n * (cfg.max_iter + cfg.recycle_dim) * 6, model.x_true.shape)
         ts = []
         for r in range(8):
             torch.cuda.synchronize()
