@@ -252,24 +252,25 @@ extern "C" int kr_qrcp_small(double* M, const int32_t* dims, int32_t batch, int3
 // accumulated with its columns distributed the same way (reflectors from L2).
 
 #include <cooperative_groups.h>
+#include <cuda_pipeline.h>
 
 namespace kr {
 namespace {
 
 namespace cgc = cooperative_groups;
-constexpr int QNC = 4;                    // CTAs per matrix
+constexpr int QNC = 8;                    // CTAs per matrix (portable cluster maximum)
 constexpr int QCN = 256;                  // threads per CTA
 constexpr int QCW = QCN / 32;
 constexpr int QCOLS = (256 + QNC - 1) / QNC;  // resident columns per CTA (t <= 256)
 
-struct QcShared {
-  double cand_v;   // this CTA's best remaining norm^2
-  int cand_g;      // its global column (-1: none)
-  int cand_pos;    // its current position
-  double beta, tau;
-  int rank;
+struct QcCand {
+  double v;  // best remaining norm^2 of a CTA
+  int g;     // its global column (-1: none)
+  int pos;   // its current position
 };
 
+// Exchange through DSMEM is push-based: a producer stores into every CTA's copy
+// before the cluster barrier (release / acquire), so reads after it are local.
 __global__ void __cluster_dims__(QNC, 1, 1) __launch_bounds__(QCN, 1) qrcp_cluster_kernel(QrcpParams P) {
   extern __shared__ double csm[];
   cgc::cluster_group cluster = cgc::this_cluster();
@@ -277,13 +278,13 @@ __global__ void __cluster_dims__(QNC, 1, 1) __launch_bounds__(QCN, 1) qrcp_clust
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = blockIdx.x / QNC, t = P.dims[b], T = P.T;
   double* cols = csm;                       // [QCOLS][T] resident columns
-  double* vb = cols + (int64_t)QCOLS * T;   // [T] Householder vector of the current step (owner's copy)
-  double* vl = vb + T;                      // [T] local copy
+  double* vl = cols + (int64_t)QCOLS * T;   // [T] Householder vector of the current step (pushed by its owner)
   __shared__ double cn[QCOLS];              // trailing norms^2 of the resident columns
   __shared__ int done[QCOLS];               // already pivoted
   __shared__ int pos[256];                  // current position of every global column (replicated)
   __shared__ int at[256];                   // global column at every position (replicated)
-  __shared__ QcShared sh;
+  __shared__ QcCand cand[QNC];              // every CTA's candidate of the step (pushed)
+  __shared__ double bt[2];                  // beta, tau of the step (pushed by the owner)
   double* M = P.M + (int64_t)b * T * T;
   const int nloc = (t - cr + QNC - 1) / QNC;  // columns g = cr + QNC * l, l < nloc
   for (int l = warp; l < nloc; l += QCW) {
@@ -305,13 +306,15 @@ __global__ void __cluster_dims__(QNC, 1, 1) __launch_bounds__(QCN, 1) qrcp_clust
     pos[g] = g;
     at[g] = g;
   }
-  if (tid == 0) sh.rank = t;
   __syncthreads();
   cluster.sync();
   double r00 = 0.0;
   int rank = t;
+#ifdef KR_QRCP_TIMING
+  long long qsec[6] = {0, 0, 0, 0, 0, 0}, qlast = clock64();
+#endif
   for (int k = 0; k < t; ++k) {
-    // 1. this CTA's candidate (warp 0)
+    // 1. this CTA's candidate (warp 0), pushed to every CTA
     if (warp == 0) {
       double best = -1.0;
       int bg = -1, bp = 1 << 30;
@@ -335,29 +338,38 @@ __global__ void __cluster_dims__(QNC, 1, 1) __launch_bounds__(QCN, 1) qrcp_clust
           bp = op;
         }
       }
-      if (lane == 0) {
-        sh.cand_v = best;
-        sh.cand_g = bg;
-        sh.cand_pos = bp;
+      if (lane < QNC) {
+        QcCand* dst = cluster.map_shared_rank(&cand[cr], lane);
+        dst->v = best;
+        dst->g = bg;
+        dst->pos = bp;
       }
     }
+#ifdef KR_QRCP_TIMING
+    __syncthreads();
+    if (tid == 0) { const long long c_ = clock64(); qsec[0] += c_ - qlast; qlast = c_; }
+#endif
     __syncwarp();
     cluster.sync();
-    // 2. the cluster's pivot, decided identically in every CTA
+#ifdef KR_QRCP_TIMING
+    __syncthreads();
+    if (tid == 0) { const long long c_ = clock64(); qsec[1] += c_ - qlast; qlast = c_; }
+#endif
+    // 2. the cluster's pivot, decided identically in every CTA from the local copies
     double best = -1.0;
     int pg = -1, pp = 1 << 30;
+#pragma unroll
     for (int r = 0; r < QNC; ++r) {
-      const QcShared* o = cluster.map_shared_rank(&sh, r);
-      const double v = o->cand_v;
-      const int g = o->cand_g, p = o->cand_pos;
+      const double v = cand[r].v;
+      const int g = cand[r].g, p = cand[r].pos;
       if (g >= 0 && (v > best || (v == best && p < pp))) {
         best = v;
         pg = g;
         pp = p;
       }
     }
-    // position bookkeeping (LAPACK's swap of positions k and pp)
-    __syncthreads();
+    // position bookkeeping (LAPACK's swap of positions k and pp); pos / at are read by
+    // warp 0 only until the final write-back (behind barriers)
     if (tid == 0) {
       const int gk = at[k];
       at[pp] = gk;
@@ -365,96 +377,147 @@ __global__ void __cluster_dims__(QNC, 1, 1) __launch_bounds__(QCN, 1) qrcp_clust
       at[k] = pg;
       pos[pg] = k;
     }
+#ifdef KR_QRCP_TIMING
+    __syncthreads();
+    if (tid == 0) { const long long c_ = clock64(); qsec[2] += c_ - qlast; qlast = c_; }
+#endif
     const int owner = pg % QNC, lslot = pg / QNC;
-    // 3. the owner forms the Householder vector of its column pg (rows k..t)
-    if (cr == owner && warp == 0) {
-      double* cp = cols + (int64_t)lslot * T;
-      double x[QR];
-      double s = 0.0;
+    // 3. the owner forms the Householder vector of its column pg (rows k..t) and
+    //    pushes it, beta and tau to every CTA (one warp per destination)
+    if (cr == owner) {
+      if (warp == 0) {
+        double* cp = cols + (int64_t)lslot * T;
+        double x[QR];
+        double s = 0.0;
 #pragma unroll
-      for (int r = 0; r < QR; ++r) {
-        const int i = k + 1 + lane + 32 * r;
-        x[r] = i < t ? cp[i] : 0.0;
-        s += x[r] * x[r];
-      }
-      s = warp_sum(s);
-      const double alpha = cp[k];
-      double beta = alpha, tk = 0.0;
-      if (s > 0.0) {
-        beta = -copysign(sqrt(alpha * alpha + s), alpha);
-        tk = (beta - alpha) / beta;
-      }
-      const double scal = tk != 0.0 ? 1.0 / (alpha - beta) : 0.0;
+        for (int r = 0; r < QR; ++r) {
+          const int i = k + 1 + lane + 32 * r;
+          x[r] = i < t ? cp[i] : 0.0;
+          s += x[r] * x[r];
+        }
+        s = warp_sum(s);
+        const double alpha = cp[k];
+        double beta = alpha, tk = 0.0;
+        if (s > 0.0) {
+          beta = -copysign(sqrt(alpha * alpha + s), alpha);
+          tk = (beta - alpha) / beta;
+        }
+        const double scal = tk != 0.0 ? 1.0 / (alpha - beta) : 0.0;
 #pragma unroll
-      for (int r = 0; r < QR; ++r) {
-        const int i = k + 1 + lane + 32 * r;
-        if (i < t) {
-          const double v = x[r] * scal;
-          vb[i] = v;
-          cp[i] = v;
+        for (int r = 0; r < QR; ++r) {
+          const int i = k + 1 + lane + 32 * r;
+          if (i < t) {
+            const double v = x[r] * scal;
+            cp[i] = v;
+            vl[i] = v;
+          }
+        }
+        if (lane == 0) {
+          vl[k] = 1.0;
+          bt[0] = beta;
+          bt[1] = tk;
+          cp[k] = beta;
+          done[lslot] = 1;
+          P.tau[(int64_t)b * T + k] = tk;
         }
       }
-      if (lane == 0) {
-        vb[k] = 1.0;
-        cp[k] = beta;
-        sh.beta = beta;
-        sh.tau = tk;
-        done[lslot] = 1;
-        P.tau[(int64_t)b * T + k] = tk;
+      __syncthreads();  // owner CTA only (cr is uniform per CTA)
+      for (int q = warp; q < QNC; q += QCW) {
+        if (q == cr) continue;
+        double* dv = cluster.map_shared_rank(vl, q);
+        for (int i = k + lane; i < t; i += 32) dv[i] = vl[i];
+        if (lane < 2) cluster.map_shared_rank(bt, q)[lane] = bt[lane];
       }
     }
+#ifdef KR_QRCP_TIMING
+    __syncthreads();
+    if (tid == 0) { const long long c_ = clock64(); qsec[3] += c_ - qlast; qlast = c_; }
+#endif
     __syncwarp();
     cluster.sync();
-    // 4. everyone: beta/tau and v from the owner over DSMEM
-    const QcShared* os = cluster.map_shared_rank(&sh, owner);
-    const double beta = os->beta, tk = os->tau;
+    // 4. beta / tau / v are local now
+    const double beta = bt[0], tk = bt[1];
     if (k == 0) r00 = fabs(beta);
     if (fabs(beta) <= P.rtol * r00 || (k == 0 && r00 == 0.0)) {  // recycling.py:194 keep rule
       rank = k;
       break;
     }
-    const double* ovb = cluster.map_shared_rank(vb, owner);
-    for (int i = k + tid; i < t; i += QCN) vl[i] = ovb[i];
+#ifdef KR_QRCP_TIMING
     __syncthreads();
-    // 5. apply H_k to the resident unpivoted columns; exact trailing norms
-    if (tk != 0.0) {
-      for (int l = warp; l < nloc; l += QCW) {
-        if (done[l]) continue;
-        double* cj = cols + (int64_t)l * T;
-        double c[QR];
-        double d = 0.0;
+    if (tid == 0) { const long long c_ = clock64(); qsec[4] += c_ - qlast; qlast = c_; }
+#endif
+    // 5. apply H_k to the resident unpivoted columns; exact trailing norms.  A warp
+    // takes QC columns at a time so their reductions are in flight together.
+    const int rch = (t - k + 31) / 32;  // row chunks below k (warp-uniform)
+    const bool app = tk != 0.0;
+    for (int l0 = warp; l0 < nloc; l0 += QC * QCW) {
+      double c[QC][QR];
+      double d[QC], nn[QC];
+      bool act[QC];
+      const double* cb[QC];
 #pragma unroll
-        for (int r = 0; r < QR; ++r) {
-          const int i = k + lane + 32 * r;
-          c[r] = i < t ? cj[i] : 0.0;
-          if (i < t) d += vl[i] * c[r];
-        }
-        d = tk * warp_sum(d);
-        double nn = 0.0;
-#pragma unroll
-        for (int r = 0; r < QR; ++r) {
-          const int i = k + lane + 32 * r;
-          if (i < t) {
-            c[r] -= d * vl[i];
-            cj[i] = c[r];
-            if (i > k) nn += c[r] * c[r];
-          }
-        }
-        nn = warp_sum(nn);
-        if (lane == 0) cn[l] = nn;
+      for (int u = 0; u < QC; ++u) {
+        const int l = l0 + u * QCW;
+        act[u] = l < nloc && !done[l < nloc ? l : 0];
+        cb[u] = cols + (int64_t)(act[u] ? l : 0) * T;
+        d[u] = 0.0;
+        nn[u] = 0.0;
       }
-    } else {
-      for (int l = warp; l < nloc; l += QCW) {
-        if (done[l]) continue;
-        const double* cj = cols + (int64_t)l * T;
-        double nn = 0.0;
-        for (int i = k + 1 + lane; i < t; i += 32) nn += cj[i] * cj[i];
-        nn = warp_sum(nn);
-        if (lane == 0) cn[l] = nn;
+      // loads are unconditional at clamped rows (masked by selects): no per-element branches
+#pragma unroll
+      for (int r = 0; r < QR; ++r) {
+        if (r >= rch) break;
+        const int i = k + lane + 32 * r;
+        const int ic = i < t ? i : t - 1;
+        const double vi = vl[ic];
+#pragma unroll
+        for (int u = 0; u < QC; ++u) {
+          const double x = cb[u][ic];
+          c[u][r] = i < t ? x : 0.0;
+          d[u] = fma(vi, c[u][r], d[u]);
+        }
+      }
+      if (app) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+          for (int u = 0; u < QC; ++u) d[u] += __shfl_xor_sync(0xffffffffu, d[u], o);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < QR; ++r) {
+        if (r >= rch) break;
+        const int i = k + lane + 32 * r;
+        const int ic = i < t ? i : t - 1;
+        const double vi = vl[ic];
+#pragma unroll
+        for (int u = 0; u < QC; ++u) {
+          const double y = app ? fma(-tk * d[u], vi, c[u][r]) : c[u][r];
+          nn[u] = fma((i > k && i < t) ? y : 0.0, y, nn[u]);
+          if (app && act[u] && i < t) const_cast<double*>(cb[u])[i] = y;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int u = 0; u < QC; ++u) nn[u] += __shfl_xor_sync(0xffffffffu, nn[u], o);
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int u = 0; u < QC; ++u)
+          if (act[u]) cn[l0 + u * QCW] = nn[u];
       }
     }
+#ifdef KR_QRCP_TIMING
     __syncthreads();
+    if (tid == 0) { const long long c_ = clock64(); qsec[5] += c_ - qlast; qlast = c_; }
+#endif
   }
+#ifdef KR_QRCP_TIMING
+  if (tid == 0 && b == 0)
+    printf("qrcp cta %d: cand %lld sync1 %lld pivot %lld house+sync2 %lld vcopy %lld apply %lld\n", cr, qsec[0], qsec[1],
+           qsec[2], qsec[3], qsec[4], qsec[5]);
+#endif
   // write back the resident columns (R_piv above the diagonal, reflectors below)
   for (int l = warp; l < nloc; l += QCW) {
     const int g = cr + QNC * l;
@@ -475,21 +538,69 @@ __global__ void __cluster_dims__(QNC, 1, 1) __launch_bounds__(QCN, 1) qrcp_clust
   for (int l = warp; l < QCOLS; l += QCW)
     for (int i = lane; i < T; i += 32) cols[(int64_t)l * T + i] = (l < qloc && i == cr + QNC * l) ? 1.0 : 0.0;
   __syncthreads();
+  // reflectors r-1 .. 0 applied backwards; the next one streams into the other
+  // buffer (cp.async) while the current one is applied, tau staged in shared memory
+  double* taus = vl + 2 * T;  // reflector buffers: vl + (k & 1) T
+  for (int i = tid; i < r; i += QCN) taus[i] = P.tau[(int64_t)b * T + i];
+  auto fetch = [&](int k2) {
+    const double* src = M + (int64_t)at[k2] * T;
+    double* dst = vl + (k2 & 1) * T;
+    for (int i = k2 + 1 + tid; i < t; i += QCN) __pipeline_memcpy_async(dst + i, src + i, sizeof(double));
+    __pipeline_commit();
+  };
+  if (r > 0) fetch(r - 1);
   for (int kk = r - 1; kk >= 0; --kk) {
-    const double tk = P.tau[(int64_t)b * T + kk];
-    if (tk == 0.0) continue;
-    const double* vk = M + (int64_t)at[kk] * T;  // reflector kk below the diagonal of pivot column kk
-    for (int i = kk + 1 + tid; i < t; i += QCN) vl[i] = vk[i];
-    if (tid == 0) vl[kk] = 1.0;
+    if (kk >= 1) {
+      fetch(kk - 1);
+      __pipeline_wait_prior(1);
+    } else {
+      __pipeline_wait_prior(0);
+    }
+    double* vc = vl + (kk & 1) * T;
+    if (tid == 0) vc[kk] = 1.0;
     __syncthreads();
-    for (int l = warp; l < qloc; l += QCW) {
-      const int j = cr + QNC * l;
-      if (j < kk) continue;
-      double* qj = cols + (int64_t)l * T;
-      double d = 0.0;
-      for (int i = kk + lane; i < t; i += 32) d += vl[i] * qj[i];
-      d = tk * warp_sum(d);
-      for (int i = kk + lane; i < t; i += 32) qj[i] -= d * vl[i];
+    const double tk = taus[kk];
+    if (tk != 0.0) {
+      const int rch = (t - kk + 31) / 32;
+      for (int l0 = warp; l0 < qloc; l0 += QC * QCW) {
+        double c[QC][QR], d[QC];
+        bool act[QC];
+        double* cb[QC];
+#pragma unroll
+        for (int u = 0; u < QC; ++u) {
+          const int l = l0 + u * QCW;
+          act[u] = l < qloc && cr + QNC * l >= kk;
+          cb[u] = cols + (int64_t)(act[u] ? l : 0) * T;
+          d[u] = 0.0;
+        }
+#pragma unroll
+        for (int rr = 0; rr < QR; ++rr) {
+          if (rr >= rch) break;
+          const int i = kk + lane + 32 * rr;
+          const int ic = i < t ? i : t - 1;
+          const double vi = i < t ? vc[ic] : 0.0;
+#pragma unroll
+          for (int u = 0; u < QC; ++u) {
+            c[u][rr] = cb[u][ic];
+            d[u] = fma(vi, c[u][rr], d[u]);
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+          for (int u = 0; u < QC; ++u) d[u] += __shfl_xor_sync(0xffffffffu, d[u], o);
+        }
+#pragma unroll
+        for (int rr = 0; rr < QR; ++rr) {
+          if (rr >= rch) break;
+          const int i = kk + lane + 32 * rr;
+          const int ic = i < t ? i : t - 1;
+          const double vi = vc[ic];
+#pragma unroll
+          for (int u = 0; u < QC; ++u)
+            if (act[u] && i < t) cb[u][i] = fma(-tk * d[u], vi, c[u][rr]);
+        }
+      }
     }
     __syncthreads();
   }
@@ -512,7 +623,7 @@ extern "C" int kr_qrcp_small_cluster(double* M, const int32_t* dims, int32_t bat
   if (batch == 0) return KR_OK;
   KR_CHECK_ARG(M && dims && Q && rank && work, "null pointer");
   QrcpParams P{M, dims, tmax, rtol, Q, rank, perm, work};
-  const size_t smem = ((size_t)QCOLS * tmax + 2 * (size_t)tmax) * sizeof(double);
+  const size_t smem = ((size_t)QCOLS * tmax + 3 * (size_t)tmax) * sizeof(double);
   KR_TRY(ensure_smem((const void*)qrcp_cluster_kernel, smem));
   qrcp_cluster_kernel<<<batch * QNC, QCN, smem, (cudaStream_t)stream>>>(P);
   return check_launch("qrcp_cluster_kernel");
