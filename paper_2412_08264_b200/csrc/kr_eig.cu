@@ -216,18 +216,10 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
   double* R = red + EIG_RED;
   __shared__ int s_int[4];
 
-#ifdef KR_EIG_TIMING
-  long long tick[5];
-#endif
-#ifdef KR_EIG_TIMING
-  __syncthreads();
-  if (threadIdx.x == 0) tick[0] = clock64();
-#endif
   // ---------------- 1. tridiagonalization ----------------
-  double* vv = R;          // Householder vector of the step
-  double* yr = R + T;      // y = tau A22 v: lower-row part, then the combined y
-  double* yc = R + 2 * T;  // column (strictly upper) part, two row halves
-  double* Ap = R + 4 * T;
+  double* vv = R;
+  double* yv = R + T;
+  double* Ap = R + 2 * T;
   const double* Ab = P.A + (int64_t)b * P.bsa;
   // (A + A^T) / 2 with coalesced reads: storage rows into the lower triangle, then
   // storage rows again onto the transposed positions
@@ -243,13 +235,8 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
     for (int i = j + 1 + lane; i < t; i += 32) Ap[pk(i, j)] = 0.5 * (Ap[pk(i, j)] + __ldg(aj + i));
   }
   __syncthreads();
-  constexpr int QC = (EIG_TPACK + 31) / 32;  // register chunks of a row (lane + 32 q)
-#ifdef KR_EIG_TIMING
-  long long sec[5] = {0, 0, 0, 0, 0}, clast = clock64();
-#endif
   for (int k = 0; k + 1 < t; ++k) {
     const int m = t - k - 1;
-    const int K = k + 1;  // A22 = rows / columns K..t-1
     double part = 0.0;
     for (int i = k + 2 + tid; i < t; i += ENT) {
       const double x = Ap[pk(i, k)];
@@ -278,124 +265,28 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
     }
     if (tk == 0.0) continue;  // block-uniform (xn2 is broadcast)
     __syncthreads();
-#ifdef KR_EIG_TIMING
-    __syncthreads();
-    if (tid == 0) { const long long c_ = clock64(); sec[0] += c_ - clast; clast = c_; }
-#endif
-    // y = A22 v = (L + D) v + L^T v (symmetric, lower storage), both parts with
-    // contiguous shared-memory rows:
-    //  (L + D) v: a warp per 4 consecutive rows (lanes over columns), 4 reductions in flight
-    // (loads are unconditional at clamped in-row addresses, masked by selects: no
-    // per-element branches, so the loads of an unrolled step overlap)
-    for (int r0 = 4 * warp; r0 < m; r0 += 4 * EW) {
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      const int rlast = min(r0 + 3, m - 1);
-      int rb[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int ru = min(r0 + u, m - 1);
-        rb[u] = (K + ru) * (K + ru + 1) / 2 + K;
-      }
-      for (int c = lane; c <= rlast; c += 32) {
-        const double vc = vv[c];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double x = Ap[rb[u] + min(c, rlast)];
-          acc[u] = fma((c <= r0 + u && r0 + u < m) ? x : 0.0, vc, acc[u]);
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
-      }
-      if (lane < 4 && r0 + lane < m) {
-        double a = acc[0];
-        if (lane == 1) a = acc[1];
-        if (lane == 2) a = acc[2];
-        if (lane == 3) a = acc[3];
-        yr[r0 + lane] = a;
-      }
-    }
-#ifdef KR_EIG_TIMING
-    __syncthreads();
-    if (tid == 0) { const long long c_ = clock64(); sec[1] += c_ - clast; clast = c_; }
-#endif
-    //  L^T v: a thread per column c, rows split into two interleaved halves; at each
-    //  step the threads of a warp read consecutive columns of one row, starting at the
-    //  first row below the warp's first column
-    {
-      const int h = tid / (ENT / 2), c = tid - h * (ENT / 2);
-      const int cw = c & ~31;  // the warp's first column
-      if (cw < m) {
-        const int cc = min(c, m - 1);
-        double a0 = 0.0, a1 = 0.0;
-        int r = (cw & ~1) + h;
-        for (; r + 6 < m; r += 8) {
-          double x[4], v4[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int ru = r + 2 * u;
-            x[u] = Ap[(K + ru) * (K + ru + 1) / 2 + K + cc];
-            v4[u] = vv[ru];
-          }
-          a0 = fma(r > c ? x[0] : 0.0, v4[0], a0);
-          a1 = fma(r + 2 > c ? x[1] : 0.0, v4[1], a1);
-          a0 = fma(r + 4 > c ? x[2] : 0.0, v4[2], a0);
-          a1 = fma(r + 6 > c ? x[3] : 0.0, v4[3], a1);
-        }
-        for (; r < m; r += 2) {
-          const double x = Ap[(K + r) * (K + r + 1) / 2 + K + cc];
-          a0 = fma(r > c ? x : 0.0, vv[r], a0);
-        }
-        if (c < m) yc[h * T + c] = a0 + a1;
-      }
-    }
-    __syncthreads();
-#ifdef KR_EIG_TIMING
-    __syncthreads();
-    if (tid == 0) { const long long c_ = clock64(); sec[2] += c_ - clast; clast = c_; }
-#endif
-    double pv = 0.0;
-    for (int r = tid; r < m; r += ENT) {
-      const double y = tk * (yr[r] + (yc[r] + yc[T + r]));
-      yr[r] = y;
-      pv += y * vv[r];
-    }
-    const double kappa = -0.5 * tk * bsum(pv, red);
-#ifdef KR_EIG_TIMING
-    __syncthreads();
-    if (tid == 0) { const long long c_ = clock64(); sec[3] += c_ - clast; clast = c_; }
-#endif
-    // A22 -= v w^T + w v^T with w = y + kappa v (lower part); the row's v, w in registers
-    double vq[QC], wq[QC];
-#pragma unroll
-    for (int q = 0; q < QC; ++q) {
-      const int c = lane + 32 * q;
-      vq[q] = c < m ? vv[c] : 0.0;
-      wq[q] = c < m ? yr[c] + kappa * vq[q] : 0.0;
-    }
+    // y = tau * A22 v, one warp per row (lower row part + column part via symmetry)
     for (int r = warp; r < m; r += EW) {
-      const double vi = vv[r], wi = yr[r] + kappa * vi;
-      const int rb = (K + r) * (K + r + 1) / 2 + K;
-#pragma unroll
-      for (int q = 0; q < QC; ++q) {
-        if (32 * q > r) break;  // warp-uniform: the row has q chunks
-        const int c = lane + 32 * q;
-        if (c <= r) Ap[rb + c] -= vi * wq[q] + wi * vq[q];
+      const int i = k + 1 + r;
+      double acc = 0.0;
+      for (int c = lane; c < m; c += 32) acc += sym_at(Ap, i, k + 1 + c) * vv[c];
+      acc = warp_sum(acc);
+      if (lane == 0) yv[r] = tk * acc;
+    }
+    __syncthreads();
+    double pv = 0.0;
+    for (int r = tid; r < m; r += ENT) pv += yv[r] * vv[r];
+    const double kappa = -0.5 * tk * bsum(pv, red);
+    // A22 -= v w^T + w v^T with w = y + kappa v (lower part)
+    for (int r = warp; r < m; r += EW) {
+      const double vi = vv[r], wi = yv[r] + kappa * vi;
+      for (int c = lane; c <= r; c += 32) {
+        const double vj = vv[c], wj = yv[c] + kappa * vj;
+        Ap[pk(k + 1 + r, k + 1 + c)] -= vi * wj + wi * vj;
       }
     }
     __syncthreads();
-#ifdef KR_EIG_TIMING
-    __syncthreads();
-    if (tid == 0) { const long long c_ = clock64(); sec[4] += c_ - clast; clast = c_; }
-#endif
   }
-#ifdef KR_EIG_TIMING
-  if (tid == 0 && b == 0)
-    printf("tridiag sections: head %lld  rows %lld  cols %lld  dot %lld  update %lld\n", sec[0], sec[1], sec[2], sec[3],
-           sec[4]);
-#endif
   if (tid == 0) {
     d[t - 1] = Ap[pk(t - 1, t - 1)];
     e[t - 1] = 0.0;
@@ -405,10 +296,6 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
   for (int64_t i = tid; i < pk(t, 0); i += ENT) Hb[i] = Ap[i];
   __syncthreads();
 
-#ifdef KR_EIG_TIMING
-  __syncthreads();
-  if (threadIdx.x == 0) tick[1] = clock64();
-#endif
   // ---------------- 2. selected eigenvalues ----------------
   if (warp == 0) {
     double gl = 1e308, gu = -1e308, tn = 0.0, em = 0.0;
@@ -455,10 +342,6 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
   }
   __syncthreads();
 
-#ifdef KR_EIG_TIMING
-  __syncthreads();
-  if (threadIdx.x == 0) tick[2] = clock64();
-#endif
   // ---------------- 3. inverse iteration ----------------
   // clusters of close selected eigenvalues (gap <= 1e-3 ||T||, LAPACK stein's ORTOL);
   // within a cluster the shifts are separated by >= 10 eps |lambda| (PERTOL)
@@ -564,10 +447,6 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
     __syncthreads();
   }
 
-#ifdef KR_EIG_TIMING
-  __syncthreads();
-  if (threadIdx.x == 0) tick[3] = clock64();
-#endif
   // ---------------- 4. back-transformation ----------------
   for (int64_t i = tid; i < pk(t, 0); i += ENT) Ap[i] = Hb[i];
   __syncthreads();
@@ -628,19 +507,11 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
     }
     if (lane == 0 && P.lam) P.lam[(int64_t)b * P.bsl + q] = sel[q];
   }
-#ifdef KR_EIG_TIMING
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    tick[4] = clock64();
-    printf("eig b=%d t=%d cycles: tridiag %lld  eigvals %lld  invit %lld  backtr %lld\n", b, t, tick[1] - tick[0],
-           tick[2] - tick[1], tick[3] - tick[2], tick[4] - tick[3]);
-  }
-#endif
 }
 
 int64_t eig_smem_doubles(int T, int* nw_out) {
   const int64_t base = 4 * (int64_t)T + EIG_MAXSEL + EIG_RED;
-  const int64_t r1 = 4 * (int64_t)T + (int64_t)T * (T + 1) / 2;
+  const int64_t r1 = 2 * (int64_t)T + (int64_t)T * (T + 1) / 2;
   const int64_t per_vec = 6 * (int64_t)T + (T + 7) / 8;
   const int64_t cap = (227 * 1024) / 8 - 8 - base;  // static smem (cl_first, s_int) kept out
   int nw = (int)((cap > r1 ? cap : r1) / per_vec);
