@@ -513,10 +513,25 @@ def _uniform_rows(mats, n, dev):
     return buf.data_ptr(), n, kmax * n, buf
 
 
-def recycle_update_native(strategy, s: int, H, J, bases, recycles, reuse_products: bool = True):
+def _scratch(cache, key, numel, dev):
+    """Grow-only device scratch kept in `cache` (per sample group: always used on the
+    group's stream, ordered across steps by the caller's stream joins)."""
+    if cache is None:
+        return torch.empty(max(numel, 1), dtype=torch.float64, device=dev)
+    buf = cache.get(key)
+    if buf is None or buf.numel() < numel:
+        cache[key] = None
+        buf = cache[key] = torch.empty(max(numel, 1), dtype=torch.float64, device=dev)
+    return buf
+
+
+def recycle_update_native(strategy, s: int, H, J, bases, recycles, reuse_products: bool = True,
+                          scratch: dict | None = None):
     """``recycle_update`` through the native orchestrator ``kr_recycle_update`` (one
     C-ABI call per batch: no Python per-op overhead, no GIL); same contract and
-    results.  Falls back to ``recycle_update`` beyond the kernels' t <= 228."""
+    results.  Falls back to ``recycle_update`` beyond the kernels' t <= 228.
+    ``scratch`` (optional, one dict per stream) keeps the temporaries -- H W and the
+    orchestrator's workspace -- across calls instead of reallocating them."""
     from .recycling import RecycleSpace
     from .stopping import NscData
 
@@ -551,8 +566,11 @@ def recycle_update_native(strategy, s: int, H, J, bases, recycles, reuse_product
     a.kdims, a.sdims = kd.ctypes.data, sd.ctypes.data
     a.tdims, a.nsel, a.status = td.ctypes.data, ns.ctypes.data, stt.ctypes.data
     f64 = dict(dtype=torch.float64, device=dev)
-    W = torch.empty(B, T, n, **f64)
-    HW = torch.empty(B, T, n, **f64)
+    # buffers sized for the largest candidate width the caller expects (scratch["tcap"]),
+    # so growing T never reaches the device allocator inside a step
+    tcap = min(max(T, int(scratch.get("tcap", 0)) if scratch is not None else 0), NATIVE_TMAX)
+    W = torch.empty(B * tcap * n, **f64)[: B * T * n].view(B, T, n)
+    HW = _scratch(scratch, "hw", B * tcap * n, dev)
     U = torch.empty(B, s, n, **f64)
     C = torch.empty(B, s, n, **f64)
     mu = torch.zeros(B, s, **f64)
@@ -561,12 +579,15 @@ def recycle_update_native(strategy, s: int, H, J, bases, recycles, reuse_product
     a.W, a.HW, a.U, a.C = W.data_ptr(), HW.data_ptr(), U.data_ptr(), C.data_ptr()
     a.mu, a.VH, a.Z = mu.data_ptr(), VH.data_ptr(), Z.data_ptr()
     L = _lib.lib()
+    a.T = tcap
+    wcap = int(L.kr_recycle_workspace(ctypes.byref(H.op), ctypes.byref(a)))
+    a.T = T
     wl = int(L.kr_recycle_workspace(ctypes.byref(H.op), ctypes.byref(a)))
-    if wl < 0:
+    if wl < 0 or wcap < 0:
         _lib.check(-1, "kr_recycle_workspace")
-    ws = torch.empty(max(wl, 1), **f64)
-    _lib.check(L.kr_recycle_update(ctypes.byref(H.op), ctypes.byref(a), ws.data_ptr(), wl, _lib.stream_ptr()),
-               "kr_recycle_update")
+    ws = _scratch(scratch, "ws", max(wl, wcap), dev)
+    _lib.check(L.kr_recycle_update(ctypes.byref(H.op), ctypes.byref(a), ws.data_ptr(), ws.numel(),
+                                   _lib.stream_ptr()), "kr_recycle_update")
     _lib.note_launch("kr_recycle_update", 40)
     del vkeep, ukeep
     if STATS is not None:

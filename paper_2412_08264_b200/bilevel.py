@@ -106,6 +106,18 @@ def _warm_thread(shape=None):
     torch.cuda.current_stream().synchronize()
 
 
+_PHASE_DEBUG = os.environ.get("KR_SOLVE_DEBUG") is not None
+
+
+def _phase_clock():
+    """Synchronised wall clock for KR_SOLVE_DEBUG phase timing (None when off)."""
+    if not _PHASE_DEBUG:
+        return None
+    import time
+    torch.cuda.synchronize()
+    return time.perf_counter()
+
+
 class SequenceSolver:
     """Solves consecutive Hessian systems of a batch of samples, carrying the
     recycling state of each sample (bilevel.py:225-288).
@@ -132,6 +144,7 @@ class SequenceSolver:
         self.native_update = os.environ.get("KR_NATIVE_RECYCLE", "1") != "0"
         self._gstreams = None
         self._gpool = None
+        self._scratch = {}  # per sample group: the native update's temporaries
         self._streams = None
         self._pool = None
 
@@ -193,9 +206,14 @@ class SequenceSolver:
         def run(lo, hi):
             hs = hessian if (lo, hi) == (0, B) else hessian.slice(lo, hi)
             js = jac if (lo, hi) == (0, B) or jac is None else jac.slice(lo, hi)
-            update = recycle_update_native if self.native_update else recycle_update
-            recs = update(cfg.strategy, cfg.recycle_dim, hs, js, self._prev_basis[lo:hi],
-                          self._prev_recycle[lo:hi], cfg.reuse_products)
+            if self.native_update:
+                recs = recycle_update_native(cfg.strategy, cfg.recycle_dim, hs, js, self._prev_basis[lo:hi],
+                                             self._prev_recycle[lo:hi], cfg.reuse_products,
+                                             scratch=self._scratch.setdefault(
+                                                 lo, {"tcap": cfg.max_iter + cfg.recycle_dim + 1}))
+            else:
+                recs = recycle_update(cfg.strategy, cfg.recycle_dim, hs, js, self._prev_basis[lo:hi],
+                                      self._prev_recycle[lo:hi], cfg.reuse_products)
             # samples the batched path declined take the per-sample reference path
             return [r if r is not None else self._recycle_one(hessian, jac, B, lo + i) for i, r in enumerate(recs)]
 
@@ -286,14 +304,20 @@ class SequenceSolver:
         n = hessian.dim
         # one batched solve for all samples: the persistent kernel is latency bound per
         # iteration, so a launch over 8 samples costs what one over 4 does
+        t0 = _phase_clock()
         if cfg.strategy.is_none or self._first:
             recycles = [RecycleSpace.empty(n) for _ in range(B)]
         else:
             recycles = self._recycle_all(hessian, jac, B)
+        t1 = _phase_clock()
         self._first = False
         init = self._prev_solution if cfg.warm_start else None
         solve = rminres if cfg.method == "minres" else rcg
         results = solve(hessian, g, recycles if B > 1 else recycles[0], self._options(recycles, init))
+        if t0 is not None:
+            t2 = _phase_clock()
+            import sys
+            print(f"solve phases: recycle {1e3 * (t1 - t0):.1f} ms, krylov {1e3 * (t2 - t1):.1f} ms", file=sys.stderr)
         res_list = [results] if single else results
         self._prev_basis = [r.basis for r in res_list]
         self._prev_recycle = recycles

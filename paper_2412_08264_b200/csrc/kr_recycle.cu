@@ -269,6 +269,16 @@ bool cholqr_ok(const std::vector<int32_t>& info, const std::vector<double>& st, 
   return info[b] < 0 && st[4 * b + 0] > CHOLQR_TOL * st[4 * b + 1] && st[4 * b + 2] > 0.0;
 }
 
+// cuSOLVER work size of the Householder branch (geqrf + orgqr of an n x T block)
+int64_t house_lwork(int64_t n, int T) {
+  cusolverDnHandle_t sh;
+  if (cusolver_handle(&sh, nullptr) != KR_OK) return 1 << 20;
+  int lw1 = 0, lw2 = 0;
+  cusolverDnDgeqrf_bufferSize(sh, (int)n, T, nullptr, (int)n, &lw1);
+  cusolverDnDorgqr_bufferSize(sh, (int)n, T, T, nullptr, (int)n, nullptr, &lw2);
+  return std::max(lw1, lw2);
+}
+
 int64_t workspace_doubles(const kr_op& op, const kr_recycle_args& a) {
   // generous per-term budget: every Ctx::take of kr_recycle_update is covered with
   // margin (each take also rounds up to 32 doubles); overruns are reported
@@ -283,7 +293,8 @@ int64_t workspace_doubles(const kr_op& op, const kr_recycle_args& a) {
   w += 4 * B * s * n + 8 * (B * s * s + 4 * B + 64);    // cand, HU, CholQR tmp; prepare factors
   w += 8 * kr_gram_workspace((int32_t)B, (int32_t)T, n);
   w += kr_jadj_workspace(&op, (int32_t)T) + 3 * kr_syev_select_workspace((int32_t)B, (int32_t)T);
-  w += 8 * T * T + 4 * T + 65536;                       // pivoted path (Householder work, tau), slack
+  w += house_lwork(n, (int)T) + 64;                     // Householder branch (cuSOLVER work)
+  w += 8 * T * T + 4 * T + 65536;                       // pivoted path (tau), slack
   return w;
 }
 
@@ -303,7 +314,28 @@ extern "C" int kr_thread_warmup(void) {
   cublasHandle_t h;
   cusolverDnHandle_t sh;
   KR_TRY(cublas_handle(&h, nullptr));
-  return cusolver_handle(&sh, nullptr);
+  KR_TRY(cusolver_handle(&sh, nullptr));
+  // one tiny Householder QR on this thread's handle (first-call setup off the hot path)
+  const int m = 64, q = 8;
+  int lw1 = 0, lw2 = 0;
+  cusolverDnDgeqrf_bufferSize(sh, m, q, nullptr, m, &lw1);
+  cusolverDnDorgqr_bufferSize(sh, m, q, q, nullptr, m, nullptr, &lw2);
+  const int lw = std::max(lw1, lw2);
+  double* buf = nullptr;
+  if (cudaMalloc(&buf, sizeof(double) * ((size_t)m * q + q + lw + 1)) != cudaSuccess)
+    return fail(KR_ENOMEM, "kr_thread_warmup");
+  cudaMemset(buf, 0, sizeof(double) * m * q);
+  double* A = buf;
+  double* tau = A + m * q;
+  double* wk = tau + q;
+  int32_t* info = reinterpret_cast<int32_t*>(wk + lw);
+  const double one = 1.0;
+  for (int i = 0; i < q; ++i) cudaMemcpy(A + (size_t)i * m + i, &one, sizeof(double), cudaMemcpyHostToDevice);
+  cusolverDnDgeqrf(sh, m, q, A, m, tau, wk, lw, info);
+  cusolverDnDorgqr(sh, m, q, q, A, m, tau, wk, lw, info);
+  const cudaError_t e = cudaDeviceSynchronize();
+  cudaFree(buf);
+  return e == cudaSuccess ? KR_OK : fail(KR_ECUDA, "kr_thread_warmup");
 }
 
 extern "C" int64_t kr_recycle_workspace(const kr_op* op, const kr_recycle_args* a) {
@@ -438,6 +470,12 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
     for (int i = 0; i < nb; ++i) tdim[i] = t[ill[i]];
     KR_TRY(h2d(c, d_misc, tdim.data(), nb));
     double* tau = c.take(T);
+    double* hwk = nullptr;
+    int64_t hwl = 0;
+    if (!hh.empty()) {
+      hwl = house_lwork(n, T) + 1;
+      hwk = c.take(hwl);
+    }
     // R factors: from the Cholesky-QR basis (R^T = A W^T) or a Householder QR
     for (int i = 0; i < nb; ++i) {
       const int b = ill[i];
@@ -460,10 +498,8 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
         cusolverDnDgeqrf_bufferSize(sh, (int)n, tb, Ab, (int)n, &lw1);
         cusolverDnDorgqr_bufferSize(sh, (int)n, tb, tb, Ab, (int)n, tau, &lw2);
         const int lw = std::max(lw1, lw2);
-        void* hw = nullptr;
-        if (cudaMallocAsync(&hw, sizeof(double) * (lw + 1) + 64, c.st) != cudaSuccess)
-          return fail(KR_ENOMEM, "kr_recycle: Householder work buffer");
-        double* wk = static_cast<double*>(hw);
+        if (hwk == nullptr || lw + 1 > hwl) return fail(KR_ENOMEM, "kr_recycle: Householder work buffer");
+        double* wk = hwk;
         int32_t* dinfo = reinterpret_cast<int32_t*>(wk + lw);
         const bool qok = cusolverDnDgeqrf(sh, (int)n, tb, Ab, (int)n, tau, wk, lw, dinfo) == CUSOLVER_STATUS_SUCCESS;
         copy_r_kernel<<<T, 256, 0, c.st>>>(Ab, n, tb, M + (int64_t)i * T * T, T);
@@ -471,7 +507,6 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
                                     CUSOLVER_STATUS_SUCCESS;
         cudaMemsetAsync(W + (int64_t)b * T * n, 0, sizeof(double) * T * n, c.st);
         cudaMemcpyAsync(W + (int64_t)b * T * n, Ab, sizeof(double) * tb * n, cudaMemcpyDeviceToDevice, c.st);
-        cudaFreeAsync(hw, c.st);
         if (debug) {
           cudaStreamSynchronize(c.st);
           house_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
