@@ -76,18 +76,28 @@ __global__ void gather_rows_kernel(const double* V, int64_t ld_v, int64_t bs_v, 
   for (int64_t p = threadIdx.x; p < n; p += blockDim.x) dst[p] = src ? src[p] : 0.0;
 }
 
-// out[b] = sum of squares of rows x cols block b (rows of length `cols`, row stride ld)
-__global__ void frob2_kernel(const double* X, int rows, int64_t cols, int64_t ld, int64_t bs, double* out) {
+// out[b] = sum of squares of rows x cols block b (rows of length `cols`, row stride ld);
+// a CTA per block, 8 independent loads in flight per thread (fixed order: deterministic)
+constexpr int FROB_NT = 512;
+__global__ void __launch_bounds__(FROB_NT) frob2_kernel(const double* X, int rows, int64_t cols, int64_t ld, int64_t bs,
+                                                        double* out) {
   const int b = blockIdx.x;
-  double s = 0.0;
   const double* Xb = X + b * bs;
-  for (int r = 0; r < rows; ++r)
-    for (int64_t e = threadIdx.x; e < cols; e += blockDim.x) {
-      const double v = Xb[r * ld + e];
-      s += v * v;
+  const int total = rows * (int)cols;
+  double s[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int e0 = threadIdx.x; e0 < total; e0 += 8 * FROB_NT) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * FROB_NT;
+      if (e < total) {
+        const int r = e / (int)cols, c = e - r * (int)cols;
+        const double v = Xb[(int64_t)r * ld + c];
+        s[u] = fma(v, v, s[u]);
+      }
     }
+  }
   __shared__ double red[8 * 33 + 8];
-  double v1[1] = {s};
+  double v1[1] = {((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]))};
   block_sum<1>(v1, red);
   if (threadIdx.x == 0) out[b] = red[0];
 }
@@ -439,7 +449,7 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
   if (cur != W) KR_TRY(cudaMemcpyAsync(W, cur, sizeof(double) * B * T * n, cudaMemcpyDeviceToDevice, c.st) == cudaSuccess
                            ? KR_OK : fail(KR_ECUDA, "kr_recycle copy W"));
   // condition bound ||A||_F ||R^-1||_F and the later passes' breakdowns
-  frob2_kernel<<<B, 256, 0, c.st>>>(F, T, T, T, (int64_t)T * T, nrm + B);
+  frob2_kernel<<<B, FROB_NT, 0, c.st>>>(F, T, T, T, (int64_t)T * T, nrm + B);
   std::vector<double> nr;
   std::vector<int32_t> i2, i3;
   KR_TRY(d2h(c, nr, nrm, 2 * B));
@@ -560,8 +570,8 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
     Factor fh = new_factor(c, B, T);
     KR_TRY(chol(c, Ht, d_td, B, T, false, nullptr, fh));
     double* hn = c.take(2 * B);
-    frob2_kernel<<<B, 256, 0, c.st>>>(Ht, T, T, T, (int64_t)T * T, hn);
-    frob2_kernel<<<B, 256, 0, c.st>>>(fh.F, T, T, T, (int64_t)T * T, hn + B);
+    frob2_kernel<<<B, FROB_NT, 0, c.st>>>(Ht, T, T, T, (int64_t)T * T, hn);
+    frob2_kernel<<<B, FROB_NT, 0, c.st>>>(fh.F, T, T, T, (int64_t)T * T, hn + B);
     // GSVD: [Jt; Ht] = Q R (CholQR2 of the rows of S)
     QrOut qs;
     qs.Q = c.take((int64_t)B * T * P);
