@@ -61,6 +61,9 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
   double* A = Lbb + NB * (NB + 1);  // packed lower t(t+1)/2
   __shared__ int s_fail;
   __shared__ unsigned char skp[CHOL_TMAX];
+#ifdef KR_CHOL_TIMING
+  long long csec[7] = {0, 0, 0, 0, 0, 0, 0}, clast = clock64();
+#endif
   const double* Gb = P.G + (int64_t)b * P.bsg;
   const bool scale = P.flags & 1, inv = P.flags & 2, skipmode = P.flags & 4;
   for (int i = tid; i < t; i += CNT) {
@@ -85,6 +88,10 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
   // numerically dependent on the previous ones (exact dependence rounds either way)
   const double piv_rtol = 4.0 * t * 1.1102230246251565e-16;
   // ---- blocked Cholesky (right-looking, NB = 32) ----
+#ifdef KR_CHOL_TIMING
+    __syncthreads();
+    if (tid == 0) { const long long c_ = clock64(); csec[0] += c_ - clast; clast = c_; }
+#endif
   const int lane = tid & 31, warp = tid >> 5;
   for (int kb = 0; kb < t; kb += NB) {
     const int nb = min(NB, t - kb);
@@ -126,6 +133,10 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
       if (lane == 0 && bad >= 0) s_fail = bad;
     }
     __syncthreads();
+#ifdef KR_CHOL_TIMING
+    __syncthreads();
+    if (tid == 0) { const long long c_ = clock64(); csec[1] += c_ - clast; clast = c_; }
+#endif
     if (s_fail >= 0) break;
     // panel: rows below solve x L_kk^T = a (forward substitution over the block columns)
     for (int r = kb + nb + tid; r < t; r += CNT) {
@@ -141,6 +152,10 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
       }
     }
     __syncthreads();
+#ifdef KR_CHOL_TIMING
+    __syncthreads();
+    if (tid == 0) { const long long c_ = clock64(); csec[2] += c_ - clast; clast = c_; }
+#endif
     // trailing update A_ij -= L_i,panel . L_j,panel (lower part), warp per row, lanes over j
     for (int i = kb + nb + warp; i < t; i += CNT / 32) {
       const double* Li = A + pk(i, kb);
@@ -153,6 +168,10 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
       }
     }
     __syncthreads();
+#ifdef KR_CHOL_TIMING
+    __syncthreads();
+    if (tid == 0) { const long long c_ = clock64(); csec[3] += c_ - clast; clast = c_; }
+#endif
   }
   __syncthreads();
   const int fail = s_fail;
@@ -193,9 +212,10 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
     return;
   }
   // ---- X = L^{-1} by blocked forward substitution ----
-  // block row I: V = E_I - L_I,<I X_<I over (row, column) pairs spread across the
-  // CTA, staged in the (not yet written) output rows of F, then X_I = L_II^{-1} V,
-  // one thread per column, from a copy of L_II; X_I overwrites L_I.
+  // Block row I (rows ib..ib+nb): V = E_I - L_I,<I X_<I, then X_I = L_II^{-1} V.  A thread
+  // owns one column c and one half h of the block rows: 8 accumulators in registers, one
+  // contiguous X load per k feeding 8 FMAs with broadcast L operands; the substitution
+  // runs on those registers (h = 0 rows first, then h = 1 with them), X_I overwrites L_I.
   for (int ib = 0; ib < t; ib += NB) {
     const int nb = min(NB, t - ib);
     const int w = ib + nb;  // columns 0 .. w-1 are nonzero in block row I
@@ -204,40 +224,71 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
       Lbb[r * (NB + 1) + m] = m <= r ? A[pk(ib + r, ib + m)] : 0.0;
       if (m == r) rdiag[r] = 1.0 / A[pk(ib + r, ib + r)];
     }
-    for (int r = warp; r < nb; r += CNT / 32) {
-      const double* Li = A + pk(ib + r, 0);
-      double* vr = Fb + (int64_t)(ib + r) * P.ldf;
-      for (int c = lane; c < w; c += 32) {
-        double acc = 0.0, a1 = 0.0;
-        if (c < ib) {
-          int k = c;
-          for (; k + 1 < ib; k += 2) {
-            acc += Li[k] * A[pk(k, c)];
-            a1 += Li[k + 1] * A[pk(k + 1, c)];
-          }
-          if (k < ib) acc += Li[k] * A[pk(k, c)];
+    const int h = tid / (CNT / 2), c = tid - h * (CNT / 2);
+    const int r0 = 8 * h;
+    double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    if (c < w && r0 < nb) {
+      const double* lp[8];  // rows ib + r0 + u of L (clamped into the matrix)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) lp[u] = A + pk(min(ib + r0 + u, t - 1), 0);
+      int k = c;
+      int xa = k * (k + 1) / 2 + c;  // packed index of X_kc, advanced by k + 1 per row
+      for (; k + 3 < ib; k += 4) {
+        double xv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          xv[j] = A[xa];  // X_(k+j),c (rows < ib hold X already)
+          xa += k + j + 1;
         }
-        vr[c] = (c == ib + r ? 1.0 : 0.0) - (acc + a1);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const double* l = lp[u] + k;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[u] = fma(l[j], xv[j], acc[u]);
+        }
+      }
+      for (; k < ib; ++k) {
+        const double xk = A[xa];
+        xa += k + 1;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = fma(lp[u][k], xk, acc[u]);
+      }
+    }
+    __syncthreads();  // every read of L_I,<I done before X_I overwrites it
+    double x[NB];
+    if (h == 0 && c < w) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        if (r < nb) {
+          double s = (c == ib + r ? 1.0 : 0.0) - acc[r];
+#pragma unroll
+          for (int m = 0; m < r; ++m) s -= Lbb[r * (NB + 1) + m] * x[m];
+          x[r] = (c <= ib + r) ? s * rdiag[r] : 0.0;
+          if (c <= ib + r) A[pk(ib + r, c)] = x[r];
+        }
       }
     }
     __syncthreads();
-    if (tid < w) {  // column c: forward substitution with L_II
-      const int c = tid;
-      double x[NB];
+    if (h == 1 && c < w && nb > 8) {
 #pragma unroll
-      for (int r = 0; r < NB; ++r) {
+      for (int m = 0; m < 8; ++m) x[m] = (c <= ib + m) ? A[pk(ib + m, c)] : 0.0;
+#pragma unroll
+      for (int r = 8; r < NB; ++r) {
         if (r < nb) {
-          double s = (c <= ib + r) ? Fb[(int64_t)(ib + r) * P.ldf + c] : 0.0;
+          double s = (c == ib + r ? 1.0 : 0.0) - acc[r - 8];
+#pragma unroll
           for (int m = 0; m < r; ++m) s -= Lbb[r * (NB + 1) + m] * x[m];
-          x[r] = s * rdiag[r];
+          x[r] = (c <= ib + r) ? s * rdiag[r] : 0.0;
+          if (c <= ib + r) A[pk(ib + r, c)] = x[r];
         }
       }
-#pragma unroll
-      for (int r = 0; r < NB; ++r)
-        if (r < nb && c <= ib + r) A[pk(ib + r, c)] = x[r];
     }
     __syncthreads();
   }
+#ifdef KR_CHOL_TIMING
+  __syncthreads();
+  if (tid == 0) { const long long c_ = clock64(); csec[4] += c_ - clast; clast = c_; }
+#endif
   // ---- F = L^{-1} D^{-1}, full row-major T x T ----
   for (int i = warp; i < T; i += CNT / 32) {
     double* fi = Fb + (int64_t)i * P.ldf;
@@ -250,6 +301,15 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
       fi[j] = v;
     }
   }
+#ifdef KR_CHOL_TIMING
+  __syncthreads();
+  if (tid == 0) { const long long c_ = clock64(); csec[5] += c_ - clast; clast = c_; }
+#endif
+#ifdef KR_CHOL_TIMING
+  if (tid == 0 && b == 0)
+    printf("chol t=%d cycles: load %lld diag %lld panel %lld trailing %lld inverse %lld output %lld\n", t, csec[0], csec[1],
+           csec[2], csec[3], csec[4], csec[5]);
+#endif
 }
 
 }  // namespace
