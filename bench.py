@@ -219,6 +219,8 @@ def run_ours(args):
         if dbg:
             from paper_2412_08264_b200 import batched as _bt
             _bt.STATS = {}
+            if dbg == "mem":  # stack traces of every caching-allocator segment allocation
+                torch.cuda.memory._record_memory_history(max_entries=200000)
         for i in range(args.warmup, steps_total):
             if dbg:
                 m0 = torch.cuda.memory_stats()
@@ -234,6 +236,15 @@ def run_ours(args):
                 torch.cuda.synchronize()
                 m1 = torch.cuda.memory_stats()
                 ds = {k: _bt.STATS[k] - s0.get(k, 0) for k in _bt.STATS}
+                if dbg == "mem" and m1.get('num_device_alloc', 0) > m0.get('num_device_alloc', 0):
+                    snap = torch.cuda.memory._snapshot()
+                    for tr in snap.get("device_traces", [[]])[0]:
+                        if tr.get("action") == "segment_alloc":
+                            fr = [f"{f['filename'].split('/')[-1]}:{f['line']}:{f['name']}" for f in tr.get("frames", [])
+                                  if "paper_2412" in f["filename"] or "bench" in f["filename"]]
+                            print(f"  segment_alloc {tr['size']} stream {tr.get('stream')} {fr[:6]}", file=sys.stderr)
+                    torch.cuda.memory._record_memory_history(enabled=None)
+                    torch.cuda.memory._record_memory_history(max_entries=200000)
                 print(f"step {i}: {e0.elapsed_time(e1):.1f} ms iters {iters[-1]} stats {ds} "
                       f"mallocs {m1.get('num_device_alloc', 0) - m0.get('num_device_alloc', 0)} "
                       f"retries {m1.get('num_alloc_retries', 0) - m0.get('num_alloc_retries', 0)}",

@@ -526,12 +526,14 @@ def _scratch(cache, key, numel, dev):
 
 
 def recycle_update_native(strategy, s: int, H, J, bases, recycles, reuse_products: bool = True,
-                          scratch: dict | None = None):
+                          scratch: dict | None = None, out: tuple | None = None, out_src: tuple | None = None):
     """``recycle_update`` through the native orchestrator ``kr_recycle_update`` (one
     C-ABI call per batch: no Python per-op overhead, no GIL); same contract and
     results.  Falls back to ``recycle_update`` beyond the kernels' t <= 228.
     ``scratch`` (optional, one dict per stream) keeps the temporaries -- H W and the
-    orchestrator's workspace -- across calls instead of reallocating them."""
+    orchestrator's workspace -- across calls instead of reallocating them.  ``out``
+    (optional): (U, C, Z) row blocks (B, s, n) to write into -- slices of whole-batch
+    buffers, so the solve reads every sample's recycle space in place."""
     from .recycling import RecycleSpace
     from .stopping import NscData
 
@@ -571,11 +573,16 @@ def recycle_update_native(strategy, s: int, H, J, bases, recycles, reuse_product
     tcap = min(max(T, int(scratch.get("tcap", 0)) if scratch is not None else 0), NATIVE_TMAX)
     W = torch.empty(B * tcap * n, **f64)[: B * T * n].view(B, T, n)
     HW = _scratch(scratch, "hw", B * tcap * n, dev)
-    U = torch.empty(B, s, n, **f64)
-    C = torch.empty(B, s, n, **f64)
+    if out is not None:
+        U, C, Z = out
+        if Z is None:
+            Z = torch.empty(B, s, n, **f64)
+    else:
+        U = torch.empty(B, s, n, **f64)
+        C = torch.empty(B, s, n, **f64)
+        Z = torch.empty(B, s, n, **f64)
     mu = torch.zeros(B, s, **f64)
     VH = torch.zeros(B, s, T, **f64)
-    Z = torch.empty(B, s, n, **f64)
     a.W, a.HW, a.U, a.C = W.data_ptr(), HW.data_ptr(), U.data_ptr(), C.data_ptr()
     a.mu, a.VH, a.Z = mu.data_ptr(), VH.data_ptr(), Z.data_ptr()
     L = _lib.lib()
@@ -593,16 +600,17 @@ def recycle_update_native(strategy, s: int, H, J, bases, recycles, reuse_product
     if STATS is not None:
         STATS["declined"] = STATS.get("declined", 0) + int((stt == 1).sum())
         STATS["samples"] = STATS.get("samples", 0) + B
-    out = []
+    res = []
     for b in range(B):
         tb, sb = int(td[b]), int(ns[b])
         if stt[b] == 2 or tb == 0 or sb == 0:
-            out.append(RecycleSpace.empty(n))
+            res.append(RecycleSpace.empty(n))
         elif stt[b] == 1:
-            out.append(None)
+            res.append(None)
         else:
             nsc = None
             if strategy.vec_type == "RGen":
                 nsc = NscData(values=mu[b, :sb], v_h=VH[b, :sb, :tb].T, w=W[b, :tb].T, z=Z[b, :sb].T)
-            out.append(RecycleSpace(U=U[b, :sb].T, C=C[b, :sb].T, nsc_data=nsc, orthonormal=True))
-    return out
+            src = None if out_src is None else (out_src[0], out_src[1], out_src[2], out_src[3] + b)
+            res.append(RecycleSpace(U=U[b, :sb].T, C=C[b, :sb].T, nsc_data=nsc, orthonormal=True, batch_src=src))
+    return res

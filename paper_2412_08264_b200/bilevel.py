@@ -202,15 +202,27 @@ class SequenceSolver:
         cfg = self.cfg
         ng = max(1, min(self.groups, B))
         bounds = [(g * B // ng, (g + 1) * B // ng) for g in range(ng)]
+        shared = None
+        if self.native_update:
+            # whole-batch (B, s, n) outputs, each group writing its rows: the solve then
+            # reads U, C, Z in place (no per-sample restacking)
+            s, n = cfg.recycle_dim, hessian.dim
+            dev = (hessian.model.device if getattr(hessian, "model", None) is not None
+                   else torch.device("cuda", torch.cuda.current_device()))
+            f64 = dict(dtype=torch.float64, device=dev)
+            shared = (torch.empty(B, s, n, **f64), torch.empty(B, s, n, **f64),
+                      torch.empty(B, s, n, **f64) if cfg.strategy.vec_type == "RGen" else None)
 
         def run(lo, hi):
             hs = hessian if (lo, hi) == (0, B) else hessian.slice(lo, hi)
             js = jac if (lo, hi) == (0, B) or jac is None else jac.slice(lo, hi)
             if self.native_update:
+                out = tuple(None if x is None else x[lo:hi] for x in shared)
                 recs = recycle_update_native(cfg.strategy, cfg.recycle_dim, hs, js, self._prev_basis[lo:hi],
                                              self._prev_recycle[lo:hi], cfg.reuse_products,
                                              scratch=self._scratch.setdefault(
-                                                 lo, {"tcap": cfg.max_iter + cfg.recycle_dim + 1}))
+                                                 lo, {"tcap": cfg.max_iter + cfg.recycle_dim + 1}),
+                                             out=out, out_src=shared + (lo,))
             else:
                 recs = recycle_update(cfg.strategy, cfg.recycle_dim, hs, js, self._prev_basis[lo:hi],
                                       self._prev_recycle[lo:hi], cfg.reuse_products)
@@ -312,6 +324,8 @@ class SequenceSolver:
         t1 = _phase_clock()
         self._first = False
         init = self._prev_solution if cfg.warm_start else None
+        if isinstance(init, list):
+            init = torch.stack(init)
         solve = rminres if cfg.method == "minres" else rcg
         results = solve(hessian, g, recycles if B > 1 else recycles[0], self._options(recycles, init))
         if t0 is not None:
@@ -323,7 +337,8 @@ class SequenceSolver:
         self._prev_recycle = recycles
         self._prev_h = hessian
         self._prev_jac = jac
-        self._prev_solution = torch.stack([r.solution for r in res_list]) if not single else res_list[0].solution
+        # kept as views; stacked only when a warm start asks for it (no per-step allocation)
+        self._prev_solution = [r.solution for r in res_list] if not single else res_list[0].solution
         if single:
             return res_list[0], recycles[0]
         return res_list, recycles

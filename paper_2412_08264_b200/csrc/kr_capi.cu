@@ -73,6 +73,11 @@ int validate_op(const kr_op& op) {
 int ensure_smem(const void* kernel, size_t bytes) {
   if (bytes > 227 * 1024) return fail(KR_EINVAL, "tile needs more than 227 KB of shared memory");
   if (bytes > 48 * 1024) {
+    // Opt in ONCE per (device, kernel) to the largest dynamic size the device allows: the
+    // launch's own smem request still sets the occupancy, and raising the attribute again
+    // later (e.g. as the candidate width t grows) would be a cudaFuncSetAttribute on a
+    // kernel that another host thread's stream may be running -- the driver serialises
+    // that call behind the running launch (measured: ~1 ms stalls of the recycle update).
     static std::mutex mu;
     static std::map<std::pair<int, const void*>, size_t> cap;
     int dev = 0;
@@ -80,9 +85,15 @@ int ensure_smem(const void* kernel, size_t bytes) {
     std::lock_guard<std::mutex> lock(mu);
     size_t& c = cap[{dev, kernel}];
     if (bytes > c) {
-      cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      int optin = 0;
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, kernel);
+      size_t lim = optin > 0 ? (size_t)optin - fa.sharedSizeBytes : bytes;
+      if (lim < bytes) lim = bytes;
+      cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
       if (e != cudaSuccess) return fail(KR_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-      c = bytes;
+      c = lim;
     }
   }
   return KR_OK;

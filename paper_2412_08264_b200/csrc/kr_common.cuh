@@ -14,6 +14,25 @@
 
 namespace kr {
 
+#ifdef KR_RMINRES_TIMING
+__device__ unsigned long long g_stencil_ns[8];
+__device__ __forceinline__ unsigned long long kr_gtime0() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define KR_SMARK(i, last)                                                     \
+  do {                                                                        \
+    if (threadIdx.x == 0 && blockIdx.x == 0) {                                \
+      const unsigned long long t_ = kr_gtime0();                              \
+      g_stencil_ns[i] += t_ - last;                                           \
+      last = t_;                                                              \
+    }                                                                         \
+  } while (0)
+#else
+#define KR_SMARK(i, last) ((void)0)
+#endif
+
 // Block barrier preceded by a full-warp reconvergence: thread-0-only sections
 // (scalar recurrences, partial reductions) leave warp 0 diverged, and the
 // .aligned bar.sync behind __syncthreads() must be reached by converged warps.
@@ -27,7 +46,7 @@ constexpr int TW = 32;        // tile cols
 constexpr int TPX = TH * TW;  // pixels per tile
 constexpr int NT = 256;       // threads per block for tile kernels
 constexpr int PPT = TPX / NT; // tile pixels per thread
-constexpr int MAX_SLOTS = 272;
+constexpr int MAX_SLOTS = 400;  // >= 2 MAX_S + 1 + MAX_NSC (C^T hv, C^T v, v.hv, Z^T hv)
 
 struct Geom {
   int rb;    // blur radius (0 if no blur)
@@ -44,20 +63,25 @@ struct Geom {
 
 __host__ __device__ inline int imax(int a, int b) { return a > b ? a : b; }
 
+constexpr int NWARP = NT / 32;  // warps per tile block (the filter stage runs one filter per warp)
+
 __host__ __device__ inline Geom make_geom(const kr_op& op) {
   Geom g;
   g.rb = (op.data_kind == KR_DATA_BLUR) ? op.blur_size / 2 : 0;
   g.rq = (op.reg_kind == KR_REG_FILTERS) ? op.ksize / 2 : 0;
   g.H = imax(imax(2 * g.rb, 2 * g.rq), 1);
-  g.RW = TW + 2 * g.H;
+  // odd row stride (in doubles): the row-run passes map lanes to rows, and an odd
+  // stride puts the 32 rows of a warp on distinct bank pairs
+  g.RW = TW + 2 * g.H + 1;
   g.RH = TH + 2 * g.H;
   g.s0 = g.RH * g.RW;
-  int s1 = (op.data_kind == KR_DATA_BLUR) ? (TH + 4 * g.rb) * (TW + 2 * g.rb) : 0;
-  int s3 = (op.data_kind == KR_DATA_BLUR) ? (TH + 2 * g.rb) * TW : 0;
-  int s4 = (op.reg_kind == KR_REG_FILTERS) ? (TH + 2 * g.rq) * (TW + 2 * g.rq) : 0;
+  const int w1p = TW + 2 * g.rb + 1;  // padded (odd) strides of the blur scratch
+  int s1 = (op.data_kind == KR_DATA_BLUR) ? (TH + 4 * g.rb) * w1p : 0;
+  int s3 = (op.data_kind == KR_DATA_BLUR) ? (TH + 2 * g.rb) * (TW + 1) : 0;
+  int s4 = (op.reg_kind == KR_REG_FILTERS) ? NWARP * (TH + 2 * g.rq) * (TW + 2 * g.rq) : 0;
   int s5 = (op.reg_kind == KR_REG_TV) ? 2 * (TH + 1) * (TW + 1) : 0;
   g.sa = imax(imax(s1, s3), imax(s4, s5));
-  g.sb = (op.data_kind == KR_DATA_BLUR) ? (TH + 2 * g.rb) * (TW + 2 * g.rb) : 0;
+  g.sb = (op.data_kind == KR_DATA_BLUR) ? (TH + 2 * g.rb) * w1p : 0;
   g.kw = (op.reg_kind == KR_REG_FILTERS) ? op.num_filters * op.ksize * op.ksize : 0;
   g.total = g.s0 + g.sa + g.sb + TPX + g.kw + KR_MAX_FILTERS + KR_MAX_BLUR + 1;
   return g;
@@ -261,9 +285,163 @@ __device__ inline void tile_hvp_dense(const kr_op& op, int b, const TileIn& in, 
   block_barrier();
 }
 
+// Run length (outputs per thread along a pass) for a pass with `lanes` independent
+// lines of `len` outputs and a BS-tap kernel: minimises rounds x (FMAs + loads) per thread.
+__host__ __device__ constexpr int pick_run(int lanes, int len, int BS) {
+  int best = 1;
+  long long best_cost = -1;
+  for (int r = 1; r <= 8; ++r) {
+    const long long items = (long long)lanes * ((len + r - 1) / r);
+    const long long rounds = (items + NT - 1) / NT;
+    const long long cost = rounds * (r * BS + r + BS - 1);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = r;
+    }
+  }
+  return best;
+}
+
+// Blur data term res += data_scale * A^T A v for a compile-time blur size BS: four
+// separable passes, taps in registers, each thread a run of outputs along the pass
+// (a sliding window: RUN + BS - 1 loads for RUN * BS FMAs).  Row passes map lanes to
+// rows (odd smem strides keep them conflict-free), column passes map lanes to columns.
+// Every output accumulates its taps in the order u = 0 .. BS-1 (the generic path's order).
+template <int BS>
+__device__ inline void blur_normal_bs(const kr_op& op, const Geom& g, Smem& sm, int y0, int x0) {
+  constexpr int RB = BS / 2;
+  constexpr int H1 = TH + 4 * RB, W1 = TW + 2 * RB, W1P = W1 + 1, H2 = TH + 2 * RB, W3P = TW + 1;
+  constexpr int RX1 = pick_run(H1, W1, BS), RY2 = pick_run(W1, H2, BS), RX3 = pick_run(H2, TW, BS),
+                RY4 = pick_run(TW, TH, BS);
+  const int H = g.H, RW = g.RW, rows = op.rows, cols = op.cols;
+  const int tid = threadIdx.x;
+  double tp[BS];
+#pragma unroll
+  for (int u = 0; u < BS; ++u) tp[u] = sm.taps[u];
+  // pass 1: S1[r][c] = sum_u tp[u] S0[r + H - 2RB][c + H - u]   (rows r < H1, cols c < W1)
+  double* S1 = sm.SA;
+  {
+    constexpr int NC = (W1 + RX1 - 1) / RX1;
+    for (int item = tid; item < H1 * NC; item += NT) {
+      const int r = item % H1, c0 = (item / H1) * RX1;
+      const double* src = sm.S0 + (r + H - 2 * RB) * RW + c0 + H - (BS - 1);  // window column m
+      double acc[RX1];
+#pragma unroll
+      for (int i = 0; i < RX1; ++i) acc[i] = 0.0;
+#pragma unroll
+      for (int m = BS + RX1 - 2; m >= 0; --m) {  // u = i + BS - 1 - m ascending
+        const double v = src[m];
+#pragma unroll
+        for (int i = 0; i < RX1; ++i) {
+          const int u = i + BS - 1 - m;
+          if (u >= 0 && u < BS) acc[i] = fma(tp[u], v, acc[i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < RX1; ++i)
+        if (c0 + i < W1) S1[r * W1P + c0 + i] = acc[i];
+    }
+  }
+  block_barrier();
+  // pass 2: S2[r][c] = sum_u tp[u] S1[r + 2RB - u][c], zero outside the image (rows r < H2)
+  double* S2 = sm.SB;
+  {
+    constexpr int NR = (H2 + RY2 - 1) / RY2;
+    for (int item = tid; item < W1 * NR; item += NT) {
+      const int c = item % W1, r0 = (item / W1) * RY2;
+      const double* src = S1 + r0 * W1P + c;  // window row m = S1 row r0 + m
+      double acc[RY2];
+#pragma unroll
+      for (int i = 0; i < RY2; ++i) acc[i] = 0.0;
+#pragma unroll
+      for (int m = BS + RY2 - 2; m >= 0; --m) {  // output i reads S1 row r0 + i + 2RB - u
+        const double v = (r0 + m < H1) ? src[m * W1P] : 0.0;
+#pragma unroll
+        for (int i = 0; i < RY2; ++i) {
+          const int u = i + 2 * RB - m;
+          if (u >= 0 && u < BS) acc[i] = fma(tp[u], v, acc[i]);
+        }
+      }
+      const int x = x0 - RB + c;
+#pragma unroll
+      for (int i = 0; i < RY2; ++i) {
+        const int r = r0 + i, y = y0 - RB + r;
+        if (r < H2) S2[r * W1P + c] = (y >= 0 && y < rows && x >= 0 && x < cols) ? acc[i] : 0.0;
+      }
+    }
+  }
+  block_barrier();
+  // pass 3: S3[r][c] = sum_u tp[u] S2[r][c + u]   (rows r < H2, cols c < TW)
+  double* S3 = sm.SA;
+  {
+    constexpr int NC = (TW + RX3 - 1) / RX3;
+    for (int item = tid; item < H2 * NC; item += NT) {
+      const int r = item % H2, c0 = (item / H2) * RX3;
+      const double* src = S2 + r * W1P + c0;
+      double acc[RX3];
+#pragma unroll
+      for (int i = 0; i < RX3; ++i) acc[i] = 0.0;
+#pragma unroll
+      for (int m = 0; m < BS + RX3 - 1; ++m) {  // u = m - i ascending
+        const double v = (c0 + m < W1) ? src[m] : 0.0;
+#pragma unroll
+        for (int i = 0; i < RX3; ++i) {
+          const int u = m - i;
+          if (u >= 0 && u < BS) acc[i] = fma(tp[u], v, acc[i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < RX3; ++i)
+        if (c0 + i < TW) S3[r * W3P + c0 + i] = acc[i];
+    }
+  }
+  block_barrier();
+  // pass 4: res[r][c] += data_scale * sum_u tp[u] S3[r + u][c]
+  {
+    const double ds = op.data_scale;
+    constexpr int NR = (TH + RY4 - 1) / RY4;
+    for (int item = tid; item < TW * NR; item += NT) {
+      const int c = item % TW, r0 = (item / TW) * RY4;
+      const double* src = S3 + r0 * W3P + c;
+      double acc[RY4];
+#pragma unroll
+      for (int i = 0; i < RY4; ++i) acc[i] = 0.0;
+#pragma unroll
+      for (int m = 0; m < BS + RY4 - 1; ++m) {
+        const double v = (r0 + m < H2) ? src[m * W3P] : 0.0;
+#pragma unroll
+        for (int i = 0; i < RY4; ++i) {
+          const int u = m - i;
+          if (u >= 0 && u < BS) acc[i] = fma(tp[u], v, acc[i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < RY4; ++i)
+        if (r0 + i < TH) sm.res[(r0 + i) * TW + c] += ds * acc[i];
+    }
+  }
+  block_barrier();
+}
+
+__device__ inline void tile_blur_normal_generic(const kr_op& op, const Geom& g, Smem& sm, int y0, int x0,
+                                                bool accumulate);
+
 // Blur data term on the loaded region: res (+)= data_scale * A^T A v.
 __device__ inline void tile_blur_normal(const kr_op& op, const Geom& g, Smem& sm, int y0, int x0,
                                         bool accumulate) {
+  if (accumulate) {
+    switch (op.blur_size) {
+      case 9: blur_normal_bs<9>(op, g, sm, y0, x0); return;
+      case 15: blur_normal_bs<15>(op, g, sm, y0, x0); return;
+      case 21: blur_normal_bs<21>(op, g, sm, y0, x0); return;
+      default: break;
+    }
+  }
+  tile_blur_normal_generic(op, g, sm, y0, x0, accumulate);
+}
+
+__device__ inline void tile_blur_normal_generic(const kr_op& op, const Geom& g, Smem& sm, int y0, int x0,
+                                                bool accumulate) {
   const int rb = g.rb, bs = op.blur_size, H = g.H;
   const int rows = op.rows, cols = op.cols;
   const double* __restrict__ tp = sm.taps;
@@ -314,30 +492,34 @@ __device__ inline void tile_blur_normal(const kr_op& op, const Geom& g, Smem& sm
   block_barrier();
 }
 
-// Learned-filter part of H v for a compile-time filter size Q (register-blocked):
-//   stage 1: e_j = kappa_j . (c_j * v) on the (TH+2R) x (TW+2R) extended tile, each
-//            thread a strip of RB1 rows of one column (loads (RB1+Q-1)Q, FMAs RB1 Q^2);
-//   stage 2: out += w_j corr(e_j, c_j) on the tile, each thread RB2 rows of one column;
-//   the filter weights live in registers, the per-thread outputs accumulate over all
-//   J filters in registers and are added to sm.res once.
+// Learned-filter part of H v for a compile-time filter size Q.  The J filters run
+// concurrently, one per warp (filters j = warp, warp + NWARP, ...), each warp with its
+// own scratch S4_w in smem and only __syncwarp between its stages:
+//   stage 1: e_j = kappa_j . (c_j * v) on the (TH+2R) x (TW+2R) extended tile, a lane a
+//            strip of RB1 rows of one column (loads (RB1+Q-1)Q, FMAs RB1 Q^2; the strip's
+//            curvatures are loaded before the FMAs);
+//   stage 2: out_w += w_j corr(e_j, c_j) on the tile, a lane RB2 rows of 4 columns;
+// then the per-warp sums are added in warp order (fixed, deterministic) to sm.res.
 template <int Q>
 __device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, int b, int y0, int x0) {
   constexpr int R = Q / 2;
-  constexpr int EW = TW + 2 * R, EH = TH + 2 * R;
+  constexpr int EW = TW + 2 * R, EH = TH + 2 * R, ES = EW * EH;
   constexpr int RB1 = Q <= 3 ? 6 : (Q <= 5 ? 5 : 4);  // taller strips: fewer smem loads per FMA
   constexpr int NCH1 = (EH + RB1 - 1) / RB1;
-  constexpr int RB2 = 4;  // stage-2 rows per thread: TW * TH / RB2 = 128 active threads
+  constexpr int RB2 = 4;
+  constexpr int NI2 = TPX / RB2 / 32;  // stage-2 items per lane
+  static_assert(TPX % (RB2 * 32) == 0 && TH % RB2 == 0, "stage-2 partition");
   const int rows = op.rows, cols = op.cols, H = g.H, RW = g.RW;
   const int64_t n = op_n(op);
-  double* S4 = sm.SA;
   const bool quad = op.potential == KR_POT_QUADRATIC;
-  const int tid = threadIdx.x;
-  const int tx2 = tid % TW, r2 = (tid / TW) * RB2;
-  const bool active2 = tid < TW * (TH / RB2);
-  double out[RB2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* S4 = sm.SA + warp * ES;
+  double out[NI2][RB2];
 #pragma unroll
-  for (int i = 0; i < RB2; ++i) out[i] = 0.0;
-  for (int j = 0; j < op.num_filters; ++j) {
+  for (int it = 0; it < NI2; ++it)
+#pragma unroll
+    for (int i = 0; i < RB2; ++i) out[it][i] = 0.0;
+  for (int j = warp; j < op.num_filters; j += NWARP) {
     double k[Q][Q];
     const double* kj = sm.kw + j * Q * Q;
 #pragma unroll
@@ -345,8 +527,25 @@ __device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, 
 #pragma unroll
       for (int bb = 0; bb < Q; ++bb) k[a][bb] = kj[a * Q + bb];
     const double* cj = quad ? nullptr : op.curv + ((int64_t)b * op.num_filters + j) * n;
-    for (int item = tid; item < EW * NCH1; item += NT) {
+    // curvature of a strip: loaded one item ahead (the L2 latency overlaps the FMAs)
+    auto load_cv = [&](int item, double (&cv)[RB1]) {
       const int c = item % EW, r0 = (item / EW) * RB1;
+      const int x = x0 - R + c;
+#pragma unroll
+      for (int i = 0; i < RB1; ++i) {
+        const int y = y0 - R + r0 + i;
+        const bool in = item < EW * NCH1 && r0 + i < EH && y >= 0 && y < rows && x >= 0 && x < cols;
+        cv[i] = in ? (quad ? 2.0 : __ldg(cj + (int64_t)y * cols + x)) : 0.0;
+      }
+    };
+    double cvn[RB1];
+    load_cv(lane, cvn);
+    for (int item = lane; item < EW * NCH1; item += 32) {
+      const int c = item % EW, r0 = (item / EW) * RB1;
+      double cv[RB1];
+#pragma unroll
+      for (int i = 0; i < RB1; ++i) cv[i] = cvn[i];
+      load_cv(item + 32, cvn);
       double acc[RB1];
 #pragma unroll
       for (int i = 0; i < RB1; ++i) acc[i] = 0.0;
@@ -366,18 +565,15 @@ __device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, 
         }
       }
 #pragma unroll
-      for (int i = 0; i < RB1; ++i) {
-        const int r = r0 + i;
-        if (r < EH) {
-          const int y = y0 - R + r, x = x0 - R + c;
-          double e = 0.0;
-          if (y >= 0 && y < rows && x >= 0 && x < cols) e = quad ? 2.0 * acc[i] : cj[(int64_t)y * cols + x] * acc[i];
-          S4[r * EW + c] = e;
-        }
-      }
+      for (int i = 0; i < RB1; ++i)
+        if (r0 + i < EH) S4[(r0 + i) * EW + c] = cv[i] * acc[i];
     }
-    block_barrier();
-    if (active2) {
+    __syncwarp();
+    const double wj = sm.fw[j];
+#pragma unroll
+    for (int it = 0; it < NI2; ++it) {
+      const int item = lane + 32 * it;
+      const int tx2 = item % TW, r2 = (item / TW) * RB2;
       double acc2[RB2];
 #pragma unroll
       for (int i = 0; i < RB2; ++i) acc2[i] = 0.0;
@@ -396,15 +592,26 @@ __device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, 
           }
         }
       }
-      const double wj = sm.fw[j];
 #pragma unroll
-      for (int i = 0; i < RB2; ++i) out[i] = fma(wj, acc2[i], out[i]);
+      for (int i = 0; i < RB2; ++i) out[it][i] = fma(wj, acc2[i], out[it][i]);
     }
-    block_barrier();
+    __syncwarp();
   }
-  if (active2) {
+  block_barrier();  // every warp is done with its S4: reuse SA for the per-warp sums
+  double* P = sm.SA;
 #pragma unroll
-    for (int i = 0; i < RB2; ++i) sm.res[(r2 + i) * TW + tx2] += out[i];
+  for (int it = 0; it < NI2; ++it) {
+    const int item = lane + 32 * it;
+    const int tx2 = item % TW, r2 = (item / TW) * RB2;
+#pragma unroll
+    for (int i = 0; i < RB2; ++i) P[warp * TPX + (r2 + i) * TW + tx2] = out[it][i];
+  }
+  block_barrier();
+  for (int l = threadIdx.x; l < TPX; l += NT) {
+    double a = 0.0;
+#pragma unroll
+    for (int w = 0; w < NWARP; ++w) a += P[w * TPX + l];
+    sm.res[l] += a;
   }
   block_barrier();
 }
@@ -426,8 +633,12 @@ __device__ inline void tile_hvp_t(const kr_op& op, const Geom& g, Smem& sm, int 
   const int y0 = (tile / tyc) * TH, x0 = (tile % tyc) * TW;
   const int rows = op.rows, cols = op.cols, H = g.H;
   const int64_t n = op_n(op);
+#ifdef KR_RMINRES_TIMING
+  unsigned long long slast = kr_gtime0();
+#endif
   load_region(op, g, in, y0, x0, sm.S0);
   block_barrier();
+  KR_SMARK(0, slast);
 
   // pointwise part: mask data term + ridge
   const double* mask = (op.data_kind == KR_DATA_MASK) ? op.mask + (int64_t)b * op.mask_bstride : nullptr;
@@ -443,10 +654,13 @@ __device__ inline void tile_hvp_t(const kr_op& op, const Geom& g, Smem& sm, int 
     sm.res[l] = acc;
   }
   block_barrier();
+  KR_SMARK(1, slast);
   if (op.data_kind == KR_DATA_BLUR) tile_blur_normal(op, g, sm, y0, x0, true);
+  KR_SMARK(2, slast);
 
   if (Q > 0 && op.reg_kind == KR_REG_FILTERS) {
     tile_filters_q<(Q > 0 ? Q : 1)>(op, g, sm, b, y0, x0);
+    KR_SMARK(3, slast);
   } else if (op.reg_kind == KR_REG_FILTERS) {
     const int q = op.ksize, rq = g.rq;
     const int w4 = TW + 2 * rq, h4 = TH + 2 * rq;

@@ -81,11 +81,33 @@ __device__ inline double* lanczos(const Params& P, int b, int k, int site = 0) {
 
 // All cross-block traffic is within a sample (its Gs blocks share partials), so the
 // "grid" barrier is a per-sample barrier: one counter per sample, Gs arrivals.
+#ifdef KR_RMINRES_TIMING
+__device__ __forceinline__ unsigned long long kr_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define KR_TMARK(i)                                   \
+  do {                                                \
+    if (threadIdx.x == 0) {                           \
+      const unsigned long long t_ = kr_gtime();       \
+      tsec[i] += t_ - tlast;                          \
+      tlast = t_;                                     \
+    }                                                 \
+  } while (0)
+#else
+#define KR_TMARK(i) ((void)0)
+#endif
+
 #define KR_GRID_SYNC() grid_barrier(reinterpret_cast<unsigned int*>(P.w.done) + 1 + bl, P.Gs, grid_target)
 
 template <int Q>
 __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
   unsigned int grid_target = 0;
+#ifdef KR_RMINRES_TIMING
+  unsigned long long tsec[12] = {0}, tlast = kr_gtime();
+  int tk = 0;
+#endif
   extern __shared__ double smem[];
   const kr_op& op = P.op;
   const kr_solve_args& A = P.a;
@@ -97,8 +119,14 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
   double* btc1 = chv + 2 * MAX_S;  // chv holds C^T hv [0,s) and C^T v [s,2s)
   double* btc2 = btc1 + MAX_S;
   double* omega = btc2 + MAX_S;
-  double* nscv = omega + MAX_S;          // MAX_NSC
-  double* red = nscv + MAX_NSC;          // RED_DOUBLES
+  // NSC in s-space: zrv = Z^T r_v, zhA / zhB = Z^T hvt_{k-1} / Z^T hvt_{k-2} (the
+  // residual recurrence krylov.py:169-181 applied to Z^T r), zhv = Z^T hv_k
+  double* nscv = omega + MAX_S;          // MAX_NSC (squared terms of the NSC value)
+  double* zrv = nscv + MAX_NSC;          // MAX_NSC
+  double* zhA = zrv + MAX_NSC;           // MAX_NSC
+  double* zhB = zhA + MAX_NSC;           // MAX_NSC
+  double* zhv = zhB + MAX_NSC;           // MAX_NSC
+  double* red = zhv + MAX_NSC;           // RED_DOUBLES
 #ifdef KR_VOLATILE_SC
   __shared__ volatile Scalars sc;
 #else
@@ -111,13 +139,15 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
   const int b = P.b0 + bl;               // global sample index
   const int64_t n = P.n;
   const int s = A.s, ns = (A.stop_kind == 1) ? A.nsc_s : 0;
-  const int SL_CHV = 0, SL_NSC = 2 * s, SL_ALPHA = 2 * s + ns, SL_BETA2 = 2 * s + ns + 1;
+  // slots: [C^T hv (s) | C^T v (s) | v.hv | Z^T hv (ns)] contiguous (one reduction in P2),
+  // then Z^T r0 (setup) and ||u||^2
+  const int SL_CHV = 0, SL_ALPHA = 2 * s, SL_ZHV = 2 * s + 1, SL_NSC = 2 * s + 1 + ns, SL_BETA2 = 2 * s + 1 + 2 * ns;
   const int64_t lo = n * j / P.Gs, hi = n * (j + 1) / P.Gs;
   const int ntiles = num_tiles(op);
   const bool leader = (j == 0);
   const bool track = A.track_residual != 0;
   const Partials PP = P.parts();
-  KR_ASSERT(b < op.batch && bl < P.nb && s <= MAX_S && 2 * s + 1 <= MAX_SLOTS && ns <= MAX_NSC && hi <= n);
+  KR_ASSERT(b < op.batch && bl < P.nb && s <= MAX_S && 2 * s + 1 + ns <= MAX_SLOTS && ns <= MAX_NSC && hi <= n);
 
   const double* U = A.U ? A.U + (int64_t)b * A.bs_uc : nullptr;
   const double* C = A.C ? A.C + (int64_t)b * A.bs_uc : nullptr;
@@ -139,6 +169,12 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
     btc1[i] = 0.0;
     btc2[i] = 0.0;
     omega[i] = 0.0;
+  }
+  for (int i = threadIdx.x; i < MAX_NSC; i += blockDim.x) {
+    zrv[i] = 0.0;
+    zhA[i] = 0.0;
+    zhB[i] = 0.0;
+    zhv[i] = 0.0;
   }
   if (threadIdx.x == 0) {
     sc.active = 1;
@@ -232,6 +268,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
   }
   KR_GRID_SYNC();
   reduce_slots(PP, bl, SL_ALPHA, 1, red1);
+  if (ns > 0) reduce_slots(PP, bl, SL_NSC, ns, zrv);  // Z^T r0_v
   block_barrier();
   if (threadIdx.x == 0) {
     double gg = red1[0];
@@ -241,6 +278,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
   block_barrier();
 
   // ---------------- main loop ----------------
+  KR_TMARK(0);
   for (int k = 1; k <= A.max_iter + 1; ++k) {
     // this sample is finished and reported: its blocks leave (sc is block-shared and
     // identical across the sample's blocks, so all of them leave at the same k)
@@ -256,10 +294,14 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
     }
 #endif
     // ===== P1 =====
+#ifdef KR_RMINRES_TIMING
+    tk = k;
+#endif
     if (sc.active) {
       reduce_slots(PP, bl, SL_BETA2, 1, red1);
       block_barrier();
     }
+    KR_TMARK(1);
     if (threadIdx.x == 0) {
       sc.do_update = 0;
       sc.do_hvp = 0;
@@ -329,6 +371,14 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
         btc2[i] = btc1[i];
         btc1[i] = bt;
       }
+      // Z^T of the tracked-residual recurrence: hvt_{k-1} = (hv_{k-1} - delta hvt_{k-2}
+      // - gamma hvt_{k-3}) / eps~, r_v -= step hvt_{k-1}
+      for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+        const double zn = (zhv[i] - sc.delta * zhA[i] - sc.gamma * zhB[i]) / sc.eps_r;
+        zrv[i] -= sc.step * zn;
+        zhB[i] = zhA[i];
+        zhA[i] = zn;
+      }
       // pointwise updates of iteration k-1
       const int km = k - 1;
       const double* v = lanczos(P, b, km, 1);
@@ -338,118 +388,43 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
       double* hvtn = vec(P.w.hvt[km & 1], n, b);
       const double* hvto = vec(P.w.hvt[(km + 1) & 1], n, b);
       const double ga = sc.gamma, de = sc.delta, er = sc.eps_r, st = sc.step;
-      for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
-        double vt = (v[p] - ga * vtn[p] - de * vto[p]) / er;
-        vtn[p] = vt;
-        wv[p] = wv[p] + st * vt;
+      // two pixels per thread per round, every load issued before the first store
+      for (int64_t p0 = lo + threadIdx.x; p0 < hi; p0 += 2 * NT) {
+        const int64_t p1 = p0 + NT;
+        const bool h1 = p1 < hi;
+        const int64_t q1 = h1 ? p1 : p0;
+        const double v0 = v[p0], v1 = v[q1], a0 = vtn[p0], a1 = vtn[q1], o0 = vto[p0], o1 = vto[q1];
+        const double w0 = wv[p0], w1 = wv[q1];
+        double x0 = 0.0, x1 = 0.0, ho0 = 0.0, ho1 = 0.0, hn0 = 0.0, hn1 = 0.0, r0 = 0.0, r1 = 0.0;
         if (track) {
-          double ht = (hvk[p] - de * hvto[p] - ga * hvtn[p]) / er;
-          hvtn[p] = ht;
-          rv[p] -= st * ht;
+          x0 = hvk[p0]; x1 = hvk[q1]; ho0 = hvto[p0]; ho1 = hvto[q1]; hn0 = hvtn[p0]; hn1 = hvtn[q1];
+          r0 = rv[p0]; r1 = rv[q1];
+        }
+        const double vt0 = (v0 - ga * a0 - de * o0) / er, vt1 = (v1 - ga * a1 - de * o1) / er;
+        vtn[p0] = vt0;
+        wv[p0] = w0 + st * vt0;
+        if (h1) {
+          vtn[p1] = vt1;
+          wv[p1] = w1 + st * vt1;
+        }
+        if (track) {
+          const double ht0 = (x0 - de * ho0 - ga * hn0) / er, ht1 = (x1 - de * ho1 - ga * hn1) / er;
+          hvtn[p0] = ht0;
+          rv[p0] = r0 - st * ht0;
+          if (h1) {
+            hvtn[p1] = ht1;
+            rv[p1] = r1 - st * ht1;
+          }
         }
       }
     }
     block_barrier();
-    if (sc.pending && k > 1 && sc.do_update) {
-      for (int i = threadIdx.x; i < ns; i += blockDim.x) slot_acc[i] = 0.0;
-      block_barrier();
-      slot_dots(Z, A.ld_z, ns, lo, hi, [&](int64_t p) { return rv[p]; }, slot_acc, red);
-      write_partials(PP, bl, j, SL_NSC, ns, slot_acc);
-    }
-    if (sc.finished && !sc.counted) {
-      // finalize: w = w_v - U Omega, r = r_v + C Omega (krylov.py:184-202 outputs)
-      double* wout = A.w + (int64_t)b * n;
-      double* rout = (track && A.r) ? A.r + (int64_t)b * n : nullptr;
-      for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
-        double uo = 0.0, co = 0.0;
-        for (int i = 0; i < s; ++i) {
-          uo += U[(int64_t)i * A.ld_uc + p] * omega[i];
-          co += C[(int64_t)i * A.ld_uc + p] * omega[i];
-        }
-        wout[p] = wv[p] - uo;
-        if (rout) rout[p] = rv[p] + co;
-      }
-    }
-    if (sc.do_hvp) {
-      const double beta_k = sc.beta;
-      double* vk = lanczos(P, b, k, 2);
-      for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) vk[p] = tmp[p] / beta_k;
-      for (int i = threadIdx.x; i < 2 * s + 1; i += blockDim.x) slot_acc[i] = 0.0;
-      block_barrier();
-      double* hvk = vec(P.w.hv[k & 1], n, b);
-      const int npass = s > 0 ? (s + 7) / 8 : 1;
-      const bool deferred = npass <= DEF_PASSES;
-      if (deferred) {  // warp sums accumulate in red over passes and tiles
-        for (int i = threadIdx.x; i < npass * 17 * DEF_STRIDE; i += blockDim.x) red[i] = 0.0;
-        block_barrier();
-      }
-      for (int tile = j; tile < ntiles; tile += P.Gs) {
-        tile_hvp_t<Q>(op, g, sm, b, TileIn{tmp, beta_k, nullptr, 0.0}, tile);
-        for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
-          int64_t p = tile_pixel(op, tile, l);
-          if (p >= 0) hvk[p] = sm.res[l];
-        }
-        // partials over this tile: C^T hv, C^T v and v . hv (alpha = v.hv - (C^T v).(C^T hv)),
-        // 8 columns per pass; with <= DEF_PASSES passes the warp sums stay in registers
-        // (accumulated over the block's tiles) and are combined once after the tile loop
-        for (int base = 0; base < (s > 0 ? s : 1); base += 8) {
-          double v16[17];
-#pragma unroll
-          for (int i = 0; i < 17; ++i) v16[i] = 0.0;
-          for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
-            int64_t p = tile_pixel(op, tile, l);
-            if (p < 0) continue;
-            const double h = sm.res[l];
-            double v;
-            if (op.data_kind == KR_DATA_DENSE) {
-              v = tmp[p] / beta_k;
-            } else {
-              const int ty = l / TW, tx = l - ty * TW;
-              v = sm.S0[(ty + g.H) * g.RW + tx + g.H];
-            }
-            if (base == 0) v16[16] += v * h;
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (base + i < s) {
-                const double c = C[(int64_t)(base + i) * A.ld_uc + p];
-                v16[i] += c * h;
-                v16[8 + i] += c * v;
-              }
-          }
-          if (deferred) {
-            def_add<17>(MultiSum<17>::reduce(v16, threadIdx.x & 31), base / 8, red);
-            continue;
-          }
-          block_sum<17>(v16, red);
-          if (threadIdx.x < 8 && base + threadIdx.x < s) {
-            slot_acc[base + threadIdx.x] += red[threadIdx.x];
-            slot_acc[s + base + threadIdx.x] += red[8 + threadIdx.x];
-          }
-          if (threadIdx.x == 0 && base == 0) slot_acc[2 * s] += red[16];
-          block_barrier();
-        }
-        block_barrier();
-      }
-      if (deferred) {
-        // value (pass q, i): i < 8 -> C^T hv column 8q+i, 8..15 -> C^T v column 8q+i-8, 16 (q = 0) -> v.hv
-        for (int c = threadIdx.x; c < s; c += blockDim.x) {
-          slot_acc[c] = def_sum(red, (c / 8) * 17 + c % 8);
-          slot_acc[s + c] = def_sum(red, (c / 8) * 17 + 8 + c % 8);
-        }
-        if (threadIdx.x == 0) slot_acc[2 * s] = def_sum(red, 16);
-        block_barrier();
-      }
-      write_partials(PP, bl, j, SL_CHV, 2 * s, slot_acc);
-      write_partial1(PP, bl, j, SL_ALPHA, slot_acc[2 * s]);
-    }
-    KR_GRID_SYNC();
-    // ===== P2 =====
+    KR_TMARK(2);
     if (sc.pending) {
-      reduce_slots(PP, bl, SL_NSC, ns, nscv);
-      block_barrier();
-      // (Z^T r)_i = (Z^T r_v)_i + (Z^T C Omega)_i, squared, one thread per column
+      // NSC of iteration pend_k (stopping.py:69-72): (Z^T r)_i = zrv_i + (Z^T C Omega)_i,
+      // decided here, before the next H v (no pass over Z, no extra grid barrier)
       for (int i = threadIdx.x; i < ns; i += blockDim.x) {
-        double z = nscv[i];
+        double z = zrv[i];
         if (ZtC) {
           double c0 = 0.0, c1 = 0.0;
           int l = 0;
@@ -480,24 +455,138 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
         sc.do_hvp = sc.do_hvp && sc.active;
       }
       block_barrier();
-      if (sc.finished && !sc.counted) {
-        double* wout = A.w + (int64_t)b * n;
-        double* rout = (track && A.r) ? A.r + (int64_t)b * n : nullptr;
-        for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
-          double uo = 0.0, co = 0.0;
-          for (int i = 0; i < s; ++i) {
-            uo += U[(int64_t)i * A.ld_uc + p] * omega[i];
-            co += C[(int64_t)i * A.ld_uc + p] * omega[i];
-          }
-          wout[p] = wv[p] - uo;
-          if (rout) rout[p] = rv[p] + co;
+    }
+    KR_TMARK(3);
+    if (sc.finished && !sc.counted) {
+      // finalize: w = w_v - U Omega, r = r_v + C Omega (krylov.py:184-202 outputs)
+      double* wout = A.w + (int64_t)b * n;
+      double* rout = (track && A.r) ? A.r + (int64_t)b * n : nullptr;
+      for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+        double uo = 0.0, co = 0.0;
+        for (int i = 0; i < s; ++i) {
+          uo += U[(int64_t)i * A.ld_uc + p] * omega[i];
+          co += C[(int64_t)i * A.ld_uc + p] * omega[i];
         }
+        wout[p] = wv[p] - uo;
+        if (rout) rout[p] = rv[p] + co;
       }
     }
     if (sc.do_hvp) {
+      const double beta_k = sc.beta;
+      double* vk = lanczos(P, b, k, 2);  // written from the stencil's region (v = u / beta)
+      for (int i = threadIdx.x; i < 2 * s + 1 + ns; i += blockDim.x) slot_acc[i] = 0.0;
+      block_barrier();
+      double* hvk = vec(P.w.hv[k & 1], n, b);
+      const int sm8 = s > ns ? s : ns;
+      const int npass = sm8 > 0 ? (sm8 + 7) / 8 : 1;
+      const bool deferred = npass <= DEF_PASSES;
+      if (deferred) {  // warp sums accumulate in red over passes and tiles
+        for (int i = threadIdx.x; i < npass * 25 * DEF_STRIDE; i += blockDim.x) red[i] = 0.0;
+        block_barrier();
+      }
+      for (int tile = j; tile < ntiles; tile += P.Gs) {
+        KR_TMARK(4);
+        tile_hvp_t<Q>(op, g, sm, b, TileIn{tmp, beta_k, nullptr, 0.0}, tile);
+        KR_TMARK(5);
+        for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
+          int64_t p = tile_pixel(op, tile, l);
+          if (p >= 0) {
+            hvk[p] = sm.res[l];
+            if (op.data_kind == KR_DATA_DENSE) {
+              vk[p] = tmp[p] / beta_k;
+            } else {
+              const int ty = l / TW, tx = l - ty * TW;
+              vk[p] = sm.S0[(ty + g.H) * g.RW + tx + g.H];
+            }
+          }
+        }
+        // partials over this tile: C^T hv, C^T v, Z^T hv (NSC) and v . hv
+        // (alpha = v.hv - (C^T v).(C^T hv)), 8 columns per pass; with <= DEF_PASSES passes
+        // the warp sums stay in registers (accumulated over the block's tiles) and are
+        // combined once after the tile loop
+        for (int base = 0; base < sm8 || base == 0; base += 8) {
+          double v25[25];
+#pragma unroll
+          for (int i = 0; i < 25; ++i) v25[i] = 0.0;
+          static_assert(TPX == 2 * NT, "two tile pixels per thread");
+          {
+            // both of the thread's pixels: all 2 x 16 column loads in flight at once
+            int64_t pp[2];
+            double hh[2], vv[2], cc[2][8], zz[2][8];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int l = threadIdx.x + u * NT;
+              pp[u] = tile_pixel(op, tile, l);
+              const int64_t q = pp[u] >= 0 ? pp[u] : 0;
+              hh[u] = sm.res[l];
+              if (op.data_kind == KR_DATA_DENSE) {
+                vv[u] = pp[u] >= 0 ? tmp[q] / beta_k : 0.0;
+              } else {
+                const int ty = l / TW, tx = l - ty * TW;
+                vv[u] = sm.S0[(ty + g.H) * g.RW + tx + g.H];
+              }
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                cc[u][i] = (pp[u] >= 0 && base + i < s) ? C[(int64_t)(base + i) * A.ld_uc + q] : 0.0;
+                zz[u][i] = (pp[u] >= 0 && base + i < ns) ? Z[(int64_t)(base + i) * A.ld_z + q] : 0.0;
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              if (pp[u] < 0) continue;
+              const double h = hh[u], v = vv[u];
+              if (base == 0) v25[24] += v * h;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                if (base + i < s) {
+                  v25[i] += cc[u][i] * h;
+                  v25[8 + i] += cc[u][i] * v;
+                }
+                if (base + i < ns) v25[16 + i] += zz[u][i] * h;
+              }
+            }
+          }
+          if (deferred) {
+            def_add<25>(MultiSum<25>::reduce(v25, threadIdx.x & 31), base / 8, red);
+            continue;
+          }
+          block_sum<25>(v25, red);
+          if (threadIdx.x < 8 && base + threadIdx.x < s) {
+            slot_acc[base + threadIdx.x] += red[threadIdx.x];
+            slot_acc[s + base + threadIdx.x] += red[8 + threadIdx.x];
+          }
+          if (threadIdx.x < 8 && base + threadIdx.x < ns) slot_acc[2 * s + 1 + base + threadIdx.x] += red[16 + threadIdx.x];
+          if (threadIdx.x == 0 && base == 0) slot_acc[2 * s] += red[24];
+          block_barrier();
+        }
+        block_barrier();
+      }
+      if (deferred) {
+        // value (pass q, i): i < 8 -> C^T hv column 8q+i, 8..15 -> C^T v column 8q+i-8,
+        // 16..23 -> Z^T hv column 8q+i-16, 24 (q = 0) -> v.hv
+        for (int c = threadIdx.x; c < s; c += blockDim.x) {
+          slot_acc[c] = def_sum(red, (c / 8) * 25 + c % 8);
+          slot_acc[s + c] = def_sum(red, (c / 8) * 25 + 8 + c % 8);
+        }
+        for (int c = threadIdx.x; c < ns; c += blockDim.x) slot_acc[2 * s + 1 + c] = def_sum(red, (c / 8) * 25 + 16 + c % 8);
+        if (threadIdx.x == 0) slot_acc[2 * s] = def_sum(red, 24);
+        block_barrier();
+      }
+      write_partials(PP, bl, j, SL_CHV, 2 * s + 1 + ns, slot_acc);  // C^T hv, C^T v, v.hv, Z^T hv
+    }
+    KR_TMARK(6);
+    KR_GRID_SYNC();
+    KR_TMARK(7);
+    // ===== P2 ===== (the NSC decision moved to P1: s-space recurrence)
+    KR_TMARK(8);
+    if (sc.do_hvp) {
       // chv = C^T hv, cv = C^T v, alpha = v.hv - cv.chv  (== v.(hv - C chv), krylov.py:269-283)
-      reduce_slots(PP, bl, SL_CHV, 2 * s, chv);  // chv[0..s) and cv at chv[s..2s) (MAX_S >= 2s is checked)
-      reduce_slots(PP, bl, SL_ALPHA, 1, red1);
+      // one reduction of the contiguous slots into slot_acc (free until the next dots phase)
+      reduce_slots(PP, bl, SL_CHV, 2 * s + 1 + ns, slot_acc);
+      block_barrier();
+      for (int i = threadIdx.x; i < 2 * s; i += blockDim.x) chv[i] = slot_acc[i];  // chv[0..s), cv at chv[s..2s)
+      for (int i = threadIdx.x; i < ns; i += blockDim.x) zhv[i] = slot_acc[2 * s + 1 + i];  // Z^T hv_k for the next P1
+      if (threadIdx.x == 0) red1[0] = slot_acc[2 * s];
       block_barrier();
       if (threadIdx.x == 0) {
         double a = red1[0];
@@ -511,17 +600,43 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
       const double* vkm = (k > 1) ? lanczos(P, b, k - 1, 4) : nullptr;
       const double* hvk = vec(P.w.hv[k & 1], n, b);
       double bsq[1] = {0.0};
-      for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
-        double x = hvk[p];
+      // two pixels per thread per round; C read 8 columns at a time with all loads in flight
+      for (int64_t p0 = lo + threadIdx.x; p0 < hi; p0 += 2 * NT) {
+        const int64_t p1 = p0 + NT;
+        const bool h1 = p1 < hi;
+        const int64_t q1 = h1 ? p1 : p0;
+        double x0 = hvk[p0], x1 = hvk[q1];
+        const double vk0 = vk[p0], vk1 = vk[q1];
+        const double vm0 = vkm ? vkm[p0] : 0.0, vm1 = vkm ? vkm[q1] : 0.0;
         if (s > 0) {
-          double cc = 0.0;
-          for (int i = 0; i < s; ++i) cc += C[(int64_t)i * A.ld_uc + p] * chv[i];
-          x = x - cc;  // vnext = hv - C chv
+          double cc0 = 0.0, cc1 = 0.0;
+          for (int i0 = 0; i0 < s; i0 += 8) {
+            double c0[8], c1[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              c0[i] = (i0 + i < s) ? C[(int64_t)(i0 + i) * A.ld_uc + p0] : 0.0;
+              c1[i] = (i0 + i < s) ? C[(int64_t)(i0 + i) * A.ld_uc + q1] : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (i0 + i < s) {
+                cc0 += c0[i] * chv[i0 + i];
+                cc1 += c1[i] * chv[i0 + i];
+              }
+          }
+          x0 = x0 - cc0;  // vnext = hv - C chv
+          x1 = x1 - cc1;
         }
-        x = x - al * vk[p];                // vnext -= alpha v
-        x = x - be * (vkm ? vkm[p] : 0.0);  // vnext -= beta v_prev
-        tmp[p] = x;
-        bsq[0] += x * x;
+        x0 = x0 - al * vk0;  // vnext -= alpha v
+        x1 = x1 - al * vk1;
+        x0 = x0 - be * vm0;  // vnext -= beta v_prev
+        x1 = x1 - be * vm1;
+        tmp[p0] = x0;
+        bsq[0] += x0 * x0;
+        if (h1) {
+          tmp[p1] = x1;
+          bsq[0] += x1 * x1;
+        }
       }
       block_sum<1>(bsq, red);
       if (threadIdx.x == 0) P.w.part[((int64_t)bl * P.nslot + SL_BETA2) * P.Gs + j] = red[0];
@@ -540,8 +655,20 @@ __global__ void __launch_bounds__(NT, 2) rminres_kernel(Params P) {
       }
       block_barrier();
     }
+    KR_TMARK(9);
     KR_GRID_SYNC();
+    KR_TMARK(10);
   }
+#ifdef KR_RMINRES_TIMING
+  if (threadIdx.x == 0 && bl == 0 && (j == 0 || j == P.Gs / 2))
+    printf("rminres timing b=%d j=%d/%d k=%d ns: setup %llu | p1-scalar %llu upd %llu nsc %llu vk+fin %llu stencil %llu "
+           "dots %llu | gsync1 %llu | p2-nsc %llu p2-u %llu | gsync2 %llu\n",
+           b, j, P.Gs, tk, tsec[0], tsec[1], tsec[2], tsec[3], tsec[4], tsec[5], tsec[6], tsec[7], tsec[8], tsec[9],
+           tsec[10]);
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    printf("stencil block0 ns: region %llu pointwise %llu blur %llu filters %llu\n", g_stencil_ns[0], g_stencil_ns[1],
+           g_stencil_ns[2], g_stencil_ns[3]);
+#endif
 }
 
 }  // namespace kr
@@ -561,12 +688,12 @@ struct Layout {
 int plan(const kr_op& op, const kr_solve_args& a, Layout& L) {
   const int64_t n = op_n(op);
   Geom g = make_geom(op);
-  L.smem = sizeof(double) * ((size_t)g.total + MAX_SLOTS + 5 * MAX_S + MAX_NSC + RED_DOUBLES);
+  L.smem = sizeof(double) * ((size_t)g.total + MAX_SLOTS + 5 * MAX_S + 5 * MAX_NSC + RED_DOUBLES);
   int sms = device_sms();
   int per_sm = 0;
   if (sms > 0) {
     if (L.smem > 48 * 1024)
-      cudaFuncSetAttribute(KR_PICK_Q(rminres_kernel, q_variant(op)), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+      ensure_smem(KR_PICK_Q(rminres_kernel, q_variant(op)), L.smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, KR_PICK_Q(rminres_kernel, q_variant(op)), NT, L.smem);
   }
   if (per_sm < 1) per_sm = 1;
@@ -583,7 +710,7 @@ int plan(const kr_op& op, const kr_solve_args& a, Layout& L) {
   if (Gs < 1) Gs = 1;
   L.Gs = Gs;
   int ns = a.stop_kind == 1 ? a.nsc_s : 0;
-  L.nslot = 2 * a.s + ns + 2;
+  L.nslot = 2 * a.s + 2 * ns + 2;
   L.vec_doubles = (int64_t)B * n * (a.basis ? 11 : 13);
   L.part_doubles = (int64_t)L.chunk * L.nslot * Gs;
   L.total = L.vec_doubles + L.part_doubles + 2 + (L.chunk + 1) / 2;  // + one barrier counter per sample

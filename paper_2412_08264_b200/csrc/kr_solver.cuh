@@ -38,7 +38,7 @@ struct Partials {
 // order as block_sum, without a block barrier per pass.
 constexpr int DEF_PASSES = 4;   // passes kept in registers
 constexpr int DEF_STRIDE = 9;   // >= warps per block (8) + 1, odd: conflict-free
-constexpr int RED_DOUBLES = 640;  // reduction scratch: max(17 * 33 + 17, 17 * DEF_PASSES * DEF_STRIDE)
+constexpr int RED_DOUBLES = 912;  // reduction scratch: max(25 * 33 + 25, 25 * DEF_PASSES * DEF_STRIDE)
 
 template <int NV>
 __device__ inline void def_add(double r, int pass, double* red) {  // r: this lane's MultiSum<NV> result
@@ -109,15 +109,16 @@ __device__ inline void write_partial1(const Partials& P, int bl, int j, int slot
 }
 
 // out[i] = sum over the sample's Gs blocks.  A warp per slot: lanes read the
-// Gs partials coalesced (4 slots in flight per warp), then a fixed shuffle tree
+// Gs partials coalesced (8 slots in flight per warp), then a fixed shuffle tree
 // -- deterministic (the same order every run and for every block).  Callers
 // synchronise the block before reading out[].
 __device__ inline void reduce_slots(const Partials& P, int bl, int slot0, int S, double* out) {
+  constexpr int INF = 8;  // slots in flight per warp
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int i0 = warp; i0 < S; i0 += 4 * nw) {
-    double acc[4];
+  for (int i0 = warp; i0 < S; i0 += INF * nw) {
+    double acc[INF];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < INF; ++u) {
       const int i = i0 + u * nw;
       double a = 0.0;
       if (i < S) {
@@ -127,7 +128,7 @@ __device__ inline void reduce_slots(const Partials& P, int bl, int slot0, int S,
       acc[u] = a;
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < INF; ++u) {
       const double v = warp_sum(acc[u]);
       const int i = i0 + u * nw;
       if (lane == 0 && i < S) out[i] = v;

@@ -135,9 +135,14 @@ def _as_batch(H, g):
         raise ValueError(f"right-hand side of shape {tuple(g.shape)}, operator dim {H.dim}")
     if G.shape[0] != H.batch:
         raise ValueError(f"{G.shape[0]} right-hand sides for an operator batch of {H.batch}")
-    if not bool(torch.isfinite(G).all()):
-        raise ValueError("right-hand side contains non-finite entries")
+    # checked with the solve's results (one device -> host transfer per launch, no sync here)
     return G.contiguous(), single
+
+
+def _batched_gram(A, Bm):
+    from .batched import gram
+
+    return gram(A, Bm)
 
 
 def _per_sample(x, B):
@@ -193,17 +198,27 @@ class _Launch:
             w0 = as_device(w0).reshape(B, n).contiguous()
             self.keep.append(w0)
             a.w0 = w0.data_ptr()
+        self.finite = torch.isfinite(G).all()  # krylov.py contract: non-finite g -> ValueError
         dims = [0 if r is None else r.dim for r in recycles]
         s = max(dims) if dims else 0
         self.dims = dims
         a.s = s
+        # recycle spaces written by the batched update into whole-batch (B, s, n) rows
+        # are read in place; anything else is stacked (zero-padded to s columns)
+        src = [getattr(r, "batch_src", None) for r in recycles]
+        self.inplace = (s > 0 and not _PAD and all(x is not None for x in src)
+                        and all(x[0] is src[0][0] and x[3] == b for b, x in enumerate(src))
+                        and tuple(src[0][0].shape) == (B, s, n) and all(d == s for d in dims))
         if s:
-            U = _buf("U", B, s, n, zero=True, dev=dev)
-            C = _buf("C", B, s, n, zero=True, dev=dev)
-            for b, r in enumerate(recycles):
-                if r is not None and r.dim:
-                    U[b, : r.dim] = r.U.T
-                    C[b, : r.dim] = r.C.T
+            if self.inplace:
+                U, C = src[0][0], src[0][1]
+            else:
+                U = _buf("U", B, s, n, zero=True, dev=dev)
+                C = _buf("C", B, s, n, zero=True, dev=dev)
+                for b, r in enumerate(recycles):
+                    if r is not None and r.dim:
+                        U[b, : r.dim] = r.U.T
+                        C[b, : r.dim] = r.C.T
             self.U, self.C = U, C
             self.keep += [U, C]
             a.U, a.C, a.ld_uc, a.bs_uc = U.data_ptr(), C.data_ptr(), n, s * n
@@ -234,13 +249,19 @@ class _Launch:
         if kind == 1:
             zs = [r.data.z_block() for r in rules]
             ns = max(z.shape[1] for z in zs)
-            Z = _buf("Z", B, ns, n, zero=True, dev=dev)
-            for b, z in enumerate(zs):
-                Z[b, : z.shape[1]] = z.T
+            zsrc = src[0][2] if s and self.inplace else None
+            if (zsrc is not None and ns == s
+                    and all(z.data_ptr() == zsrc[b].data_ptr() and z.shape[1] == s for b, z in enumerate(zs))):
+                Z = zsrc
+            else:
+                Z = _buf("Z", B, ns, n, zero=True, dev=dev)
+                for b, z in enumerate(zs):
+                    Z[b, : z.shape[1]] = z.T
             a.nsc_s, a.Z, a.ld_z, a.bs_z = ns, Z.data_ptr(), n, ns * n
             self.keep.append(Z)
             if s:
-                ZtC = torch.bmm(Z, self.C.transpose(1, 2)).contiguous()  # (B, ns, s)
+                # (B, ns, s) Z^T C: split-K Gram over the pixels when the blocks are square
+                ZtC = (_batched_gram(Z, self.C) if ns == s else torch.bmm(Z, self.C.transpose(1, 2))).contiguous()
                 a.ZtC = ZtC.data_ptr()
                 self.keep.append(ZtC)
         self.w = _buf("w", B, n, dev=dev)
@@ -285,7 +306,10 @@ class _Launch:
         # one device -> host transfer for all the per-sample scalars and histories
         m = self.max_iter + 1
         host = torch.cat([self.iters.to(torch.float64), self.reasons.to(torch.float64), self.res.reshape(-1),
-                          self.vals.reshape(-1)]).cpu().numpy()
+                          self.vals.reshape(-1), self.finite.to(torch.float64).reshape(1)]).cpu().numpy()
+        if host[-1] != 1.0:
+            raise ValueError("right-hand side contains non-finite entries")
+        host = host[:-1]
         iters = host[: self.B].astype(np.int64)
         reasons = host[self.B: 2 * self.B].astype(np.int64)
         res = host[2 * self.B: 2 * self.B + self.B * m].reshape(self.B, m)
