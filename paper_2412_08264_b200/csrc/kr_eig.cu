@@ -56,6 +56,14 @@ __device__ __forceinline__ int64_t pk(int i, int j) { return (int64_t)i * (i + 1
 
 __device__ __forceinline__ double sym_at(const double* Ap, int i, int j) { return i >= j ? Ap[pk(i, j)] : Ap[pk(j, i)]; }
 
+// 32-bit packed index (t <= EIG_TPACK keeps it far below 2^31): the hot loops' address math
+__device__ __forceinline__ int pk32(int i, int j) { return ((i * (i + 1)) >> 1) + j; }  // i >= j
+
+__device__ __forceinline__ double sym_at32(const double* Ap, int i, int j) {
+  const int hi = i >= j ? i : j, lo = i >= j ? j : i;  // branch-free: one load per lane
+  return Ap[pk32(hi, lo)];
+}
+
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -89,8 +97,8 @@ __device__ int sturm_count(const double* __restrict__ d, const double* __restric
   double p = d[0] - x;
   if (p == 0.0) p = -pivmin;
   int cnt = p < 0.0;
-  for (int i = 1; i < t; ++i) {
-    double pn = fma(d[i] - x, p, -e2[i - 1] * pm1);
+  auto step = [&](double di, double ei) {
+    double pn = fma(di - x, p, -ei * pm1);
     if (pn == 0.0) pn = -pivmin * p;
     cnt += (pn < 0.0) != (p < 0.0);
     pm1 = p;
@@ -102,7 +110,17 @@ __device__ int sturm_count(const double* __restrict__ d, const double* __restric
       p = ldexp(p, -ex);
       pm1 = ldexp(pm1, -ex);
     }
+  };
+  int i = 1;
+  for (; i + 3 < t; i += 4) {  // operands of four steps loaded ahead of the recurrence
+    const double d0 = d[i], d1 = d[i + 1], d2 = d[i + 2], d3 = d[i + 3];
+    const double f0 = e2[i - 1], f1 = e2[i], f2 = e2[i + 1], f3 = e2[i + 2];
+    step(d0, f0);
+    step(d1, f1);
+    step(d2, f2);
+    step(d3, f3);
   }
+  for (; i < t; ++i) step(d[i], e2[i - 1]);
   return cnt;
 }
 
@@ -165,20 +183,33 @@ __device__ void lagtf(const double* __restrict__ d, const double* __restrict__ e
 
 // Solve (T - lambda I) y = x in place with the factors (LAPACK lagts, job -1).
 __device__ void lagts(const TriLU& f, int t, double* __restrict__ y) {
+  // the running element stays in a register (same operations as the in-memory form)
+  double prev = y[0];
+#pragma unroll 4
   for (int k = 1; k < t; ++k) {
+    double yk = y[k];
+    const double ck = f.c[k - 1];
     if (!f.piv[k - 1]) {
-      y[k] -= f.c[k - 1] * y[k - 1];
+      yk -= ck * prev;
+      y[k - 1] = prev;
+      prev = yk;
     } else {
-      const double temp = y[k - 1];
-      y[k - 1] = y[k];
-      y[k] = temp - f.c[k - 1] * y[k];
+      const double temp = prev;
+      y[k - 1] = yk;
+      prev = temp - ck * yk;
     }
   }
+  y[t - 1] = prev;
+  double y1 = 0.0, y2 = 0.0;  // y[k + 1], y[k + 2]
+#pragma unroll 4
   for (int k = t - 1; k >= 0; --k) {
     double temp = y[k];
-    if (k + 1 < t) temp -= f.b[k] * y[k + 1];
-    if (k + 2 < t) temp -= f.dd[k] * y[k + 2];
-    y[k] = temp * f.ra[k];
+    if (k + 1 < t) temp -= f.b[k] * y1;
+    if (k + 2 < t) temp -= f.dd[k] * y2;
+    const double yk = temp * f.ra[k];
+    y[k] = yk;
+    y2 = y1;
+    y1 = yk;
   }
 }
 
@@ -216,6 +247,16 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
   double* R = red + EIG_RED;
   __shared__ int s_int[4];
 
+#ifdef KR_EIG_TIMING
+  long long ec[12] = {0}, elast = clock64();
+#define KR_EMARK(i)                                                   \
+  do {                                                                \
+    __syncthreads();                                                  \
+    if (tid == 0) { const long long c_ = clock64(); ec[i] += c_ - elast; elast = c_; } \
+  } while (0)
+#else
+#define KR_EMARK(i) ((void)0)
+#endif
   // ---------------- 1. tridiagonalization ----------------
   double* vv = R;
   double* yv = R + T;
@@ -243,6 +284,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
       part += x * x;
     }
     const double xn2 = bsum(part, red);
+    KR_EMARK(5);
     const double alpha = Ap[pk(k + 1, k)];
     double tk = 0.0, beta = alpha;
     if (xn2 > 0.0) {
@@ -265,27 +307,51 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
     }
     if (tk == 0.0) continue;  // block-uniform (xn2 is broadcast)
     __syncthreads();
+    KR_EMARK(6);
     // y = tau * A22 v, one warp per row (lower row part + column part via symmetry)
-    for (int r = warp; r < m; r += EW) {
-      const int i = k + 1 + r;
-      double acc = 0.0;
-      for (int c = lane; c < m; c += 32) acc += sym_at(Ap, i, k + 1 + c) * vv[c];
+    // two rows per warp at a time (independent chains; each row's lane order and
+    // shuffle tree as before)
+    for (int r = warp; r < m; r += 2 * EW) {
+      const int r2 = r + EW;
+      const bool two = r2 < m;
+      const int i = k + 1 + r, i2 = k + 1 + (two ? r2 : r);
+      double acc = 0.0, acc2 = 0.0;
+      for (int c = lane; c < m; c += 32) {
+        const double vc = vv[c];
+        acc += sym_at32(Ap, i, k + 1 + c) * vc;
+        acc2 += sym_at32(Ap, i2, k + 1 + c) * vc;
+      }
       acc = warp_sum(acc);
-      if (lane == 0) yv[r] = tk * acc;
-    }
-    __syncthreads();
-    double pv = 0.0;
-    for (int r = tid; r < m; r += ENT) pv += yv[r] * vv[r];
-    const double kappa = -0.5 * tk * bsum(pv, red);
-    // A22 -= v w^T + w v^T with w = y + kappa v (lower part)
-    for (int r = warp; r < m; r += EW) {
-      const double vi = vv[r], wi = yv[r] + kappa * vi;
-      for (int c = lane; c <= r; c += 32) {
-        const double vj = vv[c], wj = yv[c] + kappa * vj;
-        Ap[pk(k + 1 + r, k + 1 + c)] -= vi * wj + wi * vj;
+      acc2 = warp_sum(acc2);
+      if (lane == 0) {
+        yv[r] = tk * acc;
+        if (two) yv[r2] = tk * acc2;
       }
     }
     __syncthreads();
+    KR_EMARK(7);
+    double pv = 0.0;
+    for (int r = tid; r < m; r += ENT) pv += yv[r] * vv[r];
+    const double kappa = -0.5 * tk * bsum(pv, red);
+    KR_EMARK(8);
+    // A22 -= v w^T + w v^T with w = y + kappa v (lower part)
+    // two rows per warp at a time (every element's update is independent and unchanged)
+    for (int r = warp; r < m; r += 2 * EW) {
+      const int r2 = r + EW;
+      const bool two = r2 < m;
+      const double vi = vv[r], wi = yv[r] + kappa * vi;
+      const double vi2 = two ? vv[r2] : 0.0, wi2 = two ? yv[r2] + kappa * vi2 : 0.0;
+      double* row = Ap + pk32(k + 1 + r, k + 1);
+      double* row2 = Ap + pk32(k + 1 + (two ? r2 : r), k + 1);
+      const int cmax = two ? r2 : r;
+      for (int c = lane; c <= cmax; c += 32) {
+        const double vj = vv[c], wj = yv[c] + kappa * vj;
+        if (c <= r) row[c] -= vi * wj + wi * vj;
+        if (two) row2[c] -= vi2 * wj + wi2 * vj;
+      }
+    }
+    __syncthreads();
+    KR_EMARK(9);
   }
   if (tid == 0) {
     d[t - 1] = Ap[pk(t - 1, t - 1)];
@@ -296,6 +362,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
   for (int64_t i = tid; i < pk(t, 0); i += ENT) Hb[i] = Ap[i];
   __syncthreads();
 
+  KR_EMARK(0);
   // ---------------- 2. selected eigenvalues ----------------
   if (warp == 0) {
     double gl = 1e308, gu = -1e308, tn = 0.0, em = 0.0;
@@ -342,6 +409,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
   }
   __syncthreads();
 
+  KR_EMARK(1);
   // ---------------- 3. inverse iteration ----------------
   // clusters of close selected eigenvalues (gap <= 1e-3 ||T||, LAPACK stein's ORTOL);
   // within a cluster the shifts are separated by >= 10 eps |lambda| (PERTOL)
@@ -447,6 +515,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
     __syncthreads();
   }
 
+  KR_EMARK(2);
   // ---------------- 4. back-transformation ----------------
   for (int64_t i = tid; i < pk(t, 0); i += ENT) Ap[i] = Hb[i];
   __syncthreads();
@@ -462,17 +531,22 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
     for (int k = t - 2; k >= 0; --k) {
       const double tk = tau[k];
       if (tk == 0.0) continue;
-      double dot = 0.0;
+      double dot = 0.0, hv[RPL];
 #pragma unroll
       for (int c = 0; c < RPL; ++c) {
         const int i = lane + 32 * c;
-        if (i > k && i < t) dot += (i == k + 1 ? 1.0 : Ap[pk(i, k)]) * z[c];
+        hv[c] = (i > k + 1 && i < t) ? Ap[pk32(i, k)] : 1.0;
+      }
+#pragma unroll
+      for (int c = 0; c < RPL; ++c) {
+        const int i = lane + 32 * c;
+        if (i > k && i < t) dot += hv[c] * z[c];
       }
       dot = tk * warp_sum(dot);
 #pragma unroll
       for (int c = 0; c < RPL; ++c) {
         const int i = lane + 32 * c;
-        if (i > k && i < t) z[c] -= dot * (i == k + 1 ? 1.0 : Ap[pk(i, k)]);
+        if (i > k && i < t) z[c] -= dot * hv[c];
       }
     }
     // sign: largest-magnitude component positive (first one on ties)
@@ -507,6 +581,13 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
     }
     if (lane == 0 && P.lam) P.lam[(int64_t)b * P.bsl + q] = sel[q];
   }
+#ifdef KR_EIG_TIMING
+  KR_EMARK(3);
+  if (tid == 0 && b == 0)
+    printf("eig t=%d s=%d nw=%d cycles: tridiag %lld (norm %lld v %lld matvec %lld pv %lld rank2 %lld) sturm %lld "
+           "inverse %lld back %lld\n", t, s, P.nw, ec[0] + ec[5] + ec[6] + ec[7] + ec[8] + ec[9], ec[5], ec[6], ec[7],
+           ec[8], ec[9], ec[1], ec[2], ec[3]);
+#endif
 }
 
 int64_t eig_smem_doubles(int T, int* nw_out) {
