@@ -552,6 +552,81 @@ __global__ void jw_finish_kernel(kr_op op, const double* __restrict__ G1, const 
   }
 }
 
+// The mixed Jacobian materialised: J w is linear in w, so J W for many columns is
+// one GEMM with the p x n matrix Mt = J (operators.py:411-444 restated per pixel):
+//   Mt[j(1+q^2)]     = -w_j C_j^T phi'_j                                  (theta0 head)
+//   Mt[j(1+q^2)+1+d] = -w_j [ phi'_j(. + delta_d) + C_j^T(phi''_j . xhat(. - delta_d)) ]
+// (the two _shift_dot terms, with <C_j w, phi'' . S_d xhat> = <w, C_j^T(phi'' . S_d xhat)>).
+// One block per (tile, filter, sample): phi'_j, phi''_j on the tile + R halo and xhat on
+// the tile + 2R halo in smem; C_j^T is the correlation sum_{a,b} k[a][b] u(y-R+a, x-R+b).
+template <int Q>
+__global__ void __launch_bounds__(NT) jmat_kernel(kr_op op, double* __restrict__ Mt, int64_t bsm) {
+  constexpr int R = Q / 2, Q2 = Q * Q;
+  constexpr int EW = TW + 2 * R, EH = TH + 2 * R, XW = TW + 4 * R, XH = TH + 4 * R;
+  __shared__ double ps[EH * EW];  // phi'_j
+  __shared__ double pc[EH * EW];  // phi''_j (2 for the quadratic potential), zero outside
+  __shared__ double xs[XH * XW];  // xhat
+  const int tile = blockIdx.x, j = blockIdx.y, b = blockIdx.z, J = op.num_filters;
+  const int tyc = tiles_x(op);
+  const int y0 = (tile / tyc) * TH, x0 = (tile % tyc) * TW;
+  const int rows = op.rows, cols = op.cols;
+  const int64_t n = op_n(op);
+  const bool quad = op.potential == KR_POT_QUADRATIC;
+  const double* sl = op.slope + ((int64_t)b * J + j) * n;
+  const double* cv = quad ? nullptr : op.curv + ((int64_t)b * J + j) * n;
+  const double* xh = op.xhat + (int64_t)b * n;
+  for (int i = threadIdx.x; i < EH * EW; i += NT) {
+    const int y = y0 - R + i / EW, x = x0 - R + i % EW;
+    const bool in = y >= 0 && y < rows && x >= 0 && x < cols;
+    const int64_t pp = (int64_t)y * cols + x;
+    ps[i] = in ? sl[pp] : 0.0;
+    pc[i] = in ? (quad ? 2.0 : cv[pp]) : 0.0;
+  }
+  for (int i = threadIdx.x; i < XH * XW; i += NT) {
+    const int y = y0 - 2 * R + i / XW, x = x0 - 2 * R + i % XW;
+    xs[i] = (y >= 0 && y < rows && x >= 0 && x < cols) ? xh[(int64_t)y * cols + x] : 0.0;
+  }
+  double k[Q2];
+#pragma unroll
+  for (int i = 0; i < Q2; ++i) k[i] = op.kernels[j * Q2 + i];
+  const double nw = -op.fweights[j];
+  block_barrier();
+  double* base = Mt + (int64_t)b * bsm + (int64_t)j * (1 + Q2) * n;
+  for (int l = threadIdx.x; l < TPX; l += NT) {
+    const int ty = l / TW, tx = l - ty * TW;
+    const int y = y0 + ty, x = x0 + tx;
+    if (y >= rows || x >= cols) continue;
+    const int64_t p = (int64_t)y * cols + x;
+    double h = 0.0;
+#pragma unroll
+    for (int a = 0; a < Q; ++a)
+#pragma unroll
+      for (int bb = 0; bb < Q; ++bb) h = fma(k[a * Q + bb], ps[(ty + a) * EW + tx + bb], h);
+    base[p] = nw * h;
+    for (int d = 0; d < Q2; ++d) {
+      const int da = d / Q - R, db = d % Q - R;
+      double v = 0.0;
+      const double* xr = xs + (ty + R - da) * XW + tx + R - db;
+#pragma unroll
+      for (int a = 0; a < Q; ++a)
+#pragma unroll
+        for (int bb = 0; bb < Q; ++bb) v = fma(k[a * Q + bb], pc[(ty + a) * EW + tx + bb] * xr[a * XW + bb], v);
+      v += ps[(ty + R + da) * EW + tx + R + db];
+      base[(int64_t)(1 + d) * n + p] = nw * v;
+    }
+  }
+}
+
+static bool jw_jmat_path(const kr_op& op, int ncols) { return q_variant(op) > 0 && ncols >= 4; }
+
+// samples per jmat pass: the materialised J of a pass stays under 64 M doubles (512 MB)
+static int jmat_chunk(const kr_op& op) {
+  const int64_t per = (int64_t)op.num_filters * (1 + op.ksize * op.ksize) * op_n(op);
+  int64_t c = ((int64_t)64 << 20) / (per > 0 ? per : 1);
+  if (c < 1) c = 1;
+  return (int)(c < op.batch ? c : op.batch);
+}
+
 static bool jw_gemm_path(const kr_op& op, int ncols) { return q_variant(op) > 0 && ncols >= 4; }
 
 // split-K chunking of the pixel dimension: kc full chunks of Kc pixels + one remainder
@@ -576,6 +651,8 @@ static int64_t jw_workspace(const kr_op& op, int ncols) {
 
 extern "C" int64_t kr_jadj_workspace(const kr_op* op, int32_t ncols) {
   if (!op || validate_op(*op) != KR_OK) return -1;
+  if (jw_jmat_path(*op, ncols))
+    return (int64_t)jmat_chunk(*op) * op->num_filters * (1 + op->ksize * op->ksize) * op_n(*op);
   if (jw_gemm_path(*op, ncols)) return jw_workspace(*op, ncols);
   int64_t P = (op->reg_kind == KR_REG_TV) ? 1 : (int64_t)op->num_filters * (1 + op->ksize * op->ksize);
   return (int64_t)op->batch * ncols * num_tiles(*op) * P;
@@ -640,6 +717,42 @@ static int jadj_gemm(const kr_op& op, const double* W, int64_t ldw, int64_t bsw,
   return KR_OK;
 }
 
+// J W through the materialised Jacobian: one jmat launch for all samples, then one
+// strided-batched DGEMM  JW_b (cols x p) = W_b Mt_b^T.
+static int jadj_jmat(const kr_op& op, const double* W, int64_t ldw, int64_t bsw, int32_t ncols, double* JW,
+                     int64_t ldo, int64_t bso, double* work, cudaStream_t st) {
+  const int64_t n = op_n(op);
+  const int q = op.ksize, P = op.num_filters * (1 + q * q);
+  KR_CHECK_ARG(ldo >= P, "output leading dimension smaller than p");
+  const int64_t bsm = (int64_t)P * n;
+  const void* fn = q == 3 ? (const void*)jmat_kernel<3> : q == 5 ? (const void*)jmat_kernel<5>
+                                                               : (const void*)jmat_kernel<7>;
+  cublasHandle_t h;
+  KR_TRY(cublas_handle(&h, st));
+  const double one = 1.0, zero = 0.0;
+  const int chunk = jmat_chunk(op);
+  for (int b0 = 0; b0 < op.batch; b0 += chunk) {
+    const int nb = (op.batch - b0) < chunk ? (op.batch - b0) : chunk;
+    kr_op opv = op;  // samples b0 .. b0+nb-1 as a batch of nb
+    opv.batch = nb;
+    opv.slope = op.slope + (int64_t)b0 * op.num_filters * n;
+    if (op.curv) opv.curv = op.curv + (int64_t)b0 * op.num_filters * n;
+    opv.xhat = op.xhat + (int64_t)b0 * n;
+    double* Mt = work;
+    int64_t bsmv = bsm;
+    void* args[] = {&opv, &Mt, &bsmv};
+    cudaError_t e = cudaLaunchKernel(fn, dim3(num_tiles(op), op.num_filters, nb), dim3(NT), args, 0, st);
+    if (e != cudaSuccess) return fail(KR_ECUDA, std::string("jmat launch: ") + cudaGetErrorString(e));
+    KR_TRY(check_launch("jmat"));
+    // column-major: out (P x cols, ld ldo) = Mt^T (P x n) * W (n x cols, ld ldw)
+    KR_TRY(cublas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_T, CUBLAS_OP_N, P, ncols, (int)n, &one, Mt, (int)n,
+                                                  bsm, W + (int64_t)b0 * bsw, (int)ldw, bsw, &zero,
+                                                  JW + (int64_t)b0 * bso, (int)ldo, bso, nb),
+                        "dgemm Mt W"));
+  }
+  return KR_OK;
+}
+
 extern "C" int kr_jadj(const kr_op* op, const double* W, int64_t ldw, int64_t bsw, int32_t ncols, double* JW,
                        int64_t ldo, int64_t bso, double* work, int64_t work_len, kr_stream_t stream) {
   KR_CHECK_ARG(op != nullptr, "null operator");
@@ -651,6 +764,7 @@ extern "C" int kr_jadj(const kr_op* op, const double* W, int64_t ldw, int64_t bs
   const int ntiles = num_tiles(*op);
   dim3 grid(ntiles, ncols, op->batch);
   cudaStream_t st = (cudaStream_t)stream;
+  if (jw_jmat_path(*op, ncols)) return jadj_jmat(*op, W, ldw, bsw, ncols, JW, ldo, bso, work, st);
   if (jw_gemm_path(*op, ncols)) return jadj_gemm(*op, W, ldw, bsw, ncols, JW, ldo, bso, work, st);
   int P;
   if (op->reg_kind == KR_REG_FILTERS) {
