@@ -142,6 +142,11 @@ class SequenceSolver:
         self.groups = int(os.environ.get("KR_RECYCLE_GROUPS", "2"))
         # the update orchestrated in C++ (kr_recycle_update); 0 = the torch orchestration
         self.native_update = os.environ.get("KR_NATIVE_RECYCLE", "1") != "0"
+        # per-group solves overlapping the other groups' recycle updates (KR_PIPELINE=1).  Off by
+        # default: a persistent solve launched while another group's full-GPU kernels are still
+        # dispatching gets only part of its blocks resident, the resident ones spin at the
+        # per-sample barriers and hold SMs, and the step got slower (C2: 23 -> 28 ms)
+        self.pipelined = os.environ.get("KR_PIPELINE", "0") == "1"
         self._gstreams = None
         self._gpool = None
         self._scratch = {}  # per sample group: the native update's temporaries
@@ -195,7 +200,7 @@ class SequenceSolver:
             return False
         return st.vec_type == "Ritz" or isinstance(jac, StencilJacobian)
 
-    def _recycle_batched(self, hessian, jac, B):
+    def _recycle_batched(self, hessian, jac, B, then=None):
         """Whole-batch recycle update in ``groups`` sample groups, each on its own host
         thread and CUDA stream: a group's latency-bound t x t kernels (one CTA per
         sample) overlap the other groups' GEMMs and stencils."""
@@ -230,7 +235,8 @@ class SequenceSolver:
             return [r if r is not None else self._recycle_one(hessian, jac, B, lo + i) for i, r in enumerate(recs)]
 
         if ng == 1:
-            return run(0, B)
+            recs = run(0, B)
+            return recs if then is None else (recs, then(0, B, recs))
         main = torch.cuda.current_stream()
         if self._gstreams is None or len(self._gstreams) < ng:
             _warm_linalg()
@@ -240,19 +246,29 @@ class SequenceSolver:
         def work(g):
             st = self._gstreams[g]
             st.wait_stream(main)
+            extra = None
             with torch.cuda.stream(st):
                 recs = run(*bounds[g])
+                if then is not None:  # the group's own solve, overlapping the other groups' updates
+                    extra = then(*bounds[g], recs)
             for rec in recs:
                 for t in (rec.U, rec.C) + ((rec.nsc_data.values, rec.nsc_data.v_h, rec.nsc_data.w,
                                            rec.nsc_data.z_block()) if rec.nsc_data is not None else ()):
                     if t is not None:
                         t.record_stream(main)
-            return recs
+            for r in extra or ():
+                for t in (r.solution, r.basis, r.residual_vector):
+                    if t is not None:
+                        t.record_stream(main)
+            return recs, extra
 
-        out = [r for recs in self._gpool.map(work, range(ng)) for r in recs]
+        parts = list(self._gpool.map(work, range(ng)))
         for g in range(ng):
             main.wait_stream(self._gstreams[g])
-        return out
+        out = [r for recs, _ in parts for r in recs]
+        if then is None:
+            return out
+        return out, [r for _, extra in parts for r in extra]
 
     def _recycle_one(self, hessian, jac, B, b):
         cfg = self.cfg
@@ -317,17 +333,29 @@ class SequenceSolver:
         # one batched solve for all samples: the persistent kernel is latency bound per
         # iteration, so a launch over 8 samples costs what one over 4 does
         t0 = _phase_clock()
-        if cfg.strategy.is_none or self._first:
-            recycles = [RecycleSpace.empty(n) for _ in range(B)]
-        else:
-            recycles = self._recycle_all(hessian, jac, B)
-        t1 = _phase_clock()
-        self._first = False
         init = self._prev_solution if cfg.warm_start else None
         if isinstance(init, list):
             init = torch.stack(init)
         solve = rminres if cfg.method == "minres" else rcg
-        results = solve(hessian, g, recycles if B > 1 else recycles[0], self._options(recycles, init))
+        results = None
+        if cfg.strategy.is_none or self._first:
+            recycles = [RecycleSpace.empty(n) for _ in range(B)]
+        elif self.pipelined and B > 1 and self._batched(hessian, jac) and min(self.groups, B) > 1:
+            # each sample group solves right after its own recycle update, on its own
+            # stream: group A's solve overlaps group B's (latency-bound) update kernels.
+            # Per-sample results are bitwise those of one batched launch (same blocks per sample).
+            def then(lo, hi, recs):
+                hs = hessian.slice(lo, hi)
+                w0 = None if init is None else init[lo:hi].contiguous()
+                return solve(hs, g[lo:hi], recs, self._options(recs, w0))
+
+            recycles, results = self._recycle_batched(hessian, jac, B, then=then)
+        else:
+            recycles = self._recycle_all(hessian, jac, B)
+        t1 = _phase_clock()
+        self._first = False
+        if results is None:
+            results = solve(hessian, g, recycles if B > 1 else recycles[0], self._options(recycles, init))
         if t0 is not None:
             t2 = _phase_clock()
             import sys

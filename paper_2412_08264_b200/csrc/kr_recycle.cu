@@ -237,6 +237,38 @@ int h2d(Ctx& c, T* dev, const T* host, size_t cnt) {
   return e == cudaSuccess ? KR_OK : fail(KR_ECUDA, std::string("kr_recycle h2d: ") + cudaGetErrorString(e));
 }
 
+// A per-host-thread side stream for independent work inside one orchestrator call:
+// fork (side waits for main), enqueue, join (record on side), wait (main waits).
+struct SideStream {
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int init() {
+    if (st) return KR_OK;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess)
+      return fail(KR_ECUDA, "kr_recycle side stream");
+    return KR_OK;
+  }
+  int fork(cudaStream_t main) {
+    KR_TRY(init());
+    if (cudaEventRecord(ev_fork, main) != cudaSuccess || cudaStreamWaitEvent(st, ev_fork, 0) != cudaSuccess)
+      return fail(KR_ECUDA, "kr_recycle fork");
+    return KR_OK;
+  }
+  int join(cudaStream_t) {
+    return cudaEventRecord(ev_join, st) == cudaSuccess ? KR_OK : fail(KR_ECUDA, "kr_recycle join");
+  }
+  int wait(cudaStream_t main) {
+    return cudaStreamWaitEvent(main, ev_join, 0) == cudaSuccess ? KR_OK : fail(KR_ECUDA, "kr_recycle wait");
+  }
+};
+
+SideStream& side_stream() {
+  static thread_local SideStream ss;  // one per host thread (device fixed per thread here)
+  return ss;
+}
+
 struct Factor {  // one Cholesky-QR factor of a batch: F (B,T,T), info, stats
   double* F;
   int32_t* info;
@@ -567,11 +599,18 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
     sym_and_s_kernel<<<dim3(T, B), 256, 0, c.st>>>(Ht, Jt, p, T, Hs, S);
     Ht = Hs;
     // condition bracket of Ht: (max L_jj / min L_jj)^2 <= cond <= ||Ht||_F ||L^-1||_F^2
+    // (on a side stream: independent of the GSVD's CholQR2 below, whose one-CTA-per-matrix
+    // Cholesky kernels it would otherwise wait behind)
     Factor fh = new_factor(c, B, T);
-    KR_TRY(chol(c, Ht, d_td, B, T, false, nullptr, fh));
     double* hn = c.take(2 * B);
-    frob2_kernel<<<B, FROB_NT, 0, c.st>>>(Ht, T, T, T, (int64_t)T * T, hn);
-    frob2_kernel<<<B, FROB_NT, 0, c.st>>>(fh.F, T, T, T, (int64_t)T * T, hn + B);
+    SideStream& ss = side_stream();
+    KR_TRY(ss.fork(c.st));
+    KR_TRY(kr_chol_inv(Ht, T, (int64_t)T * T, d_td, B, T, 2, nullptr, fh.F, T, (int64_t)T * T, fh.stats, fh.info,
+                       nullptr, ss.st));
+    frob2_kernel<<<B, FROB_NT, 0, ss.st>>>(Ht, T, T, T, (int64_t)T * T, hn);
+    frob2_kernel<<<B, FROB_NT, 0, ss.st>>>(fh.F, T, T, T, (int64_t)T * T, hn + B);
+    KR_TRY(ss.join(c.st));  // joined before the host reads hn / fh (below, after the eigen launch)
+    bool joined = false;
     // GSVD: [Jt; Ht] = Q R (CholQR2 of the rows of S)
     QrOut qs;
     qs.Q = c.take((int64_t)B * T * P);
@@ -587,6 +626,10 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
     KR_TRY(kr_syev_select(Mq, T, (int64_t)T * T, d_td, B, T, 1, s, nullptr, 0, Zs, T, (int64_t)s * T, d_ns,
                           c.take(el), el, c.st));
     // the bracket decision (host), overlapping the eigen kernel
+    if (!joined) {
+      KR_TRY(ss.wait(c.st));
+      joined = true;
+    }
     std::vector<double> hnv, hst;
     std::vector<int32_t> hinf;
     KR_TRY(d2h(c, hnv, hn, 2 * B));

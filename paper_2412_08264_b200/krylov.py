@@ -206,12 +206,14 @@ class _Launch:
         # recycle spaces written by the batched update into whole-batch (B, s, n) rows
         # are read in place; anything else is stacked (zero-padded to s columns)
         src = [getattr(r, "batch_src", None) for r in recycles]
+        off = src[0][3] if src and src[0] is not None else 0
         self.inplace = (s > 0 and not _PAD and all(x is not None for x in src)
-                        and all(x[0] is src[0][0] and x[3] == b for b, x in enumerate(src))
-                        and tuple(src[0][0].shape) == (B, s, n) and all(d == s for d in dims))
+                        and all(x[0] is src[0][0] and x[3] == off + b for b, x in enumerate(src))
+                        and src[0][0].shape[0] >= off + B and tuple(src[0][0].shape[1:]) == (s, n)
+                        and all(d == s for d in dims))
         if s:
             if self.inplace:
-                U, C = src[0][0], src[0][1]
+                U, C = src[0][0][off: off + B], src[0][1][off: off + B]
             else:
                 U = _buf("U", B, s, n, zero=True, dev=dev)
                 C = _buf("C", B, s, n, zero=True, dev=dev)
@@ -249,7 +251,7 @@ class _Launch:
         if kind == 1:
             zs = [r.data.z_block() for r in rules]
             ns = max(z.shape[1] for z in zs)
-            zsrc = src[0][2] if s and self.inplace else None
+            zsrc = src[0][2][off: off + B] if s and self.inplace and src[0][2] is not None else None
             if (zsrc is not None and ns == s
                     and all(z.data_ptr() == zsrc[b].data_ptr() and z.shape[1] == s for b, z in enumerate(zs))):
                 Z = zsrc
