@@ -159,6 +159,10 @@ class SequenceSolver:
     def reserve(self, batch: int, nbytes: int, shape: tuple[int, int] | None = None) -> None:
         """Pre-size the caching-allocator pools of the per-sample worker streams (each
         stream has its own pool) so steady-state steps never call cudaMalloc."""
+        # the allocator's small-block pool (blocks <= 1 MB, 2 MB segments) on the caller's
+        # stream: the per-solve vectors (w, r, histories) come from it
+        small = [torch.empty(1 << 17, dtype=torch.float64, device="cuda") for _ in range(24)]
+        del small
         if batch <= 1 or self.max_workers <= 1:
             return
         _warm_linalg()

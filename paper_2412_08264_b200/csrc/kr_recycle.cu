@@ -321,6 +321,93 @@ int64_t house_lwork(int64_t n, int T) {
   return std::max(lw1, lw2);
 }
 
+// Orthonormal rows Wb (t x n) spanning the candidate rows Ab when the Cholesky-QR passes
+// broke down at row k1 (exactly dependent candidates -- late Lanczos bases lose
+// orthogonality): rows [0, k1) by shifted CholeskyQR3 (that block factored), rows
+// [k1, t) by a Householder QR of the remainder after two block Gram-Schmidt passes
+// against them, its completion directions projected twice more and re-orthonormalised
+// (CholQR2).  A Householder QR of n x (t - k1) instead of n x t (~0.5 ms instead of ~4.5 ms
+// at n = 16384, t = 220).  ok = false: a pass broke down (brk = its row) -- the caller
+// retries with a smaller k1 or takes the full Householder QR.
+int block_house(Ctx& c, const double* Ab, int t, int k1, int64_t n, double* Wb, double* Rem, double* hwk, int64_t hwl,
+                double* tau, bool& ok, int& brk) {
+  ok = false;
+  brk = -1;
+  const int m = t - k1;
+  const double one = 1.0, zero = 0.0, mone = -1.0;
+  int32_t* dk = reinterpret_cast<int32_t*>(c.take(2));
+  int32_t* dm = reinterpret_cast<int32_t*>(c.take(2));
+  double* dsh = c.take(1);
+  const double sh = 11.0 * ((double)n * k1 + (double)k1 * (k1 + 1)) * 2.220446049250313e-16 * k1;
+  KR_TRY(h2d(c, dk, &k1, 1));
+  KR_TRY(h2d(c, dm, &m, 1));
+  KR_TRY(h2d(c, dsh, &sh, 1));
+  double* G = c.take((int64_t)t * t);
+  double* Cp = c.take((int64_t)t * t);
+  Factor f1 = new_factor(c, 1, k1), f2 = new_factor(c, 1, k1), f3 = new_factor(c, 1, k1);
+  Factor g1 = new_factor(c, 1, m), g2 = new_factor(c, 1, m);
+  // leading block: shifted CholeskyQR3 into Wb[0, k1), Rem as scratch
+  KR_TRY(gram(c, Ab, Ab, 1, k1, n, G));
+  KR_TRY(chol(c, G, dk, 1, k1, true, dsh, f1));
+  KR_TRY(rows_mul(c, f1.F, 0, Ab, n, 0, Rem, n, 0, k1, k1, n, 1));
+  KR_TRY(gram(c, Rem, Rem, 1, k1, n, G));
+  KR_TRY(chol(c, G, dk, 1, k1, false, nullptr, f2));
+  KR_TRY(rows_mul(c, f2.F, 0, Rem, n, 0, Wb, n, 0, k1, k1, n, 1));
+  KR_TRY(gram(c, Wb, Wb, 1, k1, n, G));
+  KR_TRY(chol(c, G, dk, 1, k1, false, nullptr, f3));
+  KR_TRY(rows_mul(c, f3.F, 0, Wb, n, 0, Rem, n, 0, k1, k1, n, 1));
+  KR_TRY(cudaMemcpyAsync(Wb, Rem, sizeof(double) * k1 * n, cudaMemcpyDeviceToDevice, c.st) == cudaSuccess
+             ? KR_OK : fail(KR_ECUDA, "block_house copy"));
+  std::vector<int32_t> a1, a2, a3;
+  KR_TRY(d2h(c, a1, f1.info, 1));
+  KR_TRY(d2h(c, a2, f2.info, 1));
+  KR_TRY(d2h(c, a3, f3.info, 1));
+  for (int v : {a1[0], a2[0], a3[0]})
+    if (v >= 0 && (brk < 0 || v < brk)) brk = v;
+  if (brk >= 0) return KR_OK;
+  // remainder rows, projected twice: Rem -= W1 (W1^T Rem)   (column-major n x m / n x k1 views)
+  KR_TRY(cudaMemcpyAsync(Rem, Ab + (int64_t)k1 * n, sizeof(double) * m * n, cudaMemcpyDeviceToDevice, c.st) ==
+                 cudaSuccess ? KR_OK : fail(KR_ECUDA, "block_house copy"));
+  auto project = [&]() -> int {
+    for (int pass = 0; pass < 2; ++pass) {
+      KR_TRY(cublas_check(cublasDgemm(c.h, CUBLAS_OP_T, CUBLAS_OP_N, k1, m, (int)n, &one, Wb, (int)n, Rem, (int)n,
+                                      &zero, Cp, k1), "block_house W1^T R"));
+      KR_TRY(cublas_check(cublasDgemm(c.h, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, m, k1, &mone, Wb, (int)n, Cp, k1, &one,
+                                      Rem, (int)n), "block_house R -= W1 C"));
+    }
+    return KR_OK;
+  };
+  KR_TRY(project());
+  // Householder QR of the narrow remainder -> orthonormal Q2 (n x m) in Rem
+  cusolverDnHandle_t shd;
+  KR_TRY(cusolver_handle(&shd, c.st));
+  int lw1 = 0, lw2 = 0;
+  cusolverDnDgeqrf_bufferSize(shd, (int)n, m, Rem, (int)n, &lw1);
+  cusolverDnDorgqr_bufferSize(shd, (int)n, m, m, Rem, (int)n, tau, &lw2);
+  const int lw = std::max(lw1, lw2);
+  if (hwk == nullptr || lw + 1 > hwl) return fail(KR_ENOMEM, "kr_recycle: block Householder work buffer");
+  int32_t* dinfo = reinterpret_cast<int32_t*>(hwk + lw);
+  if (cusolverDnDgeqrf(shd, (int)n, m, Rem, (int)n, tau, hwk, lw, dinfo) != CUSOLVER_STATUS_SUCCESS ||
+      cusolverDnDorgqr(shd, (int)n, m, m, Rem, (int)n, tau, hwk, lw, dinfo) != CUSOLVER_STATUS_SUCCESS)
+    return fail(KR_ECUDA, "kr_recycle: block Householder QR");
+  // completion directions of a rank-deficient remainder are not orthogonal to W1: project, CholQR2
+  KR_TRY(project());
+  double* W2 = Wb + (int64_t)k1 * n;
+  KR_TRY(gram(c, Rem, Rem, 1, m, n, G));
+  KR_TRY(chol(c, G, dm, 1, m, false, nullptr, g1));
+  KR_TRY(rows_mul(c, g1.F, 0, Rem, n, 0, W2, n, 0, m, m, n, 1));
+  KR_TRY(gram(c, W2, W2, 1, m, n, G));
+  KR_TRY(chol(c, G, dm, 1, m, false, nullptr, g2));
+  KR_TRY(rows_mul(c, g2.F, 0, W2, n, 0, Rem, n, 0, m, m, n, 1));
+  KR_TRY(cudaMemcpyAsync(W2, Rem, sizeof(double) * m * n, cudaMemcpyDeviceToDevice, c.st) == cudaSuccess
+             ? KR_OK : fail(KR_ECUDA, "block_house copy"));
+  std::vector<int32_t> b1, b2;
+  KR_TRY(d2h(c, b1, g1.info, 1));
+  KR_TRY(d2h(c, b2, g2.info, 1));
+  ok = b1[0] < 0 && b2[0] < 0;
+  return KR_OK;
+}
+
 int64_t workspace_doubles(const kr_op& op, const kr_recycle_args& a) {
   // generous per-term budget: every Ctx::take of kr_recycle_update is covered with
   // margin (each take also rounds up to 32 doubles); overruns are reported
@@ -336,6 +423,7 @@ int64_t workspace_doubles(const kr_op& op, const kr_recycle_args& a) {
   w += 8 * kr_gram_workspace((int32_t)B, (int32_t)T, n);
   w += kr_jadj_workspace(&op, (int32_t)T) + 3 * kr_syev_select_workspace((int32_t)B, (int32_t)T);
   w += house_lwork(n, (int)T) + 64;                     // Householder branch (cuSOLVER work)
+  w += T * n + 16 * (T * T + 64);                       // block-Householder branch: remainder rows, factors
   w += 8 * T * T + 4 * T + 65536;                       // pivoted path (tau), slack
   return w;
 }
@@ -401,7 +489,7 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
   Ctx c{(cudaStream_t)stream, nullptr, work, work + work_len};
   static const bool debug = getenv("KR_RECYCLE_DEBUG") != nullptr;
   const auto t_start = std::chrono::steady_clock::now();
-  int n_ill = 0, n_house = 0, n_exact = 0;
+  int n_ill = 0, n_house = 0, n_exact = 0, n_block = 0;
   double house_ms = 0.0;
   bool was_shifted = false;
   KR_TRY(cublas_handle(&c.h, c.st));
@@ -498,9 +586,19 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
       ill.push_back(b);
       if (!okb) hh.push_back(b);
     }
+    if (debug && (!okb || cb > PIVOT_COND))
+      fprintf(stderr, "  sample %d t=%d cb=%.3e ok1=%d shifted=%d is1=%d i2=%d i3=%d -> %s\n", b, t[b], cb, (int)ok1[b],
+              (int)shifted, shifted ? is1[b] : -9, i2[b], shifted ? i3[b] : -9, okb ? "pivoted" : "householder");
   }
   n_ill = (int)ill.size();
   n_house = (int)hh.size();
+  std::vector<int> brow(B, -1);  // first breakdown row of the Cholesky-QR passes (-1: none)
+  for (int b : hh) {
+    int r = -1;
+    for (int v : {shifted ? is1[b] : -1, i2[b], shifted ? i3[b] : -1})
+      if (v >= 0 && (r < 0 || v < r)) r = v;
+    brow[b] = r;
+  }
   was_shifted = shifted;
   if (!ill.empty()) {
     const int nb = (int)ill.size();
@@ -514,15 +612,44 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
     double* tau = c.take(T);
     double* hwk = nullptr;
     int64_t hwl = 0;
+    double* house_rem = nullptr;  // remainder rows of the block Householder branch
     if (!hh.empty()) {
       hwl = house_lwork(n, T) + 1;
       hwk = c.take(hwl);
+      house_rem = c.take((int64_t)T * n);
     }
     // R factors: from the Cholesky-QR basis (R^T = A W^T) or a Householder QR
     for (int i = 0; i < nb; ++i) {
       const int b = ill[i];
       const double one = 1.0, zero = 0.0;
-      const bool house = std::find(hh.begin(), hh.end(), b) != hh.end();
+      bool house = std::find(hh.begin(), hh.end(), b) != hh.end();
+      // Cholesky-QR broke down at a row: block Householder, where the full one is expensive
+      // (n t >= 2^21: ~1 ms and up; small problems keep the full Householder QR)
+      if (house && brow[b] >= t[b] / 2 && n * (int64_t)t[b] >= ((int64_t)1 << 21)) {
+        if (debug) cudaStreamSynchronize(c.st);
+        const auto th0 = std::chrono::steady_clock::now();
+        double* Wb = W + (int64_t)b * T * n;
+        KR_TRY(cudaMemsetAsync(Wb, 0, sizeof(double) * T * n, c.st) == cudaSuccess ? KR_OK
+                                                                                    : fail(KR_ECUDA, "memset"));
+        int k1 = brow[b];
+        for (int attempt = 0; attempt < 3 && house; ++attempt) {
+          bool ok = false;
+          int brk = -1;
+          KR_TRY(block_house(c, A + (int64_t)b * T * n, t[b], k1, n, Wb, house_rem, hwk, hwl, tau, ok, brk));
+          if (ok) {
+            house = false;
+            ++n_block;
+          } else if (brk >= t[b] / 2 && brk < k1) {
+            k1 = brk;
+          } else {
+            break;
+          }
+        }
+        if (debug) {
+          cudaStreamSynchronize(c.st);
+          house_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
+        }
+      }
       if (!house) {  // M column-major R: M[j][i] = a_j . w_i  (col-major M (T x T) = W_col^T A_col)
         KR_TRY(cublas_check(cublasDgemm(c.h, CUBLAS_OP_T, CUBLAS_OP_N, T, T, (int)n, &one, W + (int64_t)b * T * n,
                                         (int)n, A + (int64_t)b * T * n, (int)n, &zero, M + (int64_t)i * T * T, T),
@@ -724,8 +851,8 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
   }
   if (c.overrun) return overrun(c, __LINE__);
   if (debug)
-    fprintf(stderr, "kr_recycle_update: B=%d T=%d shifted=%d ill=%d householder=%d exact=%d host %.2f ms (householder %.2f)\n",
-            B, T, (int)was_shifted, n_ill, n_house, n_exact,
+    fprintf(stderr, "kr_recycle_update: B=%d T=%d shifted=%d ill=%d householder=%d (block %d) exact=%d host %.2f ms (householder %.2f)\n",
+            B, T, (int)was_shifted, n_ill, n_house, n_block, n_exact,
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count(), house_ms);
   return check_launch("kr_recycle_update");
 }
