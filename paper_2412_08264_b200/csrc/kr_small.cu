@@ -156,15 +156,35 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
     __syncthreads();
     if (tid == 0) { const long long c_ = clock64(); csec[2] += c_ - clast; clast = c_; }
 #endif
-    // trailing update A_ij -= L_i,panel . L_j,panel (lower part), warp per row, lanes over j
-    for (int i = kb + nb + warp; i < t; i += CNT / 32) {
-      const double* Li = A + pk(i, kb);
-      for (int j = kb + nb + lane; j <= i; j += 32) {
+    // trailing update A_ij -= L_i,panel . L_j,panel (lower part), lanes over j; a warp takes
+    // four rows i0 + 16u at once so each lane's L_j,panel load feeds four entries (every
+    // entry still accumulates c = 0 .. nb-1 in order: same arithmetic)
+    for (int i0 = kb + nb + warp; i0 < t; i0 += 4 * (CNT / 32)) {
+      constexpr int RU = 4, RS = CNT / 32;
+      const double* Li[RU];
+      int im = i0;
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        const int i = min(i0 + RS * u, t - 1);
+        Li[u] = A + pk(i, kb);
+        if (i0 + RS * u < t) im = i0 + RS * u;
+      }
+      for (int j = kb + nb + lane; j <= im; j += 32) {
         const double* Lj = A + pk(j, kb);
-        double acc = 0.0;
-#pragma unroll 8
-        for (int c = 0; c < nb; ++c) acc += Li[c] * Lj[c];
-        A[pk(i, j)] -= acc;
+        double acc[RU] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+          if (c < nb) {
+            const double lj = Lj[c];
+#pragma unroll
+            for (int u = 0; u < RU; ++u) acc[u] += Li[u][c] * lj;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+          const int i = i0 + RS * u;
+          if (i < t && j <= i) A[pk(i, j)] -= acc[u];
+        }
       }
     }
     __syncthreads();
@@ -227,19 +247,20 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
     const int h = tid / (CNT / 2), c = tid - h * (CNT / 2);
     const int r0 = 8 * h;
     double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    if (c < w && r0 < nb) {
+    // the warp's lanes hold consecutive columns; they all start k at the warp's first
+    // column, so the L operands are warp-uniform (broadcast smem loads), and a lane adds
+    // fma(l, 0, acc) == acc for its rows k < c (bitwise the per-column loop from k = c)
+    const int cw = (c & ~31) < w ? (c & ~31) : w;  // warp's first column (clamped)
+    if (cw < w && r0 < nb) {
+      const bool act = c < w;
       const double* lp[8];  // rows ib + r0 + u of L (clamped into the matrix)
 #pragma unroll
       for (int u = 0; u < 8; ++u) lp[u] = A + pk(min(ib + r0 + u, t - 1), 0);
-      int k = c;
-      int xa = k * (k + 1) / 2 + c;  // packed index of X_kc, advanced by k + 1 per row
+      int k = cw;
       for (; k + 3 < ib; k += 4) {
         double xv[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          xv[j] = A[xa];  // X_(k+j),c (rows < ib hold X already)
-          xa += k + j + 1;
-        }
+        for (int j = 0; j < 4; ++j) xv[j] = (act && k + j >= c) ? A[pk(k + j, c)] : 0.0;  // X_(k+j),c
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const double* l = lp[u] + k;
@@ -248,8 +269,7 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
         }
       }
       for (; k < ib; ++k) {
-        const double xk = A[xa];
-        xa += k + 1;
+        const double xk = (act && k >= c) ? A[pk(k, c)] : 0.0;
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc[u] = fma(lp[u][k], xk, acc[u]);
       }
