@@ -181,7 +181,9 @@ int kr_syev_select(const double* A, int64_t lda, int64_t bsa, const int32_t* dim
  * G + b*bsg + i*ldg + j (symmetrised), t_b = dims[b] <= tmax <= 228 (DEVICE int32).
  * flags bit 0: scale by D = sqrt(diag G); bit 1: write F; bit 2: skip mode -- a row
  * whose pivot falls below 4 t eps times its diagonal is removed (zero column of L,
- * zero row of F, skipped[b*tmax + i] = 1) instead of stopping.  shift (nullable,
+ * zero row of F, skipped[b*tmax + i] = 1) instead of stopping; bit 3: partial -- on a
+ * breakdown at row i, F keeps the inverse of the leading i x i factor and zero rows
+ * i..t_b-1 (otherwise F is the identity).  shift (nullable,
  * DEVICE, per sample) is added to the scaled diagonal.  G_s = L L^T; F = L^{-1} D^{-1}
  * row-major (F + b*bsf + i*ldf + j), zero upper triangle, identity pad block.
  * info[b] = -1 or the first row whose pivot is not positive; stats[4b..4b+3] =

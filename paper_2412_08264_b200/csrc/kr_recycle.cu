@@ -275,9 +275,10 @@ struct Factor {  // one Cholesky-QR factor of a batch: F (B,T,T), info, stats
   double* stats;
 };
 
-int chol(Ctx& c, const double* G, const int32_t* dims, int B, int T, bool scale, const double* shift, Factor& f) {
-  return kr_chol_inv(G, T, (int64_t)T * T, dims, B, T, (scale ? 1 : 0) | 2, shift, f.F, T, (int64_t)T * T, f.stats,
-                     f.info, nullptr, c.st);
+int chol(Ctx& c, const double* G, const int32_t* dims, int B, int T, bool scale, const double* shift, Factor& f,
+         bool partial = false) {
+  return kr_chol_inv(G, T, (int64_t)T * T, dims, B, T, (scale ? 1 : 0) | 2 | (partial ? 8 : 0), shift, f.F, T,
+                     (int64_t)T * T, f.stats, f.info, nullptr, c.st);
 }
 
 // CholQR2 of rows A (B, T, L) with dims; Q out (B,T,L) (may alias nothing), F = R^{-T} (B,T,T).
@@ -330,7 +331,7 @@ int64_t house_lwork(int64_t n, int T) {
 // at n = 16384, t = 220).  ok = false: a pass broke down (brk = its row) -- the caller
 // retries with a smaller k1 or takes the full Householder QR.
 int block_house(Ctx& c, const double* Ab, int t, int k1, int64_t n, double* Wb, double* Rem, double* hwk, int64_t hwl,
-                double* tau, bool& ok, int& brk) {
+                double* tau, bool& ok, int& brk, bool prefix_ready) {
   ok = false;
   brk = -1;
   const int m = t - k1;
@@ -346,7 +347,9 @@ int block_house(Ctx& c, const double* Ab, int t, int k1, int64_t n, double* Wb, 
   double* Cp = c.take((int64_t)t * t);
   Factor f1 = new_factor(c, 1, k1), f2 = new_factor(c, 1, k1), f3 = new_factor(c, 1, k1);
   Factor g1 = new_factor(c, 1, m), g2 = new_factor(c, 1, m);
-  // leading block: shifted CholeskyQR3 into Wb[0, k1), Rem as scratch
+  // leading block: shifted CholeskyQR3 into Wb[0, k1), Rem as scratch -- unless the
+  // caller's partial Cholesky-QR passes already left those rows orthonormalised
+  if (!prefix_ready) {
   KR_TRY(gram(c, Ab, Ab, 1, k1, n, G));
   KR_TRY(chol(c, G, dk, 1, k1, true, dsh, f1));
   KR_TRY(rows_mul(c, f1.F, 0, Ab, n, 0, Rem, n, 0, k1, k1, n, 1));
@@ -364,7 +367,10 @@ int block_house(Ctx& c, const double* Ab, int t, int k1, int64_t n, double* Wb, 
   KR_TRY(d2h(c, a3, f3.info, 1));
   for (int v : {a1[0], a2[0], a3[0]})
     if (v >= 0 && (brk < 0 || v < brk)) brk = v;
+  if (getenv("KR_RECYCLE_DEBUG") && brk >= 0)
+    fprintf(stderr, "  block_house t=%d k1=%d leading block breakdown rows %d %d %d\n", t, k1, a1[0], a2[0], a3[0]);
   if (brk >= 0) return KR_OK;
+  }
   // remainder rows, projected twice: Rem -= W1 (W1^T Rem)   (column-major n x m / n x k1 views)
   KR_TRY(cudaMemcpyAsync(Rem, Ab + (int64_t)k1 * n, sizeof(double) * m * n, cudaMemcpyDeviceToDevice, c.st) ==
                  cudaSuccess ? KR_OK : fail(KR_ECUDA, "block_house copy"));
@@ -405,6 +411,9 @@ int block_house(Ctx& c, const double* Ab, int t, int k1, int64_t n, double* Wb, 
   KR_TRY(d2h(c, b1, g1.info, 1));
   KR_TRY(d2h(c, b2, g2.info, 1));
   ok = b1[0] < 0 && b2[0] < 0;
+  if (getenv("KR_RECYCLE_DEBUG"))
+    fprintf(stderr, "  block_house t=%d k1=%d prefix=%d completion breakdown rows %d %d\n", t, k1, (int)prefix_ready,
+            b1[0], b2[0]);
   return KR_OK;
 }
 
@@ -527,7 +536,9 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
   KR_TRY(gram(c, A, A, B, T, n, G));
   double* nrm = c.take(2 * B);  // ||A||_F^2 = tr(A A^T) (the Gram is reused below), ||R^-1||_F^2
   trace_kernel<<<B, 256, 0, c.st>>>(G, T, nrm);
-  KR_TRY(chol(c, G, d_td, B, T, true, nullptr, f1));
+  // (partial factors: a sample whose passes break down keeps its orthonormalised leading
+  // rows -- the block-Householder branch below starts from them)
+  KR_TRY(chol(c, G, d_td, B, T, true, nullptr, f1, true));
   std::vector<int32_t> info1;
   std::vector<double> st1;
   KR_TRY(d2h(c, info1, f1.info, B));
@@ -547,7 +558,7 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
       }
     double* d_sh = c.take(B);
     KR_TRY(h2d(c, d_sh, sh.data(), B));
-    KR_TRY(chol(c, G, d_td, B, T, true, d_sh, f1));
+    KR_TRY(chol(c, G, d_td, B, T, true, d_sh, f1, true));
   }
   std::vector<int32_t> is1;
   if (shifted) KR_TRY(d2h(c, is1, f1.info, B));
@@ -560,7 +571,7 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
              ? KR_OK : fail(KR_ECUDA, "kr_recycle copy"));
   for (int pass = 0; pass < (shifted ? 2 : 1); ++pass) {
     KR_TRY(gram(c, cur, cur, B, T, n, G));
-    KR_TRY(chol(c, G, d_td, B, T, false, nullptr, *fp[pass]));
+    KR_TRY(chol(c, G, d_td, B, T, false, nullptr, *fp[pass], true));
     KR_TRY(rows_mul(c, fp[pass]->F, (int64_t)T * T, cur, n, (int64_t)T * n, nxt, n, (int64_t)T * n, T, T, n, B));
     KR_TRY(rows_mul(c, fp[pass]->F, (int64_t)T * T, F, T, (int64_t)T * T, Ft, T, (int64_t)T * T, T, T, T, B));
     std::swap(F, Ft);
@@ -629,16 +640,22 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
         if (debug) cudaStreamSynchronize(c.st);
         const auto th0 = std::chrono::steady_clock::now();
         double* Wb = W + (int64_t)b * T * n;
-        KR_TRY(cudaMemsetAsync(Wb, 0, sizeof(double) * T * n, c.st) == cudaSuccess ? KR_OK
-                                                                                    : fail(KR_ECUDA, "memset"));
+        // rows [0, brow) of W are the partial passes' orthonormalised leading rows; rows
+        // [t, T) stay zero; [brow, t) are written by block_house
+        if (T > t[b])
+          KR_TRY(cudaMemsetAsync(Wb + (int64_t)t[b] * n, 0, sizeof(double) * (T - t[b]) * n, c.st) == cudaSuccess
+                     ? KR_OK : fail(KR_ECUDA, "memset"));
         int k1 = brow[b];
-        for (int attempt = 0; attempt < 3 && house; ++attempt) {
+        for (int attempt = 0; attempt < 4 && house; ++attempt) {
           bool ok = false;
           int brk = -1;
-          KR_TRY(block_house(c, A + (int64_t)b * T * n, t[b], k1, n, Wb, house_rem, hwk, hwl, tau, ok, brk));
+          KR_TRY(block_house(c, A + (int64_t)b * T * n, t[b], k1, n, Wb, house_rem, hwk, hwl, tau, ok, brk,
+                             attempt == 0));
           if (ok) {
             house = false;
             ++n_block;
+          } else if (attempt == 0) {
+            continue;  // recompute the leading block (shifted CholeskyQR3) instead of reusing it
           } else if (brk >= t[b] / 2 && brk < k1) {
             k1 = brk;
           } else {

@@ -224,20 +224,24 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
     for (int i = tid; i < T; i += CNT) P.skipped[(int64_t)b * T + i] = i < t ? skp[i] : 0;
   if (!inv) return;
   double* Fb = P.F + (int64_t)b * P.bsf;
-  if (fail >= 0) {  // no factor: identity (callers discard the sample)
+  const bool partial = P.flags & 8;
+  if (fail >= 0 && !partial) {  // no factor: identity (callers discard the sample)
     for (int64_t e = tid; e < (int64_t)T * T; e += CNT) {
       const int i = (int)(e / T), j = (int)(e % T);
       Fb[(int64_t)i * P.ldf + j] = i == j ? 1.0 : 0.0;
     }
     return;
   }
+  // partial mode: the leading `fail` rows factored (Cholesky is prefix-consistent), so
+  // F keeps their inverse and zero rows from the breakdown row on
+  const int tf = fail >= 0 ? fail : t;
   // ---- X = L^{-1} by blocked forward substitution ----
   // Block row I (rows ib..ib+nb): V = E_I - L_I,<I X_<I, then X_I = L_II^{-1} V.  A thread
   // owns one column c and one half h of the block rows: 8 accumulators in registers, one
   // contiguous X load per k feeding 8 FMAs with broadcast L operands; the substitution
   // runs on those registers (h = 0 rows first, then h = 1 with them), X_I overwrites L_I.
-  for (int ib = 0; ib < t; ib += NB) {
-    const int nb = min(NB, t - ib);
+  for (int ib = 0; ib < tf; ib += NB) {
+    const int nb = min(NB, tf - ib);
     const int w = ib + nb;  // columns 0 .. w-1 are nonzero in block row I
     for (int e = tid; e < nb * nb; e += CNT) {
       const int r = e / nb, m = e % nb;
@@ -255,7 +259,7 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
       const bool act = c < w;
       const double* lp[8];  // rows ib + r0 + u of L (clamped into the matrix)
 #pragma unroll
-      for (int u = 0; u < 8; ++u) lp[u] = A + pk(min(ib + r0 + u, t - 1), 0);
+      for (int u = 0; u < 8; ++u) lp[u] = A + pk(min(ib + r0 + u, tf - 1), 0);
       int k = cw;
       for (; k + 3 < ib; k += 4) {
         double xv[4];
@@ -315,7 +319,7 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
     for (int j = lane; j < T; j += 32) {
       double v;
       if (i < t && j < t)
-        v = (j <= i && !skp[i]) ? A[pk(i, j)] / D[j] : 0.0;
+        v = (i < tf && j <= i && !skp[i]) ? A[pk(i, j)] / D[j] : 0.0;
       else
         v = i == j ? 1.0 : 0.0;
       fi[j] = v;
