@@ -29,6 +29,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstring>
+#include <functional>
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
@@ -229,11 +231,75 @@ int d2h(Ctx& c, std::vector<T>& host, const T* dev, size_t cnt) {
   return e == cudaSuccess ? KR_OK : fail(KR_ECUDA, std::string("kr_recycle d2h: ") + cudaGetErrorString(e));
 }
 
+// Several small device -> host reads with ONE stream synchronisation: the copies go
+// into a per-thread pinned staging buffer (a pageable destination would make every
+// cudaMemcpyAsync synchronous on its own), then out into the host vectors.
+struct Fetch {
+  struct Item {
+    const void* dev;
+    size_t bytes, off;
+    std::function<void(const char*)> out;
+  };
+  std::vector<Item> items;
+  size_t total = 0;
+  template <typename T>
+  Fetch& add(std::vector<T>& host, const T* dev, size_t cnt) {
+    const size_t bytes = cnt * sizeof(T), off = (total + 15) & ~(size_t)15;
+    total = off + bytes;
+    items.push_back({dev, bytes, off, [&host, cnt](const char* src) {
+                       host.resize(cnt);
+                       if (cnt) memcpy(host.data(), src, cnt * sizeof(T));
+                     }});
+    return *this;
+  }
+  int run(Ctx& c) {
+    static thread_local char* buf = nullptr;
+    static thread_local size_t cap = 0;
+    if (total > cap) {
+      if (buf) cudaFreeHost(buf);
+      cap = std::max<size_t>(total, 65536);
+      if (cudaMallocHost(&buf, cap) != cudaSuccess) {
+        buf = nullptr;
+        cap = 0;
+        return fail(KR_ECUDA, "kr_recycle: pinned staging buffer");
+      }
+    }
+    for (const Item& it : items)
+      if (it.bytes && cudaMemcpyAsync(buf + it.off, it.dev, it.bytes, cudaMemcpyDeviceToHost, c.st) != cudaSuccess)
+        return fail(KR_ECUDA, "kr_recycle fetch");
+    const cudaError_t e = cudaStreamSynchronize(c.st);
+    if (e != cudaSuccess) return fail(KR_ECUDA, std::string("kr_recycle fetch: ") + cudaGetErrorString(e));
+    for (const Item& it : items) it.out(buf + it.off);
+    return KR_OK;
+  }
+};
+
+// Small host -> device uploads through a per-thread pinned ring (no stream sync: each
+// upload has its own slot for the duration of one kr_recycle_update call, whose final
+// reads synchronise the stream before the next call resets the ring).
+struct UpRing {
+  char* buf = nullptr;
+  size_t cap = 0, off = 0;
+};
+UpRing& up_ring() {
+  static thread_local UpRing r;
+  return r;
+}
+
 template <typename T>
 int h2d(Ctx& c, T* dev, const T* host, size_t cnt) {
   if (cnt == 0) return KR_OK;
-  cudaError_t e = cudaMemcpyAsync(dev, host, cnt * sizeof(T), cudaMemcpyHostToDevice, c.st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(c.st);  // host buffer may go out of scope
+  UpRing& r = up_ring();
+  const size_t bytes = cnt * sizeof(T), off = (r.off + 15) & ~(size_t)15;
+  if (r.buf == nullptr || off + bytes > r.cap) {  // first use / overflow: synchronous fallback
+    cudaError_t e = cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, c.st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c.st);
+    if (r.buf == nullptr && cudaMallocHost(&r.buf, 1 << 16) == cudaSuccess) r.cap = 1 << 16;
+    return e == cudaSuccess ? KR_OK : fail(KR_ECUDA, std::string("kr_recycle h2d: ") + cudaGetErrorString(e));
+  }
+  memcpy(r.buf + off, host, bytes);
+  r.off = off + bytes;
+  const cudaError_t e = cudaMemcpyAsync(dev, r.buf + off, bytes, cudaMemcpyHostToDevice, c.st);
   return e == cudaSuccess ? KR_OK : fail(KR_ECUDA, std::string("kr_recycle h2d: ") + cudaGetErrorString(e));
 }
 
@@ -362,9 +428,7 @@ int block_house(Ctx& c, const double* Ab, int t, int k1, int64_t n, double* Wb, 
   KR_TRY(cudaMemcpyAsync(Wb, Rem, sizeof(double) * k1 * n, cudaMemcpyDeviceToDevice, c.st) == cudaSuccess
              ? KR_OK : fail(KR_ECUDA, "block_house copy"));
   std::vector<int32_t> a1, a2, a3;
-  KR_TRY(d2h(c, a1, f1.info, 1));
-  KR_TRY(d2h(c, a2, f2.info, 1));
-  KR_TRY(d2h(c, a3, f3.info, 1));
+  KR_TRY(Fetch().add(a1, f1.info, 1).add(a2, f2.info, 1).add(a3, f3.info, 1).run(c));
   for (int v : {a1[0], a2[0], a3[0]})
     if (v >= 0 && (brk < 0 || v < brk)) brk = v;
   if (getenv("KR_RECYCLE_DEBUG") && brk >= 0)
@@ -408,8 +472,7 @@ int block_house(Ctx& c, const double* Ab, int t, int k1, int64_t n, double* Wb, 
   KR_TRY(cudaMemcpyAsync(W2, Rem, sizeof(double) * m * n, cudaMemcpyDeviceToDevice, c.st) == cudaSuccess
              ? KR_OK : fail(KR_ECUDA, "block_house copy"));
   std::vector<int32_t> b1, b2;
-  KR_TRY(d2h(c, b1, g1.info, 1));
-  KR_TRY(d2h(c, b2, g2.info, 1));
+  KR_TRY(Fetch().add(b1, g1.info, 1).add(b2, g2.info, 1).run(c));
   ok = b1[0] < 0 && b2[0] < 0;
   if (getenv("KR_RECYCLE_DEBUG"))
     fprintf(stderr, "  block_house t=%d k1=%d prefix=%d completion breakdown rows %d %d\n", t, k1, (int)prefix_ready,
@@ -496,6 +559,8 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
   const int p = op->reg_kind == KR_REG_TV ? 1 : op->num_filters * (1 + op->ksize * op->ksize);
   const int P = p + T;
   Ctx c{(cudaStream_t)stream, nullptr, work, work + work_len};
+  // the previous call ended with a synchronising read, so its uploads are done
+  up_ring().off = 0;
   static const bool debug = getenv("KR_RECYCLE_DEBUG") != nullptr;
   const auto t_start = std::chrono::steady_clock::now();
   int n_ill = 0, n_house = 0, n_exact = 0, n_block = 0;
@@ -541,8 +606,7 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
   KR_TRY(chol(c, G, d_td, B, T, true, nullptr, f1, true));
   std::vector<int32_t> info1;
   std::vector<double> st1;
-  KR_TRY(d2h(c, info1, f1.info, B));
-  KR_TRY(d2h(c, st1, f1.stats, 4 * B));
+  KR_TRY(Fetch().add(info1, f1.info, B).add(st1, f1.stats, 4 * B).run(c));
   std::vector<char> ok1(B);
   bool shifted = false;
   for (int b = 0; b < B; ++b) {
@@ -583,9 +647,12 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
   frob2_kernel<<<B, FROB_NT, 0, c.st>>>(F, T, T, T, (int64_t)T * T, nrm + B);
   std::vector<double> nr;
   std::vector<int32_t> i2, i3;
-  KR_TRY(d2h(c, nr, nrm, 2 * B));
-  KR_TRY(d2h(c, i2, f2.info, B));
-  if (shifted) KR_TRY(d2h(c, i3, f3.info, B));
+  {
+    Fetch fe;
+    fe.add(nr, nrm, 2 * B).add(i2, f2.info, B);
+    if (shifted) fe.add(i3, f3.info, B);
+    KR_TRY(fe.run(c));
+  }
   std::vector<int> ill, hh;  // samples for the pivoted path; of those, the ones needing Householder
   for (int b = 0; b < B; ++b) {
     if (t[b] == 0) continue;
@@ -776,9 +843,7 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
     }
     std::vector<double> hnv, hst;
     std::vector<int32_t> hinf;
-    KR_TRY(d2h(c, hnv, hn, 2 * B));
-    KR_TRY(d2h(c, hst, fh.stats, 4 * B));
-    KR_TRY(d2h(c, hinf, fh.info, B));
+    KR_TRY(Fetch().add(hnv, hn, 2 * B).add(hst, fh.stats, 4 * B).add(hinf, fh.info, B).run(c));
     std::vector<int> exact;
     for (int b = 0; b < B; ++b) {
       if (t[b] == 0) continue;
@@ -814,9 +879,7 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
     // QR breakdowns of [Jt; Ht]
     std::vector<int32_t> qi1, qi2;
     std::vector<double> qs1;
-    KR_TRY(d2h(c, qi1, qs.f1.info, B));
-    KR_TRY(d2h(c, qs1, qs.f1.stats, 4 * B));
-    KR_TRY(d2h(c, qi2, qs.f2.info, B));
+    KR_TRY(Fetch().add(qi1, qs.f1.info, B).add(qs1, qs.f1.stats, 4 * B).add(qi2, qs.f2.info, B).run(c));
     for (int b = 0; b < B; ++b)
       if (t[b] > 0 && !(cholqr_ok(qi1, qs1, b) && qi2[b] < 0)) status[b] = 1;
   }
@@ -850,11 +913,12 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
   // ---- 6. per-sample outcome
   std::vector<int32_t> ns, ui1, ui2, bd;
   std::vector<double> us1;
-  KR_TRY(d2h(c, ns, d_ns, B));
-  KR_TRY(d2h(c, ui1, qu.f1.info, B));
-  KR_TRY(d2h(c, us1, qu.f1.stats, 4 * B));
-  KR_TRY(d2h(c, ui2, qu.f2.info, B));
-  if (a->vec_type == 1) KR_TRY(d2h(c, bd, d_bad, B));
+  {
+    Fetch fe;
+    fe.add(ns, d_ns, B).add(ui1, qu.f1.info, B).add(us1, qu.f1.stats, 4 * B).add(ui2, qu.f2.info, B);
+    if (a->vec_type == 1) fe.add(bd, d_bad, B);
+    KR_TRY(fe.run(c));
+  }
   for (int b = 0; b < B; ++b) {
     a->tdims[b] = t[b];
     a->nsel[b] = ns[b];
