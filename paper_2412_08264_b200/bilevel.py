@@ -107,6 +107,10 @@ def _warm_thread(shape=None):
 
 
 _PHASE_DEBUG = os.environ.get("KR_SOLVE_DEBUG") is not None
+# sample-group streams at high priority: the orchestrator's H W (thousands of blocks) runs
+# on a lowest-priority side stream, so the other group's latency-bound kernels are not
+# queued behind it (KR_GROUP_PRIORITY=0 restores default priorities)
+_GROUP_PRIORITY = int(os.environ.get("KR_GROUP_PRIORITY", "-1"))
 
 
 def _phase_clock():
@@ -169,7 +173,7 @@ class SequenceSolver:
         ng = max(1, min(self.groups, batch))
         if self.batched_update and ng > 1:
             if self._gstreams is None or len(self._gstreams) < ng:
-                self._gstreams = [torch.cuda.Stream() for _ in range(ng)]
+                self._gstreams = [torch.cuda.Stream(priority=_GROUP_PRIORITY) for _ in range(ng)]
                 self._gpool = ThreadPoolExecutor(max_workers=ng)
             for st in self._gstreams:
                 with torch.cuda.stream(st):
@@ -244,7 +248,7 @@ class SequenceSolver:
         main = torch.cuda.current_stream()
         if self._gstreams is None or len(self._gstreams) < ng:
             _warm_linalg()
-            self._gstreams = [torch.cuda.Stream() for _ in range(ng)]
+            self._gstreams = [torch.cuda.Stream(priority=_GROUP_PRIORITY) for _ in range(ng)]
             self._gpool = ThreadPoolExecutor(max_workers=ng)
 
         def work(g):
