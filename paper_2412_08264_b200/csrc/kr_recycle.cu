@@ -310,7 +310,9 @@ struct SideStream {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int init() {
     if (st) return KR_OK;
-    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess ||
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    if (cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, greatest) != cudaSuccess ||
         cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess)
       return fail(KR_ECUDA, "kr_recycle side stream");
@@ -366,6 +368,39 @@ LowStream& low_stream() {
   return ls;
 }
 
+// The update's latency-bound one-CTA-per-matrix kernels (Cholesky, eigen-select, pivoted
+// QR) on a highest-priority side stream: fork, launch, join.  With the group streams at
+// default priority, a sample group's critical-path kernel is dispatched ahead of the
+// other group's pending GEMM / stencil blocks.
+struct HiStream {
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  template <typename F>
+  int run(cudaStream_t main, F&& launch) {
+    static const bool on = getenv("KR_HI_LATENCY") == nullptr || getenv("KR_HI_LATENCY")[0] != '0';
+    if (!on) return launch(main);
+    if (!st) {
+      int least = 0, greatest = 0;
+      cudaDeviceGetStreamPriorityRange(&least, &greatest);
+      if (cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, greatest) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) != cudaSuccess)
+        return fail(KR_ECUDA, "kr_recycle high-priority stream");
+    }
+    if (cudaEventRecord(ev_fork, main) != cudaSuccess || cudaStreamWaitEvent(st, ev_fork, 0) != cudaSuccess)
+      return fail(KR_ECUDA, "kr_recycle fork");
+    KR_TRY(launch(st));
+    if (cudaEventRecord(ev_join, st) != cudaSuccess || cudaStreamWaitEvent(main, ev_join, 0) != cudaSuccess)
+      return fail(KR_ECUDA, "kr_recycle join");
+    return KR_OK;
+  }
+};
+
+HiStream& hi_stream() {
+  static thread_local HiStream hs;
+  return hs;
+}
+
 struct Factor {  // one Cholesky-QR factor of a batch: F (B,T,T), info, stats
   double* F;
   int32_t* info;
@@ -374,8 +409,10 @@ struct Factor {  // one Cholesky-QR factor of a batch: F (B,T,T), info, stats
 
 int chol(Ctx& c, const double* G, const int32_t* dims, int B, int T, bool scale, const double* shift, Factor& f,
          bool partial = false) {
-  return kr_chol_inv(G, T, (int64_t)T * T, dims, B, T, (scale ? 1 : 0) | 2 | (partial ? 8 : 0), shift, f.F, T,
-                     (int64_t)T * T, f.stats, f.info, nullptr, c.st);
+  return hi_stream().run(c.st, [&](cudaStream_t st) {
+    return kr_chol_inv(G, T, (int64_t)T * T, dims, B, T, (scale ? 1 : 0) | 2 | (partial ? 8 : 0), shift, f.F, T,
+                       (int64_t)T * T, f.stats, f.info, nullptr, st);
+  });
 }
 
 // CholQR2 of rows A (B, T, L) with dims; Q out (B,T,L) (may alias nothing), F = R^{-T} (B,T,T).
@@ -799,7 +836,9 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
       }
     }
     double* qw = c.take(nb * T + 1);
-    KR_TRY(kr_qrcp_small_cluster(M, d_misc, nb, T, RANK_TOL, Qr, d_rank, nullptr, qw, nb * T + 1, c.st));
+    KR_TRY(hi_stream().run(c.st, [&](cudaStream_t st) {
+      return kr_qrcp_small_cluster(M, d_misc, nb, T, RANK_TOL, Qr, d_rank, nullptr, qw, nb * T + 1, st);
+    }));
     // W_b <- Q_R[:, :r]^T W_b  (rows beyond the rank are zero)
     for (int i = 0; i < nb; ++i) {
       const int b = ill[i];
@@ -833,8 +872,8 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
     sym_and_s_kernel<<<dim3(T, B), 256, 0, c.st>>>(Ht, nullptr, 0, T, Hs, nullptr);
     Ht = Hs;
     const int64_t el = kr_syev_select_workspace(B, T);
-    KR_TRY(kr_syev_select(Ht, T, (int64_t)T * T, d_td, B, T, a->size_code, s, nullptr, 0, coeffs, T,
-                          (int64_t)s * T, d_ns, c.take(el), el, c.st));
+    KR_TRY(hi_stream().run(c.st, [&](cudaStream_t st) { return kr_syev_select(Ht, T, (int64_t)T * T, d_td, B, T, a->size_code, s, nullptr, 0, coeffs, T,
+                          (int64_t)s * T, d_ns, c.take(el), el, st); }));
   } else {
     // J W
     double* Jt = c.take((int64_t)B * T * p);
@@ -869,8 +908,8 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
     KR_TRY(small_gram(c, qs.Q, P, (int64_t)T * P, Mq, T, p, B));
     const int64_t el = kr_syev_select_workspace(B, T);
     double* Zs = c.take((int64_t)B * s * T);
-    KR_TRY(kr_syev_select(Mq, T, (int64_t)T * T, d_td, B, T, 1, s, nullptr, 0, Zs, T, (int64_t)s * T, d_ns,
-                          c.take(el), el, c.st));
+    KR_TRY(hi_stream().run(c.st, [&](cudaStream_t st) { return kr_syev_select(Mq, T, (int64_t)T * T, d_td, B, T, 1, s, nullptr, 0, Zs, T, (int64_t)s * T, d_ns,
+                          c.take(el), el, st); }));
     // the bracket decision (host), overlapping the eigen kernel
     if (!joined) {
       KR_TRY(ss.wait(c.st));
@@ -890,8 +929,8 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
     if (!exact.empty()) {  // exact extreme eigenvalues where the bracket straddles the limit
       double* ext = c.take(2 * (int64_t)B);
       double* zz = c.take(2 * (int64_t)B * T);
-      KR_TRY(kr_syev_select(Ht, T, (int64_t)T * T, d_td, B, T, 2, 2, ext, 2, zz, T, 2 * (int64_t)T, nullptr,
-                            c.take(el), el, c.st));
+      KR_TRY(hi_stream().run(c.st, [&](cudaStream_t st) { return kr_syev_select(Ht, T, (int64_t)T * T, d_td, B, T, 2, 2, ext, 2, zz, T, 2 * (int64_t)T, nullptr,
+                            c.take(el), el, st); }));
       std::vector<double> ex;
       KR_TRY(d2h(c, ex, ext, 2 * B));
       for (int b : exact) {
