@@ -287,3 +287,59 @@ def test_gram_split_k(B, T, n):
     got = gram(A, Bm)
     assert torch.allclose(got, ref, rtol=0, atol=1e-11 * float(ref.abs().max()))
     assert torch.equal(gram(A, Bm), got)  # deterministic
+
+
+def _span_dist(A, B):
+    """|| (I - P_A) Q_B ||_F for the orthonormal bases of two equal-width column blocks
+    (no n x n projector: n = 16384 here)."""
+    Qa, _ = torch.linalg.qr(A)
+    Qb, _ = torch.linalg.qr(B)
+    return float(torch.linalg.matrix_norm(Qb - Qa @ (Qa.T @ Qb)))
+
+
+def test_recycle_update_rank_drop_block_householder():
+    """Exactly dependent candidates in a block large enough (n t >= 2^21) for the
+    native orchestrator's block-Householder branch: shifted CholeskyQR3 breaks down at
+    the first dependent row, the leading rows are reused, only the remainder goes
+    through a Householder QR -- the candidate span, the drop count and the recycle
+    space agree with the per-sample reference-semantics path."""
+    from paper_2412_08264_b200 import HessianSolveConfig, SequenceSolver, batched
+    from paper_2412_08264_b200.bilevel import hypergradients
+    from paper_2412_08264_b200.problems import DeblurConfig, make_batch, synthetic_sequence
+    from paper_2412_08264_b200.recycling import next_recycle
+
+    cfg = DeblurConfig(128, 2, 5, 1.0, 0.01, "filters", 4, 3)
+    model = make_batch(cfg)
+    th, xh = synthetic_sequence(cfg, model.x_true.cpu().numpy(), 3)
+    seq = SequenceSolver(HessianSolveConfig.from_strategy("RGen-L(R)-NSC", recycle_dim=10, delta=1e-14,
+                                                          max_iter=150))
+    seq.batched_update = False
+    for i in range(2):
+        hypergradients(model, th[i], torch.as_tensor(xh[i], device="cuda"), seq)
+    H, J = model.at(th[2], torch.as_tensor(xh[2], device="cuda"))
+    st = seq.cfg.strategy
+    bases = list(seq._prev_basis)
+    V0 = bases[0]
+    assert V0.shape[1] >= 128
+    bases[0] = torch.cat([V0, V0[:, :2] - V0[:, 7:9], 3.0 * V0[:, 5:6]], dim=1)  # three dependent columns, last
+    assert model.n * (bases[0].shape[1] + seq._prev_recycle[0].dim) >= 1 << 21
+    batched.STATS = {}
+    try:
+        got = batched.recycle_update_native(st, seq.cfg.recycle_dim, H, J, bases, seq._prev_recycle)
+        assert batched.STATS["declined"] == 0, batched.STATS
+    finally:
+        batched.STATS = None
+    ref = next_recycle(st, h_current=H.sample(0), jac_current=J.sample(0), prev_basis=bases[0],
+                       prev_recycle=seq._prev_recycle[0], s=seq.cfg.recycle_dim)
+    t_kept = V0.shape[1] + seq._prev_recycle[0].dim
+    assert got[0].nsc_data.w.shape[1] == ref.nsc_data.w.shape[1] == t_kept
+    # candidate spans: the same subspace
+    assert _span_dist(got[0].nsc_data.w, ref.nsc_data.w) <= 1e-8
+    C = got[0].C
+    assert torch.allclose(C.T @ C, torch.eye(C.shape[1], dtype=torch.float64, device="cuda"), atol=1e-13)
+    HU = H.sample(0).apply_matrix(got[0].U)
+    assert torch.dist(HU, C) <= 1e-10 * torch.linalg.norm(HU)
+    if _selection_well_posed(st, H.sample(0), J.sample(0), type("S", (), {"_prev_basis": bases, "_prev_recycle":
+                             seq._prev_recycle, "cfg": seq.cfg})(), 0):
+        assert _span_dist(C, ref.C) <= 1e-8
+        assert torch.allclose(got[0].nsc_data.values, ref.nsc_data.values, rtol=1e-8)
