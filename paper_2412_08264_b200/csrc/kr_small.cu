@@ -93,9 +93,9 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
     if (tid == 0) { const long long c_ = clock64(); csec[0] += c_ - clast; clast = c_; }
 #endif
   const int lane = tid & 31, warp = tid >> 5;
-  for (int kb = 0; kb < t; kb += NB) {
+  // diagonal block kb in registers (warp 0): lane = row, column j broadcast by shuffles
+  auto diag = [&](int kb) {
     const int nb = min(NB, t - kb);
-    if (warp == 0) {  // diagonal block in registers: lane = row, column j broadcast by shuffles
       double a[NB];
 #pragma unroll
       for (int k = 0; k < NB; ++k) a[k] = (lane < nb && k <= lane) ? A[pk(kb + lane, kb + k)] : 0.0;
@@ -131,8 +131,50 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
         rdiag[lane] = 1.0 / a[lane];  // (outside the unrolled code)
       }
       if (lane == 0 && bad >= 0) s_fail = bad;
+      };
+  // trailing update A_ij -= L_i,panel . L_j,panel for rows i >= rs, columns
+  // j in [jlo, min(i + 1, jhi)), by warps w = 0 .. nw-1: lanes over j, four rows i0 + nw u
+  // at once so each lane's L_j,panel load feeds four entries (every entry accumulates
+  // c = 0 .. nb-1 in order)
+  auto trailing = [&](int kb, int nb, int rs, int jlo, int jhi, int w, int nw) {
+    constexpr int RU = 4;
+    for (int i0 = rs + w; i0 < t; i0 += RU * nw) {
+      const double* Li[RU];
+      int im = i0;
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        const int i = min(i0 + nw * u, t - 1);
+        Li[u] = A + pk(i, kb);
+        if (i0 + nw * u < t) im = i0 + nw * u;
+      }
+      const int jm = min(im, jhi - 1);
+      for (int j = jlo + lane; j <= jm; j += 32) {
+        const double* Lj = A + pk(j, kb);
+        double acc[RU] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+          if (c < nb) {
+            const double lj = Lj[c];
+#pragma unroll
+            for (int u = 0; u < RU; ++u) acc[u] += Li[u][c] * lj;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+          const int i = i0 + nw * u;
+          if (i < t && j <= i) A[pk(i, j)] -= acc[u];
+        }
+      }
     }
-    __syncthreads();
+  };
+  // right-looking blocked Cholesky with one block of look-ahead: after the panel of block
+  // kb, the trailing update of the next block column comes first (all warps), then warp 0
+  // factors the next diagonal block while warps 1.. finish the rest of the trailing
+  // update (the same operations on every entry, reordered across independent entries)
+  if (t > 0 && warp == 0) diag(0);
+  __syncthreads();
+  for (int kb = 0; kb < t; kb += NB) {
+    const int nb = min(NB, t - kb);
 #ifdef KR_CHOL_TIMING
     __syncthreads();
     if (tid == 0) { const long long c_ = clock64(); csec[1] += c_ - clast; clast = c_; }
@@ -156,38 +198,17 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
     __syncthreads();
     if (tid == 0) { const long long c_ = clock64(); csec[2] += c_ - clast; clast = c_; }
 #endif
-    // trailing update A_ij -= L_i,panel . L_j,panel (lower part), lanes over j; a warp takes
-    // four rows i0 + 16u at once so each lane's L_j,panel load feeds four entries (every
-    // entry still accumulates c = 0 .. nb-1 in order: same arithmetic)
-    for (int i0 = kb + nb + warp; i0 < t; i0 += 4 * (CNT / 32)) {
-      constexpr int RU = 4, RS = CNT / 32;
-      const double* Li[RU];
-      int im = i0;
-#pragma unroll
-      for (int u = 0; u < RU; ++u) {
-        const int i = min(i0 + RS * u, t - 1);
-        Li[u] = A + pk(i, kb);
-        if (i0 + RS * u < t) im = i0 + RS * u;
-      }
-      for (int j = kb + nb + lane; j <= im; j += 32) {
-        const double* Lj = A + pk(j, kb);
-        double acc[RU] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int c = 0; c < NB; ++c) {
-          if (c < nb) {
-            const double lj = Lj[c];
-#pragma unroll
-            for (int u = 0; u < RU; ++u) acc[u] += Li[u][c] * lj;
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < RU; ++u) {
-          const int i = i0 + RS * u;
-          if (i < t && j <= i) A[pk(i, j)] -= acc[u];
-        }
-      }
+    const int kn = kb + nb;
+    if (kn < t) {
+      const int nbn = min(NB, t - kn);
+      trailing(kb, nb, kn, kn, kn + nbn, warp, CNT / 32);  // next block column
+      __syncthreads();
+      if (warp == 0)
+        diag(kn);
+      else
+        trailing(kb, nb, kn + nbn, kn + nbn, t, warp - 1, CNT / 32 - 1);  // the rest
+      __syncthreads();
     }
-    __syncthreads();
 #ifdef KR_CHOL_TIMING
     __syncthreads();
     if (tid == 0) { const long long c_ = clock64(); csec[3] += c_ - clast; clast = c_; }
