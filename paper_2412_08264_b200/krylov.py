@@ -225,17 +225,18 @@ class _Launch:
             self.keep += [U, C]
             a.U, a.C, a.ld_uc, a.bs_uc = U.data_ptr(), C.data_ptr(), n, s * n
             if deflate:  # recycled CG: Minv = (U^T C)^{-1}, identity on padded columns
-                live = torch.zeros(B, s, dtype=torch.float64, device=dev)
-                for b, d in enumerate(dims):
-                    live[b, :d] = 1.0
+                # one Cholesky+inverse launch (kr_chol_inv on the leading dims[b] block, identity
+                # pad), Minv = F^T F with F = L^{-1}; a failed factorization (U^T H U not SPD) is
+                # reported with the results (no host sync before the solve launch)
+                from .batched import _chol_inv
+
                 M = U @ C.transpose(1, 2)
-                M = 0.5 * (M + M.transpose(1, 2)) * (live.unsqueeze(2) * live.unsqueeze(1))
-                M = M + torch.diag_embed(1.0 - live)
-                L, info = torch.linalg.cholesky_ex(M)
-                if bool((info != 0).any()):
-                    raise ValueError("U^T H U is not positive definite; the recycle space does not fit H")
-                Minv = torch.cholesky_inverse(L).contiguous()
-                self.keep.append(Minv)
+                M = 0.5 * (M + M.transpose(1, 2))
+                d = torch.tensor(dims, dtype=torch.int32)
+                F, info, _ = _chol_inv(M, d, scale=False)
+                Minv = (F.transpose(1, 2) @ F).contiguous()
+                self.spd_info = info
+                self.keep += [Minv, F]
                 a.Minv = Minv.data_ptr()
         kinds = {_rule_kind(r) for r in rules}
         if len(kinds) != 1:
@@ -307,11 +308,16 @@ class _Launch:
     def results(self, H, flop_fn):
         # one device -> host transfer for all the per-sample scalars and histories
         m = self.max_iter + 1
+        spd = getattr(self, "spd_info", None)
+        spd_ok = torch.ones(1, dtype=torch.float64, device=self.iters.device) if spd is None else \
+            (spd < 0).all().to(torch.float64).reshape(1)
         host = torch.cat([self.iters.to(torch.float64), self.reasons.to(torch.float64), self.res.reshape(-1),
-                          self.vals.reshape(-1), self.finite.to(torch.float64).reshape(1)]).cpu().numpy()
-        if host[-1] != 1.0:
+                          self.vals.reshape(-1), self.finite.to(torch.float64).reshape(1), spd_ok]).cpu().numpy()
+        if host[-2] != 1.0:
             raise ValueError("right-hand side contains non-finite entries")
-        host = host[:-1]
+        if host[-1] != 1.0:
+            raise ValueError("U^T H U is not positive definite; the recycle space does not fit H")
+        host = host[:-2]
         iters = host[: self.B].astype(np.int64)
         reasons = host[self.B: 2 * self.B].astype(np.int64)
         res = host[2 * self.B: 2 * self.B + self.B * m].reshape(self.B, m)
