@@ -611,6 +611,6 @@ def recycle_update_native(strategy, s: int, H, J, bases, recycles, reuse_product
             nsc = None
             if strategy.vec_type == "RGen":
                 nsc = NscData(values=mu[b, :sb], v_h=VH[b, :sb, :tb].T, w=W[b, :tb].T, z=Z[b, :sb].T)
-            src = None if out_src is None else (out_src[0], out_src[1], out_src[2], out_src[3] + b)
+            src = None if out_src is None else (out_src[0], out_src[1], out_src[2], out_src[3] + b) + tuple(out_src[4:])
             res.append(RecycleSpace(U=U[b, :sb].T, C=C[b, :sb].T, nsc_data=nsc, orthonormal=True, batch_src=src))
     return res

@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 
 import torch
 
-from .batched import recycle_update, recycle_update_native, supports as batched_supports
+from .batched import gram as batched_gram, recycle_update, recycle_update_native, supports as batched_supports
 from .krylov import SolveOptions, SolveResult, rcg, rminres
 from .operators import (DenseOperator, FoEParams, HessianOperator, ImageVector, InpaintingProblem, Model,
                         StencilJacobian, as_device, _foe_model)
@@ -225,6 +225,9 @@ class SequenceSolver:
             f64 = dict(dtype=torch.float64, device=dev)
             shared = (torch.empty(B, s, n, **f64), torch.empty(B, s, n, **f64),
                       torch.empty(B, s, n, **f64) if cfg.strategy.vec_type == "RGen" else None)
+            # Z^T C of every group's rows, formed on the group's stream right after its update
+            # (off the path between the last update and the solve launch)
+            ztc = torch.empty(B, s, s, **f64) if shared[2] is not None else None
 
         def run(lo, hi):
             hs = hessian if (lo, hi) == (0, B) else hessian.slice(lo, hi)
@@ -235,7 +238,9 @@ class SequenceSolver:
                                              self._prev_recycle[lo:hi], cfg.reuse_products,
                                              scratch=self._scratch.setdefault(
                                                  lo, {"tcap": cfg.max_iter + cfg.recycle_dim + 1}),
-                                             out=out, out_src=shared + (lo,))
+                                             out=out, out_src=shared + (lo, ztc))
+                if ztc is not None and all(r is not None and r.dim == cfg.recycle_dim for r in recs):
+                    ztc[lo:hi] = batched_gram(shared[2][lo:hi], shared[1][lo:hi])
             else:
                 recs = recycle_update(cfg.strategy, cfg.recycle_dim, hs, js, self._prev_basis[lo:hi],
                                       self._prev_recycle[lo:hi], cfg.reuse_products)

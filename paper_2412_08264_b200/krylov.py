@@ -263,8 +263,13 @@ class _Launch:
             a.nsc_s, a.Z, a.ld_z, a.bs_z = ns, Z.data_ptr(), n, ns * n
             self.keep.append(Z)
             if s:
-                # (B, ns, s) Z^T C: split-K Gram over the pixels when the blocks are square
-                ZtC = (_batched_gram(Z, self.C) if ns == s else torch.bmm(Z, self.C.transpose(1, 2))).contiguous()
+                # (B, ns, s) Z^T C: formed by the batched update on the group streams when Z and C
+                # are its in-place rows, else a split-K Gram over the pixels here
+                pre = src[0][4] if (Z is zsrc and zsrc is not None and len(src[0]) > 4) else None
+                if pre is not None:
+                    ZtC = pre[off: off + B]
+                else:
+                    ZtC = (_batched_gram(Z, self.C) if ns == s else torch.bmm(Z, self.C.transpose(1, 2))).contiguous()
                 a.ZtC = ZtC.data_ptr()
                 self.keep.append(ZtC)
         self.w = _buf("w", B, n, dev=dev)
