@@ -249,6 +249,12 @@ typedef struct kr_recycle_args {
   int32_t* status;               /* HOST out [batch] */
 } kr_recycle_args;
 
+/* out[j] = (((rows[0][j] + rows[1][j]) + rows[2][j]) + ...), j < p: the sample-ordered sum of
+ * per-sample hypergradients (rows: count x p, row stride ld), left to right as the
+ * reference accumulates them (bilevel.py:439-446 over samples) -- one launch instead of
+ * count - 1 vector adds.  Used after the cross-rank all-gather. */
+int kr_ordered_sum(const double* rows, int32_t count, int32_t p, int64_t ld, double* out, kr_stream_t stream);
+
 /* Creates this host thread's cuBLAS / cuSOLVER handles on the current device (both are
  * per thread and expensive on first use); optional, for callers that pin update work
  * to long-lived threads.  Host-side setup only, no reference counterpart. */

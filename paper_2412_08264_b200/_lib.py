@@ -111,6 +111,7 @@ def _declare(lib):
         "kr_recycle_workspace": (_c_i64, [P(KrOp), P(KrRecycleArgs)]),
         "kr_thread_warmup": (ctypes.c_int, []),
         "kr_recycle_update": (_c_i32, [P(KrOp), P(KrRecycleArgs), _c_p, _c_i64, _c_p]),
+        "kr_ordered_sum": (_c_i32, [_c_p, _c_i32, _c_i32, _c_i64, _c_p, _c_p]),
         "kr_gram_workspace": (_c_i64, [_c_i32, _c_i32, _c_i64]),
         "kr_gram": (_c_i32, [_c_p, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_i64,
                              _c_p]),
@@ -128,6 +129,7 @@ EXPORTED = (
     "kr_rminres_workspace", "kr_rminres", "kr_cg_workspace", "kr_cg",
     "kr_syev_select_workspace", "kr_syev_select", "kr_chol_inv", "kr_qrcp_small", "kr_qrcp_small_cluster",
     "kr_gram_workspace", "kr_gram", "kr_recycle_workspace", "kr_recycle_update", "kr_thread_warmup",
+    "kr_ordered_sum",
 )
 
 

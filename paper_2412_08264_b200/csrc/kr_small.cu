@@ -453,3 +453,29 @@ extern "C" int kr_gram(const double* A, const double* Bm, int64_t ld, int64_t bs
   gram_sum_kernel<<<grid, 256, 0, st>>>(part, S, tt, rows, G, ldg, bsg);
   return check_launch("kr_gram");
 }
+
+// ---------------------------------------------------------------------------
+// Sample-ordered sum of per-sample hypergradient rows (a thread per entry j, the rows
+// accumulated left to right: bitwise the reference's sequential accumulation).
+
+namespace kr {
+namespace {
+__global__ void ordered_sum_kernel(const double* __restrict__ rows, int count, int p, int64_t ld,
+                                   double* __restrict__ out) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p; j += gridDim.x * blockDim.x) {
+    double acc = rows[j];
+    for (int k = 1; k < count; ++k) acc += rows[(int64_t)k * ld + j];
+    out[j] = acc;
+  }
+}
+}  // namespace
+}  // namespace kr
+
+extern "C" int kr_ordered_sum(const double* rows, int32_t count, int32_t p, int64_t ld, double* out,
+                              kr_stream_t stream) {
+  KR_CHECK_ARG(count >= 1 && p >= 0 && ld >= p, "bad ordered-sum shape");
+  if (p == 0) return KR_OK;
+  KR_CHECK_ARG(rows && out, "null pointer");
+  ordered_sum_kernel<<<(p + 255) / 256, 256, 0, (cudaStream_t)stream>>>(rows, count, p, ld, out);
+  return check_launch("kr_ordered_sum");
+}

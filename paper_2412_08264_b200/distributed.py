@@ -27,7 +27,18 @@ def shard(batch: int, world: int, rank: int) -> range:
 
 
 def ordered_sum(per_sample: torch.Tensor) -> torch.Tensor:
-    """Sum of the rows in sample order (the reference's left-to-right accumulation)."""
+    """Sum of the rows in sample order (the reference's left-to-right accumulation):
+    one ``kr_ordered_sum`` launch on CUDA tensors (a thread per entry adding the rows
+    left to right), the same row-by-row accumulation elsewhere."""
+    if per_sample.is_cuda and per_sample.dtype == torch.float64 and per_sample.dim() == 2:
+        from . import _lib
+
+        rows = per_sample.contiguous()
+        out = torch.empty(rows.shape[1], dtype=torch.float64, device=rows.device)
+        _lib.check(_lib.lib().kr_ordered_sum(rows.data_ptr(), rows.shape[0], rows.shape[1], rows.shape[1],
+                                             out.data_ptr(), _lib.stream_ptr()), "kr_ordered_sum")
+        _lib.note_launch("kr_ordered_sum")
+        return out
     acc = per_sample[0].clone()
     for k in range(1, per_sample.shape[0]):
         acc += per_sample[k]

@@ -127,3 +127,17 @@ def test_foe_reference_entry_points(cuda):
     assert abs(foe_cost(x, params, prob) - im.lower_cost(model, theta, x.data)) <= 1e-12 * abs(
         im.lower_cost(model, theta, x.data))
     assert rel(to_np(foe_gradient(x, params, prob)), im.lower_grad(model, theta, x.data)) <= 1e-12
+
+
+def test_ordered_sum_kernel_is_left_to_right(cuda):
+    """kr_ordered_sum (the sample-ordered hypergradient sum after the all-gather) is
+    bitwise the sequential row-by-row accumulation."""
+    from paper_2412_08264_b200.distributed import ordered_sum
+
+    g = torch.Generator(device="cpu").manual_seed(5)
+    rows = torch.randn(64, 1200, generator=g, dtype=torch.float64) * torch.logspace(-8, 8, 64, dtype=torch.float64)[:, None]
+    ref = rows[0].clone()
+    for k in range(1, rows.shape[0]):
+        ref += rows[k]
+    got = ordered_sum(rows.to(cuda)).cpu()
+    assert torch.equal(got, ref)
