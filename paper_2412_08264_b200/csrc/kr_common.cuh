@@ -504,7 +504,10 @@ template <int Q>
 __device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, int b, int y0, int x0) {
   constexpr int R = Q / 2;
   constexpr int EW = TW + 2 * R, EH = TH + 2 * R, ES = EW * EH;
-  constexpr int RB1 = Q <= 3 ? 6 : (Q <= 5 ? 5 : 4);  // taller strips: fewer smem loads per FMA
+#ifndef KR_RB1_Q5
+#define KR_RB1_Q5 4  // measured: 4 > 5 > 3, 6 (C2, 10-step A/B on one box)
+#endif
+  constexpr int RB1 = Q <= 3 ? 6 : (Q <= 5 ? KR_RB1_Q5 : 4);  // taller strips: fewer smem loads per FMA
   constexpr int NCH1 = (EH + RB1 - 1) / RB1;
   constexpr int RB2 = 4;
   constexpr int NI2 = TPX / RB2 / 32;  // stage-2 items per lane
