@@ -258,7 +258,10 @@ namespace kr {
 namespace {
 
 namespace cgc = cooperative_groups;
-constexpr int QNC = 8;                    // CTAs per matrix (portable cluster maximum)
+#ifndef KR_QRCP_CLUSTER
+#define KR_QRCP_CLUSTER 8
+#endif
+constexpr int QNC = KR_QRCP_CLUSTER;      // CTAs per matrix (8, the portable maximum; 16 measured slower: 1.18 vs 1.02 ms at B=4, t=220)
 constexpr int QCN = 256;                  // threads per CTA
 constexpr int QCW = QCN / 32;
 constexpr int QCOLS = (256 + QNC - 1) / QNC;  // resident columns per CTA (t <= 256)
@@ -625,6 +628,13 @@ extern "C" int kr_qrcp_small_cluster(double* M, const int32_t* dims, int32_t bat
   QrcpParams P{M, dims, tmax, rtol, Q, rank, perm, work};
   const size_t smem = ((size_t)QCOLS * tmax + 3 * (size_t)tmax) * sizeof(double);
   KR_TRY(ensure_smem((const void*)qrcp_cluster_kernel, smem));
+  if (QNC > 8) {
+    static bool np = false;
+    if (!np) {
+      cudaFuncSetAttribute((const void*)qrcp_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      np = true;
+    }
+  }
   qrcp_cluster_kernel<<<batch * QNC, QCN, smem, (cudaStream_t)stream>>>(P);
   return check_launch("qrcp_cluster_kernel");
 }
