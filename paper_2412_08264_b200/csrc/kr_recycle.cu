@@ -743,6 +743,10 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
     int r = -1;
     for (int v : {shifted ? is1[b] : -1, i2[b], shifted ? i3[b] : -1})
       if (v >= 0 && (r < 0 || v < r)) r = v;
+    // no breakdown of the shifted passes but a condition bound beyond their range: split at
+    // the unshifted first pass's breakdown row (the leading rows of the successful shifted
+    // passes are the shifted CholeskyQR3 of the leading, well-conditioned block)
+    if (r < 0 && info1[b] >= 0) r = info1[b];
     brow[b] = r;
   }
   was_shifted = shifted;
