@@ -143,7 +143,7 @@ class SequenceSolver:
         self._prev_solution = None
         self.max_workers = 8
         self.batched_update = True
-        self.groups = int(os.environ.get("KR_RECYCLE_GROUPS", "2"))
+        self.groups = int(os.environ.get("KR_RECYCLE_GROUPS", "4"))
         # the update orchestrated in C++ (kr_recycle_update); 0 = the torch orchestration
         self.native_update = os.environ.get("KR_NATIVE_RECYCLE", "1") != "0"
         # per-group solves overlapping the other groups' recycle updates (KR_PIPELINE=1).  Off by
