@@ -189,6 +189,9 @@ class SequenceSolver:
                 return g
 
             list(self._gpool.map(warm, range(ng)))
+            # group 0 runs on the calling thread (_recycle_batched): warm its handles too
+            with torch.cuda.stream(self._gstreams[0]):
+                _warm_thread(shape)
             torch.cuda.synchronize()
             return
         if self._streams is None or len(self._streams) < batch:
@@ -275,7 +278,9 @@ class SequenceSolver:
                         t.record_stream(main)
             return recs, extra
 
-        parts = list(self._gpool.map(work, range(ng)))
+        # groups 1.. on the pool, group 0 on this thread (one thread hand-off fewer)
+        futs = [self._gpool.submit(work, g) for g in range(1, ng)]
+        parts = [work(0)] + [f.result() for f in futs]
         for g in range(ng):
             main.wait_stream(self._gstreams[g])
         out = [r for recs, _ in parts for r in recs]
