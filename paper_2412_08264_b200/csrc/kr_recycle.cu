@@ -31,6 +31,7 @@
 #include <chrono>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
@@ -450,12 +451,20 @@ bool cholqr_ok(const std::vector<int32_t>& info, const std::vector<double>& st, 
 
 // cuSOLVER work size of the Householder branch (geqrf + orgqr of an n x T block)
 int64_t house_lwork(int64_t n, int T) {
+  // the cuSOLVER size queries are slow host calls and every workspace query makes them:
+  // cached per host thread and shape
+  static thread_local std::map<std::pair<int64_t, int>, int64_t> cache;
+  const auto key = std::make_pair(n, T);
+  const auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
   cusolverDnHandle_t sh;
   if (cusolver_handle(&sh, nullptr) != KR_OK) return 1 << 20;
   int lw1 = 0, lw2 = 0;
   cusolverDnDgeqrf_bufferSize(sh, (int)n, T, nullptr, (int)n, &lw1);
   cusolverDnDorgqr_bufferSize(sh, (int)n, T, T, nullptr, (int)n, nullptr, &lw2);
-  return std::max(lw1, lw2);
+  const int64_t lw = std::max(lw1, lw2);
+  cache[key] = lw;
+  return lw;
 }
 
 // Orthonormal rows Wb (t x n) spanning the candidate rows Ab when the Cholesky-QR passes
