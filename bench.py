@@ -1,20 +1,25 @@
 """Benchmark: hypergradients/sec of the recycled hypergradient solve (BASELINE.json metric).
 
 A "step" is one upper-level system of the replay protocol (experiments.py:390-463)
-for every sample of the batch: next_recycle (RGen-L(R): candidate basis, H W,
-J W, projected GSVD, prepare_recycle) + the batched recycled-MINRES solve with
-the NSC stop rule + J w, summed over samples (and over ranks for N > 1).
+for every sample a rank owns: next_recycle (RGen-L(R): candidate basis, H W, J W,
+projected GSVD, prepare_recycle) + the batched recycled-MINRES solve with the NSC
+stop rule + J w, and the sample-ordered sum of the per-sample hypergradients
+(all-gathered across ranks for N > 1).
 
-Workload (N=1): BASELINE configs[1] ("C2"): 8 samples of 128x128, blur 9x9
-sigma 1.5, 1% noise, J=8 learned 5x5 filters (p=208), phi_eps eps=1e-2,
-recycle dimension 20, max 200 Krylov iterations, NSC tolerance 1e-6.
-Inputs: seeded synthetic (problems.py); the frozen sequence of systems is
+Workload (default, N = 1): BASELINE configs[2] ("C3", the largest config that fits
+one GPU): 64 samples of 256x256, 15x15 blur sigma 2.5, 2% noise, J = 8 learned 5x5
+filters (p = 208), phi_eps with eps = 1e-2, recycle dimension 30, at most 300
+Krylov iterations, NSC tolerance 1e-6.  `--config C2` runs configs[1].
+Inputs: seeded synthetic data (problems.py); the frozen sequence of systems is
 synthetic (theta drifting, xhat = x_true + slowly drifting smooth field).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3]
 
-Multi-GPU (torchrun): weak scaling, each rank owns its own 8 samples
-(seeds offset by rank); the per-rank hypergradient sums are all-reduced.
+Multi-GPU: `--gpus N` without a torchrun environment re-launches itself under
+torch.distributed.run (one process per GPU, NCCL).  C3 is strong scaling: its fixed
+64-sample batch is sharded across the ranks (distributed.shard); C2 / C4 are weak
+scaling (8 / 16 samples per GPU, BASELINE's per-GPU share); C1 / C5 are
+single-sample configs and run one replica per GPU.
 """
 
 from __future__ import annotations
@@ -23,6 +28,7 @@ import argparse
 import gc
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -32,7 +38,7 @@ from pathlib import Path
 import numpy as np
 
 # load every CUDA module at context creation: a library kernel first used inside
-# the timed region (e.g. the Householder rank-drop path) must not pay module loading there
+# the timed region must not pay module loading there
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 ROOT = Path(__file__).resolve().parent
@@ -40,6 +46,12 @@ sys.path.insert(0, str(ROOT))
 
 STRATEGY = "RGen-L(R)-NSC"
 DELTA = 1e-6
+METRIC = "hypergradients/sec (recycled solve incl. HVP) + achieved HBM GB/s vs peak"
+# how each config's samples map onto ranks (BASELINE.json configs): C3 shards one fixed
+# 64-sample batch over 1/2/4/8 GPUs; C4 is 128 samples over 8 GPUs = 16 per GPU
+SHARDING = {"C1": "replica", "C2": "weak", "C3": "strong", "C4": "weak", "C5": "replica"}
+PER_GPU = {"C4": 16}
+THREAD_ENV = ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS")
 
 
 def parse():
@@ -48,16 +60,43 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C3")
     ap.add_argument("--strategy", default=STRATEGY)
     ap.add_argument("--delta", type=float, default=DELTA)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=40.0, help="seconds of timed CPU work (cpu_baseline)")
+    ap.add_argument("--ref-budget", type=float, default=150.0, help="seconds of timed CPU work (--impl reference)")
     return ap.parse_args()
 
 
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def relaunch_if_needed(args):
+    """`--gpus N` (N > 1) outside torchrun: run this script under torch.distributed.run."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def samples_for(name: str, cfg, world: int, rank: int):
+    """(first global sample, count on this rank, total samples of the job)."""
+    mode = SHARDING.get(name, "weak")
+    if mode == "strong":
+        from paper_2412_08264_b200.distributed import shard
+
+        r = shard(cfg.batch, world, rank)
+        return r.start, len(r), cfg.batch
+    per = PER_GPU.get(name, cfg.batch)
+    return rank * per, per, per * world
 
 
 class ClockSampler:
@@ -134,20 +173,29 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def measured_fp64_peak():
+    """fp64 DMMA peak measured on this pool's B200s (scripts/fp64_peak.cu, profiles/r2_fp64_peak.json)."""
+    p = ROOT / "profiles" / "r2_fp64_peak.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["dmma_tflops"]), "measured (profiles/r2_fp64_peak.json dmma_tflops)"
+    return 37.0, "fallback (nominal B200 fp64)"
+
+
 def measured_traffic(config: str, kernel: str):
     """DRAM bytes per launch of the dominant kernel from the committed ncu capture
-    (profiles/r1_traffic.json), or None when this config/kernel was not captured."""
-    p = Path(__file__).resolve().parent / "profiles" / "r1_traffic.json"
+    (profiles/traffic.json), or None when this config/kernel was not captured."""
+    p = ROOT / "profiles" / "traffic.json"
     if not p.exists():
         return None
     d = json.loads(p.read_text()).get(config)
     if not d or d.get("kernel") != kernel:
         return None
-    return int(d["dram_bytes_per_launch"]), d.get("source")
+    return int(d["dram_bytes_per_launch"]), d.get("source"), d.get("iterations_per_launch")
 
 
 def krylov_bytes_per_iter(kernel, n, s, nsc, w):
-    """Algorithmic HBM bytes per iteration per sample (DESIGN.md section 5).
+    """Algorithmic HBM bytes per iteration per sample (DESIGN.md section 6).
     RMINRES: 8n(21 + 3s + s_nsc) + the HVP's 8n(2 + w).
     Recycled CG: direction p = r + beta p - U mu (read r, p_old, U; write p), the
     stencil re-forming p on its tiles (r, p_old, U again), hp, the x/r update (read
@@ -156,6 +204,19 @@ def krylov_bytes_per_iter(kernel, n, s, nsc, w):
     if kernel == "kr_cg":
         return 8 * n * (12 + 3 * s + nsc) + 8 * n * w
     return 8 * n * (21 + 3 * s + nsc) + 8 * n * (2 + w)
+
+
+def hvp_flops_per_pixel(cfg):
+    """F = 8b + J(4q^2 + 2) + 2 (TV: 8b + 16)."""
+    if cfg.reg == "tv":
+        return 8 * cfg.blur_size + 16
+    return 8 * cfg.blur_size + cfg.num_filters * (4 * cfg.kernel_size ** 2 + 2) + 2
+
+
+def workload_text(name, cfg, count, total, args):
+    return (f"{name}: {total} samples x {cfg.size}^2 ({count} on this rank), blur {cfg.blur_size} sigma "
+            f"{cfg.blur_sigma}, J={cfg.num_filters} q={cfg.kernel_size}, s={cfg.recycle_dim}, max {cfg.max_iter} it, "
+            f"{args.strategy} delta={args.delta}, {'recycled CG' if cfg.method == 'cg' else 'RMINRES'}")
 
 
 # ---------------------------------------------------------------------------
@@ -167,32 +228,30 @@ def run_ours(args):
 
     from paper_2412_08264_b200 import HessianSolveConfig, SequenceSolver, _lib
     from paper_2412_08264_b200.bilevel import hypergradients
+    from paper_2412_08264_b200.distributed import allgather_sum
     from paper_2412_08264_b200.problems import CONFIGS, make_batch, synthetic_sequence
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = CONFIGS[args.config]
-    B = cfg.batch
-    model = make_batch(cfg, first=rank * B, count=B)
+    first, B, total = samples_for(args.config, cfg, world, rank)
+    model = make_batch(cfg, first=first, count=B)
     n = model.n
     steps_total = args.warmup + args.steps
     xt = model.x_true.cpu().numpy()
-    thetas, xhats_np = synthetic_sequence(cfg, xt, steps_total, seed=1234 + rank)
+    thetas, xhats_np = synthetic_sequence(cfg, xt, steps_total, seed=1234, first=first)
     xhats = [torch.as_tensor(x, device="cuda") for x in xhats_np]
     solver_cfg = HessianSolveConfig.from_strategy(args.strategy, recycle_dim=cfg.recycle_dim, delta=args.delta,
-                                                  method=cfg.method,
-                                                  max_iter=cfg.max_iter)
-
-    from paper_2412_08264_b200.distributed import allgather_sum
+                                                  method=cfg.method, max_iter=cfg.max_iter)
 
     def step(seq, i, X):
         hg, res, rec = hypergradients(model, thetas[i], X, seq)
-        d = allgather_sum(hg, B * world)  # sample-ordered sum, bitwise equal for any world size
+        d = allgather_sum(hg, total)  # sample-ordered sum, bitwise equal for any world size
         return d, res
 
-    # ---- device-resident run: warmup + timed ----
     # reserve the caching allocator's pool up front so per-step shape changes (t grows
     # with the previous solve's iteration count) do not hit cudaMalloc inside the timed region
     torch.empty(3 * 1024**3 // 8, dtype=torch.float64, device="cuda")
@@ -208,23 +267,13 @@ def run_ours(args):
     torch.cuda.synchronize()
     _lib.LAUNCHES.clear()
     _lib.PROFILE = []
-    evs = []
-    iters = []
-    # no cyclic-GC pauses inside timed regions (collect now, re-enable afterwards)
-    gc.collect()
+    evs, iters = [], []
+    gc.collect()  # no cyclic-GC pauses inside timed regions
     gc.disable()
     clk = ClockSampler(local)
+    dbg = os.environ.get("KR_BENCH_DEBUG")
     with clk:
-        dbg = os.environ.get("KR_BENCH_DEBUG")
-        if dbg:
-            from paper_2412_08264_b200 import batched as _bt
-            _bt.STATS = {}
-            if dbg == "mem":  # stack traces of every caching-allocator segment allocation
-                torch.cuda.memory._record_memory_history(max_entries=200000)
         for i in range(args.warmup, steps_total):
-            if dbg:
-                m0 = torch.cuda.memory_stats()
-                s0 = dict(_bt.STATS)
             flush.zero_()  # L2 flush between timed steps (outside the events)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -234,21 +283,7 @@ def run_ours(args):
             iters.append([r.iterations for r in res])
             if dbg:
                 torch.cuda.synchronize()
-                m1 = torch.cuda.memory_stats()
-                ds = {k: _bt.STATS[k] - s0.get(k, 0) for k in _bt.STATS}
-                if dbg == "mem" and m1.get('num_device_alloc', 0) > m0.get('num_device_alloc', 0):
-                    snap = torch.cuda.memory._snapshot()
-                    for tr in snap.get("device_traces", [[]])[0]:
-                        if tr.get("action") == "segment_alloc":
-                            fr = [f"{f['filename'].split('/')[-1]}:{f['line']}:{f['name']}" for f in tr.get("frames", [])
-                                  if "paper_2412" in f["filename"] or "bench" in f["filename"]]
-                            print(f"  segment_alloc {tr['size']} stream {tr.get('stream')} {fr[:6]}", file=sys.stderr)
-                    torch.cuda.memory._record_memory_history(enabled=None)
-                    torch.cuda.memory._record_memory_history(max_entries=200000)
-                print(f"step {i}: {e0.elapsed_time(e1):.1f} ms iters {iters[-1]} stats {ds} "
-                      f"mallocs {m1.get('num_device_alloc', 0) - m0.get('num_device_alloc', 0)} "
-                      f"retries {m1.get('num_alloc_retries', 0) - m0.get('num_alloc_retries', 0)}",
-                      file=sys.stderr, flush=True)
+                print(f"step {i}: {e0.elapsed_time(e1):.1f} ms iters {iters[-1]}", file=sys.stderr, flush=True)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -262,24 +297,31 @@ def run_ours(args):
         t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    hg_count = B * args.steps * world
+    hg_count = total * args.steps
     value = hg_count / (total_ms / 1e3)
 
     # roofline of the dominant kernel (the persistent RMINRES / recycled-CG solve)
     kname = "kr_cg" if cfg.method == "cg" else "kr_rminres"
     wts = 3 if cfg.reg == "tv" else cfg.num_filters
-    k_ms, k_bytes, k_iters = 0.0, 0.0, 0
+    k_ms, k_bytes, k_iters, k_launch = 0.0, 0.0, 0, 0
     for a, b, info in prof:
         if info["kernel"] != kname:
             continue
-        ms = a.elapsed_time(b)
+        k_ms += a.elapsed_time(b)
         its = int(info["iters"].sum().item())
-        k_ms += ms
         k_iters += its
+        k_launch += 1
         k_bytes += its * krylov_bytes_per_iter(kname, info["n"], info["s"], info["nsc"], wts)
     peak, peak_src = measured_peak()
     achieved = (k_bytes / 1e9) / (k_ms / 1e3) if k_ms > 0 else 0.0
     traffic = measured_traffic(args.config, kname)
+    bytes_per_iter = k_bytes / max(k_iters, 1)
+    traffic_per_launch = None
+    if traffic is not None and traffic[2]:
+        # the capture's DRAM bytes per batched iteration x this run's iterations per launch
+        traffic_per_launch = traffic[0] / traffic[2] * (k_iters / max(k_launch, 1))
+
+    hvp_line = hvp_fp64_roofline(model, thetas[-1], xhats[-1], cfg) if rank == 0 else None
 
     # ---- e2e through the public API with host buffers ----
     e2e = None
@@ -289,7 +331,7 @@ def run_ours(args):
         seq2.reserve(B, per_sample, shape=(n, t_max))
         for i in range(args.warmup):
             X = pinned[i].to("cuda", non_blocking=True)
-            step(seq2, i, X).__getitem__(0).cpu()
+            step(seq2, i, X)[0].cpu()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -312,42 +354,42 @@ def run_ours(args):
 
     cpu_base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu_base = cpu_baseline(cfg, xt, thetas, xhats_np, args)
+        cpu_base = cpu_baseline(args)
     if rank == 0:
         flat_iters = [x for row in iters for x in row]
         line = {
-            "metric": "hypergradients/sec (recycled solve incl. HVP) + achieved HBM GB/s vs peak",
-            "value": value, "unit": "hypergradients/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": "hypergradients/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {B} samples x {cfg.size}^2, blur {cfg.blur_size} "
-                                   f"sigma {cfg.blur_sigma}, J={cfg.num_filters} q={cfg.kernel_size}, "
-                                   f"s={cfg.recycle_dim}, max {cfg.max_iter} it, {args.strategy} delta={args.delta}, "
-                                   f"{'recycled CG' if cfg.method == 'cg' else 'RMINRES'}",
-                       "samples_per_gpu": B, "image": cfg.size, "recycle_dim": cfg.recycle_dim,
-                       "max_iter": cfg.max_iter, "strategy": args.strategy, "delta": args.delta,
-                       "krylov": cfg.method,
+            "scaling": {"strong": "strong", "weak": "weak", "replica": "weak"}[SHARDING.get(args.config, "weak")],
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_text(args.config, cfg, B, total, args),
+                       "samples_total": total, "samples_per_gpu": B, "image": cfg.size,
+                       "recycle_dim": cfg.recycle_dim, "max_iter": cfg.max_iter, "strategy": args.strategy,
+                       "delta": args.delta, "krylov": cfg.method,
                        "sequence": "synthetic frozen sequence (problems.synthetic_sequence)",
                        "l2": "flushed (256 MB write) before every timed step",
-                       "parallelism": f"sample-sharded dp{world}"},
+                       "parallelism": f"sample-sharded dp{world} ({SHARDING.get(args.config, 'weak')})"},
             "step_ms": [round(x, 3) for x in step_ms],
             "iterations_per_solve": {"mean": float(np.mean(flat_iters)), "min": int(np.min(flat_iters)),
-                                     "max": int(np.max(flat_iters))},
+                                     "max": int(np.max(flat_iters)), "at_max_iter": int(np.sum(
+                                         np.asarray(flat_iters) >= cfg.max_iter))},
             "roofline": {"kernel": f"{kname} (persistent {'recycled CG' if kname == 'kr_cg' else 'RMINRES'}, "
                                    "all iterations of all samples)",
                          "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if peak else None,
-                         "traffic": None if traffic is None else traffic[0],
-                         "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
+                         "traffic": traffic_per_launch,
+                         "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum "
+                                         "per batched iteration of the capture x this run's iterations per launch)",
                          "traffic_source": None if traffic is None else traffic[1],
-                         "algorithmic_bytes_per_launch": (k_bytes / max(len([1 for _, _, i in prof
-                                                                            if i["kernel"] == kname]), 1)),
+                         "algorithmic_bytes_per_launch": k_bytes / max(k_launch, 1),
+                         "algorithmic_bytes_per_iteration": bytes_per_iter,
                          "peak_source": peak_src,
                          "algorithmic_bytes": ("per iteration per sample 8n(12+3s+s_nsc)+8n*w (recycled CG)"
                                                if kname == "kr_cg" else
                                                "SURVEY 8(d): per iteration per sample 8n(21+3s+s_nsc)+8n(2+J)"),
                          "kernel_ms_total": k_ms, "kernel_share_of_step": k_ms / total_ms if total_ms else None,
                          "krylov_iterations": k_iters},
+            "hvp_fp64": hvp_line,
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
             "e2e": e2e,
@@ -358,128 +400,159 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def _oracle_solve_sample(payload):
-    """One hypergradient of one sample through the CPU oracle (reference algorithm)."""
+def hvp_fp64_roofline(model, theta, xhat, cfg, cols: int = 64):
+    """The H W product of the recycle update (kr_hvp over `cols` columns of every sample)
+    timed alone with CUDA events, against the measured fp64 peak: SURVEY 8(d)'s
+    n F flops per column (F = 8b + J(4q^2 + 2) + 2)."""
+    import torch
+
+    H, _ = model.at(theta, xhat)
+    B, n = model.batch, model.n
+    W = torch.randn(B, cols, n, dtype=torch.float64, device="cuda").transpose(1, 2)  # (B, n, t), columns contiguous
+    for _ in range(2):
+        H._apply_cols(W)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 3
+    e0.record()
+    for _ in range(reps):
+        H._apply_cols(W)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    flops = B * cols * n * hvp_flops_per_pixel(cfg)
+    peak, src = measured_fp64_peak()
+    achieved = flops / (ms / 1e3) / 1e12
+    return {"kernel": "hvp_kernel (H W of the recycle update)", "bound": "fp64", "columns": B * cols,
+            "ms": ms, "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "flops_per_pixel": hvp_flops_per_pixel(cfg), "peak_source": src}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs: the oracle port of the reference algorithm (oracle/ restates krecycle's
+# SequenceSolver / rminres / next_recycle / NscRule with the config operators).  Worker
+# processes are started with the spawn method AFTER the BLAS thread variables are set, so
+# each one imports numpy single-threaded.
+
+
+def _cpu_worker(conn, name, k, strategy, delta):
+    """Owns sample k's oracle SequenceSolver; runs the systems it is sent, returns wall times."""
     from oracle import cpu_bilevel as ob
     from oracle import cpu_imaging as im
-
-    cfg, k, x_true, y, thetas, xhats, strategy, delta, systems = payload
-    taps = im.gaussian_taps(cfg.blur_size, cfg.blur_sigma)
-    shape = (cfg.size, cfg.size)
-    data = im.DataTerm("blur", shape, y, scale=2.0, ridge=0.0, taps=taps, x_true=x_true)
-    reg = im.Regularizer("filters", cfg.num_filters, cfg.kernel_size, "smooth_abs", cfg.eps) if cfg.reg != "tv" \
-        else im.Regularizer("tv", eps=cfg.eps)
-    model = im.Model(data, reg)
-    solver = ob.SequenceSolver(ob.SolveConfig.from_strategy(strategy, recycle_dim=cfg.recycle_dim, delta=delta,
-                                                            max_iter=cfg.max_iter, method=cfg.method))
-    count = 0
-    for i in systems:
-        H = im.hessian(model, thetas[i], xhats[i])
-        J = im.jacobian(model, thetas[i], xhats[i])
-        res, _ = solver.solve(H, xhats[i] - x_true, J)
-        J.apply_adjoint(res.solution)
-        count += 1
-    return count
-
-
-def cpu_baseline(cfg, xt, thetas, xhats_np, args):
-    """The oracle port timed on this host, single core, bounded sample."""
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    from paper_2412_08264_b200.problems import sample_arrays
-
-    _, y = sample_arrays(cfg, 0)
-    systems = [0, 1]
-    t0 = time.perf_counter()
-    cnt = _oracle_solve_sample((cfg, 0, xt[0], y, thetas, [x[0] for x in xhats_np], args.strategy, args.delta,
-                                systems))
-    dt = time.perf_counter() - t0
-    return {"value": cnt / dt, "unit": "hypergradients/s", "cores": 1, "kind": "port",
-            "sample": f"sample 0, systems 0-1 of the same frozen sequence ({cnt} hypergradients, {dt:.1f} s)"}
-
-
-def _reference_worker(conn, payload):
-    """Persistent CPU worker owning one sample's SequenceSolver (recycling state carries over)."""
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    from oracle import cpu_bilevel as ob
-    from oracle import cpu_imaging as im
-
-    cfg, k, x_true, y, thetas, xhats, strategy, delta = payload
-    taps = im.gaussian_taps(cfg.blur_size, cfg.blur_sigma)
-    data = im.DataTerm("blur", (cfg.size, cfg.size), y, scale=2.0, ridge=0.0, taps=taps, x_true=x_true)
-    reg = im.Regularizer("filters", cfg.num_filters, cfg.kernel_size, "smooth_abs", cfg.eps) if cfg.reg != "tv" \
-        else im.Regularizer("tv", eps=cfg.eps)
-    model = im.Model(data, reg)
-    solver = ob.SequenceSolver(ob.SolveConfig.from_strategy(strategy, recycle_dim=cfg.recycle_dim, delta=delta,
-                                                            max_iter=cfg.max_iter, method=cfg.method))
-    while True:
-        i = conn.recv()
-        if i is None:
-            break
-        H = im.hessian(model, thetas[i], xhats[i])
-        J = im.jacobian(model, thetas[i], xhats[i])
-        res, _ = solver.solve(H, xhats[i] - x_true, J)
-        J.apply_adjoint(res.solution)
-        conn.send(res.iterations)
-
-
-def run_reference(args):
-    """The reference's CPU path: the oracle port of krecycle's SequenceSolver / rminres /
-    next_recycle / NscRule with the config's operators, one process per host core, each
-    process owning one sample's recycling state across steps (same workload as ours,
-    bounded to min(cores, batch) samples)."""
-    rank, world, _ = dist_env()
-    if rank != 0:
-        return
-    import multiprocessing as mp
-
     from paper_2412_08264_b200.problems import CONFIGS, sample_arrays, synthetic_sequence
 
-    cfg = CONFIGS[args.config]
-    cores = len(os.sched_getaffinity(0))
-    nproc = max(1, min(cores, cfg.batch))
-    data = [sample_arrays(cfg, k) for k in range(cfg.batch)]
-    xt = np.stack([d[0] for d in data])
-    warm = min(args.warmup, 1)
-    steps_total = warm + args.steps
-    thetas, xhats_np = synthetic_sequence(cfg, xt, args.warmup + args.steps, seed=1234)
-    ctx = mp.get_context("fork")
+    cfg = CONFIGS[name]
+    x_true, y = sample_arrays(cfg, k)
+    taps = im.gaussian_taps(cfg.blur_size, cfg.blur_sigma)
+    data = im.DataTerm("blur", (cfg.size, cfg.size), y, scale=2.0, ridge=0.0, taps=taps, x_true=x_true)
+    reg = (im.Regularizer("filters", cfg.num_filters, cfg.kernel_size, "smooth_abs", cfg.eps) if cfg.reg != "tv"
+           else im.Regularizer("tv", eps=cfg.eps))
+    model = im.Model(data, reg)
+    solver = ob.SequenceSolver(ob.SolveConfig.from_strategy(strategy, recycle_dim=cfg.recycle_dim, delta=delta,
+                                                            max_iter=cfg.max_iter, method=cfg.method))
+    thetas = xhats = None
+    conn.send("ready")
+    while True:
+        msg = conn.recv()
+        if msg is None:
+            break
+        i, steps = msg
+        if thetas is None or len(thetas) < steps:
+            thetas, xs = synthetic_sequence(cfg, x_true[None], steps, seed=1234, first=k)
+            xhats = [x[0] for x in xs]
+        t0 = time.perf_counter()
+        H = im.hessian(model, thetas[i], xhats[i])
+        J = im.jacobian(model, thetas[i], xhats[i])
+        res, _ = solver.solve(H, xhats[i] - x_true, J)
+        J.apply_adjoint(res.solution)
+        conn.send((res.iterations, time.perf_counter() - t0))
+
+
+def _spawn_workers(name, samples, strategy, delta):
+    import multiprocessing as mp
+
+    for v in THREAD_ENV:
+        os.environ[v] = "1"
+    ctx = mp.get_context("spawn")
     conns, procs = [], []
-    for k in range(nproc):
+    for k in samples:
         parent, child = ctx.Pipe()
-        payload = (cfg, k, xt[k], data[k][1], thetas, [x[k] for x in xhats_np], args.strategy, args.delta)
-        pr = ctx.Process(target=_reference_worker, args=(child, payload), daemon=True)
+        pr = ctx.Process(target=_cpu_worker, args=(child, name, k, strategy, delta), daemon=True)
         pr.start()
         conns.append(parent)
         procs.append(pr)
+    for c in conns:
+        assert c.recv() == "ready"
+    return conns, procs
 
-    def one_step(i):
+
+def _run_cpu(name, samples, strategy, delta, steps_cap, budget):
+    """System 0 (cold, untimed), then recycled systems 1, 2, ... on every worker in parallel
+    until steps_cap systems or `budget` seconds of timed work (at least one system)."""
+    conns, procs = _spawn_workers(name, samples, strategy, delta)
+    total_systems = steps_cap + 1
+
+    def one(i):
         for c in conns:
-            c.send(i)
+            c.send((i, total_systems))
         return [c.recv() for c in conns]
 
-    for i in range(warm):
-        one_step(i)
+    one(0)
     t0 = time.perf_counter()
-    its = []
-    for i in range(warm, steps_total):
-        its += one_step(i)
+    done, its = 0, []
+    while done < steps_cap:
+        its += [r[0] for r in one(1 + done)]
+        done += 1
+        if time.perf_counter() - t0 >= budget:
+            break
     dt = time.perf_counter() - t0
     for c in conns:
         c.send(None)
     for pr in procs:
         pr.join(timeout=30)
-    done = nproc * args.steps
-    value = done / dt
+    return done, dt, its
+
+
+def cpu_baseline(args):
+    """The oracle port on ONE host core (a spawned single-threaded process), sample 0:
+    system 0 untimed, then recycled systems until --cpu-budget seconds."""
+    done, dt, its = _run_cpu(args.config, [0], args.strategy, args.delta, max(args.steps, 1), args.cpu_budget)
+    return {"value": done / dt, "unit": "hypergradients/s", "cores": 1, "kind": "port",
+            "sample": f"sample 0, recycled systems 1..{done} after an untimed cold system 0 ({done} hypergradients, "
+                      f"{dt:.1f} s, iterations {its}); single-threaded BLAS in a spawned process"}
+
+
+def run_reference(args):
+    """The reference's CPU path: the oracle port of krecycle's SequenceSolver / rminres /
+    next_recycle / NscRule with the config's operators, one single-threaded process per
+    host core, each owning one sample's recycling state (samples 0..cores-1 of the
+    config's N=1 workload).  Bounded: one untimed cold system, then recycled systems
+    until --steps or --ref-budget seconds.  Under torchrun only rank 0 runs."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2412_08264_b200.problems import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    _, count, _ = samples_for(args.config, cfg, 1, 0)
+    cores = len(os.sched_getaffinity(0))
+    nproc = max(1, min(cores, count))
+    done, dt, its = _run_cpu(args.config, list(range(nproc)), args.strategy, args.delta, max(args.steps, 1),
+                             args.ref_budget)
+    value = nproc * done / dt
     line = {
-        "metric": "hypergradients/sec (recycled solve incl. HVP) + achieved HBM GB/s vs peak", "impl": "reference",
-        "value": value, "unit": "hypergradients/s", "n_gpus": world, "steps": args.steps, "warmup": warm,
-        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}, bounded to {nproc} of {cfg.batch} samples (one per core); "
-                               f"systems {warm}..{steps_total - 1} timed, {warm} warm-up system",
+        "metric": METRIC, "impl": "reference",
+        "value": value, "unit": "hypergradients/s", "n_gpus": world, "steps": done, "warmup": 1,
+        "ms_per_step": 1e3 * dt / done, "higher_is_better": True,
+        "scaling": {"strong": "strong", "weak": "weak", "replica": "weak"}[SHARDING.get(args.config, "weak")],
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_text(args.config, cfg, count, count, args),
+                   "bounded": f"samples 0..{nproc - 1} ({nproc} of {count}; one process per core), "
+                              f"recycled systems 1..{done} timed after an untimed cold system 0 "
+                              f"(--steps {args.steps}, budget {args.ref_budget:.0f} s)",
                    "strategy": args.strategy, "delta": args.delta, "iterations_mean": float(np.mean(its))},
         "cpu_baseline": {"value": value, "unit": "hypergradients/s", "cores": nproc, "kind": "port",
-                         "sample": f"{nproc} samples x {args.steps} recycled systems, one process per core"},
+                         "sample": f"{nproc} samples x {done} recycled systems, one single-threaded process per core"},
         "e2e": {"value": value, "unit": "hypergradients/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -487,6 +560,7 @@ def run_reference(args):
 
 if __name__ == "__main__":
     a = parse()
+    relaunch_if_needed(a)
     if a.impl == "reference":
         run_reference(a)
     else:

@@ -50,7 +50,11 @@ extern "C" {
 
 typedef struct CUstream_st* kr_stream_t; /* == cudaStream_t */
 
-#define KR_ABI_VERSION 2
+#define KR_ABI_VERSION 3
+
+/* Largest candidate width t = k_prev + s_prev of the small dense kernels and the recycle
+ * update: BASELINE C5 with s = 80 and 500 iterations (t <= 580), with margin. */
+#define KR_TMAX 640
 
 #define KR_OK 0
 #define KR_EINVAL (-1)
@@ -178,7 +182,9 @@ int kr_syev_select(const double* A, int64_t lda, int64_t bsa, const int32_t* dim
  * Cholesky-QR passes (recycling._cholqr2 batched; the reference's pivoted QR at
  * recycling.py:187-199, 362-383 and the QR of [Jt; Ht] at :305) and of the
  * W^T H W condition screen (recycling.py:290-296).  G b: element (i, j) at
- * G + b*bsg + i*ldg + j (symmetrised), t_b = dims[b] <= tmax <= 228 (DEVICE int32).
+ * G + b*bsg + i*ldg + j (symmetrised), t_b = dims[b] <= tmax <= KR_TMAX (DEVICE int32).
+ * tmax <= 228 works in shared memory (work may be null); larger tmax needs
+ * kr_chol_inv_workspace(batch, tmax) doubles of DEVICE work (the packed factors).
  * flags bit 0: scale by D = sqrt(diag G); bit 1: write F; bit 2: skip mode -- a row
  * whose pivot falls below 4 t eps times its diagonal is removed (zero column of L,
  * zero row of F, skipped[b*tmax + i] = 1) instead of stopping; bit 3: partial -- on a
@@ -188,9 +194,11 @@ int kr_syev_select(const double* A, int64_t lda, int64_t bsa, const int32_t* dim
  * row-major (F + b*bsf + i*ldf + j), zero upper triangle, identity pad block.
  * info[b] = -1 or the first row whose pivot is not positive; stats[4b..4b+3] =
  * (min L_jj, max L_jj, min D, 0) (nullable). */
+int64_t kr_chol_inv_workspace(int32_t batch, int32_t tmax);
 int kr_chol_inv(const double* G, int64_t ldg, int64_t bsg, const int32_t* dims, int32_t batch,
                 int32_t tmax, int32_t flags, const double* shift, double* F, int64_t ldf, int64_t bsf,
-                double* stats, int32_t* info, uint8_t* skipped, kr_stream_t stream);
+                double* stats, int32_t* info, uint8_t* skipped, double* work, int64_t work_len,
+                kr_stream_t stream);
 
 /* QR with column pivoting of small matrices (t_b <= tmax <= 256), one CTA each:
  * the pivoted QR of build_candidate_basis / prepare_recycle (recycling.py:187-199,

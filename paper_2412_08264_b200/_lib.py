@@ -39,7 +39,7 @@ class KrOp(ctypes.Structure):
     ]
 
 
-ABI_VERSION = 2  # KR_ABI_VERSION of include/krecycle_b200.h
+ABI_VERSION = 3  # KR_ABI_VERSION of include/krecycle_b200.h
 
 
 class KrSolveArgs(ctypes.Structure):
@@ -102,8 +102,9 @@ def _declare(lib):
         "kr_syev_select_workspace": (_c_i64, [_c_i32, _c_i32]),
         "kr_syev_select": (_c_i32, [_c_p, _c_i64, _c_i64, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_i64,
                                     _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_p]),
+        "kr_chol_inv_workspace": (_c_i64, [_c_i32, _c_i32]),
         "kr_chol_inv": (_c_i32, [_c_p, _c_i64, _c_i64, _c_p, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_i64, _c_i64,
-                                 _c_p, _c_p, _c_p, _c_p]),
+                                 _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p]),
         "kr_qrcp_small": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, ctypes.c_double, _c_p, _c_p, _c_p, _c_p, _c_i64,
                                    _c_p]),
         "kr_qrcp_small_cluster": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, ctypes.c_double, _c_p, _c_p, _c_p, _c_p,
@@ -127,7 +128,7 @@ EXPORTED = (
     "kr_abi_version", "kr_last_error", "kr_device_info", "kr_struct_sizes", "kr_op_prepare",
     "kr_hvp", "kr_jadj_workspace", "kr_jadj", "kr_lower_workspace", "kr_lower_eval",
     "kr_rminres_workspace", "kr_rminres", "kr_cg_workspace", "kr_cg",
-    "kr_syev_select_workspace", "kr_syev_select", "kr_chol_inv", "kr_qrcp_small", "kr_qrcp_small_cluster",
+    "kr_syev_select_workspace", "kr_syev_select", "kr_chol_inv_workspace", "kr_chol_inv", "kr_qrcp_small", "kr_qrcp_small_cluster",
     "kr_gram_workspace", "kr_gram", "kr_recycle_workspace", "kr_recycle_update", "kr_thread_warmup",
     "kr_ordered_sum",
 )

@@ -25,7 +25,7 @@ import torch
 from . import _lib
 
 SIZE_CODES = {"S": 0, "L": 1, "M": 2}
-EIG_TMAX = 228
+EIG_TMAX = 640  # KR_TMAX
 
 
 def syev_select(M: torch.Tensor, dims: torch.Tensor, size: str, s: int):
@@ -101,7 +101,7 @@ def gram(A: torch.Tensor, Bm: torch.Tensor | None = None) -> torch.Tensor:
     return G
 
 
-QRCP_TMAX = 256
+QRCP_TMAX = 640  # KR_TMAX (kr_qrcp_small_cluster)
 PIVOT_COND = 1e9   # below this cond(A) bound pivoted QR keeps every column (|R_kk| ~ sigma_k > 1e-10 |R_00|)
 
 CHOLQR_TOL = 1e-7   # recycling.CHOLQR_TOL
@@ -125,7 +125,7 @@ def _masked_extrema(d: torch.Tensor, mask: torch.Tensor):
     return torch.where(live, d, -big).amax(1), torch.where(live, d, big).amin(1)
 
 
-CHOL_TMAX = 228          # kr_chol_inv's shared-memory limit
+CHOL_TMAX = 640          # KR_TMAX: kr_chol_inv (shared memory to 228, an L2-resident workspace above)
 SKIP_DEPENDENT = False   # remove dependent rows inside the Cholesky passes (kr_chol_inv skip mode)
 SHIFTED_COND_MAX = 1e14  # shifted CholeskyQR3 is backward stable below ~1/u; keep a margin
 
@@ -136,7 +136,7 @@ def _chol_inv(G: torch.Tensor, dims: torch.Tensor, scale: bool, shift: torch.Ten
     leading dims[b] block, G_s = L L^T.  Returns (F, info, stats): F = L^-1 D^-1
     (row-major, identity pad; None unless inverse), info[b] = first failing row or
     -1, stats[b] = (min L_jj, max L_jj, min D).  kr_chol_inv (one CTA per matrix)
-    for T <= 228, torch.linalg otherwise.  skip=True (kernel only): dependent rows
+    for T <= KR_TMAX (640), torch.linalg otherwise.  skip=True (kernel only): dependent rows
     are removed instead of failing; returns a 4th value, the (B, T) removed mask
     (None on the torch path, which reports the first failing row instead)."""
     B, T, _ = G.shape
@@ -150,11 +150,14 @@ def _chol_inv(G: torch.Tensor, dims: torch.Tensor, scale: bool, shift: torch.Ten
         skipped = torch.empty(B, T, dtype=torch.uint8, device=dev) if skip else None
         sh = None if shift is None else shift.to(torch.float64).contiguous()
         flags = int(scale) | (2 if inverse else 0) | (4 if skip else 0)
-        _lib.check(_lib.lib().kr_chol_inv(G.data_ptr(), T, T * T, dims.data_ptr(), B, T, flags,
-                                          0 if sh is None else sh.data_ptr(), 0 if F is None else F.data_ptr(),
-                                          T, T * T, stats.data_ptr(), info.data_ptr(),
-                                          0 if skipped is None else skipped.data_ptr(), _lib.stream_ptr()),
-                   "kr_chol_inv")
+        L = _lib.lib()
+        wl = int(L.kr_chol_inv_workspace(B, T))
+        ws = torch.empty(max(wl, 1), dtype=torch.float64, device=dev)
+        _lib.check(L.kr_chol_inv(G.data_ptr(), T, T * T, dims.data_ptr(), B, T, flags,
+                                 0 if sh is None else sh.data_ptr(), 0 if F is None else F.data_ptr(),
+                                 T, T * T, stats.data_ptr(), info.data_ptr(),
+                                 0 if skipped is None else skipped.data_ptr(), ws.data_ptr(), wl,
+                                 _lib.stream_ptr()), "kr_chol_inv")
         _lib.note_launch("kr_chol_inv")
         if skip:
             return F, info, stats, skipped.bool()
@@ -487,7 +490,7 @@ def recycle_update(strategy, s: int, H, J, bases, recycles, reuse_products: bool
     return out
 
 
-NATIVE_TMAX = 228
+NATIVE_TMAX = 640  # KR_TMAX
 
 
 def _uniform_rows(mats, n, dev):
@@ -529,7 +532,7 @@ def recycle_update_native(strategy, s: int, H, J, bases, recycles, reuse_product
                           scratch: dict | None = None, out: tuple | None = None, out_src: tuple | None = None):
     """``recycle_update`` through the native orchestrator ``kr_recycle_update`` (one
     C-ABI call per batch: no Python per-op overhead, no GIL); same contract and
-    results.  Falls back to ``recycle_update`` beyond the kernels' t <= 228.
+    results.  Falls back to ``recycle_update`` beyond the kernels' t <= KR_TMAX (640).
     ``scratch`` (optional, one dict per stream) keeps the temporaries -- H W and the
     orchestrator's workspace -- across calls instead of reallocating them.  ``out``
     (optional): (U, C, Z) row blocks (B, s, n) to write into -- slices of whole-batch

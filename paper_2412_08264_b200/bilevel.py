@@ -93,8 +93,6 @@ def _warm_thread(shape=None):
     torch.linalg.cholesky_ex(g)
     torch.linalg.solve_triangular(torch.linalg.cholesky(g), g, upper=False)
     torch.linalg.qr(torch.randn(4096, 64, dtype=torch.float64, device="cuda"))
-    if shape is not None:  # the tall Householder QR of the pivoted rank-drop path
-        torch.linalg.qr(torch.randn(*shape, dtype=torch.float64, device="cuda"))
     torch.linalg.eigh(g)
     torch.linalg.eigvalsh(g)
     torch.bmm(a.unsqueeze(0), a.unsqueeze(0))

@@ -9,7 +9,11 @@
 // Here one CTA owns one matrix for the whole computation:
 //
 //   1. Householder tridiagonalization (LAPACK sytd2, lower) on the packed
-//      lower triangle held in shared memory (t <= EIG_TPACK);
+//      lower triangle held in shared memory (t <= EIG_TPACK), or -- for the wider
+//      candidate blocks of C3-C5 (t <= KR_TMAX) -- on the full symmetric matrix in
+//      a global workspace (L2-resident; rows read coalesced, both triangles
+//      updated with a symmetric rounding order so the matrix stays bitwise
+//      symmetric, reflector k stored in row k);
 //   2. the selected eigenvalues by Sturm-count multisection: the 32 lanes of a
 //      warp evaluate 32 points of the bracket per round (x33 per round), with
 //      the division-free three-term recurrence (rescaled by powers of two);
@@ -34,6 +38,7 @@ namespace {
 constexpr int ENT = 512;
 constexpr int EW = ENT / 32;
 constexpr int EIG_TPACK = 228;
+constexpr int EIG_TGLOB = KR_TMAX;
 constexpr int EIG_MAXSEL = 128;
 constexpr int EIG_RED = 64;
 constexpr int MAXITS = 5;
@@ -49,7 +54,7 @@ struct EigParams {
   double* Z;
   int64_t ldz, bsz;
   int32_t* nsel;
-  double* work;  // per sample: packed reflectors T(T+1)/2
+  double* work;  // per sample: packed reflectors T(T+1)/2 (shared-memory variant) or the full T x T matrix
 };
 
 __device__ __forceinline__ int64_t pk(int i, int j) { return (int64_t)i * (i + 1) / 2 + j; }  // i >= j
@@ -224,6 +229,7 @@ __device__ __forceinline__ double start_value(int q, int i) {
   return (double)(h >> 8) * (2.0 / 16777216.0) - 1.0;
 }
 
+template <int RPL, bool GLOB>
 __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
   extern __shared__ double sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -262,6 +268,87 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
   double* yv = R + T;
   double* Ap = R + 2 * T;
   const double* Ab = P.A + (int64_t)b * P.bsa;
+  double* Af = P.work + (int64_t)b * T * T;  // GLOB: full matrix, row i at Af + i T
+  if constexpr (GLOB) {
+    double* ww = R + 2 * T;
+    for (int i = warp; i < t; i += EW) {
+      const double* ai = Ab + (int64_t)i * P.lda;
+      for (int j = lane; j < t; j += 32)
+        Af[(int64_t)i * T + j] = i == j ? __ldg(ai + j) : 0.5 * (__ldg(ai + j) + __ldg(Ab + (int64_t)j * P.lda + i));
+    }
+    __syncthreads();
+    for (int k = 0; k + 1 < t; ++k) {
+      const int m = t - k - 1;
+      double* rk = Af + (int64_t)k * T;  // row k == column k (symmetric)
+      double part = 0.0;
+      for (int i = k + 2 + tid; i < t; i += ENT) {
+        const double x = rk[i];
+        part += x * x;
+      }
+      const double xn2 = bsum(part, red);
+      const double alpha = rk[k + 1];
+      double tk = 0.0, beta = alpha;
+      if (xn2 > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+        tk = (beta - alpha) / beta;
+        const double scal = 1.0 / (alpha - beta);
+        for (int i = tid; i < m; i += ENT) {
+          double v = 1.0;
+          if (i > 0) {
+            v = rk[k + 1 + i] * scal;
+            rk[k + 1 + i] = v;
+          }
+          vv[i] = v;
+        }
+      }
+      if (tid == 0) {
+        e[k] = beta;
+        tau[k] = tk;
+        d[k] = rk[k];
+      }
+      if (tk == 0.0) continue;  // block-uniform (xn2 is broadcast)
+      __syncthreads();
+      // y = tau A22 v: a warp per row, two rows in flight, coalesced row reads
+      for (int r = warp; r < m; r += 2 * EW) {
+        const int r2 = r + EW;
+        const bool two = r2 < m;
+        const double* a1 = Af + (int64_t)(k + 1 + r) * T + k + 1;
+        const double* a2 = Af + (int64_t)(k + 1 + (two ? r2 : r)) * T + k + 1;
+        double acc = 0.0, acc2 = 0.0;
+        for (int c = lane; c < m; c += 32) {
+          const double vc = vv[c];
+          acc += a1[c] * vc;
+          acc2 += a2[c] * vc;
+        }
+        acc = warp_sum(acc);
+        acc2 = warp_sum(acc2);
+        if (lane == 0) {
+          yv[r] = tk * acc;
+          if (two) yv[r2] = tk * acc2;
+        }
+      }
+      __syncthreads();
+      double pv = 0.0;
+      for (int r = tid; r < m; r += ENT) pv += yv[r] * vv[r];
+      const double kappa = -0.5 * tk * bsum(pv, red);
+      for (int r = tid; r < m; r += ENT) ww[r] = fma(kappa, vv[r], yv[r]);
+      __syncthreads();
+      // A22 -= v w^T + w v^T on both triangles; (r, c) and (c, r) round identically
+      for (int r = warp; r < m; r += EW) {
+        const double vi = vv[r], wi = ww[r];
+        double* row = Af + (int64_t)(k + 1 + r) * T + k + 1;
+        for (int c = lane; c < m; c += 32)
+          row[c] -= __dadd_rn(__dmul_rn(vi, ww[c]), __dmul_rn(wi, vv[c]));
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      d[t - 1] = Af[(int64_t)(t - 1) * T + t - 1];
+      e[t - 1] = 0.0;
+      tau[t - 1] = 0.0;
+    }
+    __syncthreads();
+  } else {
   // (A + A^T) / 2 with coalesced reads: storage rows into the lower triangle, then
   // storage rows again onto the transposed positions
   for (int i = warp; i < t; i += EW) {
@@ -361,6 +448,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
   double* Hb = P.work + (int64_t)b * ((int64_t)T * (T + 1) / 2);
   for (int64_t i = tid; i < pk(t, 0); i += ENT) Hb[i] = Ap[i];
   __syncthreads();
+  }  // !GLOB
 
   KR_EMARK(0);
   // ---------------- 2. selected eigenvalues ----------------
@@ -517,9 +605,11 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
 
   KR_EMARK(2);
   // ---------------- 4. back-transformation ----------------
-  for (int64_t i = tid; i < pk(t, 0); i += ENT) Ap[i] = Hb[i];
-  __syncthreads();
-  constexpr int RPL = (EIG_TPACK + 31) / 32;  // rows per lane
+  if constexpr (!GLOB) {
+    const double* Hb = P.work + (int64_t)b * ((int64_t)T * (T + 1) / 2);
+    for (int64_t i = tid; i < pk(t, 0); i += ENT) Ap[i] = Hb[i];
+    __syncthreads();
+  }
   for (int q = warp; q < s; q += EW) {
     double* zq = Zb + (int64_t)q * P.ldz;
     double z[RPL];
@@ -535,7 +625,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
 #pragma unroll
       for (int c = 0; c < RPL; ++c) {
         const int i = lane + 32 * c;
-        hv[c] = (i > k + 1 && i < t) ? Ap[pk32(i, k)] : 1.0;
+        hv[c] = (i > k + 1 && i < t) ? (GLOB ? Af[(int64_t)k * T + i] : Ap[pk32(i, k)]) : 1.0;
       }
 #pragma unroll
       for (int c = 0; c < RPL; ++c) {
@@ -592,7 +682,7 @@ __global__ void __launch_bounds__(ENT, 1) eig_select_kernel(EigParams P) {
 
 int64_t eig_smem_doubles(int T, int* nw_out) {
   const int64_t base = 4 * (int64_t)T + EIG_MAXSEL + EIG_RED;
-  const int64_t r1 = 2 * (int64_t)T + (int64_t)T * (T + 1) / 2;
+  const int64_t r1 = T > EIG_TPACK ? 3 * (int64_t)T : 2 * (int64_t)T + (int64_t)T * (T + 1) / 2;
   const int64_t per_vec = 6 * (int64_t)T + (T + 7) / 8;
   const int64_t cap = (227 * 1024) / 8 - 8 - base;  // static smem (cl_first, s_int) kept out
   int nw = (int)((cap > r1 ? cap : r1) / per_vec);
@@ -610,7 +700,7 @@ using namespace kr;
 
 extern "C" int64_t kr_syev_select_workspace(int32_t batch, int32_t tmax) {
   if (batch < 0 || tmax < 0) return -1;
-  return (int64_t)batch * ((int64_t)tmax * (tmax + 1) / 2);
+  return (int64_t)batch * (tmax > EIG_TPACK ? (int64_t)tmax * tmax : (int64_t)tmax * (tmax + 1) / 2);
 }
 
 extern "C" int kr_syev_select(const double* A, int64_t lda, int64_t bsa, const int32_t* dims, int32_t batch,
@@ -618,7 +708,7 @@ extern "C" int kr_syev_select(const double* A, int64_t lda, int64_t bsa, const i
                               int64_t ldz, int64_t bsz, int32_t* nsel, double* work, int64_t work_len,
                               kr_stream_t stream) {
   KR_CHECK_ARG(batch >= 0 && tmax >= 0 && s >= 0, "negative size");
-  KR_CHECK_ARG(tmax <= EIG_TPACK, "kr_syev_select: t exceeds the shared-memory limit (228); use a library eigensolver");
+  KR_CHECK_ARG(tmax <= EIG_TGLOB, "kr_syev_select: t exceeds KR_TMAX (640)");
   KR_CHECK_ARG(s <= EIG_MAXSEL, "kr_syev_select: more than 128 selected pairs");
   KR_CHECK_ARG(size_code >= 0 && size_code <= 2, "size code must be 0 (S), 1 (L) or 2 (M)");
   KR_CHECK_ARG(lda >= tmax && ldz >= tmax, "leading dimension smaller than t");
@@ -627,7 +717,12 @@ extern "C" int kr_syev_select(const double* A, int64_t lda, int64_t bsa, const i
   KR_CHECK_ARG(A && dims && Z && work, "null pointer");
   EigParams P{A, lda, bsa, dims, tmax, size_code, s, 0, lam, bsl, Z, ldz, bsz, nsel, work};
   const size_t smem = (size_t)eig_smem_doubles(tmax, &P.nw) * sizeof(double);
-  KR_TRY(ensure_smem((const void*)eig_select_kernel, smem));
-  eig_select_kernel<<<batch, ENT, smem, (cudaStream_t)stream>>>(P);
+  if (tmax <= EIG_TPACK) {
+    KR_TRY(ensure_smem((const void*)eig_select_kernel<(EIG_TPACK + 31) / 32, false>, smem));
+    eig_select_kernel<(EIG_TPACK + 31) / 32, false><<<batch, ENT, smem, (cudaStream_t)stream>>>(P);
+  } else {
+    KR_TRY(ensure_smem((const void*)eig_select_kernel<(EIG_TGLOB + 31) / 32, true>, smem));
+    eig_select_kernel<(EIG_TGLOB + 31) / 32, true><<<batch, ENT, smem, (cudaStream_t)stream>>>(P);
+  }
   return check_launch("eig_select_kernel");
 }

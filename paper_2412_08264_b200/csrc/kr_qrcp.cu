@@ -258,14 +258,13 @@ namespace kr {
 namespace {
 
 namespace cgc = cooperative_groups;
-#ifndef KR_QRCP_CLUSTER
-#define KR_QRCP_CLUSTER 8
-#endif
-constexpr int QNC = KR_QRCP_CLUSTER;      // CTAs per matrix (8, the portable maximum; 16 measured slower: 1.18 vs 1.02 ms at B=4, t=220)
 constexpr int QCN = 256;                  // threads per CTA
 constexpr int QCW = QCN / 32;
-constexpr int QCOLS = (256 + QNC - 1) / QNC;  // resident columns per CTA (t <= 256)
 
+// Variants by the largest t: cluster size QNC (8 portable, 16 non-portable), rows per
+// lane QRR (registers of a column chunk), columns per warp per round QCC.  Resident
+// columns per CTA: ceil(t / QNC) (<= 40 x 640 doubles = 200 KB at t = 640).
+//   t <= 256: <8, 8, 4>   t <= 448: <8, 14, 2>   t <= 640: <16, 20, 2>
 struct QcCand {
   double v;  // best remaining norm^2 of a CTA
   int g;     // its global column (-1: none)
@@ -274,18 +273,23 @@ struct QcCand {
 
 // Exchange through DSMEM is push-based: a producer stores into every CTA's copy
 // before the cluster barrier (release / acquire), so reads after it are local.
-__global__ void __cluster_dims__(QNC, 1, 1) __launch_bounds__(QCN, 1) qrcp_cluster_kernel(QrcpParams P) {
+template <int QNC, int QRR, int QCC, int TMX>
+__global__ void __launch_bounds__(QCN, 1) qrcp_cluster_kernel(QrcpParams P) {
+  constexpr int QR = QRR;
+  constexpr int QC = QCC;
+  constexpr int QCOLS = (TMX + QNC - 1) / QNC;
   extern __shared__ double csm[];
   cgc::cluster_group cluster = cgc::this_cluster();
   const int cr = (int)cluster.block_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = blockIdx.x / QNC, t = P.dims[b], T = P.T;
-  double* cols = csm;                       // [QCOLS][T] resident columns
-  double* vl = cols + (int64_t)QCOLS * T;   // [T] Householder vector of the current step (pushed by its owner)
+  const int qcols = (T + QNC - 1) / QNC;    // resident column slots (runtime T)
+  double* cols = csm;                       // [qcols][T] resident columns
+  double* vl = cols + (int64_t)qcols * T;   // [T] Householder vector of the current step (pushed by its owner)
   __shared__ double cn[QCOLS];              // trailing norms^2 of the resident columns
   __shared__ int done[QCOLS];               // already pivoted
-  __shared__ int pos[256];                  // current position of every global column (replicated)
-  __shared__ int at[256];                   // global column at every position (replicated)
+  __shared__ int pos[TMX];                  // current position of every global column (replicated)
+  __shared__ int at[TMX];                   // global column at every position (replicated)
   __shared__ QcCand cand[QNC];              // every CTA's candidate of the step (pushed)
   __shared__ double bt[2];                  // beta, tau of the step (pushed by the owner)
   double* M = P.M + (int64_t)b * T * T;
@@ -538,7 +542,7 @@ __global__ void __cluster_dims__(QNC, 1, 1) __launch_bounds__(QCN, 1) qrcp_clust
   const int r = rank;
   double* Qb = P.Q + (int64_t)b * T * T;
   const int qloc = (r - cr + QNC - 1) / QNC;  // Q columns j = cr + QNC * l, l < qloc
-  for (int l = warp; l < QCOLS; l += QCW)
+  for (int l = warp; l < qcols; l += QCW)
     for (int i = lane; i < T; i += 32) cols[(int64_t)l * T + i] = (l < qloc && i == cr + QNC * l) ? 1.0 : 0.0;
   __syncthreads();
   // reflectors r-1 .. 0 applied backwards; the next one streams into the other
@@ -617,24 +621,51 @@ __global__ void __cluster_dims__(QNC, 1, 1) __launch_bounds__(QCN, 1) qrcp_clust
 }  // namespace
 }  // namespace kr
 
+namespace kr {
+namespace {
+template <int QNC, int QRR, int QCC, int TMX>
+int launch_qrcp_cluster(const QrcpParams& P, int batch, cudaStream_t st) {
+  const auto kern = qrcp_cluster_kernel<QNC, QRR, QCC, TMX>;
+  const int T = P.T;
+  const size_t smem = ((size_t)((T + QNC - 1) / QNC) * T + 3 * (size_t)T) * sizeof(double);
+  KR_TRY(ensure_smem((const void*)kern, smem));
+  if (QNC > 8) {
+    static bool np = false;  // per instantiation
+    if (!np) {
+      if (cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+        return fail(KR_ECUDA, "qrcp: non-portable cluster size");
+      np = true;
+    }
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(batch * QNC);
+  cfg.blockDim = dim3(QCN);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = QNC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, P);
+  return check_launch("qrcp_cluster_kernel");
+}
+}  // namespace
+}  // namespace kr
+
 extern "C" int kr_qrcp_small_cluster(double* M, const int32_t* dims, int32_t batch, int32_t tmax, double rtol,
                                      double* Q, int32_t* rank, int32_t* perm, double* work, int64_t work_len,
                                      kr_stream_t stream) {
   using namespace kr;
-  KR_CHECK_ARG(batch >= 0 && tmax >= 0 && tmax <= 256, "kr_qrcp_small: t must be in [0, 256]");
+  KR_CHECK_ARG(batch >= 0 && tmax >= 0 && tmax <= KR_TMAX, "kr_qrcp_small_cluster: t must be in [0, KR_TMAX]");
   KR_CHECK_ARG(work_len >= (int64_t)batch * tmax, "workspace too small");
   if (batch == 0) return KR_OK;
   KR_CHECK_ARG(M && dims && Q && rank && work, "null pointer");
   QrcpParams P{M, dims, tmax, rtol, Q, rank, perm, work};
-  const size_t smem = ((size_t)QCOLS * tmax + 3 * (size_t)tmax) * sizeof(double);
-  KR_TRY(ensure_smem((const void*)qrcp_cluster_kernel, smem));
-  if (QNC > 8) {
-    static bool np = false;
-    if (!np) {
-      cudaFuncSetAttribute((const void*)qrcp_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      np = true;
-    }
-  }
-  qrcp_cluster_kernel<<<batch * QNC, QCN, smem, (cudaStream_t)stream>>>(P);
-  return check_launch("qrcp_cluster_kernel");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (tmax <= 256) return launch_qrcp_cluster<8, 8, 4, 256>(P, batch, st);
+  if (tmax <= 448) return launch_qrcp_cluster<8, 14, 2, 448>(P, batch, st);
+  return launch_qrcp_cluster<16, 20, 2, KR_TMAX>(P, batch, st);
 }

@@ -45,9 +45,10 @@ extern "C" {
 int64_t kr_gram_workspace(int32_t batch, int32_t rows, int64_t n);
 int kr_gram(const double* A, const double* B, int64_t ld, int64_t bs, int32_t batch, int32_t rows, int64_t n,
             double* G, int64_t ldg, int64_t bsg, double* work, int64_t work_len, kr_stream_t stream);
+int64_t kr_chol_inv_workspace(int32_t batch, int32_t tmax);
 int kr_chol_inv(const double* G, int64_t ldg, int64_t bsg, const int32_t* dims, int32_t batch, int32_t tmax,
                 int32_t flags, const double* shift, double* F, int64_t ldf, int64_t bsf, double* stats,
-                int32_t* info, uint8_t* skipped, kr_stream_t stream);
+                int32_t* info, uint8_t* skipped, double* work, int64_t work_len, kr_stream_t stream);
 int64_t kr_syev_select_workspace(int32_t batch, int32_t tmax);
 int kr_syev_select(const double* A, int64_t lda, int64_t bsa, const int32_t* dims, int32_t batch, int32_t tmax,
                    int32_t size_code, int32_t s, double* lam, int64_t bsl, double* Z, int64_t ldz, int64_t bsz,
@@ -64,7 +65,7 @@ constexpr double RANK_TOL = 1e-10;    // recycling.RANK_TOL (recycling.py:194)
 constexpr double PIVOT_COND = 1e9;    // below: pivoted QR keeps every column
 constexpr double SHIFT_COND_MAX = 1e14;
 constexpr double COND_LIMIT = 1e12;   // recycling.py:291
-constexpr int RC_TMAX = 228;
+constexpr int RC_TMAX = KR_TMAX;
 
 // ---------------------------------------------------------------- small kernels
 
@@ -178,17 +179,24 @@ __global__ void copy_r_kernel(const double* A, int64_t n, int t, double* M, int 
 
 // ---------------------------------------------------------------- host helpers
 
+// Thrown by Ctx::take when the caller's workspace is exhausted: the piece is never
+// handed out, so nothing is queued on memory past the buffer; kr_recycle_update
+// catches it at the C boundary and returns KR_ENOMEM.
+struct WorkspaceOverrun {
+  int64_t used, cap, want;
+};
+
 struct Ctx {
   cudaStream_t st;
   cublasHandle_t h;
   double* cur;
   double* end;
   double* base = cur;
-  bool overrun = false;
   double* take(int64_t cnt) {
+    const int64_t c = (cnt + 31) & ~int64_t(31);  // 256-byte aligned pieces
+    if (cnt < 0 || cur + c > end) throw WorkspaceOverrun{cur - base, end - base, cnt};
     double* r = cur;
-    cur += (cnt + 31) & ~int64_t(31);  // 256-byte aligned pieces
-    if (cur > end) overrun = true;
+    cur += c;
     return r;
   }
 };
@@ -276,11 +284,21 @@ struct Fetch {
 };
 
 // Small host -> device uploads through a per-thread pinned ring (no stream sync: each
-// upload has its own slot for the duration of one kr_recycle_update call, whose final
-// reads synchronise the stream before the next call resets the ring).
+// upload has its own slot for the duration of one kr_recycle_update call).  An event
+// recorded after every upload lets the next call wait for the last one before it
+// resets the ring (a call that returned early on an error may leave copies in flight).
 struct UpRing {
   char* buf = nullptr;
   size_t cap = 0, off = 0;
+  cudaEvent_t done = nullptr;
+  bool pending = false;
+  int reset() {
+    if (pending && done && cudaEventSynchronize(done) != cudaSuccess)
+      return fail(KR_ECUDA, "kr_recycle: upload ring wait");
+    pending = false;
+    off = 0;
+    return KR_OK;
+  }
 };
 UpRing& up_ring() {
   static thread_local UpRing r;
@@ -300,7 +318,11 @@ int h2d(Ctx& c, T* dev, const T* host, size_t cnt) {
   }
   memcpy(r.buf + off, host, bytes);
   r.off = off + bytes;
-  const cudaError_t e = cudaMemcpyAsync(dev, r.buf + off, bytes, cudaMemcpyHostToDevice, c.st);
+  if (!r.done && cudaEventCreateWithFlags(&r.done, cudaEventDisableTiming) != cudaSuccess)
+    return fail(KR_ECUDA, "kr_recycle h2d event");
+  cudaError_t e = cudaMemcpyAsync(dev, r.buf + off, bytes, cudaMemcpyHostToDevice, c.st);
+  if (e == cudaSuccess) e = cudaEventRecord(r.done, c.st);
+  r.pending = true;
   return e == cudaSuccess ? KR_OK : fail(KR_ECUDA, std::string("kr_recycle h2d: ") + cudaGetErrorString(e));
 }
 
@@ -412,9 +434,11 @@ struct Factor {  // one Cholesky-QR factor of a batch: F (B,T,T), info, stats
 
 int chol(Ctx& c, const double* G, const int32_t* dims, int B, int T, bool scale, const double* shift, Factor& f,
          bool partial = false) {
+  const int64_t wl = kr_chol_inv_workspace(B, T);
+  double* ws = wl > 0 ? c.take(wl) : nullptr;  // packed factors of t > 228 (L2-resident)
   return hi_stream().run(c.st, [&](cudaStream_t st) {
     return kr_chol_inv(G, T, (int64_t)T * T, dims, B, T, (scale ? 1 : 0) | 2 | (partial ? 8 : 0), shift, f.F, T,
-                       (int64_t)T * T, f.stats, f.info, nullptr, st);
+                       (int64_t)T * T, f.stats, f.info, nullptr, ws, wl, st);
   });
 }
 
@@ -576,6 +600,8 @@ int64_t workspace_doubles(const kr_op& op, const kr_recycle_args& a) {
   w += house_lwork(n, (int)T) + 64;                     // Householder branch (cuSOLVER work)
   w += T * n + 16 * (T * T + 64);                       // block-Householder branch: remainder rows, factors
   w += 8 * T * T + 4 * T + 65536;                       // pivoted path (tau), slack
+  w += 12 * (kr_chol_inv_workspace((int32_t)B, (int32_t)T) + 64);  // packed factors of t > 228 (per Cholesky)
+  w += 24 * (kr_chol_inv_workspace(1, (int32_t)T) + 64);          // block-Householder branch's factors
   return w;
 }
 
@@ -584,12 +610,6 @@ int64_t workspace_doubles(const kr_op& op, const kr_recycle_args& a) {
 
 using namespace kr;
 
-int overrun(const Ctx& c, int line) {
-  char msg[160];
-  snprintf(msg, sizeof msg, "kr_recycle_update: workspace estimate exceeded at line %d (%lld of %lld doubles)", line,
-           (long long)(c.cur - c.base), (long long)(c.end - c.base));
-  return fail(KR_ENOMEM, msg);
-}
 
 extern "C" int kr_thread_warmup(void) {
   cublasHandle_t h;
@@ -624,22 +644,36 @@ extern "C" int64_t kr_recycle_workspace(const kr_op* op, const kr_recycle_args* 
   return workspace_doubles(*op, *a);
 }
 
+static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double* work, int64_t work_len,
+                               kr_stream_t stream);
+
 extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, double* work, int64_t work_len,
                                  kr_stream_t stream) {
+  try {
+    return recycle_update_impl(op, a, work, work_len, stream);
+  } catch (const WorkspaceOverrun& e) {
+    char msg[200];
+    snprintf(msg, sizeof msg, "kr_recycle_update: workspace exhausted (%lld of %lld doubles used, %lld more asked)",
+             (long long)e.used, (long long)e.cap, (long long)e.want);
+    return fail(KR_ENOMEM, msg);
+  }
+}
+
+static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double* work, int64_t work_len,
+                               kr_stream_t stream) {
   KR_CHECK_ARG(op && a, "null argument");
   KR_TRY(validate_op(*op));
   const int B = a->batch, T = a->T, s = a->s;
   const int64_t n = op_n(*op);
   KR_CHECK_ARG(op->batch == B, "operator batch must equal args.batch");
-  KR_CHECK_ARG(T >= 1 && T <= RC_TMAX && s >= 1 && s <= T, "need 1 <= s <= T <= 228");
+  KR_CHECK_ARG(T >= 1 && T <= RC_TMAX && s >= 1 && s <= T, "need 1 <= s <= T <= KR_TMAX");
   KR_CHECK_ARG(a->vec_type == 0 || (a->vec_type == 1 && a->size_code == 1), "vec_type: Ritz, or RGen with size L");
   KR_CHECK_ARG(a->vec_type == 0 || op->reg_kind != KR_REG_NONE, "RGen needs a mixed Jacobian");
   KR_CHECK_ARG(work && work_len >= workspace_doubles(*op, *a), "kr_recycle workspace too small");
   const int p = op->reg_kind == KR_REG_TV ? 1 : op->num_filters * (1 + op->ksize * op->ksize);
   const int P = p + T;
   Ctx c{(cudaStream_t)stream, nullptr, work, work + work_len};
-  // the previous call ended with a synchronising read, so its uploads are done
-  up_ring().off = 0;
+  KR_TRY(up_ring().reset());
   static const bool debug = getenv("KR_RECYCLE_DEBUG") != nullptr;
   const auto t_start = std::chrono::steady_clock::now();
   int n_ill = 0, n_house = 0, n_exact = 0, n_block = 0;
@@ -868,7 +902,6 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
     KR_TRY(h2d(c, d_td, ht.data(), B));
   }
 
-  if (c.overrun) return overrun(c, __LINE__);
   // ---- 3. H W and the projected Hessian
   double* HW = a->HW;
   static const bool lowpri = getenv("KR_HVP_LOWPRI") == nullptr || getenv("KR_HVP_LOWPRI")[0] != '0';
@@ -905,8 +938,10 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
     double* hn = c.take(2 * B);
     SideStream& ss = side_stream();
     KR_TRY(ss.fork(c.st));
+    const int64_t hwl_c = kr_chol_inv_workspace(B, T);
+    double* hws_c = hwl_c > 0 ? c.take(hwl_c) : nullptr;
     KR_TRY(kr_chol_inv(Ht, T, (int64_t)T * T, d_td, B, T, 2, nullptr, fh.F, T, (int64_t)T * T, fh.stats, fh.info,
-                       nullptr, ss.st));
+                       nullptr, hws_c, hwl_c, ss.st));
     frob2_kernel<<<B, FROB_NT, 0, ss.st>>>(Ht, T, T, T, (int64_t)T * T, hn);
     frob2_kernel<<<B, FROB_NT, 0, ss.st>>>(fh.F, T, T, T, (int64_t)T * T, hn + B);
     KR_TRY(ss.join(c.st));  // joined before the host reads hn / fh (below, after the eigen launch)
@@ -951,6 +986,7 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
       for (int b : exact) {
         const double lo = ex[2 * b], hi = ex[2 * b + 1], smax = std::max(fabs(lo), fabs(hi));
         if (!(lo > 0.0 && lo >= smax / COND_LIMIT)) status[b] = 1;  // singular: the per-sample path raises
+        if (debug && status[b]) fprintf(stderr, "  sample %d declined: W^T H W singular (lo %.3e hi %.3e)\n", b, lo, hi);
       }
     }
     // alpha, beta, mu, V_H from Y = Z Q^T rows; X = R^-1 z
@@ -970,10 +1006,14 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
     std::vector<double> qs1;
     KR_TRY(Fetch().add(qi1, qs.f1.info, B).add(qs1, qs.f1.stats, 4 * B).add(qi2, qs.f2.info, B).run(c));
     for (int b = 0; b < B; ++b)
-      if (t[b] > 0 && !(cholqr_ok(qi1, qs1, b) && qi2[b] < 0)) status[b] = 1;
+      if (t[b] > 0 && !(cholqr_ok(qi1, qs1, b) && qi2[b] < 0)) {
+        status[b] = 1;
+        if (debug)
+          fprintf(stderr, "  sample %d declined: GSVD CholQR2 (info %d/%d, pivots %.3e..%.3e)\n", b, qi1[b], qi2[b],
+                  qs1[4 * b], qs1[4 * b + 1]);
+      }
   }
 
-  if (c.overrun) return overrun(c, __LINE__);
   // ---- 5. U~ = W coeffs, H U~, C R = H U~, U = U~ R^-1
   double* cand = c.take((int64_t)B * s * n);
   double* HU = c.take((int64_t)B * s * n);
@@ -1017,9 +1057,11 @@ extern "C" int kr_recycle_update(const kr_op* op, const kr_recycle_args* a, doub
     }
     if (!(cholqr_ok(ui1, us1, b) && ui2[b] < 0)) status[b] = 1;
     if (a->vec_type == 1 && bd[b]) status[b] = 1;
+    if (debug && status[b])
+      fprintf(stderr, "  sample %d declined: prepare CholQR2 (info %d/%d, pivots %.3e..%.3e) beta0 %d\n", b, ui1[b],
+              ui2[b], us1[4 * b], us1[4 * b + 1], a->vec_type == 1 ? bd[b] : 0);
     a->status[b] = status[b];
   }
-  if (c.overrun) return overrun(c, __LINE__);
   if (debug)
     fprintf(stderr, "kr_recycle_update: B=%d T=%d shifted=%d ill=%d householder=%d (block %d) exact=%d host %.2f ms (householder %.2f)\n",
             B, T, (int)was_shifted, n_ill, n_house, n_block, n_exact,

@@ -3,7 +3,9 @@
 // batched path, and the _hessian_condition screen, recycling.py:290-296).
 //
 // One CTA per matrix, the t x t lower triangle packed in shared memory
-// (t <= CHOL_TMAX): scale by D = sqrt(diag G) (optional), add a diagonal shift
+// (t <= CHOL_TMAX), or for larger t (<= CHOL_TMAX_G, the candidate widths of
+// C3-C5) in a caller-provided global workspace that stays L2-resident -- the same
+// code and arithmetic order either way, so both give bitwise the same factor: scale by D = sqrt(diag G) (optional), add a diagonal shift
 // (optional, shifted CholeskyQR), factor G = L L^T (blocked right-looking),
 // report the first failing row and the extreme pivots, and overwrite L by
 // L^{-1} (blocked forward substitution, one thread per column).  Output F = L^{-1} D^{-1}, a full
@@ -18,7 +20,9 @@ namespace {
 
 constexpr int CNT = 512;
 constexpr int CHOL_TMAX = 228;
+constexpr int CHOL_TMAX_G = KR_TMAX;
 constexpr int NB = 16;
+constexpr int NCH_G = (CHOL_TMAX_G + CNT / 2 - 1) / (CNT / 2);  // column chunks of the inverse at t <= 640
 
 struct CholParams {
   const double* G;
@@ -31,6 +35,7 @@ struct CholParams {
   double* stats;  // per sample: [min L_jj, max L_jj, min D, 0]
   int32_t* info;  // per sample: -1 = factored, else the first failing row
   uint8_t* skipped;  // per sample and row (skip mode): 1 = dependent row removed
+  double* gwork;     // nullable: per sample T(T+1)/2 doubles holding the packed factor (t > CHOL_TMAX)
 };
 
 __device__ __forceinline__ int64_t pk(int i, int j) { return (int64_t)i * (i + 1) / 2 + j; }
@@ -48,6 +53,7 @@ __device__ __forceinline__ double rsqrt_nr(double d) {
   return y;
 }
 
+template <int NCH>  // column chunks of CNT/2 in the inverse (1 for t <= 256)
 __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
   extern __shared__ double sm[];
   const int tid = threadIdx.x;
@@ -58,9 +64,10 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
   double* col = D + T;            // T (cached column)
   double* rdiag = col + T;        // NB reciprocal pivots of the current block
   double* Lbb = rdiag + NB;       // NB x (NB + 1) copy of a diagonal block
-  double* A = Lbb + NB * (NB + 1);  // packed lower t(t+1)/2
+  // packed lower t(t+1)/2: shared memory, or the sample's slice of the global workspace
+  double* A = P.gwork ? P.gwork + (int64_t)blockIdx.x * ((int64_t)P.T * (P.T + 1) / 2) : Lbb + NB * (NB + 1);
   __shared__ int s_fail;
-  __shared__ unsigned char skp[CHOL_TMAX];
+  __shared__ unsigned char skp[CHOL_TMAX_G];
 #ifdef KR_CHOL_TIMING
   long long csec[7] = {0, 0, 0, 0, 0, 0, 0}, clast = clock64();
 #endif
@@ -71,7 +78,7 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
     D[i] = (scale && g > 0.0) ? sqrt(g) : 1.0;
   }
   if (tid == 0) s_fail = -1;
-  for (int i = tid; i < CHOL_TMAX; i += CNT) skp[i] = 0;
+  for (int i = tid; i < CHOL_TMAX_G; i += CNT) skp[i] = 0;
   __syncthreads();
   const double sh = P.shift ? P.shift[b] : 0.0;
   // lower triangle (as potrf 'L'), rows coalesced, independent loads in flight
@@ -269,62 +276,78 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
       Lbb[r * (NB + 1) + m] = m <= r ? A[pk(ib + r, ib + m)] : 0.0;
       if (m == r) rdiag[r] = 1.0 / A[pk(ib + r, ib + r)];
     }
-    const int h = tid / (CNT / 2), c = tid - h * (CNT / 2);
+    // columns in chunks of CNT/2 (t > 256 needs up to NCH of them): the accumulators of every
+    // chunk are formed before any X_I write (they read L_I,<I, which X_I overwrites)
+    const int h = tid / (CNT / 2), c0 = tid - h * (CNT / 2);
     const int r0 = 8 * h;
-    double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    // the warp's lanes hold consecutive columns; they all start k at the warp's first
-    // column, so the L operands are warp-uniform (broadcast smem loads), and a lane adds
-    // fma(l, 0, acc) == acc for its rows k < c (bitwise the per-column loop from k = c)
-    const int cw = (c & ~31) < w ? (c & ~31) : w;  // warp's first column (clamped)
-    if (cw < w && r0 < nb) {
-      const bool act = c < w;
-      const double* lp[8];  // rows ib + r0 + u of L (clamped into the matrix)
+    double acc[NCH][8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) lp[u] = A + pk(min(ib + r0 + u, tf - 1), 0);
-      int k = cw;
-      for (; k + 3 < ib; k += 4) {
-        double xv[4];
+    for (int ch = 0; ch < NCH; ++ch) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) xv[j] = (act && k + j >= c) ? A[pk(k + j, c)] : 0.0;  // X_(k+j),c
+      for (int u = 0; u < 8; ++u) acc[ch][u] = 0.0;
+      const int c = c0 + ch * (CNT / 2);
+      // the warp's lanes hold consecutive columns; they all start k at the warp's first
+      // column, so the L operands are warp-uniform (broadcast smem loads), and a lane adds
+      // fma(l, 0, acc) == acc for its rows k < c (bitwise the per-column loop from k = c)
+      const int cw = (c & ~31) < w ? (c & ~31) : w;  // warp's first column (clamped)
+      if (cw < w && r0 < nb) {
+        const bool act = c < w;
+        const double* lp[8];  // rows ib + r0 + u of L (clamped into the matrix)
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const double* l = lp[u] + k;
+        for (int u = 0; u < 8; ++u) lp[u] = A + pk(min(ib + r0 + u, tf - 1), 0);
+        int k = cw;
+        for (; k + 3 < ib; k += 4) {
+          double xv[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[u] = fma(l[j], xv[j], acc[u]);
+          for (int j = 0; j < 4; ++j) xv[j] = (act && k + j >= c) ? A[pk(k + j, c)] : 0.0;  // X_(k+j),c
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const double* l = lp[u] + k;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[ch][u] = fma(l[j], xv[j], acc[ch][u]);
+          }
         }
-      }
-      for (; k < ib; ++k) {
-        const double xk = (act && k >= c) ? A[pk(k, c)] : 0.0;
+        for (; k < ib; ++k) {
+          const double xk = (act && k >= c) ? A[pk(k, c)] : 0.0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) acc[u] = fma(lp[u][k], xk, acc[u]);
+          for (int u = 0; u < 8; ++u) acc[ch][u] = fma(lp[u][k], xk, acc[ch][u]);
+        }
       }
     }
     __syncthreads();  // every read of L_I,<I done before X_I overwrites it
     double x[NB];
-    if (h == 0 && c < w) {
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        if (r < nb) {
-          double s = (c == ib + r ? 1.0 : 0.0) - acc[r];
+    for (int ch = 0; ch < NCH; ++ch) {
+      const int c = c0 + ch * (CNT / 2);
+      if (h == 0 && c < w) {
 #pragma unroll
-          for (int m = 0; m < r; ++m) s -= Lbb[r * (NB + 1) + m] * x[m];
-          x[r] = (c <= ib + r) ? s * rdiag[r] : 0.0;
-          if (c <= ib + r) A[pk(ib + r, c)] = x[r];
+        for (int r = 0; r < 8; ++r) {
+          if (r < nb) {
+            double s = (c == ib + r ? 1.0 : 0.0) - acc[ch][r];
+#pragma unroll
+            for (int m = 0; m < r; ++m) s -= Lbb[r * (NB + 1) + m] * x[m];
+            x[r] = (c <= ib + r) ? s * rdiag[r] : 0.0;
+            if (c <= ib + r) A[pk(ib + r, c)] = x[r];
+          }
         }
       }
     }
     __syncthreads();
-    if (h == 1 && c < w && nb > 8) {
 #pragma unroll
-      for (int m = 0; m < 8; ++m) x[m] = (c <= ib + m) ? A[pk(ib + m, c)] : 0.0;
+    for (int ch = 0; ch < NCH; ++ch) {
+      const int c = c0 + ch * (CNT / 2);
+      if (h == 1 && c < w && nb > 8) {
 #pragma unroll
-      for (int r = 8; r < NB; ++r) {
-        if (r < nb) {
-          double s = (c == ib + r ? 1.0 : 0.0) - acc[r - 8];
+        for (int m = 0; m < 8; ++m) x[m] = (c <= ib + m) ? A[pk(ib + m, c)] : 0.0;
 #pragma unroll
-          for (int m = 0; m < r; ++m) s -= Lbb[r * (NB + 1) + m] * x[m];
-          x[r] = (c <= ib + r) ? s * rdiag[r] : 0.0;
-          if (c <= ib + r) A[pk(ib + r, c)] = x[r];
+        for (int r = 8; r < NB; ++r) {
+          if (r < nb) {
+            double s = (c == ib + r ? 1.0 : 0.0) - acc[ch][r - 8];
+#pragma unroll
+            for (int m = 0; m < r; ++m) s -= Lbb[r * (NB + 1) + m] * x[m];
+            x[r] = (c <= ib + r) ? s * rdiag[r] : 0.0;
+            if (c <= ib + r) A[pk(ib + r, c)] = x[r];
+          }
         }
       }
     }
@@ -362,19 +385,36 @@ __global__ void __launch_bounds__(CNT, 1) chol_inv_kernel(CholParams P) {
 
 using namespace kr;
 
+extern "C" int64_t kr_chol_inv_workspace(int32_t batch, int32_t tmax) {
+  if (batch < 0 || tmax < 0) return -1;
+  return tmax <= CHOL_TMAX ? 0 : (int64_t)batch * ((int64_t)tmax * (tmax + 1) / 2);
+}
+
 extern "C" int kr_chol_inv(const double* G, int64_t ldg, int64_t bsg, const int32_t* dims, int32_t batch,
                            int32_t tmax, int32_t flags, const double* shift, double* F, int64_t ldf, int64_t bsf,
-                           double* stats, int32_t* info, uint8_t* skipped, kr_stream_t stream) {
+                           double* stats, int32_t* info, uint8_t* skipped, double* work, int64_t work_len,
+                           kr_stream_t stream) {
   KR_CHECK_ARG(batch >= 0 && tmax >= 0, "negative size");
-  KR_CHECK_ARG(tmax <= CHOL_TMAX, "kr_chol_inv: t exceeds the shared-memory limit (228)");
+  KR_CHECK_ARG(tmax <= CHOL_TMAX_G, "kr_chol_inv: t exceeds 640");
+  KR_CHECK_ARG(work_len >= kr_chol_inv_workspace(batch, tmax) && (tmax <= CHOL_TMAX || work),
+               "kr_chol_inv: workspace too small (kr_chol_inv_workspace)");
+  KR_CHECK_ARG(!(flags & 16) || (work && work_len >= (int64_t)batch * ((int64_t)tmax * (tmax + 1) / 2)),
+               "kr_chol_inv: flag 16 needs a batch * t(t+1)/2 workspace");
   KR_CHECK_ARG(ldg >= tmax, "leading dimension smaller than t");
   KR_CHECK_ARG(!(flags & 2) || (F && ldf >= tmax), "inverse requested without an output");
   if (batch == 0) return KR_OK;
   KR_CHECK_ARG(G && dims && info, "null pointer");
-  CholParams P{G, ldg, bsg, dims, tmax, flags, shift, F, ldf, bsf, stats, info, skipped};
-  const size_t smem = (size_t)(2 * tmax + NB + NB * (NB + 1) + (int64_t)tmax * (tmax + 1) / 2) * sizeof(double);
-  KR_TRY(ensure_smem((const void*)chol_inv_kernel, smem));
-  chol_inv_kernel<<<batch, CNT, smem, (cudaStream_t)stream>>>(P);
+  const bool glob = tmax > CHOL_TMAX || (flags & 16);  // bit 4: the workspace variant at any size (tests)
+  CholParams P{G, ldg, bsg, dims, tmax, flags, shift, F, ldf, bsf, stats, info, skipped, glob ? work : nullptr};
+  const size_t smem =
+      (size_t)(2 * tmax + NB + NB * (NB + 1) + (glob ? 0 : (int64_t)tmax * (tmax + 1) / 2)) * sizeof(double);
+  if (tmax <= CNT / 2) {
+    KR_TRY(ensure_smem((const void*)chol_inv_kernel<1>, smem));
+    chol_inv_kernel<1><<<batch, CNT, smem, (cudaStream_t)stream>>>(P);
+  } else {
+    KR_TRY(ensure_smem((const void*)chol_inv_kernel<NCH_G>, smem));
+    chol_inv_kernel<NCH_G><<<batch, CNT, smem, (cudaStream_t)stream>>>(P);
+  }
   return check_launch("chol_inv_kernel");
 }
 

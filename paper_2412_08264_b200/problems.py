@@ -110,10 +110,14 @@ def make_batch(cfg: DeblurConfig, first: int = 0, count: int | None = None, devi
                  potential="smooth_abs", eps=cfg.eps, num_filters=cfg.num_filters, ksize=cfg.kernel_size)
 
 
-def synthetic_sequence(cfg: DeblurConfig, x_trues: np.ndarray, steps: int, seed: int = 1234):
+def synthetic_sequence(cfg: DeblurConfig, x_trues: np.ndarray, steps: int, seed: int = 1234, first: int = 0):
     """Frozen systems i = 0..steps-1: theta_i = theta_0 + i * dtheta and
     xhat_i = x_true + smooth_i, with smooth_i a blurred 3%-level field that drifts
-    slowly with i (consecutive-system relative changes O(1e-2))."""
+    slowly with i (consecutive-system relative changes O(1e-2)).
+
+    The fields of sample k (global index first + b) come from their own generator
+    default_rng([seed, kind, k]), so a rank that owns samples [first, first + B)
+    sees exactly the systems the single-process batch holds for them."""
     rng = np.random.default_rng(seed)
     th0 = theta0(cfg)
     dth = 0.002 * rng.standard_normal(th0.size)
@@ -122,12 +126,13 @@ def synthetic_sequence(cfg: DeblurConfig, x_trues: np.ndarray, steps: int, seed:
     taps = gaussian_taps(9, 2.0)
     k2 = np.outer(taps, taps)
 
-    def field():
-        f = rng.standard_normal((B, size, size))
-        return np.stack([convolve2d(f[b], k2, mode="same", boundary="fill") for b in range(B)]).reshape(B, n)
+    def field(kind, b):
+        f = np.random.default_rng([seed, kind, first + b]).standard_normal((size, size))
+        return convolve2d(f, k2, mode="same", boundary="fill").ravel()
 
-    base, drift = field(), field()
-    scale = 0.03 / max(np.abs(base).max(), 1e-12)
+    base = np.stack([field(0, b) for b in range(B)])
+    drift = np.stack([field(1, b) for b in range(B)])
+    scale = 0.03 / np.maximum(np.abs(base).max(axis=1, keepdims=True), 1e-12)
     thetas, xhats = [], []
     for i in range(steps):
         thetas.append(th0 + i * dth)

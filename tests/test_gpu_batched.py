@@ -206,7 +206,7 @@ def test_recycle_update_rank_drop(impl):
     assert torch.allclose(got[0].nsc_data.values, ref.nsc_data.values, rtol=1e-8)
 
 
-@pytest.mark.parametrize("T", [1, 7, 64, 228])
+@pytest.mark.parametrize("T", [1, 7, 64, 228, 229, 330, 580])
 def test_chol_inv_kernel_matches_torch(T, monkeypatch):
     """kr_chol_inv (one CTA per matrix) against the torch.linalg formulation."""
     from paper_2412_08264_b200 import batched
@@ -226,15 +226,15 @@ def test_chol_inv_kernel_matches_torch(T, monkeypatch):
             F, info, st = batched._chol_inv(G, dims, scale, sh)
             monkeypatch.setattr(batched, "CHOL_TMAX", -1)
             Ft, infot, stt = batched._chol_inv(G, dims, scale, sh)
-            monkeypatch.setattr(batched, "CHOL_TMAX", 228)
+            monkeypatch.setattr(batched, "CHOL_TMAX", 640)
             assert info.tolist() == infot.tolist()
             good = info < 0
             assert torch.allclose(st[good, :3], stt[good, :3], rtol=1e-12, atol=0)
             assert torch.allclose(F[good], Ft[good], rtol=1e-9, atol=1e-12 * float(Ft[good].abs().max()))
 
 
-@pytest.mark.parametrize("cluster", [True, False])
-def test_qrcp_small_matches_scipy_pivoted_qr(cluster, monkeypatch):
+@pytest.mark.parametrize("cluster,wide", [(True, ()), (False, ()), (True, (330,)), (True, (330, 580))])
+def test_qrcp_small_matches_scipy_pivoted_qr(cluster, wide, monkeypatch):
     """kr_qrcp_small on R against scipy.linalg.qr(A, pivoting=True), the reference's
     candidate-basis QR (recycling.py:187-199): same pivots, |R_kk|, rank under the
     1e-10 rule, and the same kept span."""
@@ -246,8 +246,8 @@ def test_qrcp_small_matches_scipy_pivoted_qr(cluster, monkeypatch):
     monkeypatch.setattr(batched, "QRCP_CLUSTER", cluster)
     rng = np.random.default_rng(17)
     mats = []
-    for t in (1, 5, 40, 120, 220):
-        A = rng.standard_normal((600, t)) * np.logspace(0, -6, t)
+    for t in (1, 5, 40, 120, 220) + wide:
+        A = rng.standard_normal((1200, t)) * np.logspace(0, -6, t)
         if t >= 40:
             A[:, 7] = A[:, 3] * (1 + 1e-13)       # numerically dependent
             A[:, 20] = 2.5 * A[:, 11]              # exactly dependent
@@ -343,3 +343,46 @@ def test_recycle_update_rank_drop_block_householder():
                              seq._prev_recycle, "cfg": seq.cfg})(), 0):
         assert _span_dist(C, ref.C) <= 1e-8
         assert torch.allclose(got[0].nsc_data.values, ref.nsc_data.values, rtol=1e-8)
+
+
+@pytest.mark.parametrize("strategy", ["RGen-L(R)-NSC", "Ritz-L"])
+def test_recycle_update_wide_candidates(strategy):
+    """Candidate widths beyond the shared-memory kernels (t ~ 330, the C3 regime): the
+    native orchestrator (global-workspace Cholesky / eigen-select, 8-CTA cluster QRCP)
+    against the per-sample reference-semantics path."""
+    from paper_2412_08264_b200 import HessianSolveConfig, SequenceSolver, batched
+    from paper_2412_08264_b200.bilevel import hypergradients
+    from paper_2412_08264_b200.problems import DeblurConfig, make_batch, synthetic_sequence
+    from paper_2412_08264_b200.recycling import next_recycle
+
+    cfg = DeblurConfig(64, 2, 9, 1.5, 0.01, "filters", 8, 5)
+    model = make_batch(cfg)
+    th, xh = synthetic_sequence(cfg, model.x_true.cpu().numpy(), 3)
+    seq = SequenceSolver(HessianSolveConfig.from_strategy(strategy, recycle_dim=30, delta=1e-14, max_iter=290))
+    seq.batched_update = False
+    for i in range(2):
+        hypergradients(model, th[i], torch.as_tensor(xh[i], device="cuda"), seq)
+    H, J = model.at(th[2], torch.as_tensor(xh[2], device="cuda"))
+    st = seq.cfg.strategy
+    T = max(int(V.shape[1]) + r.dim for V, r in zip(seq._prev_basis, seq._prev_recycle))
+    assert T > 228, T
+    batched.STATS = {}
+    try:
+        got = batched.recycle_update_native(st, 30, H, J, list(seq._prev_basis), seq._prev_recycle)
+        assert batched.STATS["declined"] == 0, batched.STATS
+    finally:
+        batched.STATS = None
+    for b in range(2):
+        ref = next_recycle(st, h_current=H.sample(b), jac_current=J.sample(b), prev_basis=seq._prev_basis[b],
+                           prev_recycle=seq._prev_recycle[b], s=30)
+        C = got[b].C
+        assert torch.allclose(C.T @ C, torch.eye(C.shape[1], dtype=torch.float64, device="cuda"), atol=1e-12)
+        HU = H.sample(b).apply_matrix(got[b].U)
+        assert torch.dist(HU, C) <= 1e-9 * torch.linalg.norm(HU)
+        if st.vec_type == "RGen":
+            assert got[b].nsc_data.w.shape[1] == ref.nsc_data.w.shape[1]
+            assert _span_dist(got[b].nsc_data.w, ref.nsc_data.w) <= 1e-8
+        if _selection_well_posed(st, H.sample(b), J.sample(b), seq, b):
+            assert _span_dist(C, ref.C) <= 1e-7
+            if st.vec_type == "RGen":
+                assert torch.allclose(got[b].nsc_data.values, ref.nsc_data.values, rtol=1e-8)

@@ -117,8 +117,27 @@ def test_diagonal_and_tridiagonal_inputs():
     _check([D, Tm, np.eye(t)], "M", 12)
 
 
-def test_rejects_large_t():
+@pytest.mark.parametrize("size", ["S", "L", "M"])
+def test_wide_candidates_global_variant(size):
+    """t > 228 (C3-C5 candidate widths): the full matrix lives in the global workspace."""
+    rng = np.random.default_rng(23)
+    mats = [_rand_sym(rng, t) for t in (229, 330, 401, 580, 640)]
+    _check(mats, size, 40)
+
+
+def test_wide_gram_like_spectra():
+    """C3-like GSVD input: p = 208 < t = 330 (zero cluster of 122) and C4-like p = 1200 > t = 540."""
+    rng = np.random.default_rng(29)
+    mats = []
+    for t, p in ((330, 208), (540, 600)):
+        Q, _ = np.linalg.qr(rng.standard_normal((p + t, t)) * np.logspace(0, -6, t))
+        Q1 = Q[:p]
+        mats.append(Q1.T @ Q1)
+    _check(mats, "L", 40)
+
+
+def test_rejects_too_large_t():
     from paper_2412_08264_b200.batched import syev_select
 
     with pytest.raises(ValueError):
-        syev_select(torch.zeros(1, 229, 229, dtype=torch.float64, device="cuda"), torch.tensor([229]), "L", 4)
+        syev_select(torch.zeros(1, 641, 641, dtype=torch.float64, device="cuda"), torch.tensor([641]), "L", 4)
