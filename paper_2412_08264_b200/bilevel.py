@@ -337,8 +337,10 @@ class SequenceSolver:
                 rules.append(NscRule(cfg.delta, rec.nsc_data))
             else:  # res, or nsc on the first system (bilevel.py:269-273)
                 rules.append(ResidualNormRule(cfg.delta))
+        # the residual vector is not materialised (the reference's SequenceSolver never reads
+        # it; NSC runs in s-space on the device)
         return SolveOptions(max_iter=cfg.max_iter, stop_rule=rules if len(rules) > 1 else rules[0],
-                            track_basis=self._needs_basis(), initial_guess=init)
+                            track_basis=self._needs_basis(), initial_guess=init, residual_vector=False)
 
     def solve(self, hessian, g, jac):
         cfg = self.cfg

@@ -32,6 +32,7 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <tuple>
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
@@ -477,15 +478,21 @@ bool cholqr_ok(const std::vector<int32_t>& info, const std::vector<double>& st, 
 int64_t house_lwork(int64_t n, int T) {
   // the cuSOLVER size queries are slow host calls and every workspace query makes them:
   // cached per host thread and shape
-  static thread_local std::map<std::pair<int64_t, int>, int64_t> cache;
-  const auto key = std::make_pair(n, T);
+  // (keyed by device too: the cuSOLVER handles are per device); a failed query is
+  // never cached and falls back to a generous bound
+  static thread_local std::map<std::tuple<int, int64_t, int>, int64_t> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, n, T);
   const auto it = cache.find(key);
   if (it != cache.end()) return it->second;
+  const int64_t fallback = std::max<int64_t>(1 << 20, 64 * (int64_t)T * T);
   cusolverDnHandle_t sh;
-  if (cusolver_handle(&sh, nullptr) != KR_OK) return 1 << 20;
+  if (cusolver_handle(&sh, nullptr) != KR_OK) return fallback;
   int lw1 = 0, lw2 = 0;
-  cusolverDnDgeqrf_bufferSize(sh, (int)n, T, nullptr, (int)n, &lw1);
-  cusolverDnDorgqr_bufferSize(sh, (int)n, T, T, nullptr, (int)n, nullptr, &lw2);
+  if (cusolverDnDgeqrf_bufferSize(sh, (int)n, T, nullptr, (int)n, &lw1) != CUSOLVER_STATUS_SUCCESS ||
+      cusolverDnDorgqr_bufferSize(sh, (int)n, T, T, nullptr, (int)n, nullptr, &lw2) != CUSOLVER_STATUS_SUCCESS)
+    return fallback;
   const int64_t lw = std::max(lw1, lw2);
   cache[key] = lw;
   return lw;

@@ -717,7 +717,7 @@ int plan(const kr_op& op, const kr_solve_args& a, Layout& L) {
   return KR_OK;
 }
 
-int check_args(const kr_op& op, const kr_solve_args& a) {
+int check_args(const kr_op& op, const kr_solve_args& a, bool dyn) {
   KR_CHECK_ARG(a.max_iter >= 1, "max_iter must be >= 1");
   KR_CHECK_ARG(a.s >= 0 && a.s <= MAX_S, "recycle dimension must be in [0, 128]");
   KR_CHECK_ARG(a.s == 0 || (a.U && a.C && a.ld_uc >= op_n(op)), "recycle space U/C missing or bad ld");
@@ -727,7 +727,9 @@ int check_args(const kr_op& op, const kr_solve_args& a) {
     KR_CHECK_ARG(a.nsc_s >= 1 && a.nsc_s <= MAX_NSC, "NSC needs 1..128 columns");
     KR_CHECK_ARG(a.Z && a.ld_z >= op_n(op), "NSC needs Z");
     KR_CHECK_ARG(a.s == 0 || a.ZtC, "NSC with recycling needs Z^T C");
-    KR_CHECK_ARG(a.track_residual, "NSC needs the tracked residual");
+    // the per-sample kernel evaluates NSC through the tracked residual; the shared-block
+    // kernel keeps Z^T r in s-space and forms the vector only when it is asked for
+    KR_CHECK_ARG(dyn || a.track_residual, "NSC needs the tracked residual");
   }
   KR_CHECK_ARG(a.g && a.w && a.res_norms && a.stop_vals && a.iters && a.reasons, "missing output buffer");
   KR_CHECK_ARG(!a.basis || a.ld_basis >= op_n(op), "basis leading dimension smaller than n");
@@ -740,8 +742,15 @@ int check_args(const kr_op& op, const kr_solve_args& a) {
 
 }  // namespace
 
+namespace kr {
+bool rminres_dyn_applies(const kr_op& op, const kr_solve_args& a);
+int64_t rminres_dyn_workspace(const kr_op& op, const kr_solve_args& a);
+int rminres_dyn(const kr_op& op, const kr_solve_args& a, double* work, int64_t work_len, cudaStream_t st);
+}  // namespace kr
+
 extern "C" int64_t kr_rminres_workspace(const kr_op* op, const kr_solve_args* a) {
   if (!op || !a || validate_op(*op) != KR_OK) return -1;
+  if (rminres_dyn_applies(*op, *a)) return rminres_dyn_workspace(*op, *a);
   Layout L;
   plan(*op, *a, L);
   return L.total;
@@ -752,7 +761,11 @@ extern "C" int kr_rminres(const kr_op* op, const kr_solve_args* a, double* work,
   KR_CHECK_ARG(op && a, "null argument");
   KR_TRY(validate_op(*op));
   if (op->batch == 0) return KR_OK;
-  KR_TRY(check_args(*op, *a));
+  const bool dyn = rminres_dyn_applies(*op, *a);
+  KR_TRY(check_args(*op, *a, dyn));
+  // with the Lanczos basis kept (every recycled sequence solve): blocks shared by all
+  // running samples (kr_rminres_dyn.cu)
+  if (dyn) return rminres_dyn(*op, *a, work, work_len, (cudaStream_t)stream);
   Layout L;
   plan(*op, *a, L);
   KR_CHECK_ARG(work && work_len >= L.total, "rminres workspace too small");

@@ -46,6 +46,11 @@ class SolveOptions:
     collect_states: bool = False
     collect_iterates: bool = False
     collect_residual_history: bool = False
+    # not in the reference: None = the reference's behaviour (the residual vector is
+    # tracked and returned when the stop rule needs it, krylov.py:214-215); False = do not
+    # materialise it (the device solver evaluates NSC in s-space and, with the basis kept,
+    # needs no residual vector at all -- SequenceSolver uses this)
+    residual_vector: bool | None = None
 
     def __post_init__(self):
         if self.max_iter < 1:
@@ -184,7 +189,7 @@ def _buf(tag, *shape, zero=False, dev=None):
 class _Launch:
     """Device buffers + kr_solve_args for one batched solve."""
 
-    def __init__(self, H, G, recycles, rules, opts, want_basis, deflate=False):
+    def __init__(self, H, G, recycles, rules, opts, want_basis, deflate=False, plain_cg=False):
         B, n = G.shape
         dev = G.device
         self.B, self.n = B, n
@@ -198,7 +203,9 @@ class _Launch:
             w0 = as_device(w0).reshape(B, n).contiguous()
             self.keep.append(w0)
             a.w0 = w0.data_ptr()
-        self.finite = torch.isfinite(G).all()  # krylov.py contract: non-finite g -> ValueError
+        # (r)minres contract: non-finite g -> ValueError; the reference's cg has no such
+        # check (krylov.py:408-483) and runs the NaNs through to max_iter
+        self.finite = torch.ones((), dtype=torch.bool, device=dev) if plain_cg else torch.isfinite(G).all()
         dims = [0 if r is None else r.dim for r in recycles]
         s = max(dims) if dims else 0
         self.dims = dims
@@ -247,7 +254,11 @@ class _Launch:
             raise ValueError("one launch needs one tolerance")
         a.stop_kind = kind
         a.delta = deltas.pop()
-        track = opts.track_residual_vector or kind == 1
+        # cg always returns its final residual (krylov.py:482: residual_vector=r.copy());
+        # (r)minres tracks it when asked or when NSC needs it (krylov.py:214-215) -- unless the
+        # caller waived it and the basis is kept (then the kernel keeps Z^T r in s-space)
+        want_r = opts.track_residual_vector or (kind == 1 and opts.residual_vector is not False)
+        track = want_r or plain_cg or (kind == 1 and not want_basis)
         a.track_residual = int(track)
         if kind == 1:
             zs = [r.data.z_block() for r in rules]
@@ -394,7 +405,7 @@ def _solve(H, g, recycle, opts, kind):
         if kind == "cg":
             if any(r is not None and r.dim for r in rec):
                 raise ValueError("plain CG takes no recycle space; use rcg")
-            launch = _Launch(Hs, Gs, [None] * len(idx), rs, sub_opts, opts.track_basis)
+            launch = _Launch(Hs, Gs, [None] * len(idx), rs, sub_opts, opts.track_basis, plain_cg=True)
             launch.run(Hs, L.kr_cg_workspace, L.kr_cg)
             res = launch.results(Hs, lambda k, s: flops_cg(k, n, H.apply_cost))
         elif kind == "rcg":
