@@ -36,7 +36,9 @@
 namespace kr {
 namespace dyn {
 
-enum Mode : unsigned { M_DONE = 0, M_RUN = 1, M_FIN = 2, M_INIT = 0xff };
+// M_RUN: next step is phase A (stencil + dots) of iteration k; M_RUNB: phase B of k;
+// M_FIN: finalisation (w, r); M_WAIT: skips one super-phase (pipelining offset)
+enum Mode : unsigned { M_DONE = 0, M_RUN = 1, M_FIN = 2, M_RUNB = 3, M_WAIT = 4, M_INIT = 0xff };
 
 struct St {
   double beta;       // beta_k: v_k = tmp / beta_k
@@ -68,8 +70,33 @@ struct DParams {
   unsigned long long* mode;    // [B]: (phase stamp << 32) | (mode before that phase << 8) | mode
   int* cnt;                    // [B] arrivals in the current phase
   unsigned int* bar;           // grid barrier counter
+  unsigned int* grab;          // [2] unit tickets of the current / next super-phase
   int track;                   // residual vector requested (hv keeps every column)
+  int vec2;                    // even image width and 16-byte aligned columns: pixel pairs as double2
+  int pipe;                    // odd samples run one phase behind the even ones (A and B units overlap)
 };
+
+__device__ __forceinline__ double2 ld2cg(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ double2 ld2g(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
+
+// The thread's pixel pair of a tile (vec2 mode): row threadIdx.x / 16, columns 2 (threadIdx.x % 16) + {0, 1}.
+struct Pair {
+  int l;       // tile-local index of the first pixel
+  int64_t q;   // global pixel index of the first pixel (0 when outside)
+  bool ok;
+};
+__device__ inline Pair tile_pair(const kr_op& op, int tile) {
+  const int tyc = tiles_x(op);
+  const int ty = threadIdx.x >> 4, tx = (threadIdx.x & 15) * 2;
+  const int y = (tile / tyc) * TH + ty, x = (tile % tyc) * TW + tx;
+  Pair r;
+  r.l = ty * TW + tx;
+  r.ok = y < op.rows && x < op.cols;  // cols even: x + 1 < cols as well
+  r.q = r.ok ? (int64_t)y * op.cols + x : 0;
+  return r;
+}
+static_assert(TPX == 2 * NT && TW == 32, "vec2 mode: one pixel pair per thread per tile");
 
 __device__ inline double* vecp(const DParams& P, int b, int which) {
   return P.vecs + ((int64_t)b * NVEC + which) * MAX_S;
@@ -227,6 +254,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(DParams P) {
   __shared__ int list[MAX_B];
   __shared__ int wsum[NWARP];
   __shared__ int s_flag;
+  __shared__ int s_unit;
   __shared__ double sc[8];
   const int64_t n = P.n;
   const int s = A.s, ns = A.stop_kind == 1 ? A.nsc_s : 0;
@@ -331,6 +359,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(DParams P) {
         unsigned m = M_RUN;
         if (val < A.delta) { S.iters = 0; S.reason = R_TOL; m = M_FIN; }
         else if (broke) { S.iters = 0; S.reason = R_BREAK; m = M_FIN; }
+        if (m == M_RUN && P.pipe && (b & 1)) m = M_WAIT;
         S.k = 1;
         mode_set(P, b, ph, M_INIT, m);
       }
@@ -349,11 +378,29 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(DParams P) {
   const int npass = (s > ns ? s : ns) > 0 ? ((s > ns ? s : ns) + 7) / 8 : 1;
   const bool deferred = npass <= DEF_PASSES;
   for (;;) {
-    // ===== phase A: RUN -> stencil + dots of v_k;  FIN -> w (and r) from the stored basis =====
-    const int na = build_list(P, ph, (1u << M_RUN) | (1u << M_FIN), list, wsum);
-    if (na == 0) break;  // identical in every block
-    for (int u = blockIdx.x; u < na * nt; u += G) {
-      const int b = list[u / nt], tile = u % nt;
+    // One super-phase: every sample with work takes its next step -- phase A (M_RUN: stencil
+    // + dots of v_k), phase B (M_RUNB: u, ||u||^2, finish iteration k) or the finalisation
+    // (M_FIN: w and r from the stored basis).  Without pipelining all samples are in step
+    // (A, B, A, ...); with it the odd samples run one phase behind, so every super-phase
+    // mixes compute-heavy A units with streaming B units on the same SMs.
+    const int na = build_list(P, ph, (1u << M_RUN) | (1u << M_FIN) | (1u << M_RUNB), list, wsum);
+    if (na == 0) break;  // identical in every block (M_WAIT only ever coexists with M_RUN samples)
+    if (blockIdx.x == 0)
+      for (int b = threadIdx.x; b < P.B; b += NT)
+        if (mode_at(P, b, ph) == M_WAIT) mode_set(P, b, ph, M_WAIT, M_RUN);
+    // units are taken from a ticket counter (the next ticket requested while the current
+    // unit runs): blocks that drew heavy units take fewer -- the super-phase ends when the
+    // work does, not when the unluckiest block's fixed share does.  Unit u is tile u / na
+    // of list sample u % na (samples interleaved: A and B units mix on every SM, and
+    // neighbouring tiles of a sample run concurrently for the halo's L2 reuse).
+    unsigned int* tickets = P.grab + (ph & 1);
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(P.grab + ((ph + 1) & 1), 0u);
+    if (threadIdx.x == 0) s_unit = (int)atomicAdd(tickets, 1u);
+    block_barrier();
+    for (int u = s_unit; u < na * nt; u = s_unit) {
+      unsigned int next_ticket = 0;
+      if (threadIdx.x == 0) next_ticket = atomicAdd(tickets, 1u);
+      const int b = list[u % na], tile = u / na;
       const unsigned md = mode_at(P, b, ph);
       if (md == M_RUN) {
         const double beta = __ldcg(&P.st[b].beta);
@@ -364,6 +411,52 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(DParams P) {
         double* hvk = hvcol(P, b, k);
         double* vk = vcol(P, b, k);
         tile_hvp_t<Q>(op, g, sm, b, TileIn{tb, beta, nullptr, 0.0}, tile);
+        if (deferred) {
+          for (int i = threadIdx.x; i < npass * 25 * DEF_STRIDE; i += NT) red[i] = 0.0;
+          block_barrier();
+        }
+        if (P.vec2) {
+          // one pixel pair per thread: H v_k and v_k written as double2, C / Z read as double2,
+          // 8 + 8 column pairs in flight per pass
+          const Pair pr = tile_pair(op, tile);
+          const int c0 = (pr.l / TW + g.H) * g.RW + (pr.l % TW) + g.H;
+          double2 h2 = make_double2(sm.res[pr.l], sm.res[pr.l + 1]);
+          double2 v2 = make_double2(sm.S0[c0], sm.S0[c0 + 1]);
+          if (pr.ok) {
+            st2(hvk + pr.q, h2);
+            st2(vk + pr.q, v2);
+          } else {
+            h2 = v2 = make_double2(0.0, 0.0);
+          }
+          for (int base = 0; base < 8 * npass; base += 8) {
+            double2 cc[8], zz[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              cc[i] = (pr.ok && base + i < s) ? ld2g(C + (int64_t)(base + i) * A.ld_uc + pr.q) : make_double2(0.0, 0.0);
+              zz[i] = (pr.ok && base + i < ns) ? ld2g(Z + (int64_t)(base + i) * A.ld_z + pr.q) : make_double2(0.0, 0.0);
+            }
+            double v25[25];
+            v25[24] = base == 0 ? v2.x * h2.x + v2.y * h2.y : 0.0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              v25[i] = cc[i].x * h2.x + cc[i].y * h2.y;
+              v25[8 + i] = cc[i].x * v2.x + cc[i].y * v2.y;
+              v25[16 + i] = zz[i].x * h2.x + zz[i].y * h2.y;
+            }
+            if (deferred) {
+              def_add<25>(MultiSum<25>::reduce(v25, threadIdx.x & 31), base / 8, red);
+              continue;
+            }
+            block_sum<25>(v25, red);
+            if (threadIdx.x < 8 && base + threadIdx.x < s) {
+              partp(P, b, SL_CHV + base + threadIdx.x)[tile] = red[threadIdx.x];
+              partp(P, b, SL_CV + base + threadIdx.x)[tile] = red[8 + threadIdx.x];
+            }
+            if (threadIdx.x < 8 && base + threadIdx.x < ns) partp(P, b, SL_ZHV + base + threadIdx.x)[tile] = red[16 + threadIdx.x];
+            if (threadIdx.x == 0 && base == 0) partp(P, b, SL_VHV)[tile] = red[24];
+            block_barrier();
+          }
+        } else {
         for (int l = threadIdx.x; l < TPX; l += NT) {
           const int64_t p = tile_pixel(op, tile, l);
           if (p < 0) continue;
@@ -376,10 +469,6 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(DParams P) {
           }
         }
         // tile partials: C^T hv, C^T v, v.hv, Z^T hv -- 8 columns per pass, 2 pixels per thread
-        if (deferred) {
-          for (int i = threadIdx.x; i < npass * 25 * DEF_STRIDE; i += NT) red[i] = 0.0;
-          block_barrier();
-        }
         for (int base = 0; base < 8 * npass; base += 8) {
           double v25[25];
 #pragma unroll
@@ -429,6 +518,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(DParams P) {
           if (threadIdx.x == 0 && base == 0) partp(P, b, SL_VHV)[tile] = red[24];
           block_barrier();
         }
+        }
         if (deferred) {
           block_barrier();
           for (int c = threadIdx.x; c < s; c += NT) {
@@ -452,89 +542,12 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(DParams P) {
             double corr = 0.0;
             for (int i = 0; i < s; ++i) corr += slot[SL_CV + i] * slot[SL_CHV + i];
             P.st[b].alpha = slot[SL_VHV] - corr;
+            mode_set(P, b, ph, M_RUN, M_RUNB);
           }
         }
         block_barrier();
-      } else {  // M_FIN: w = w0 + U (t0 - Omega) + V y;  r = r0 - C (t0 - Omega) - HV y
-        const int K = *reinterpret_cast<volatile int*>(&P.st[b].iters);
-        const double* U = s ? A.U + (int64_t)b * A.bs_uc : nullptr;
-        const double* C = s ? A.C + (int64_t)b * A.bs_uc : nullptr;
-        const double* Yb = P.y + (int64_t)b * A.max_iter;
-        for (int i = threadIdx.x; i < s; i += NT) sv[i] = __ldcg(vecp(P, b, V_TMO) + i);
-        block_barrier();
-        double wacc[PPT], racc[PPT];
-        int64_t pp[PPT];
-#pragma unroll
-        for (int uu = 0; uu < PPT; ++uu) {
-          pp[uu] = tile_pixel(op, tile, threadIdx.x + uu * NT);
-          const int64_t q = pp[uu] >= 0 ? pp[uu] : 0;
-          double w = A.w0 ? A.w0[(int64_t)b * n + q] : 0.0;
-          double r = 0.0;
-          if (P.track) r = A.w0 ? P.r0[(int64_t)b * n + q] : A.g[(int64_t)b * n + q];
-          double uo = 0.0, co = 0.0;
-          for (int i = 0; i < s; ++i) {
-            uo += U[(int64_t)i * A.ld_uc + q] * sv[i];
-            if (P.track) co += C[(int64_t)i * A.ld_uc + q] * sv[i];
-          }
-          wacc[uu] = w + uo;
-          racc[uu] = r - co;
-        }
-        double* ys = sm.S0;  // y staged in chunks (the stencil scratch is free here)
-        for (int j0 = 0; j0 < K; j0 += CH) {
-          const int m = (K - j0) < CH ? (K - j0) : CH;
-          block_barrier();
-          for (int i = threadIdx.x; i < m; i += NT) ys[i] = __ldcg(Yb + j0 + i);
-          block_barrier();
-#pragma unroll
-          for (int uu = 0; uu < PPT; ++uu) {
-            const int64_t q = pp[uu] >= 0 ? pp[uu] : 0;
-            const double* V = A.basis + (int64_t)b * A.bs_basis + (int64_t)j0 * A.ld_basis + q;
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-            int j = 0;
-            for (; j + 3 < m; j += 4) {
-              a0 += V[(int64_t)j * A.ld_basis] * ys[j];
-              a1 += V[(int64_t)(j + 1) * A.ld_basis] * ys[j + 1];
-              a2 += V[(int64_t)(j + 2) * A.ld_basis] * ys[j + 2];
-              a3 += V[(int64_t)(j + 3) * A.ld_basis] * ys[j + 3];
-            }
-            for (; j < m; ++j) a0 += V[(int64_t)j * A.ld_basis] * ys[j];
-            wacc[uu] += (a0 + a1) + (a2 + a3);
-            if (P.track) {
-              const double* HVc = P.hv + ((int64_t)b * A.max_iter + j0) * n + q;
-              double h0 = 0.0, h1 = 0.0;
-              int jj = 0;
-              for (; jj + 1 < m; jj += 2) {
-                h0 += HVc[(int64_t)jj * n] * ys[jj];
-                h1 += HVc[(int64_t)(jj + 1) * n] * ys[jj + 1];
-              }
-              if (jj < m) h0 += HVc[(int64_t)jj * n] * ys[jj];
-              racc[uu] -= h0 + h1;
-            }
-          }
-        }
-#pragma unroll
-        for (int uu = 0; uu < PPT; ++uu) {
-          if (pp[uu] < 0) continue;
-          A.w[(int64_t)b * n + pp[uu]] = wacc[uu];
-          if (P.track && A.r) A.r[(int64_t)b * n + pp[uu]] = racc[uu];
-        }
-        if (arrive(P, b, &s_flag)) {
-          if (threadIdx.x == 0) {
-            A.iters[b] = P.st[b].iters;
-            A.reasons[b] = P.st[b].reason;
-            mode_set(P, b, ph, M_FIN, M_DONE);
-          }
-        }
-        block_barrier();
-      }
-    }
-    DYN_GRID_SYNC();
-    ++ph;
-
-    // ===== phase B: u = hv_k - C chv - alpha v_k - beta_k v_{k-1}, ||u||^2; then finish iteration k =====
-    const int nb = build_list(P, ph, 1u << M_RUN, list, wsum);
-    for (int u = blockIdx.x; u < nb * nt; u += G) {
-      const int b = list[u / nt], tile = u % nt;
+      } else if (md == M_RUNB) {
+        // ===== phase B: u = hv_k - C chv - alpha v_k - beta_k v_{k-1}, ||u||^2; then finish iteration k =====
       St* S = P.st + b;
       const int k = *reinterpret_cast<volatile int*>(&S->k);
       const double al = __ldcg(&S->alpha), be = __ldcg(&S->beta);
@@ -546,6 +559,32 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(DParams P) {
       const double* hvk = hvcol(P, b, k);
       double* tb = P.tmp + (int64_t)b * n;
       double bsq[1] = {0.0};
+      if (P.vec2) {
+        // one pixel pair per thread, every load of the pass issued before the first use
+        const Pair pr = tile_pair(op, tile);
+        if (pr.ok) {
+          const double2 h2 = ld2cg(hvk + pr.q), v2 = ld2cg(vk + pr.q);
+          const double2 m2 = vkm ? ld2cg(vkm + pr.q) : make_double2(0.0, 0.0);
+          double ccx = 0.0, ccy = 0.0;
+          for (int i0 = 0; i0 < s; i0 += 16) {
+            double2 c16[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              c16[i] = (i0 + i < s) ? ld2g(C + (int64_t)(i0 + i) * A.ld_uc + pr.q) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (i0 + i < s) {
+                ccx += c16[i].x * sv[i0 + i];
+                ccy += c16[i].y * sv[i0 + i];
+              }
+          }
+          double2 x;
+          x.x = ((h2.x - ccx) - al * v2.x) - be * m2.x;  // vnext = hv - C chv - alpha v - beta v_prev
+          x.y = ((h2.y - ccy) - al * v2.y) - be * m2.y;
+          st2(tb + pr.q, x);
+          bsq[0] = x.x * x.x + x.y * x.y;
+        }
+      } else
       for (int l = threadIdx.x; l < TPX; l += NT) {
         const int64_t p = tile_pixel(op, tile, l);
         if (p < 0) continue;
@@ -660,7 +699,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(DParams P) {
             else S->k = k + 1;
           }
           sc[6] = (double)m;
-          if (m == M_FIN) mode_set(P, b, ph, M_RUN, M_FIN);
+          mode_set(P, b, ph, M_RUNB, m);
         }
         block_barrier();
         if (sc[6] == (double)M_FIN) {
@@ -672,6 +711,81 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(DParams P) {
           for (int i = threadIdx.x; i < s; i += NT) tmo[i] = t0[i] - om[i];
         }
       }
+      block_barrier();
+      } else {  // M_FIN: w = w0 + U (t0 - Omega) + V y;  r = r0 - C (t0 - Omega) - HV y
+        const int K = *reinterpret_cast<volatile int*>(&P.st[b].iters);
+        const double* U = s ? A.U + (int64_t)b * A.bs_uc : nullptr;
+        const double* C = s ? A.C + (int64_t)b * A.bs_uc : nullptr;
+        const double* Yb = P.y + (int64_t)b * A.max_iter;
+        for (int i = threadIdx.x; i < s; i += NT) sv[i] = __ldcg(vecp(P, b, V_TMO) + i);
+        block_barrier();
+        double wacc[PPT], racc[PPT];
+        int64_t pp[PPT];
+#pragma unroll
+        for (int uu = 0; uu < PPT; ++uu) {
+          pp[uu] = tile_pixel(op, tile, threadIdx.x + uu * NT);
+          const int64_t q = pp[uu] >= 0 ? pp[uu] : 0;
+          double w = A.w0 ? A.w0[(int64_t)b * n + q] : 0.0;
+          double r = 0.0;
+          if (P.track) r = A.w0 ? P.r0[(int64_t)b * n + q] : A.g[(int64_t)b * n + q];
+          double uo = 0.0, co = 0.0;
+          for (int i = 0; i < s; ++i) {
+            uo += U[(int64_t)i * A.ld_uc + q] * sv[i];
+            if (P.track) co += C[(int64_t)i * A.ld_uc + q] * sv[i];
+          }
+          wacc[uu] = w + uo;
+          racc[uu] = r - co;
+        }
+        double* ys = sm.S0;  // y staged in chunks (the stencil scratch is free here)
+        for (int j0 = 0; j0 < K; j0 += CH) {
+          const int m = (K - j0) < CH ? (K - j0) : CH;
+          block_barrier();
+          for (int i = threadIdx.x; i < m; i += NT) ys[i] = __ldcg(Yb + j0 + i);
+          block_barrier();
+#pragma unroll
+          for (int uu = 0; uu < PPT; ++uu) {
+            const int64_t q = pp[uu] >= 0 ? pp[uu] : 0;
+            const double* V = A.basis + (int64_t)b * A.bs_basis + (int64_t)j0 * A.ld_basis + q;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            int j = 0;
+            for (; j + 3 < m; j += 4) {
+              a0 += V[(int64_t)j * A.ld_basis] * ys[j];
+              a1 += V[(int64_t)(j + 1) * A.ld_basis] * ys[j + 1];
+              a2 += V[(int64_t)(j + 2) * A.ld_basis] * ys[j + 2];
+              a3 += V[(int64_t)(j + 3) * A.ld_basis] * ys[j + 3];
+            }
+            for (; j < m; ++j) a0 += V[(int64_t)j * A.ld_basis] * ys[j];
+            wacc[uu] += (a0 + a1) + (a2 + a3);
+            if (P.track) {
+              const double* HVc = P.hv + ((int64_t)b * A.max_iter + j0) * n + q;
+              double h0 = 0.0, h1 = 0.0;
+              int jj = 0;
+              for (; jj + 1 < m; jj += 2) {
+                h0 += HVc[(int64_t)jj * n] * ys[jj];
+                h1 += HVc[(int64_t)(jj + 1) * n] * ys[jj + 1];
+              }
+              if (jj < m) h0 += HVc[(int64_t)jj * n] * ys[jj];
+              racc[uu] -= h0 + h1;
+            }
+          }
+        }
+#pragma unroll
+        for (int uu = 0; uu < PPT; ++uu) {
+          if (pp[uu] < 0) continue;
+          A.w[(int64_t)b * n + pp[uu]] = wacc[uu];
+          if (P.track && A.r) A.r[(int64_t)b * n + pp[uu]] = racc[uu];
+        }
+        if (arrive(P, b, &s_flag)) {
+          if (threadIdx.x == 0) {
+            A.iters[b] = P.st[b].iters;
+            A.reasons[b] = P.st[b].reason;
+            mode_set(P, b, ph, M_FIN, M_DONE);
+          }
+        }
+        block_barrier();
+      }
+      block_barrier();
+      if (threadIdx.x == 0) s_unit = (int)next_ticket;
       block_barrier();
     }
     DYN_GRID_SYNC();
@@ -765,6 +879,16 @@ int rminres_dyn(const kr_op& op, const kr_solve_args& a, double* work, int64_t w
   P.mode = reinterpret_cast<unsigned long long*>(take(B));
   P.cnt = reinterpret_cast<int*>(take(B + 2));
   P.bar = reinterpret_cast<unsigned int*>(P.cnt + B + 1);
+  P.grab = reinterpret_cast<unsigned int*>(P.cnt + B + 2);
+  // pipelining pays when every super-phase still has several units per block
+  const char* pe = getenv("KR_DYN_PIPE");
+  P.pipe = pe ? (pe[0] == '1') : 0;  // measured: no gain once units are ticketed (C3: 1326 vs 1315 ms)
+  auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  const int ns = a.stop_kind == 1 ? a.nsc_s : 0;
+  P.vec2 = op.data_kind != KR_DATA_DENSE && op.cols % 2 == 0 && al16(P.tmp) && al16(P.hv) && al16(a.basis) &&
+           a.ld_basis % 2 == 0 && a.bs_basis % 2 == 0 &&
+           (a.s == 0 || (al16(a.C) && a.ld_uc % 2 == 0 && a.bs_uc % 2 == 0)) &&
+           (ns == 0 || (al16(a.Z) && a.ld_z % 2 == 0 && a.bs_z % 2 == 0)) && getenv("KR_DYN_SCALAR") == nullptr;
   const void* kfn = KR_PICK_Q(rminres_dyn_kernel, q_variant(op));
   KR_TRY(ensure_smem(kfn, L.smem));
   cudaMemsetAsync(P.vecs, 0, sizeof(double) * (size_t)B * NVEC * MAX_S, st);

@@ -9,7 +9,8 @@ deblurring operators, for speed at 256^2 / 512^2).  It stores, per system and sa
 iterations, stop reason, final stop value, the hypergradient J w, the candidate width
 t = k_prev + s_prev the recycle update saw -- and the same for P control runs whose
 Hessian products are perturbed at roundoff level (cpu_imaging.perturbed, 2e-16
-relative, per-run seeds): the reference algorithm's own roundoff floor, against which
+relative, per-run seeds) and whose carried Lanczos basis is perturbed by 1e-15 relative
+before each recycle update: the reference algorithm's own roundoff floor, against which
 the GPU results are judged (tests/test_gpu_configs.py).
 
     python tests/golden/make_config_fixtures.py [C2|C3s|C4s ...]
@@ -110,6 +111,13 @@ def run_case(name: str):
             row["tdim"].append(t)
             for c in range(ncontrol):
                 rc, _ = controls[c][b].solve(im.perturbed(H, 2e-16, seed=1000 * c + 10 * k + b), g, J)
+                # ... and its carried Lanczos basis perturbed at 1e-15 relative: the roundoff an
+                # implementation that orthonormalises the candidates differently (CholQR2 /
+                # projected eigenproblem instead of pivoted Householder QR / SVD) puts into the
+                # next recycle space
+                prng = np.random.default_rng([7, c, k, b])
+                cb = controls[c][b]
+                cb.prev_basis = cb.prev_basis * (1.0 + 1e-15 * prng.standard_normal(cb.prev_basis.shape))
                 crow["iters"][c].append(rc.iterations)
                 crow["hg"][c].append(J.apply_adjoint(rc.solution))
             print(f"{name} system {k} sample {b}: t={t} iters {r.iterations} ({r.stop_reason}) control "
