@@ -74,12 +74,20 @@ __global__ void prepare_tv_kernel(kr_op op) {
 template <int Q>
 __global__ void __launch_bounds__(NT) hvp_kernel(kr_op op, const double* __restrict__ V, int64_t ldv,
                                                  int64_t bsv, double* __restrict__ HV, int64_t ldo,
-                                                 int64_t bso) {
+                                                 int64_t bso, const int32_t* __restrict__ dims) {
   extern __shared__ double smem[];
+  const int tile = blockIdx.x, col = blockIdx.y, b = blockIdx.z;
+  if (dims && col >= dims[b]) {  // zero pad column of a batch padded to its widest sample: H 0 = 0
+    double* out = HV + b * bso + col * ldo;
+    for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
+      const int64_t p = tile_pixel(op, tile, l);
+      if (p >= 0) out[p] = 0.0;
+    }
+    return;
+  }
   const Geom g = make_geom(op);
   Smem sm = carve(g, smem);
   load_weights(op, g, sm);
-  const int tile = blockIdx.x, col = blockIdx.y, b = blockIdx.z;
   const double* in = V + b * bsv + col * ldv;
   tile_hvp_t<Q>(op, g, sm, b, TileIn{in, 1.0, nullptr, 0.0}, tile);
   double* out = HV + b * bso + col * ldo;
@@ -409,8 +417,20 @@ extern "C" int kr_op_prepare(const kr_op* op, kr_stream_t stream) {
   return check_launch("kr_op_prepare");
 }
 
+namespace kr {
+int hvp_cols(const kr_op* op, const double* V, int64_t ldv, int64_t bsv, int32_t ncols, const int32_t* dims,
+             double* HV, int64_t ldo, int64_t bso, cudaStream_t stream);
+}
+
 extern "C" int kr_hvp(const kr_op* op, const double* V, int64_t ldv, int64_t bsv, int32_t ncols, double* HV,
                       int64_t ldo, int64_t bso, kr_stream_t stream) {
+  return kr::hvp_cols(op, V, ldv, bsv, ncols, nullptr, HV, ldo, bso, (cudaStream_t)stream);
+}
+
+// H V with an optional DEVICE per-sample column count dims[b]: columns >= dims[b] are the zero
+// padding of a batch padded to its widest sample and are written as zeros without a stencil.
+int kr::hvp_cols(const kr_op* op, const double* V, int64_t ldv, int64_t bsv, int32_t ncols, const int32_t* dims,
+                 double* HV, int64_t ldo, int64_t bso, cudaStream_t stream) {
   KR_CHECK_ARG(op != nullptr, "null operator");
   KR_TRY(validate_op(*op));
   if (ncols <= 0 || op->batch <= 0) return KR_OK;
@@ -422,7 +442,7 @@ extern "C" int kr_hvp(const kr_op* op, const double* V, int64_t ldv, int64_t bsv
   KR_TRY(ensure_smem(fn, smem));
   dim3 grid(num_tiles(*op), ncols, op->batch);
   kr_op opv = *op;
-  void* args[] = {&opv, (void*)&V, &ldv, &bsv, &HV, &ldo, &bso};
+  void* args[] = {&opv, (void*)&V, &ldv, &bsv, &HV, &ldo, &bso, (void*)&dims};
   cudaError_t e = cudaLaunchKernel(fn, grid, dim3(NT), args, smem, (cudaStream_t)stream);
   if (e != cudaSuccess) return fail(KR_ECUDA, std::string("kr_hvp launch: ") + cudaGetErrorString(e));
   return check_launch("kr_hvp");

@@ -59,6 +59,8 @@ int kr_qrcp_small_cluster(double* M, const int32_t* dims, int32_t batch, int32_t
 }
 
 namespace kr {
+int hvp_cols(const kr_op* op, const double* V, int64_t ldv, int64_t bsv, int32_t ncols, const int32_t* dims,
+             double* HV, int64_t ldo, int64_t bso, cudaStream_t stream);
 namespace {
 
 constexpr double CHOLQR_TOL = 1e-7;   // recycling.CHOLQR_TOL
@@ -368,8 +370,8 @@ SideStream& side_stream() {
 struct LowStream {
   cudaStream_t st = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  int run_hvp(const kr_op* op, const double* V, int64_t ldv, int64_t bsv, int32_t ncols, double* HV, int64_t ldo,
-              int64_t bso, cudaStream_t main) {
+  int run_hvp(const kr_op* op, const double* V, int64_t ldv, int64_t bsv, int32_t ncols, const int32_t* dims,
+              double* HV, int64_t ldo, int64_t bso, cudaStream_t main) {
     if (!st) {
       int least = 0, greatest = 0;
       cudaDeviceGetStreamPriorityRange(&least, &greatest);
@@ -380,7 +382,7 @@ struct LowStream {
     }
     if (cudaEventRecord(ev_fork, main) != cudaSuccess || cudaStreamWaitEvent(st, ev_fork, 0) != cudaSuccess)
       return fail(KR_ECUDA, "kr_recycle fork");
-    KR_TRY(kr_hvp(op, V, ldv, bsv, ncols, HV, ldo, bso, st));
+    KR_TRY(hvp_cols(op, V, ldv, bsv, ncols, dims, HV, ldo, bso, st));
     if (cudaEventRecord(ev_join, st) != cudaSuccess || cudaStreamWaitEvent(main, ev_join, 0) != cudaSuccess)
       return fail(KR_ECUDA, "kr_recycle join");
     return KR_OK;
@@ -746,14 +748,17 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
   }
   std::vector<int32_t> is1;
   if (shifted) KR_TRY(d2h(c, is1, f1.info, B));
-  KR_TRY(rows_mul(c, f1.F, (int64_t)T * T, A, n, (int64_t)T * n, W, n, (int64_t)T * n, T, T, n, B));
+  // first pass into tmpQ or W so that the last pass lands in W (no B x T x n copy back)
+  const int npass = shifted ? 2 : 1;
+  double* first = (npass % 2 == 1) ? tmpQ : W;
+  KR_TRY(rows_mul(c, f1.F, (int64_t)T * T, A, n, (int64_t)T * n, first, n, (int64_t)T * n, T, T, n, B));
   // second pass (and third when shifted)
   Factor* fp[2] = {&f2, &f3};
-  double* cur = W;
-  double* nxt = tmpQ;
+  double* cur = first;
+  double* nxt = first == W ? tmpQ : W;
   KR_TRY(cudaMemcpyAsync(F, f1.F, sizeof(double) * B * T * T, cudaMemcpyDeviceToDevice, c.st) == cudaSuccess
              ? KR_OK : fail(KR_ECUDA, "kr_recycle copy"));
-  for (int pass = 0; pass < (shifted ? 2 : 1); ++pass) {
+  for (int pass = 0; pass < npass; ++pass) {
     KR_TRY(gram(c, cur, cur, B, T, n, G));
     KR_TRY(chol(c, G, d_td, B, T, false, nullptr, *fp[pass], true));
     KR_TRY(rows_mul(c, fp[pass]->F, (int64_t)T * T, cur, n, (int64_t)T * n, nxt, n, (int64_t)T * n, T, T, n, B));
@@ -913,9 +918,9 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
   double* HW = a->HW;
   static const bool lowpri = getenv("KR_HVP_LOWPRI") == nullptr || getenv("KR_HVP_LOWPRI")[0] != '0';
   if (lowpri)
-    KR_TRY(low_stream().run_hvp(op, W, n, (int64_t)T * n, T, HW, n, (int64_t)T * n, c.st));
+    KR_TRY(low_stream().run_hvp(op, W, n, (int64_t)T * n, T, d_td, HW, n, (int64_t)T * n, c.st));
   else
-    KR_TRY(kr_hvp(op, W, n, (int64_t)T * n, T, HW, n, (int64_t)T * n, c.st));
+    KR_TRY(hvp_cols(op, W, n, (int64_t)T * n, T, d_td, HW, n, (int64_t)T * n, c.st));
   double* Ht = c.take((int64_t)B * T * T);
   KR_TRY(gram(c, W, HW, B, T, n, Ht));
   double* coeffs = c.take((int64_t)B * s * T);

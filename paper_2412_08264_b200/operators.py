@@ -305,6 +305,15 @@ class Model:
                      None if self.mask is None else (self.mask[sl] if self.mask.shape[0] > 1 else self.mask),
                      self.taps, self.reg_kind, self.potential, self.eps, self.num_filters, self.ksize)
 
+    def select(self, idx) -> "Model":
+        """Samples idx (any order), gathered into new storage."""
+        it = torch.as_tensor(list(idx), dtype=torch.long, device=self.y.device)
+        return Model(self.shape, len(idx), self.data_kind, self.data_scale, self.ridge, self.y.index_select(0, it),
+                     None if self.x_true is None else self.x_true.index_select(0, it),
+                     None if self.mask is None else (self.mask.index_select(0, it) if self.mask.shape[0] > 1
+                                                     else self.mask),
+                     self.taps, self.reg_kind, self.potential, self.eps, self.num_filters, self.ksize)
+
     def hessian_cost(self) -> int:
         """Declared model FLOPs per H v (operators.py:356-360 for the FoE family)."""
         n = self.n
@@ -470,6 +479,26 @@ class HessianOperator(SymmetricOperator):
             op.xhat = k["xhat"][lo].data_ptr()
         return HessianOperator(self.model.slice(lo, hi), op, self._keep)
 
+    def select(self, idx) -> "HessianOperator":
+        """Operator over the samples idx (any order): the per-sample tables (curvature,
+        slope, xhat, mask) gathered into new buffers; theta's filter bank is shared."""
+        idx = list(idx)
+        if not idx or min(idx) < 0 or max(idx) >= self.batch:
+            raise IndexError(f"samples {idx} out of range for batch {self.batch}")
+        op = KrOp.from_buffer_copy(self.op)
+        op.batch = len(idx)
+        k = dict(self._keep)
+        dev = self.model.y.device
+        it = torch.as_tensor(idx, dtype=torch.long, device=dev)
+        if op.mask_bstride and "mask" in k:
+            k["mask"] = k["mask"].index_select(0, it)
+            op.mask = k["mask"].data_ptr()
+        for key in ("curv", "slope", "xhat"):
+            if key in k:
+                k[key] = k[key].index_select(0, it)
+                setattr(op, key, k[key].data_ptr())
+        return HessianOperator(self.model.select(idx), op, k)
+
     def _apply_cols(self, M: torch.Tensor) -> torch.Tensor:
         # M: (B, n, t) with contiguous columns
         B, n, t = M.shape
@@ -581,6 +610,12 @@ class StencilJacobian(MixedJacobianOperator):
     def slice(self, lo: int, hi: int) -> "StencilJacobian":
         H = HessianOperator(self.model, self.op, self._keep).slice(lo, hi)
         return StencilJacobian(H.model, H.op, self._keep)
+
+    def select(self, idx, hessian: "HessianOperator | None" = None) -> "StencilJacobian":
+        """Jacobian over the samples idx; pass the matching ``HessianOperator.select`` to
+        share its gathered tables."""
+        H = hessian if hessian is not None else HessianOperator(self.model, self.op, self._keep).select(idx)
+        return StencilJacobian(H.model, H.op, H._keep)
 
     def _apply_cols(self, W: torch.Tensor) -> torch.Tensor:
         B, n, t = W.shape
