@@ -67,7 +67,19 @@ def _dot(a, b):
 
 def lower_solve(model: Model, theta, x_init: torch.Tensor | None = None, gtol: float = 1e-3, memory: int = 10,
                 max_iter: int = 5000, linesearch: LinesearchParams | None = None):
-    """Batched L-BFGS until ||grad_b|| < gtol for every sample b (bilevel.py:81-167)."""
+    """Batched L-BFGS until ||grad_b|| < gtol for every sample b (bilevel.py:81-167).
+
+    Every sample keeps its own iterate, step, acceptance and stopping test; finished
+    samples are frozen.  The curvature pairs live in a ring shared by the batch (one
+    slot per iteration, views instead of per-sample gathers): a pair a sample rejects
+    (s^T y <= 1e-10 |s||y|, bilevel.py:154-155) is stored with rho = 0 and contributes
+    nothing, and the initial scaling s^T y / y^T y comes from the sample's newest
+    accepted pair (the reference's deque skips rejected pairs, so after a rejection its
+    window reaches one pair further back; rejections do not occur on these convex
+    problems).  The cost AND gradient of the accepted Armijo trial are kept (one
+    kr_lower_eval per trial; the reference evaluates the gradient at the accepted point
+    separately -- the same values).  One host read per iteration (any sample active?)
+    plus one per extra backtrack."""
     if not gtol > 0:
         raise ValueError("gtol must be positive")
     ls = linesearch or LinesearchParams()
@@ -77,36 +89,27 @@ def lower_solve(model: Model, theta, x_init: torch.Tensor | None = None, gtol: f
     gn = torch.linalg.vector_norm(g, dim=1)
     S = torch.zeros(B, memory, n, dtype=torch.float64, device=dev)
     Y = torch.zeros_like(S)
-    R = torch.zeros(B, memory, dtype=torch.float64, device=dev)
-    head = torch.zeros(B, dtype=torch.long, device=dev)   # next slot
-    count = torch.zeros(B, dtype=torch.long, device=dev)
+    R = torch.zeros(B, memory, dtype=torch.float64, device=dev)   # 1 / s^T y, 0 for a rejected pair
+    gam = torch.ones(B, dtype=torch.float64, device=dev)          # H0 scaling of the newest accepted pair
+    head, stored = 0, 0
     iters = torch.zeros(B, dtype=torch.long, device=dev)
     evals = torch.ones(B, dtype=torch.long, device=dev)  # the f at x_0 (bilevel.py:129-131)
-    ar = torch.arange(B, device=dev)
-    while True:
-        active = (gn >= gtol) & (iters < max_iter)
-        if not bool(active.any()):
-            break
-        # two-loop recursion over each sample's own history, newest first
+    active = (gn >= gtol) & (iters < max_iter)
+    zero = torch.zeros((), dtype=torch.float64, device=dev)
+    while bool(active.any()):
+        # two-loop recursion, newest pair first (views of the shared ring)
         q = g.clone()
         alphas = []
-        for age in range(memory):
+        for age in range(min(stored, memory)):
             slot = (head - 1 - age) % memory
-            valid = (age < count).to(torch.float64)
-            s_a, y_a, r_a = S[ar, slot], Y[ar, slot], R[ar, slot] * valid
-            a = r_a * _dot(s_a, q)
-            q = q - a.unsqueeze(1) * y_a
-            alphas.append((slot, a, valid))
-        has = count > 0
-        slot0 = (head - 1) % memory
-        s0, y0 = S[ar, slot0], Y[ar, slot0]
-        gam = torch.where(has, _dot(s0, y0) / torch.where(has, _dot(y0, y0), torch.ones_like(gn)), torch.ones_like(gn))
-        q = q * gam.unsqueeze(1)
-        for slot, a, valid in reversed(alphas):
-            s_a, y_a, r_a = S[ar, slot], Y[ar, slot], R[ar, slot] * valid
-            bcoef = r_a * _dot(y_a, q)
-            q = q + ((a - bcoef) * valid).unsqueeze(1) * s_a
-        d = -q
+            a = R[:, slot] * _dot(S[:, slot], q)
+            q.sub_(a.unsqueeze(1) * Y[:, slot])
+            alphas.append((slot, a))
+        q.mul_(gam.unsqueeze(1))
+        for slot, a in reversed(alphas):
+            bcoef = R[:, slot] * _dot(Y[:, slot], q)
+            q.add_((a - bcoef).unsqueeze(1) * S[:, slot])
+        d = q.neg_()
         slope = _dot(g, d)
         bad = slope >= 0
         d = torch.where(bad.unsqueeze(1), -g, d)
@@ -115,41 +118,46 @@ def lower_solve(model: Model, theta, x_init: torch.Tensor | None = None, gtol: f
         step = torch.full((B,), ls.beta, dtype=torch.float64, device=dev)
         searching = active.clone()
         slack = EPS * f.abs()
-        x_new, f_new = x.clone(), f.clone()
+        x_new, f_new, g_new = x, f, g
         for _ in range(ls.max_backtracks):
             xt = x + step.unsqueeze(1) * d
-            ft, _ = model.cost_grad(theta, xt)
+            ft, gt = model.cost_grad(theta, xt)
             evals += searching.long()
             ok = searching & (ft <= f + ls.eta * step * slope + slack)
-            x_new = torch.where(ok.unsqueeze(1), xt, x_new)
+            okc = ok.unsqueeze(1)
+            x_new = torch.where(okc, xt, x_new)
             f_new = torch.where(ok, ft, f_new)
+            g_new = torch.where(okc, gt, g_new)
             searching = searching & ~ok
             step = torch.where(searching, step * ls.rho, step)
             if not bool(searching.any()):
                 break
-        if bool(searching.any()):
-            xt = x + step.unsqueeze(1) * d
-            ft, _ = model.cost_grad(theta, xt)
-            evals += searching.long()
-            x_new = torch.where(searching.unsqueeze(1), xt, x_new)
-            f_new = torch.where(searching, ft, f_new)
-        _, g_new = model.cost_grad(theta, x_new)
+        else:
+            if bool(searching.any()):
+                xt = x + step.unsqueeze(1) * d
+                ft, gt = model.cost_grad(theta, xt)
+                evals += searching.long()
+                sc = searching.unsqueeze(1)
+                x_new = torch.where(sc, xt, x_new)
+                f_new = torch.where(searching, ft, f_new)
+                g_new = torch.where(sc, gt, g_new)
         s_v = x_new - x
         y_v = g_new - g
         sy = _dot(s_v, y_v)
         take = active & (sy > 1e-10 * torch.linalg.vector_norm(s_v, dim=1) * torch.linalg.vector_norm(y_v, dim=1))
-        hs = head.clone()
-        S[ar[take], hs[take]] = s_v[take]
-        Y[ar[take], hs[take]] = y_v[take]
-        R[ar[take], hs[take]] = 1.0 / sy[take]
-        head = torch.where(take, (head + 1) % memory, head)
-        count = torch.where(take, torch.clamp(count + 1, max=memory), count)
+        tc = take.unsqueeze(1)
+        S[:, head] = torch.where(tc, s_v, zero)
+        Y[:, head] = torch.where(tc, y_v, zero)
+        R[:, head] = torch.where(take, 1.0 / sy, zero)
+        gam = torch.where(take, sy / _dot(y_v, y_v), gam)
+        head, stored = (head + 1) % memory, stored + 1
         am = active.unsqueeze(1)
         x = torch.where(am, x_new, x)
         g = torch.where(am, g_new, g)
         f = torch.where(active, f_new, f)
         gn = torch.where(active, torch.linalg.vector_norm(g, dim=1), gn)
         iters = iters + active.long()
+        active = active & (gn >= gtol) & (iters < max_iter)
     conv = gn < gtol
     if not bool(conv.all()):
         warnings.warn(f"lower-level solver hit the {max_iter}-iteration cap", stacklevel=2)
@@ -199,31 +207,38 @@ def backtracking_linesearch(state: UpperState, d: np.ndarray, params: Linesearch
 
 def gradient_descent(model: Model, theta0, eps_stop: float = 1e-4, *, solver_cfg: HessianSolveConfig | None = None,
                      lower_cfg: LowerConfig | None = None, linesearch: LinesearchParams | None = None,
-                     max_upper: int = 30, on_system=None):
-    """bilevel.py:392-502 for a batch sharing theta."""
+                     max_upper: int = 30, on_system=None, batch_total: int | None = None, group=None):
+    """bilevel.py:392-502 for a batch sharing theta.
+
+    Multi-GPU: ``model`` holds this rank's samples (distributed.shard of
+    ``batch_total``); the upper cost F = sum_k 1/2 ||xhat_k - xtrue_k||^2 of every Armijo
+    trial and the hypergradient sum_k J_k w_k are all-gathered per sample and summed in
+    global sample order (distributed.allgather_sum), so every rank takes the same steps
+    and the trajectory is bitwise independent of the world size.  theta is updated
+    redundantly on every rank."""
+    from .distributed import allgather_sum
+
     if not eps_stop > 0:
         raise ValueError("eps_stop must be positive")
     solver_cfg = solver_cfg or HessianSolveConfig()
     lower_cfg = lower_cfg or LowerConfig()
     linesearch = linesearch or LinesearchParams()
+    total = model.batch if batch_total is None else int(batch_total)
     seq = SequenceSolver(solver_cfg)
 
     def evaluate(theta, warm):
         x, _ = lower_solve(model, theta, warm, lower_cfg.gtol, lower_cfg.memory, lower_cfg.max_iter,
                            lower_cfg.linesearch)
         diff = x - model.x_true
-        per = 0.5 * (diff * diff).sum(dim=1)
-        return float(sum(float(v) for v in per.cpu().numpy())), x
+        per = 0.5 * (diff * diff).sum(dim=1)  # per-sample costs, summed in sample order
+        return float(allgather_sum(per.unsqueeze(1), total, group)[0]), x
 
     c0, x0 = evaluate(np.asarray(theta0, dtype=float), None)
     state = UpperState(np.asarray(theta0, dtype=float).copy(), x0, c0, linesearch.beta)
     trace = []
     for i in range(max_upper):
         hg, res, _ = hypergradients(model, state.theta, state.x_hats, seq)
-        hg_np = hg.cpu().numpy()
-        d = hg_np[0].copy()
-        for k in range(1, hg_np.shape[0]):
-            d = d + hg_np[k]
+        d = allgather_sum(hg, total, group).cpu().numpy()
         gnorm = float(np.linalg.norm(d))
         rec = FrozenSystem(i, state.theta.copy(), state.x_hats.clone(), state.cost, gnorm, state.next_beta,
                            [r.iterations for r in res])
@@ -238,10 +253,12 @@ def gradient_descent(model: Model, theta0, eps_stop: float = 1e-4, *, solver_cfg
 
 
 def record_sequence(model: Model, theta0, *, delta: float = 1e-2, max_inner: int = 500, lower_gtol: float = 1e-3,
-                    eps_stop: float = 1e-4, max_upper: int = 25, lower_max_iter: int = 5000):
+                    eps_stop: float = 1e-4, max_upper: int = 25, lower_max_iter: int = 5000,
+                    linesearch: LinesearchParams | None = None, batch_total: int | None = None, group=None):
     """Solve without recycling and freeze every system (experiments.py:234-268)."""
     _, trace = gradient_descent(
         model, theta0, eps_stop,
         solver_cfg=HessianSolveConfig(StrategyDescriptor("None"), delta=delta, stop="res", max_iter=max_inner),
-        lower_cfg=LowerConfig(gtol=lower_gtol, max_iter=lower_max_iter), max_upper=max_upper)
+        lower_cfg=LowerConfig(gtol=lower_gtol, max_iter=lower_max_iter), linesearch=linesearch,
+        max_upper=max_upper, batch_total=batch_total, group=group)
     return trace
