@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--strategy", default=STRATEGY)
     ap.add_argument("--delta", type=float, default=DELTA)
+    ap.add_argument("--sequence", default="solved",
+                    help="solved (lower-level minimisers along the synthetic theta path, cached under .seqcache/), "
+                         "recorded (device-recorded bilevel run), synthetic, or a krecycle-sequence-v1 directory")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=40.0, help="seconds of timed CPU work (cpu_baseline)")
@@ -222,6 +225,96 @@ def workload_text(name, cfg, count, total, args):
 # ---------------------------------------------------------------------------
 
 
+# ---------------------------------------------------------------------------
+# The workload's frozen sequence (the replay protocol's input, experiments.py:390-463).
+# "solved" (default): the synthetic theta path (problems.synthetic_sequence: theta_0 plus a
+# small seeded drift per system) with x_hat_i = the device L-BFGS minimiser of every sample's
+# lower problem at theta_i (sequence.solve_path, gradient norm SOLVE_GTOL, warm-started) --
+# real lower-level solutions, so H and g = x_hat - x_true are what a bilevel run sees.  It is
+# made for the WHOLE batch once per box on cuda:0, cached as a krecycle-sequence-v1 directory
+# under .seqcache/ and loaded by every arm and rank (identical inputs for the GPU arm, the
+# cpu_baseline leg and --impl reference).  "recorded": the reference's record_sequence
+# pattern (device gradient descent with Armijo line searches; slow at these configs, whose
+# hypergradients are O(1e4) at theta_0).  "synthetic": xhat = x_true + a smooth 3 % field.
+
+SOLVE_GTOL, SEQ_SYSTEMS = 1e-6, 16
+REC_GTOL, REC_BETA0, REC_DELTA = 1e-6, 1e-5, 1e-8
+
+
+def sequence_dir(name: str, kind: str, systems: int) -> Path:
+    tag = f"gtol{SOLVE_GTOL:g}" if kind == "solved" else f"gtol{REC_GTOL:g}_beta{REC_BETA0:g}"
+    return ROOT / ".seqcache" / f"{name}_{kind}_sys{systems}_{tag}"
+
+
+def ensure_sequence(args, systems: int):
+    """Path of the workload's frozen sequence (made on cuda:0 if not cached); None for the
+    synthetic sequence."""
+    if args.sequence == "synthetic":
+        return None
+    if args.sequence not in ("solved", "recorded"):
+        return Path(args.sequence)
+    systems = max(systems, SEQ_SYSTEMS)
+    path = sequence_dir(args.config, args.sequence, systems)
+    if (path / "manifest.json").exists():
+        return path
+    import torch
+
+    from paper_2412_08264_b200.lower import LinesearchParams
+    from paper_2412_08264_b200.problems import CONFIGS, sample_arrays, synthetic_sequence
+    from paper_2412_08264_b200.sequence import record, save_sequence, solve_path
+
+    cfg = CONFIGS[args.config]
+    t0 = time.perf_counter()
+    with torch.cuda.device(0):
+        if args.sequence == "solved":
+            thetas, _ = synthetic_sequence(cfg, sample_arrays(cfg, 0)[0][None], systems, seed=1234)
+            seq = solve_path(cfg, thetas, lower_gtol=SOLVE_GTOL)
+        else:
+            seq = record(cfg, systems, lower_gtol=REC_GTOL, delta=REC_DELTA,
+                         linesearch=LinesearchParams(beta=REC_BETA0))
+    tmp = path.with_name(path.name + f".tmp{os.getpid()}")
+    save_sequence(seq, tmp)
+    if not path.exists():
+        os.replace(tmp, path)
+    print(f"bench: {args.sequence} sequence of {args.config}, {systems} systems, made in "
+          f"{time.perf_counter() - t0:.1f} s -> {path}", file=sys.stderr, flush=True)
+    return path
+
+
+def sequence_text(path) -> str:
+    if path is None:
+        return "synthetic frozen sequence (problems.synthetic_sequence: theta drift, xhat = x_true + smooth field)"
+    rel = path.relative_to(ROOT) if str(path).startswith(str(ROOT)) else path
+    if "_solved_" in path.name:
+        return (f"frozen sequence {rel} (krecycle-sequence-v1): the synthetic theta path with xhat_i = the "
+                f"device L-BFGS minimiser of every sample's lower problem at theta_i (gradient norm "
+                f"{SOLVE_GTOL:g}, warm-started; sequence.solve_path)")
+    return (f"recorded frozen sequence {rel} (krecycle-sequence-v1; recycling-free bilevel run recorded on "
+            f"the device: batched L-BFGS to gradient norm {REC_GTOL:g}, Armijo upper steps from theta_0 with "
+            f"initial step {REC_BETA0:g}, hypergradients by RMINRES to residual {REC_DELTA:g})")
+
+
+def load_systems(path, first: int, count: int, systems: int):
+    """(thetas, xhats [systems][count][n]) of samples [first, first + count) of a recorded sequence
+    (only those samples' rows are read)."""
+    import json as _json
+
+    man = _json.loads((Path(path) / "manifest.json").read_text())
+    B, n = int(man["batch"]), int(man["n"])
+    if man["num_systems"] < systems:
+        raise ValueError(f"{path}: {man['num_systems']} systems recorded, {systems} needed")
+    if first + count > B:
+        raise ValueError(f"{path}: samples [{first}, {first + count}) beyond its batch of {B}")
+    arr = Path(path) / "arrays"
+    thetas, xhats = [], []
+    for m in man["systems"][:systems]:
+        tag = f"{m['index']:03d}"
+        thetas.append(np.fromfile(arr / f"theta_{tag}.f64", dtype="<f8"))
+        xhats.append(np.fromfile(arr / f"xhat_{tag}.f64", dtype="<f8", count=count * n,
+                                 offset=first * n * 8).reshape(count, n))
+    return thetas, xhats
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -242,7 +335,18 @@ def run_ours(args):
     n = model.n
     steps_total = args.warmup + args.steps
     xt = model.x_true.cpu().numpy()
-    thetas, xhats_np = synthetic_sequence(cfg, xt, steps_total, seed=1234, first=first)
+    # the frozen sequence: recorded once (rank 0 records the whole batch; the others wait)
+    seq_path = None
+    if rank == 0:
+        seq_path = ensure_sequence(args, steps_total)
+    if world > 1:
+        obj = [None if seq_path is None else str(seq_path)]
+        dist.broadcast_object_list(obj, src=0)
+        seq_path = None if obj[0] is None else Path(obj[0])
+    if seq_path is None:
+        thetas, xhats_np = synthetic_sequence(cfg, xt, steps_total, seed=1234, first=first)
+    else:
+        thetas, xhats_np = load_systems(seq_path, first, B, steps_total)
     xhats = [torch.as_tensor(x, device="cuda") for x in xhats_np]
     solver_cfg = HessianSolveConfig.from_strategy(args.strategy, recycle_dim=cfg.recycle_dim, delta=args.delta,
                                                   method=cfg.method, max_iter=cfg.max_iter)
@@ -366,7 +470,7 @@ def run_ours(args):
                        "samples_total": total, "samples_per_gpu": B, "image": cfg.size,
                        "recycle_dim": cfg.recycle_dim, "max_iter": cfg.max_iter, "strategy": args.strategy,
                        "delta": args.delta, "krylov": cfg.method,
-                       "sequence": "synthetic frozen sequence (problems.synthetic_sequence)",
+                       "sequence": sequence_text(seq_path),
                        "l2": "flushed (256 MB write) before every timed step",
                        "parallelism": f"sample-sharded dp{world} ({SHARDING.get(args.config, 'weak')})"},
             "step_ms": [round(x, 3) for x in step_ms],
@@ -435,7 +539,7 @@ def hvp_fp64_roofline(model, theta, xhat, cfg, cols: int = 64):
 # each one imports numpy single-threaded.
 
 
-def _cpu_worker(conn, name, k, strategy, delta):
+def _cpu_worker(conn, name, k, strategy, delta, seq_path=None):
     """Owns sample k's oracle SequenceSolver; runs the systems it is sent, returns wall times."""
     from oracle import cpu_bilevel as ob
     from oracle import cpu_imaging as im
@@ -458,7 +562,10 @@ def _cpu_worker(conn, name, k, strategy, delta):
             break
         i, steps = msg
         if thetas is None or len(thetas) < steps:
-            thetas, xs = synthetic_sequence(cfg, x_true[None], steps, seed=1234, first=k)
+            if seq_path is None:
+                thetas, xs = synthetic_sequence(cfg, x_true[None], steps, seed=1234, first=k)
+            else:
+                thetas, xs = load_systems(seq_path, k, 1, steps)
             xhats = [x[0] for x in xs]
         t0 = time.perf_counter()
         H = im.hessian(model, thetas[i], xhats[i])
@@ -468,7 +575,7 @@ def _cpu_worker(conn, name, k, strategy, delta):
         conn.send((res.iterations, time.perf_counter() - t0))
 
 
-def _spawn_workers(name, samples, strategy, delta):
+def _spawn_workers(name, samples, strategy, delta, seq_path=None):
     import multiprocessing as mp
 
     for v in THREAD_ENV:
@@ -477,7 +584,7 @@ def _spawn_workers(name, samples, strategy, delta):
     conns, procs = [], []
     for k in samples:
         parent, child = ctx.Pipe()
-        pr = ctx.Process(target=_cpu_worker, args=(child, name, k, strategy, delta), daemon=True)
+        pr = ctx.Process(target=_cpu_worker, args=(child, name, k, strategy, delta, seq_path), daemon=True)
         pr.start()
         conns.append(parent)
         procs.append(pr)
@@ -486,10 +593,10 @@ def _spawn_workers(name, samples, strategy, delta):
     return conns, procs
 
 
-def _run_cpu(name, samples, strategy, delta, steps_cap, budget):
+def _run_cpu(name, samples, strategy, delta, steps_cap, budget, seq_path=None):
     """System 0 (cold, untimed), then recycled systems 1, 2, ... on every worker in parallel
     until steps_cap systems or `budget` seconds of timed work (at least one system)."""
-    conns, procs = _spawn_workers(name, samples, strategy, delta)
+    conns, procs = _spawn_workers(name, samples, strategy, delta, seq_path)
     total_systems = steps_cap + 1
 
     def one(i):
@@ -516,7 +623,9 @@ def _run_cpu(name, samples, strategy, delta, steps_cap, budget):
 def cpu_baseline(args):
     """The oracle port on ONE host core (a spawned single-threaded process), sample 0:
     system 0 untimed, then recycled systems until --cpu-budget seconds."""
-    done, dt, its = _run_cpu(args.config, [0], args.strategy, args.delta, max(args.steps, 1), args.cpu_budget)
+    seq_path = ensure_sequence(args, args.warmup + args.steps)
+    done, dt, its = _run_cpu(args.config, [0], args.strategy, args.delta, max(args.steps, 1), args.cpu_budget,
+                             seq_path)
     return {"value": done / dt, "unit": "hypergradients/s", "cores": 1, "kind": "port",
             "sample": f"sample 0, recycled systems 1..{done} after an untimed cold system 0 ({done} hypergradients, "
                       f"{dt:.1f} s, iterations {its}); single-threaded BLAS in a spawned process"}
@@ -537,8 +646,9 @@ def run_reference(args):
     _, count, _ = samples_for(args.config, cfg, 1, 0)
     cores = len(os.sched_getaffinity(0))
     nproc = max(1, min(cores, count))
+    seq_path = ensure_sequence(args, args.warmup + args.steps)
     done, dt, its = _run_cpu(args.config, list(range(nproc)), args.strategy, args.delta, max(args.steps, 1),
-                             args.ref_budget)
+                             args.ref_budget, seq_path)
     value = nproc * done / dt
     line = {
         "metric": METRIC, "impl": "reference",
@@ -550,7 +660,8 @@ def run_reference(args):
                    "bounded": f"samples 0..{nproc - 1} ({nproc} of {count}; one process per core), "
                               f"recycled systems 1..{done} timed after an untimed cold system 0 "
                               f"(--steps {args.steps}, budget {args.ref_budget:.0f} s)",
-                   "strategy": args.strategy, "delta": args.delta, "iterations_mean": float(np.mean(its))},
+                   "strategy": args.strategy, "delta": args.delta, "iterations_mean": float(np.mean(its)),
+                   "sequence": sequence_text(seq_path)},
         "cpu_baseline": {"value": value, "unit": "hypergradients/s", "cores": nproc, "kind": "port",
                          "sample": f"{nproc} samples x {done} recycled systems, one single-threaded process per core"},
         "e2e": {"value": value, "unit": "hypergradients/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

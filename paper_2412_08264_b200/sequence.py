@@ -34,7 +34,8 @@ import torch
 from .operators import Model, as_device
 from .problems import DeblurConfig, gaussian_taps, make_batch
 
-__all__ = ["FORMAT_NAME", "FrozenSequence", "FrozenSystem", "load_sequence", "record", "save_sequence"]
+__all__ = ["FORMAT_NAME", "FrozenSequence", "FrozenSystem", "load_sequence", "record", "save_sequence",
+           "solve_path"]
 
 FORMAT_NAME = "krecycle-sequence-v1"
 
@@ -159,7 +160,7 @@ def load_sequence(in_dir) -> FrozenSequence:
 
 def record(cfg: DeblurConfig, systems: int, *, first: int = 0, count: int | None = None, lower_gtol: float = 1e-8,
            delta: float = 1e-2, max_inner: int | None = None, lower_max_iter: int = 20000, device=None,
-           theta0=None, eps_stop: float = 0.0) -> FrozenSequence:
+           theta0=None, eps_stop: float = 0.0, linesearch=None) -> FrozenSequence:
     """Record ``systems`` upper-level systems of the recycling-free bilevel run
     (experiments.py:234-268): device L-BFGS to ``lower_gtol``, Armijo upper steps,
     hypergradients with RMINRES (no recycling, residual rule ``delta``)."""
@@ -169,7 +170,8 @@ def record(cfg: DeblurConfig, systems: int, *, first: int = 0, count: int | None
     model = make_batch(cfg, first, count, device=device)
     th0 = default_theta0(cfg) if theta0 is None else np.asarray(theta0, dtype=float)
     trace = record_sequence(model, th0, delta=delta, max_inner=max_inner or cfg.max_iter, lower_gtol=lower_gtol,
-                            eps_stop=max(eps_stop, 1e-300), max_upper=systems, lower_max_iter=lower_max_iter)
+                            eps_stop=max(eps_stop, 1e-300), max_upper=systems, lower_max_iter=lower_max_iter,
+                            linesearch=linesearch)
     recs = []
     for i, r in enumerate(trace):
         nxt = trace[i + 1].theta if i + 1 < len(trace) else None
@@ -178,6 +180,34 @@ def record(cfg: DeblurConfig, systems: int, *, first: int = 0, count: int | None
                                  r.beta_init, None if nxt is None else np.asarray(nxt, dtype=float).copy()))
     seq = FrozenSequence(cfg, first, model.x_true.cpu().numpy().copy(), model.y.cpu().numpy().copy(), recs,
                          {"recorder": "paper_2412_08264_b200.lower.record_sequence (device L-BFGS + Armijo GD)",
-                          "lower_gtol": lower_gtol, "delta": delta})
+                          "lower_gtol": lower_gtol, "delta": delta,
+                          "beta0": None if linesearch is None else linesearch.beta})
+    seq.validate()
+    return seq
+
+
+def solve_path(cfg: DeblurConfig, thetas, *, first: int = 0, count: int | None = None, lower_gtol: float = 1e-6,
+               lower_max_iter: int = 5000, device=None) -> FrozenSequence:
+    """Frozen systems at a prescribed theta path: x_hat_i = the device L-BFGS minimiser of
+    the lower problem at theta_i (bilevel.py:81-167, to gradient norm ``lower_gtol``),
+    warm-started from x_hat_{i-1}.  The systems are real lower-level solutions (H and
+    g = x_hat - x_true as a bilevel run produces them); only the upper-level path is
+    prescribed instead of taken by gradient descent (one lower solve per system instead
+    of a line search of them)."""
+    from .lower import lower_solve
+
+    model = make_batch(cfg, first, count, device=device)
+    recs, x = [], None
+    for i, th in enumerate(thetas):
+        th = np.asarray(th, dtype=float)
+        x, st = lower_solve(model, th, x, gtol=lower_gtol, max_iter=lower_max_iter)
+        diff = x - model.x_true
+        cost = float((0.5 * (diff * diff).sum(dim=1)).sum())
+        recs.append(FrozenSystem(i, th.copy(), x.detach().cpu().numpy().copy(), [int(v) for v in st.iterations],
+                                 cost, float("nan"), float("nan"),
+                                 np.asarray(thetas[i + 1], dtype=float).copy() if i + 1 < len(thetas) else None))
+    seq = FrozenSequence(cfg, first, model.x_true.cpu().numpy().copy(), model.y.cpu().numpy().copy(), recs,
+                         {"recorder": "sequence.solve_path (device L-BFGS minimiser at each theta of a prescribed "
+                                      "path; iterations = L-BFGS iterations)", "lower_gtol": lower_gtol})
     seq.validate()
     return seq
