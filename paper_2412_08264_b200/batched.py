@@ -354,15 +354,19 @@ def orth_rows(A: torch.Tensor, dims: list[int]):
     return W, dims, torch.ones_like(ok)
 
 
-def supports(strategy) -> bool:
+def supports(strategy, native: bool = False) -> bool:
     """Strategies the whole-batch update computes to the reference's accuracy.
 
     RGen takes its vectors from the eigenpairs of Q1^T Q1 (alpha^2), which are as
     accurate as the reference's SVD of Q1 for alpha near 1 -- the largest mu,
     size L -- but square the gaps between small alpha (sizes S, M); those stay on
-    the per-sample SVD path.  Ritz uses eigh(W^T H W) exactly as the reference."""
+    the per-sample SVD path.  Ritz uses eigh(W^T H W) exactly as the reference.
+    Harmonic Ritz (harmonic_ritz_select, recycling.py:239-272) runs in the native
+    orchestrator only (Cholesky reduction of the pencil, kr_recycle_update)."""
     if strategy.placement != "outer":
         return False
+    if strategy.vec_type == "HRitz":
+        return native
     return strategy.vec_type == "Ritz" or (strategy.vec_type == "RGen" and strategy.size == "L")
 
 
@@ -384,8 +388,8 @@ def recycle_update(strategy, s: int, H, J, bases, recycles, reuse_products: bool
     from .recycling import RecycleSpace
     from .stopping import NscData
 
-    if not supports(strategy):
-        raise ValueError(f"the batched recycle update covers outer RGen-L / Ritz, not {strategy}")
+    if not supports(strategy, native=True):
+        raise ValueError(f"the batched recycle update covers outer RGen-L / Ritz / HRitz, not {strategy}")
     B = len(bases)
     n = H.dim
     k = [0 if V is None else int(V.shape[1]) for V in bases]
@@ -540,8 +544,8 @@ def recycle_update_native(strategy, s: int, H, J, bases, recycles, reuse_product
     from .recycling import RecycleSpace
     from .stopping import NscData
 
-    if not supports(strategy):
-        raise ValueError(f"the batched recycle update covers outer RGen-L / Ritz, not {strategy}")
+    if not supports(strategy, native=True):
+        raise ValueError(f"the batched recycle update covers outer RGen-L / Ritz / HRitz, not {strategy}")
     B = len(bases)
     n = H.dim
     k = [0 if V is None else int(V.shape[1]) for V in bases]
@@ -551,13 +555,15 @@ def recycle_update_native(strategy, s: int, H, J, bases, recycles, reuse_product
     if T == 0 or s == 0:
         return [RecycleSpace.empty(n) for _ in range(B)]
     if T > NATIVE_TMAX or s > T:
+        if strategy.vec_type == "HRitz":  # the torch batched path has no harmonic Ritz: per-sample path
+            return [None] * B
         return recycle_update(strategy, s, H, J, bases, recycles, reuse_products)
     dev = H.model.y.device if getattr(H, "model", None) is not None else bases[0].device
     vptr, ldv, bsv, vkeep = _uniform_rows(list(bases), n, dev)
     uptr, ldu, bsu, ukeep = _uniform_rows([None if r is None else r.U for r in recycles], n, dev)
     a = _lib.KrRecycleArgs()
     a.batch, a.T, a.s = B, T, s
-    a.vec_type = 1 if strategy.vec_type == "RGen" else 0
+    a.vec_type = {"Ritz": 0, "RGen": 1, "HRitz": 2}[strategy.vec_type]
     a.size_code = SIZE_CODES[strategy.size]
     a.side = {"R": 0, "L": 1, "M": 2}.get(strategy.side or "R", 0)
     a.reuse_products = int(reuse_products)

@@ -204,7 +204,7 @@ class SequenceSolver:
     def _batched(self, hessian, jac) -> bool:
         """Whether the whole-batch recycle update (batched.recycle_update) applies."""
         st = self.cfg.strategy
-        if not self.batched_update or not batched_supports(st):
+        if not self.batched_update or not batched_supports(st, native=self.native_update):
             return False
         if not isinstance(hessian, HessianOperator) or isinstance(hessian, DenseOperator):
             return False

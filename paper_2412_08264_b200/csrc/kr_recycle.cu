@@ -600,7 +600,7 @@ int64_t workspace_doubles(const kr_op& op, const kr_recycle_args& a) {
   const int64_t P = p + T;
   int64_t w = 0;
   w += 2 * B * T * n;                                   // A, tmpQ
-  w += 24 * (B * T * T + 4 * B + 64);                   // T x T factors, Grams, Ht, Hs, Mq, M, Q_R
+  w += 30 * (B * T * T + 4 * B + 64);                   // T x T factors, Grams, Ht, Hs, Mq, M, Q_R (+ harmonic pencil)
   w += 5 * B * T * P;                                   // Jt, S, QS, CholQR tmp
   w += 8 * B * s * T + 2 * B * s * P;                   // Z, X, coeffs, VH mu, Y, extremes
   w += 4 * B * s * n + 8 * (B * s * s + 4 * B + 64);    // cand, HU, CholQR tmp; prepare factors
@@ -676,7 +676,8 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
   const int64_t n = op_n(*op);
   KR_CHECK_ARG(op->batch == B, "operator batch must equal args.batch");
   KR_CHECK_ARG(T >= 1 && T <= RC_TMAX && s >= 1 && s <= T, "need 1 <= s <= T <= KR_TMAX");
-  KR_CHECK_ARG(a->vec_type == 0 || (a->vec_type == 1 && a->size_code == 1), "vec_type: Ritz, or RGen with size L");
+  KR_CHECK_ARG(a->vec_type == 0 || a->vec_type == 2 || (a->vec_type == 1 && a->size_code == 1),
+               "vec_type: Ritz, harmonic Ritz, or RGen with size L");
   KR_CHECK_ARG(a->vec_type == 0 || op->reg_kind != KR_REG_NONE, "RGen needs a mixed Jacobian");
   KR_CHECK_ARG(work && work_len >= workspace_doubles(*op, *a), "kr_recycle workspace too small");
   const int p = op->reg_kind == KR_REG_TV ? 1 : op->num_filters * (1 + op->ksize * op->ksize);
@@ -927,13 +928,54 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
   double* Xc = nullptr;
   double* VHmu = nullptr;
   std::vector<int32_t> bad(B, 0);
-  if (a->vec_type == 0) {  // Ritz: eigenpairs of sym(W^T H W)
+  if (a->vec_type == 0 || a->vec_type == 2) {
+    // Ritz (ritz_select, recycling.py:226-236): eigenpairs of sym(W^T H W).
+    // Harmonic Ritz (harmonic_ritz_select, :239-272): the pencil A rho = theta B rho with
+    // A = sym((HW)^T HW), B = sym((HW)^T W) = sym(W^T H W), reduced by B's Cholesky factor
+    // (F = L^-1 D^-1, F B F^T = I): M = F A F^T, rho = F^T z, selection by |theta| (theta > 0
+    // for SPD H), candidates W rho / ||W rho|| (= rho / ||rho||, W orthonormal).  A
+    // near-singular B (the reference's null-direction branch) is declined to the
+    // per-sample path.
     double* Hs = c.take((int64_t)B * T * T);
     sym_and_s_kernel<<<dim3(T, B), 256, 0, c.st>>>(Ht, nullptr, 0, T, Hs, nullptr);
     Ht = Hs;
+    double* Msel = Ht;
+    Factor fb;
+    if (a->vec_type == 2) {
+      double* Ag = c.take((int64_t)B * T * T);
+      KR_TRY(gram(c, HW, HW, B, T, n, Ag));
+      double* As = c.take((int64_t)B * T * T);
+      sym_and_s_kernel<<<dim3(T, B), 256, 0, c.st>>>(Ag, nullptr, 0, T, As, nullptr);
+      fb = new_factor(c, B, T);
+      KR_TRY(chol(c, Ht, d_td, B, T, true, nullptr, fb));
+      double* FA = c.take((int64_t)B * T * T);
+      double* Mh = c.take((int64_t)B * T * T);
+      KR_TRY(rows_mul(c, fb.F, (int64_t)T * T, As, T, (int64_t)T * T, FA, T, (int64_t)T * T, T, T, T, B));
+      const double one = 1.0, zero = 0.0;  // Mh = F (F A)^T = F A F^T (symmetric)
+      KR_TRY(cublas_check(cublasDgemmStridedBatched(c.h, CUBLAS_OP_T, CUBLAS_OP_N, T, T, T, &one, fb.F, T,
+                                                    (int64_t)T * T, FA, T, (int64_t)T * T, &zero, Mh, T,
+                                                    (int64_t)T * T, B),
+                          "kr_recycle harmonic congruence"));
+      Msel = Mh;
+    }
     const int64_t el = kr_syev_select_workspace(B, T);
-    KR_TRY(hi_stream().run(c.st, [&](cudaStream_t st) { return kr_syev_select(Ht, T, (int64_t)T * T, d_td, B, T, a->size_code, s, nullptr, 0, coeffs, T,
+    double* zc = a->vec_type == 2 ? c.take((int64_t)B * s * T) : coeffs;
+    KR_TRY(hi_stream().run(c.st, [&](cudaStream_t st) { return kr_syev_select(Msel, T, (int64_t)T * T, d_td, B, T, a->size_code, s, nullptr, 0, zc, T,
                           (int64_t)s * T, d_ns, c.take(el), el, st); }));
+    if (a->vec_type == 2) {
+      KR_TRY(rows_mul(c, zc, (int64_t)s * T, fb.F, T, (int64_t)T * T, coeffs, T, (int64_t)s * T, s, T, T, B));
+      normalize_rows_kernel<<<dim3(s, B), 256, 0, c.st>>>(coeffs, s, T);
+      std::vector<int32_t> bi;
+      std::vector<double> bst;
+      KR_TRY(Fetch().add(bi, fb.info, B).add(bst, fb.stats, 4 * B).run(c));
+      for (int b = 0; b < B; ++b) {
+        const double r = bst[4 * b + 1] > 0.0 ? bst[4 * b] / bst[4 * b + 1] : 0.0;
+        if (t[b] > 0 && !(bi[b] < 0 && r * r > 10.0 * RANK_TOL)) {
+          status[b] = 1;  // (near-)singular pencil: the reference restricts to B's non-null directions
+          if (debug) fprintf(stderr, "  sample %d declined: harmonic pencil B (info %d, pivot ratio %.3e)\n", b, bi[b], r);
+        }
+      }
+    }
   } else {
     // J W
     double* Jt = c.take((int64_t)B * T * p);

@@ -110,6 +110,47 @@ def test_declines_small_mu_selections():
     assert supports(S.parse("RGen-L(R)-NSC")) and supports(S.parse("Ritz-S")) and supports(S.parse("RGen-L(M)"))
     assert not supports(S.parse("RGen-S(L)")) and not supports(S.parse("RGen-M(R)"))
     assert not supports(S.parse("inner:RGen-L(R)")) and not supports(S.parse("HRitz-S"))
+    # harmonic Ritz: the native orchestrator only
+    assert supports(S.parse("HRitz-S"), native=True) and not supports(S.parse("inner:HRitz-S"), native=True)
+
+
+def _harmonic_keys(W, HW):
+    """|theta| of the pencil (HW)^T HW rho = theta (HW)^T W rho, ascending (recycling.py:239-272)."""
+    import scipy.linalg as sl
+
+    A = (HW.T @ HW).cpu().numpy()
+    Bm = (HW.T @ W).cpu().numpy()
+    vals = sl.eigh(0.5 * (A + A.T), 0.5 * (Bm + Bm.T), eigvals_only=True)
+    return torch.as_tensor(np.sort(np.abs(vals)))
+
+
+@pytest.mark.parametrize("strategy", ["HRitz-S", "HRitz-L", "HRitz-M"])
+def test_harmonic_ritz_native_matches_per_sample(strategy):
+    """Harmonic Ritz in the native orchestrator (Cholesky reduction of the pencil) against
+    the per-sample reference-semantics path (recycling.harmonic_ritz_select)."""
+    from paper_2412_08264_b200.batched import recycle_update_native
+    from paper_2412_08264_b200.recycling import _select_indices, build_candidate_basis, next_recycle
+
+    model, seq, H, J = _setup(strategy)
+    st = seq.cfg.strategy
+    got_all = recycle_update_native(st, seq.cfg.recycle_dim, H, J, seq._prev_basis, seq._prev_recycle)
+    for b in range(model.batch):
+        ref = next_recycle(st, h_current=H.sample(b), jac_current=J.sample(b), prev_basis=seq._prev_basis[b],
+                           prev_recycle=seq._prev_recycle[b], s=seq.cfg.recycle_dim)
+        got = got_all[b]
+        assert got is not None and got.dim == ref.dim
+        W = build_candidate_basis(seq._prev_basis[b], seq._prev_recycle[b].U).W
+        key = _harmonic_keys(W, H.sample(b).apply_matrix(W))
+        t, sdim = key.numel(), min(seq.cfg.recycle_dim, key.numel())
+        sel = set(_select_indices(t, sdim, st.size, "cpu").tolist())
+        posed = all(not ((i in sel) != (i + 1 in sel) and float(key[i + 1] - key[i]) <= 1e-6 * float(key.max()))
+                    for i in range(t - 1))
+        if posed:
+            assert torch.dist(_proj(got.C), _proj(ref.C)) <= 1e-8
+            assert torch.dist(_proj(got.U), _proj(ref.U)) <= 1e-8
+        assert torch.allclose(got.C.T @ got.C, torch.eye(got.dim, dtype=torch.float64, device="cuda"), atol=1e-13)
+        HU = H.sample(b).apply_matrix(got.U)
+        assert torch.dist(HU, got.C) <= 1e-10 * torch.linalg.norm(HU)
 
 
 @pytest.mark.parametrize("impl", ["python", "native"])
