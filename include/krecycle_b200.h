@@ -50,7 +50,7 @@ extern "C" {
 
 typedef struct CUstream_st* kr_stream_t; /* == cudaStream_t */
 
-#define KR_ABI_VERSION 3
+#define KR_ABI_VERSION 4
 
 /* Largest candidate width t = k_prev + s_prev of the small dense kernels and the recycle
  * update: BASELINE C5 with s = 80 and 500 iterations (t <= 580), with margin. */
@@ -225,9 +225,9 @@ int kr_gram(const double* A, const double* B, int64_t ld, int64_t bs, int32_t ba
             double* G, int64_t ldg, int64_t bsg, double* work, int64_t work_len, kr_stream_t stream);
 
 /* Whole-batch recycle update (recycling.py:386-465 next_recycle for every sample of
- * the batch at once; outer placement; RGen with size L -- rgen_select :316-359 +
- * gsvd_pair :275-313 -- or Ritz -- ritz_select :226-236; prepare_recycle
- * :362-383), orchestrated natively: candidate basis with the reference's pivoted-QR
+ * the batch at once; outer or inner placement; RGen with size L -- rgen_select :316-359 +
+ * gsvd_pair :275-313 -- Ritz -- ritz_select :226-236 -- or harmonic Ritz --
+ * harmonic_ritz_select :239-272; prepare_recycle :362-383), orchestrated natively: candidate basis with the reference's pivoted-QR
  * rank drop, H W / J W, the projected pencil, the selected eigenpairs, the new
  * (U, C) and the NSC block Z = W V_H diag(mu).  `op` is the operator of the
  * upcoming system with op->batch == batch.  Host arrays are marked HOST, the rest
@@ -236,7 +236,7 @@ int kr_gram(const double* A, const double* B, int64_t ld, int64_t bs, int32_t ba
  * breakdown in the GSVD / prepare QR), 2 empty recycle space. */
 typedef struct kr_recycle_args {
   int32_t batch, T, s;           /* samples; padded candidate count (<= 228); recycle dim */
-  int32_t vec_type;              /* 0 = Ritz, 1 = RGen */
+  int32_t vec_type;              /* 0 = Ritz, 1 = RGen, 2 = harmonic Ritz */
   int32_t size_code, side;       /* size S/L/M = 0/1/2 (RGen: L only); side R/L/M = 0/1/2 */
   int32_t reuse_products;        /* H U~ = (H W) X_sel instead of s more H v */
   const double* V;               /* previous Lanczos bases: sample b, column j at V + b*bs_v + j*ld_v */
@@ -255,6 +255,10 @@ typedef struct kr_recycle_args {
   int32_t* tdims;                /* HOST out [batch] candidates kept */
   int32_t* nsel;                 /* HOST out [batch] recycle dims */
   int32_t* status;               /* HOST out [batch] */
+  const kr_op* op_proj;          /* HOST, nullable: inner placement (recycling.py:409-415) -- H W and J W
+                                    use this operator (the previous system's H and J) while H U~ and
+                                    C = H U R^-1 use `op` (the upcoming H); reuse_products is then
+                                    ignored (H U~ is s fresh products with the upcoming H) */
 } kr_recycle_args;
 
 /* out[j] = (((rows[0][j] + rows[1][j]) + rows[2][j]) + ...), j < p: the sample-ordered sum of

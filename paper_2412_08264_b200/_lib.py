@@ -39,7 +39,7 @@ class KrOp(ctypes.Structure):
     ]
 
 
-ABI_VERSION = 3  # KR_ABI_VERSION of include/krecycle_b200.h
+ABI_VERSION = 4  # KR_ABI_VERSION of include/krecycle_b200.h
 
 
 class KrSolveArgs(ctypes.Structure):
@@ -66,7 +66,7 @@ class KrRecycleArgs(ctypes.Structure):
         ("V", _c_p), ("ld_v", _c_i64), ("bs_v", _c_i64), ("kdims", _c_p),
         ("Uprev", _c_p), ("ld_u", _c_i64), ("bs_u", _c_i64), ("sdims", _c_p),
         ("W", _c_p), ("HW", _c_p), ("U", _c_p), ("C", _c_p), ("mu", _c_p), ("VH", _c_p), ("Z", _c_p),
-        ("tdims", _c_p), ("nsel", _c_p), ("status", _c_p),
+        ("tdims", _c_p), ("nsel", _c_p), ("status", _c_p), ("op_proj", _c_p),
     ]
 
 

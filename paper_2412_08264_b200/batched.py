@@ -361,10 +361,11 @@ def supports(strategy, native: bool = False) -> bool:
     accurate as the reference's SVD of Q1 for alpha near 1 -- the largest mu,
     size L -- but square the gaps between small alpha (sizes S, M); those stay on
     the per-sample SVD path.  Ritz uses eigh(W^T H W) exactly as the reference.
-    Harmonic Ritz (harmonic_ritz_select, recycling.py:239-272) runs in the native
-    orchestrator only (Cholesky reduction of the pencil, kr_recycle_update)."""
-    if strategy.placement != "outer":
-        return False
+    Harmonic Ritz (harmonic_ritz_select, recycling.py:239-272) and inner placement
+    (:409-415) run in the native orchestrator only (Cholesky reduction of the pencil;
+    the previous system's operator as op_proj, kr_recycle_update)."""
+    if strategy.placement != "outer" and not native:
+        return False  # inner placement (recycling.py:409-415): the native orchestrator only
     if strategy.vec_type == "HRitz":
         return native
     return strategy.vec_type == "Ritz" or (strategy.vec_type == "RGen" and strategy.size == "L")
@@ -533,7 +534,8 @@ def _scratch(cache, key, numel, dev):
 
 
 def recycle_update_native(strategy, s: int, H, J, bases, recycles, reuse_products: bool = True,
-                          scratch: dict | None = None, out: tuple | None = None, out_src: tuple | None = None):
+                          scratch: dict | None = None, out: tuple | None = None, out_src: tuple | None = None,
+                          H_proj=None, J_proj=None):
     """``recycle_update`` through the native orchestrator ``kr_recycle_update`` (one
     C-ABI call per batch: no Python per-op overhead, no GIL); same contract and
     results.  Falls back to ``recycle_update`` beyond the kernels' t <= KR_TMAX (640).
@@ -554,8 +556,11 @@ def recycle_update_native(strategy, s: int, H, J, bases, recycles, reuse_product
     T = max(t) if t else 0
     if T == 0 or s == 0:
         return [RecycleSpace.empty(n) for _ in range(B)]
+    inner = strategy.placement != "outer"
+    if inner and H_proj is None:
+        raise ValueError("inner placement needs the previous system's operator (H_proj)")
     if T > NATIVE_TMAX or s > T:
-        if strategy.vec_type == "HRitz":  # the torch batched path has no harmonic Ritz: per-sample path
+        if strategy.vec_type == "HRitz" or inner:  # not in the torch batched path: per-sample path
             return [None] * B
         return recycle_update(strategy, s, H, J, bases, recycles, reuse_products)
     dev = H.model.y.device if getattr(H, "model", None) is not None else bases[0].device
@@ -569,6 +574,9 @@ def recycle_update_native(strategy, s: int, H, J, bases, recycles, reuse_product
     a.reuse_products = int(reuse_products)
     a.V, a.ld_v, a.bs_v = vptr, ldv, bsv
     a.Uprev, a.ld_u, a.bs_u = uptr, ldu, bsu
+    if inner:
+        # J W of the GSVD uses the previous Jacobian: same kr_op as H_proj (one prepare serves both)
+        a.op_proj = ctypes.addressof(H_proj.op)
     kd = np.asarray(k, dtype=np.int32)
     sd = np.asarray(sp, dtype=np.int32)
     td = np.zeros(B, dtype=np.int32)

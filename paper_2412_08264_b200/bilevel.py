@@ -208,7 +208,9 @@ class SequenceSolver:
             return False
         if not isinstance(hessian, HessianOperator) or isinstance(hessian, DenseOperator):
             return False
-        return st.vec_type == "Ritz" or isinstance(jac, StencilJacobian)
+        if st.placement != "outer" and not isinstance(self._prev_h, HessianOperator):
+            return False
+        return st.vec_type in ("Ritz", "HRitz") or isinstance(jac, StencilJacobian)
 
     def _group_members(self, B: int, ng: int):
         """Sample groups of the batched update.  Sorted by candidate width t_b (default):
@@ -246,12 +248,18 @@ class SequenceSolver:
         def run(g, idx):
             lo, hi = idx[0], idx[-1] + 1
             contiguous = idx == list(range(lo, hi))
+            inner = cfg.strategy.placement != "outer"
+            hp = None
             if contiguous:
                 hs = hessian if (lo, hi) == (0, B) else hessian.slice(lo, hi)
                 js = jac if (lo, hi) == (0, B) or jac is None else jac.slice(lo, hi)
+                if inner:  # inner placement projects with the previous system's operator
+                    hp = self._prev_h if (lo, hi) == (0, B) else self._prev_h.slice(lo, hi)
             else:  # the group's per-sample tables gathered (a few hundred MB at C3: ~0.1 ms)
                 hs = hessian.select(idx)
                 js = None if jac is None else jac.select(idx, hs)
+                if inner:
+                    hp = self._prev_h.select(idx)
             bases = [self._prev_basis[i] for i in idx]
             prevs = [self._prev_recycle[i] for i in idx]
             if self.native_update:
@@ -259,7 +267,8 @@ class SequenceSolver:
                 if contiguous:
                     out = tuple(None if x is None else x[lo:hi] for x in shared)
                     recs = recycle_update_native(cfg.strategy, cfg.recycle_dim, hs, js, bases, prevs,
-                                                 cfg.reuse_products, scratch=sc, out=out, out_src=shared + (lo, ztc))
+                                                 cfg.reuse_products, scratch=sc, out=out, out_src=shared + (lo, ztc),
+                                                 H_proj=hp)
                     full = all(r is not None and r.dim == cfg.recycle_dim for r in recs)
                     if ztc is not None and full:
                         ztc[lo:hi] = batched_gram(shared[2][lo:hi], shared[1][lo:hi])
@@ -272,7 +281,7 @@ class SequenceSolver:
                                     for x in shared)
                         sc["out"] = loc
                     recs = recycle_update_native(cfg.strategy, cfg.recycle_dim, hs, js, bases, prevs,
-                                                 cfg.reuse_products, scratch=sc, out=loc, out_src=None)
+                                                 cfg.reuse_products, scratch=sc, out=loc, out_src=None, H_proj=hp)
                     it = torch.as_tensor(idx, dtype=torch.long, device=shared[0].device)
                     for x, y in zip(shared, loc):
                         if x is not None:

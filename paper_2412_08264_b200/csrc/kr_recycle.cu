@@ -682,6 +682,15 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
   KR_CHECK_ARG(work && work_len >= workspace_doubles(*op, *a), "kr_recycle workspace too small");
   const int p = op->reg_kind == KR_REG_TV ? 1 : op->num_filters * (1 + op->ksize * op->ksize);
   const int P = p + T;
+  // inner placement (recycling.py:409-415): project with the previous system's operator
+  const kr_op* pop = a->op_proj ? a->op_proj : op;
+  const bool inner = a->op_proj != nullptr;
+  if (inner) {
+    KR_TRY(validate_op(*pop));
+    KR_CHECK_ARG(pop->batch == B && pop->rows == op->rows && pop->cols == op->cols && pop->reg_kind == op->reg_kind &&
+                     pop->num_filters == op->num_filters && pop->ksize == op->ksize,
+                 "op_proj must describe the same batch and model family as op");
+  }
   Ctx c{(cudaStream_t)stream, nullptr, work, work + work_len};
   KR_TRY(up_ring().reset());
   static const bool debug = getenv("KR_RECYCLE_DEBUG") != nullptr;
@@ -919,9 +928,9 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
   double* HW = a->HW;
   static const bool lowpri = getenv("KR_HVP_LOWPRI") == nullptr || getenv("KR_HVP_LOWPRI")[0] != '0';
   if (lowpri)
-    KR_TRY(low_stream().run_hvp(op, W, n, (int64_t)T * n, T, d_td, HW, n, (int64_t)T * n, c.st));
+    KR_TRY(low_stream().run_hvp(pop, W, n, (int64_t)T * n, T, d_td, HW, n, (int64_t)T * n, c.st));
   else
-    KR_TRY(hvp_cols(op, W, n, (int64_t)T * n, T, d_td, HW, n, (int64_t)T * n, c.st));
+    KR_TRY(hvp_cols(pop, W, n, (int64_t)T * n, T, d_td, HW, n, (int64_t)T * n, c.st));
   double* Ht = c.take((int64_t)B * T * T);
   KR_TRY(gram(c, W, HW, B, T, n, Ht));
   double* coeffs = c.take((int64_t)B * s * T);
@@ -979,8 +988,8 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
   } else {
     // J W
     double* Jt = c.take((int64_t)B * T * p);
-    const int64_t jl = kr_jadj_workspace(op, T);
-    KR_TRY(kr_jadj(op, W, n, (int64_t)T * n, T, Jt, p, (int64_t)T * p, c.take(jl), jl, c.st));
+    const int64_t jl = kr_jadj_workspace(pop, T);
+    KR_TRY(kr_jadj(pop, W, n, (int64_t)T * n, T, Jt, p, (int64_t)T * p, c.take(jl), jl, c.st));
     double* S = c.take((int64_t)B * T * P);
     double* Hs = c.take((int64_t)B * T * T);
     sym_and_s_kernel<<<dim3(T, B), 256, 0, c.st>>>(Ht, Jt, p, T, Hs, S);
@@ -1078,7 +1087,7 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
     KR_TRY(kr_hvp(op, cand, n, (int64_t)s * n, s, HU, n, (int64_t)s * n, c.st));
   } else {
     KR_TRY(rows_mul(c, coeffs, (int64_t)s * T, W, n, (int64_t)T * n, cand, n, (int64_t)s * n, s, T, n, B));
-    if (a->reuse_products)
+    if (a->reuse_products && !inner)  // (inner: H W is the previous H's, H U~ needs the upcoming one)
       KR_TRY(rows_mul(c, coeffs, (int64_t)s * T, HW, n, (int64_t)T * n, HU, n, (int64_t)s * n, s, T, n, B));
     else
       KR_TRY(kr_hvp(op, cand, n, (int64_t)s * n, s, HU, n, (int64_t)s * n, c.st));

@@ -41,7 +41,7 @@ DELTA = 1e-6
 # case -> (BASELINE config, image size, global sample indices, systems, s, max_iter, control runs[, delta])
 CASES = {
     # C2 exactly: 8 x 128^2, 9x9 blur, J=8 q=5, s=20, max 200, delta 1e-6
-    "C2": ("C2", 128, list(range(8)), 5, 20, 200, 2),
+    "C2": ("C2", 128, list(range(8)), 5, 20, 200, 4),
     # C3's operators (256^2, 15x15 sigma 2.5 blur, 2 % noise) on two of its samples:
     # s=30, max 300 -> candidate widths up to 330 (> 228, the round-1 shared-memory limit)
     "C3s": ("C3", 256, [0, 1], 5, 30, 300, 2),
@@ -77,7 +77,7 @@ def run_case(name: str):
     mk = lambda: ob.SequenceSolver(ob.SolveConfig.from_strategy(STRATEGY, recycle_dim=s, delta=delta,
                                                                  max_iter=max_iter))
     B, P = len(samples), models[0].reg.num_params
-    out = {k: [] for k in ("iters", "reasons", "stopval", "hg", "tdim", "hg_adj")}
+    out = {k: [] for k in ("iters", "reasons", "stopval", "hg", "tdim", "hg_adj", "kept")}
     ctl = {k: [] for k in ("iters", "hg")}
     solvers = [mk() for _ in range(B)]
     controls = [[mk() for _ in range(B)] for _ in range(ncontrol)]
@@ -104,6 +104,8 @@ def run_case(name: str):
                     if 0 <= kk - 1 + d < len(rr.iterates):
                         adj[d] = J.apply_adjoint(rr.iterates[kk - 1 + d])
             row["hg_adj"].append(adj)
+            # candidate columns kept by the pivoted-QR rank drop (recycling.py:187-199)
+            row["kept"].append(0 if rec.nsc_data is None or rec.nsc_data.w is None else int(rec.nsc_data.w.shape[1]))
             row["iters"].append(r.iterations)
             row["reasons"].append(r.stop_reason)
             row["stopval"].append(r.stop_values[-1])
@@ -133,6 +135,7 @@ def run_case(name: str):
         iters=np.array(out["iters"]), reasons=np.array(out["reasons"]), stopval=np.array(out["stopval"]),
         hg=np.array(out["hg"]).reshape(systems, B, P), tdim=np.array(out["tdim"]),
         hg_adj=np.array(out["hg_adj"]).reshape(systems, B, 3, P),  # iterations k-1, k, k+1
+        kept=np.array(out["kept"]),
         ctl_iters=np.array(ctl["iters"]).transpose(1, 0, 2),  # (control, system, sample)
         ctl_hg=np.array(ctl["hg"]).transpose(1, 0, 2, 3),
     )

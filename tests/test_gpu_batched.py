@@ -110,8 +110,9 @@ def test_declines_small_mu_selections():
     assert supports(S.parse("RGen-L(R)-NSC")) and supports(S.parse("Ritz-S")) and supports(S.parse("RGen-L(M)"))
     assert not supports(S.parse("RGen-S(L)")) and not supports(S.parse("RGen-M(R)"))
     assert not supports(S.parse("inner:RGen-L(R)")) and not supports(S.parse("HRitz-S"))
-    # harmonic Ritz: the native orchestrator only
-    assert supports(S.parse("HRitz-S"), native=True) and not supports(S.parse("inner:HRitz-S"), native=True)
+    # harmonic Ritz and inner placement: the native orchestrator only
+    assert supports(S.parse("HRitz-S"), native=True) and supports(S.parse("inner:HRitz-S"), native=True)
+    assert supports(S.parse("inner:RGen-L(R)"), native=True) and not supports(S.parse("inner:RGen-S(R)"), native=True)
 
 
 def _harmonic_keys(W, HW):
@@ -427,3 +428,40 @@ def test_recycle_update_wide_candidates(strategy):
             assert _span_dist(C, ref.C) <= 1e-7
             if st.vec_type == "RGen":
                 assert torch.allclose(got[b].nsc_data.values, ref.nsc_data.values, rtol=1e-8)
+
+
+@pytest.mark.parametrize("strategy", ["inner:RGen-L(R)-NSC", "inner:Ritz-S", "inner:HRitz-L"])
+def test_inner_placement_native_matches_per_sample(strategy):
+    """Inner placement (recycling.py:409-415): the candidates are projected with the
+    PREVIOUS system's H (and J), then normalised against the upcoming H -- the native
+    orchestrator with op_proj against the per-sample reference-semantics path."""
+    from paper_2412_08264_b200.batched import recycle_update_native
+    from paper_2412_08264_b200.recycling import _select_indices, build_candidate_basis, next_recycle
+
+    model, seq, H, J = _setup(strategy)
+    st = seq.cfg.strategy
+    Hp, Jp = seq._prev_h, seq._prev_jac
+    got_all = recycle_update_native(st, seq.cfg.recycle_dim, H, J, seq._prev_basis, seq._prev_recycle, H_proj=Hp)
+    for b in range(model.batch):
+        ref = next_recycle(st, h_current=H.sample(b), h_previous=Hp.sample(b), jac_current=J.sample(b),
+                           jac_previous=Jp.sample(b), prev_basis=seq._prev_basis[b],
+                           prev_recycle=seq._prev_recycle[b], s=seq.cfg.recycle_dim)
+        got = got_all[b]
+        assert got is not None and got.dim == ref.dim
+        if st.vec_type == "HRitz":
+            W = build_candidate_basis(seq._prev_basis[b], seq._prev_recycle[b].U).W
+            key = _harmonic_keys(W, Hp.sample(b).apply_matrix(W))
+            t, sdim = key.numel(), min(seq.cfg.recycle_dim, key.numel())
+            sel = set(_select_indices(t, sdim, st.size, "cpu").tolist())
+            posed = all(not ((i in sel) != (i + 1 in sel) and float(key[i + 1] - key[i]) <= 1e-6 * float(key.max()))
+                        for i in range(t - 1))
+        else:
+            posed = _selection_well_posed(st, Hp.sample(b), Jp.sample(b), seq, b)
+        if posed:
+            assert torch.dist(_proj(got.C), _proj(ref.C)) <= 1e-8
+            assert torch.dist(_proj(got.U), _proj(ref.U)) <= 1e-8
+        assert torch.allclose(got.C.T @ got.C, torch.eye(got.dim, dtype=torch.float64, device="cuda"), atol=1e-13)
+        HU = H.sample(b).apply_matrix(got.U)  # C = H_current U, whatever H projected
+        assert torch.dist(HU, got.C) <= 1e-10 * torch.linalg.norm(HU)
+        if ref.nsc_data is not None:
+            assert torch.allclose(got.nsc_data.values, ref.nsc_data.values, rtol=1e-8, atol=1e-12)
