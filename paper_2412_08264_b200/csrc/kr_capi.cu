@@ -92,7 +92,10 @@ int ensure_smem(const void* kernel, size_t bytes) {
       size_t lim = optin > 0 ? (size_t)optin - fa.sharedSizeBytes : bytes;
       if (lim < bytes) lim = bytes;
       cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
-      if (e != cudaSuccess) return fail(KR_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+      if (e != cudaSuccess)
+        return fail(KR_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e) + " (dynamic " +
+                                  std::to_string(bytes) + " B + static " + std::to_string(fa.sharedSizeBytes) +
+                                  " B > opt-in " + std::to_string(optin) + " B)");
       c = lim;
     }
   }

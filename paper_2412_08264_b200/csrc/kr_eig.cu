@@ -684,7 +684,8 @@ int64_t eig_smem_doubles(int T, int* nw_out) {
   const int64_t base = 4 * (int64_t)T + EIG_MAXSEL + EIG_RED;
   const int64_t r1 = T > EIG_TPACK ? 3 * (int64_t)T : 2 * (int64_t)T + (int64_t)T * (T + 1) / 2;
   const int64_t per_vec = 6 * (int64_t)T + (T + 7) / 8;
-  const int64_t cap = (227 * 1024) / 8 - 8 - base;  // static smem (cl_first, s_int) kept out
+  // static smem (cl_first: EIG_MAXSEL shorts, s_int) kept out of the 227 KB opt-in
+  const int64_t cap = (227 * 1024 - (int64_t)sizeof(short) * EIG_MAXSEL - 64) / 8 - base;
   int nw = (int)((cap > r1 ? cap : r1) / per_vec);
   if (nw > EW) nw = EW;
   if (nw < 1) nw = 1;

@@ -68,3 +68,36 @@ def test_desk_sequence_totals(cuda, strategy):
     ref_hg = d[f"{_key(strategy)}__hg"]
     worst = max(rel(hgs[i], ref_hg[i]) for i in range(len(its)) if its[i] == ref_its[i])
     assert worst <= 1e-8, worst
+
+
+# pkg/plots/sample_data/sweep.csv (the reference's dimension_sweep of the foe12 sequence,
+# experiments.py:505-535): Ritz-S, recycle dims 0 / 2 / 4 / 8 / 12 ->
+# (total iterations, total flops, max and mean relative hypergradient error vs J w*)
+SWEEP_GOLDEN = {
+    0: (76, 3768192, 0.033694827195256682, 0.016520784270208023),
+    2: (72, 3741718, 0.026326296642218004, 0.013062908269928819),
+    4: (66, 3554132, 0.024341119751564732, 0.01341575650779959),
+    8: (63, 3600160, 0.020297843837332619, 0.010121535657028299),
+    12: (60, 3618571, 0.023730413966896402, 0.011710216193678263),
+}
+
+
+def test_dimension_sweep_matches_reference_sweep_csv(cuda):
+    """experiments.dimension_sweep on the device over the reference's frozen foe12
+    sequence reproduces the reference's sweep.csv: total iterations and flops exactly,
+    the hypergradient error statistics against the stored J w* to 1e-6 relative."""
+    from paper_2412_08264_b200 import ImageVector, InpaintingProblem
+    from paper_2412_08264_b200.experiments import dimension_sweep
+
+    d = golden("foe12_seq.npz")
+    shape = tuple(int(v) for v in d["shape"])
+    prob = InpaintingProblem(d["mask_rows"], d["y"], float(d["ridge"]), shape, ImageVector(d["x_true"], shape))
+    model = prob.model()
+    model.num_filters, model.ksize = int(d["num_filters"]), int(d["kernel_size"])
+    refs = [torch.as_tensor(r, device=cuda).reshape(1, -1) for r in d["ref_hg"]]
+    rows = dimension_sweep(model, list(d["theta"]), list(d["x_hat"]), "Ritz-S", sorted(SWEEP_GOLDEN), delta=1e-2,
+                           max_inner=500, refs=refs)
+    for strat, s, its, flops, emax, emean in rows:
+        g_its, g_flops, g_max, g_mean = SWEEP_GOLDEN[s]
+        assert (its, flops) == (g_its, g_flops), (s, its, flops)
+        assert abs(emax - g_max) <= 1e-6 * g_max and abs(emean - g_mean) <= 1e-6 * g_mean, (s, emax, emean)
