@@ -101,3 +101,31 @@ def test_dimension_sweep_matches_reference_sweep_csv(cuda):
         g_its, g_flops, g_max, g_mean = SWEEP_GOLDEN[s]
         assert (its, flops) == (g_its, g_flops), (s, its, flops)
         assert abs(emax - g_max) <= 1e-6 * g_max and abs(emean - g_mean) <= 1e-6 * g_mean, (s, emax, emean)
+
+
+@pytest.mark.parametrize("strategy", ["Eig-S", "Eig-L", "GSVD-L(R)", "GSVD-L(R)-NSC", "inner:Eig-S",
+                                      "HRitz-S", "inner:RGen-L(R)-NSC"])
+def test_remaining_strategies_match_oracle(cuda, strategy):
+    """The strategies outside the bench path: dense Eig / GSVD
+    (recycling.py:416-445, the n x n projections through the library eigensolver), harmonic
+    Ritz (:239-272, native batched update) and inner placement (:409-415, native with the
+    previous operator) replayed over the reference's foe12 sequence against the CPU oracle:
+    iterations within +-1, hypergradients within 1e-8 where the iteration counts agree."""
+    from oracle import cpu_bilevel as ob
+    from oracle import cpu_imaging as im
+
+    d = golden("foe12_seq.npz")
+    its, hgs = _replay(d, strategy, 10)
+    shape = tuple(int(v) for v in d["shape"])
+    data = im.DataTerm("mask", shape, d["y"], scale=1.0, ridge=float(d["ridge"]), mask_rows=d["mask_rows"],
+                       x_true=d["x_true"])
+    model = im.Model(data, im.Regularizer("filters", int(d["num_filters"]), int(d["kernel_size"]), "quadratic"))
+    solver = ob.SequenceSolver(ob.SolveConfig.from_strategy(strategy, recycle_dim=10, delta=1e-2, max_iter=500))
+    for i in range(d["theta"].shape[0]):
+        H = im.hessian(model, d["theta"][i], d["x_hat"][i])
+        J = im.jacobian(model, d["theta"][i], d["x_hat"][i])
+        res, _ = solver.solve(H, d["g"][i], J)
+        ref = J.apply_adjoint(res.solution)
+        assert abs(int(its[i]) - res.iterations) <= 1, (i, its[i], res.iterations)
+        if its[i] == res.iterations:
+            assert rel(hgs[i], ref) <= 1e-8, (i, rel(hgs[i], ref))
