@@ -358,11 +358,17 @@ def run_ours(args):
 
     # reserve the caching allocator's pool up front so per-step shape changes (t grows
     # with the previous solve's iteration count) do not hit cudaMalloc inside the timed region
-    torch.empty(3 * 1024**3 // 8, dtype=torch.float64, device="cuda")
     t_max = cfg.max_iter + cfg.recycle_dim
     per_sample = 8 * n * t_max * 6  # W, H W, candidates, QR workspaces of one sample's recycle update
+    # Per-stream pools cannot lend memory to each other: when the job's working set (bases,
+    # recycle state, update scratch: ~12 n t_max doubles per sample) is a large part of the device
+    # (C4: 16 x 512^2 x 540), pre-sizing the pools would strand memory on the wrong streams; the
+    # warm-up steps grow the pools instead.
+    total_mem = torch.cuda.get_device_properties(local).total_memory
     seq = SequenceSolver(solver_cfg)
-    seq.reserve(B, per_sample, shape=(n, t_max))
+    if B * 12 * 8 * n * t_max < 0.35 * total_mem:
+        torch.empty(3 * 1024**3 // 8, dtype=torch.float64, device="cuda")
+        seq.reserve(B, per_sample, shape=(n, t_max))
     for i in range(args.warmup):
         step(seq, i, xhats[i])
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
@@ -431,8 +437,14 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         pinned = [torch.from_numpy(x).pin_memory() for x in xhats_np]
+        # the timed run's solver state (bases, recycle spaces, update scratch: ~100 GB at C4) is
+        # released before the e2e pass builds its own
+        del seq
+        gc.collect()
+        torch.cuda.empty_cache()
         seq2 = SequenceSolver(solver_cfg)
-        seq2.reserve(B, per_sample, shape=(n, t_max))
+        if B * 12 * 8 * n * t_max < 0.35 * total_mem:
+            seq2.reserve(B, per_sample, shape=(n, t_max))
         for i in range(args.warmup):
             X = pinned[i].to("cuda", non_blocking=True)
             step(seq2, i, X)[0].cpu()

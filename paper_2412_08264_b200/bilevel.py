@@ -174,9 +174,13 @@ class SequenceSolver:
             if self._gstreams is None or len(self._gstreams) < ng:
                 self._gstreams = [torch.cuda.Stream(priority=_GROUP_PRIORITY) for _ in range(ng)]
                 self._gpool = ThreadPoolExecutor(max_workers=ng)
-            for st in self._gstreams:
+            # only the lanes that will run (see _recycle_batched) get a pool
+            per_group = -(-batch // ng) * nbytes
+            budget = int(0.45 * torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory)
+            nl = max(1, min(ng, budget // max(per_group, 1)))
+            for st in self._gstreams[:nl]:
                 with torch.cuda.stream(st):
-                    torch.empty(-(-batch // ng) * nbytes // 8, dtype=torch.float64, device="cuda")
+                    torch.empty(min(per_group, budget // nl) // 8, dtype=torch.float64, device="cuda")
             # torch creates cuBLAS / cuSOLVER handles per host thread on first use (tens of
             # ms): touch them on every worker thread now, not inside a step
             gate = threading.Barrier(ng)
@@ -245,6 +249,15 @@ class SequenceSolver:
             # (off the path between the last update and the solve launch)
             ztc = torch.empty(B, s, s, **f64) if shared[2] is not None else None
 
+        # concurrent lanes: each lane runs its groups one after another on its own stream with
+        # one set of scratch buffers (H W, W, candidates, QR workspaces: ~48 n t bytes per
+        # sample); as many lanes as the memory budget holds (C2/C3: one per group; C4 -- 16
+        # samples x 512^2 x t 540 -- two)
+        tcap = cfg.max_iter + cfg.recycle_dim + 1
+        per_group = 48 * hessian.dim * tcap * max(len(m) for m in members)
+        budget = int(0.45 * torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory)
+        nl = max(1, min(ng, budget // max(per_group, 1)))
+
         def run(g, idx):
             lo, hi = idx[0], idx[-1] + 1
             contiguous = idx == list(range(lo, hi))
@@ -263,7 +276,7 @@ class SequenceSolver:
             bases = [self._prev_basis[i] for i in idx]
             prevs = [self._prev_recycle[i] for i in idx]
             if self.native_update:
-                sc = self._scratch.setdefault(g, {"tcap": cfg.max_iter + cfg.recycle_dim + 1})
+                sc = self._scratch.setdefault(g % nl, {"tcap": tcap})
                 if contiguous:
                     out = tuple(None if x is None else x[lo:hi] for x in shared)
                     recs = recycle_update_native(cfg.strategy, cfg.recycle_dim, hs, js, bases, prevs,
@@ -312,7 +325,7 @@ class SequenceSolver:
             self._gpool = ThreadPoolExecutor(max_workers=ng)
 
         def work(g):
-            st = self._gstreams[g]
+            st = self._gstreams[g % nl]
             st.wait_stream(main)
             extra = None
             idx = members[g]
@@ -333,11 +346,18 @@ class SequenceSolver:
                         t.record_stream(main)
             return recs, extra
 
-        # groups 1.. on the pool, group 0 on this thread (one thread hand-off fewer)
-        futs = [self._gpool.submit(work, g) for g in range(1, ng)]
-        parts = [work(0)] + [f.result() for f in futs]
-        for g in range(ng):
-            main.wait_stream(self._gstreams[g])
+        def lane(l):
+            return [work(g) for g in range(l, ng, nl)]
+
+        # lanes 1.. on the pool, lane 0 on this thread (one thread hand-off fewer)
+        futs = [self._gpool.submit(lane, l) for l in range(1, nl)]
+        done = [lane(0)] + [f.result() for f in futs]
+        parts = [None] * ng
+        for l, res in enumerate(done):
+            for j, r in enumerate(res):
+                parts[l + j * nl] = r
+        for l in range(nl):
+            main.wait_stream(self._gstreams[l])
         out = assemble([recs for recs, _ in parts])
         if then is None:
             return out
