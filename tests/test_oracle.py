@@ -305,3 +305,22 @@ def test_rcg_sequence_tv():
 
 def _dense(H):
     return np.column_stack([H(e) for e in np.eye(H.dim)])
+
+
+def test_c_stencil_matches_numpy_oracle():
+    """oracle/cpu_stencil.c (the fixture generator's fast operators) against cpu_imaging's
+    scipy restatement: H v and J w to roundoff on config-shaped small problems."""
+    import dataclasses
+
+    from oracle import cpu_fast as cf
+
+    for name, size in (("C2", 24), ("C3", 40), ("C4", 48)):
+        cfg = dataclasses.replace(im.CONFIGS[name], size=size)
+        m, xt = im.deblur_sample(cfg, 1)
+        th = im.deblur_theta0(cfg)
+        xh = xt + 0.03 * np.random.default_rng(2).standard_normal(xt.size)
+        v = np.random.default_rng(3).standard_normal(m.data.n)
+        a, b = cf.hessian(m, th, xh)(v), im.hessian(m, th, xh)(v)
+        assert np.linalg.norm(a - b) <= 1e-13 * np.linalg.norm(b)
+        ja, jb = cf.jacobian(m, th, xh).apply_adjoint(v), im.jacobian(m, th, xh).apply_adjoint(v)
+        assert np.linalg.norm(ja - jb) <= 1e-12 * np.linalg.norm(jb)
