@@ -5,6 +5,9 @@
 #include <utility>
 #include <string>
 
+#include <cudaTypedefs.h>
+#include <cstdlib>
+
 #include "kr_common.cuh"
 #include "kr_internal.h"
 
@@ -100,6 +103,31 @@ int ensure_smem(const void* kernel, size_t bytes) {
     }
   }
   return KR_OK;
+}
+
+bool make_region_tmap(CUtensorMap* map, const double* base, int cols, int rows, int64_t ncols, int64_t batch,
+                      int64_t ld, int64_t bs, int box_w, int box_h) {
+  static const bool off = getenv("KR_TMA") && getenv("KR_TMA")[0] == '0';
+  if (off || !base || ((uintptr_t)base & 15) || cols % 2 || ld % 2 || bs % 2 || box_w % 2 || box_w > 256 ||
+      box_h > 256 || cols < 2 || rows < 1 || ncols < 1 || batch < 1)
+    return false;
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      enc = nullptr;
+  }
+  if (!enc) return false;
+  const cuuint64_t dims[4] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)ncols, (cuuint64_t)batch};
+  const cuuint64_t strides[3] = {(cuuint64_t)cols * 8, (cuuint64_t)ld * 8, (cuuint64_t)bs * 8};
+  const cuuint32_t box[4] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1, 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 int device_sms() {

@@ -7,6 +7,7 @@
 // blur / TV / phi_eps generalisation is documented in DESIGN.md.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (type only; the encoder is resolved through the runtime)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -74,7 +75,7 @@ __host__ __device__ inline Geom make_geom(const kr_op& op) {
   // stride puts the 32 rows of a warp on distinct bank pairs
   g.RW = TW + 2 * g.H + 1;
   g.RH = TH + 2 * g.H;
-  g.s0 = g.RH * g.RW;
+  g.s0 = (g.RH * g.RW + 15) & ~15;  // SA starts 128-byte aligned: it is the TMA staging buffer
   const int w1p = TW + 2 * g.rb + 1;  // padded (odd) strides of the blur scratch
   int s1 = (op.data_kind == KR_DATA_BLUR) ? (TH + 4 * g.rb) * w1p : 0;
   int s3 = (op.data_kind == KR_DATA_BLUR) ? (TH + 2 * g.rb) * (TW + 1) : 0;
@@ -256,6 +257,62 @@ struct TileIn {
     return v;
   }
 };
+
+// TMA-staged region load (sm_100a cp.async.bulk.tensor): the (RH x (TW + 2H)) box of the
+// input vector around the tile is fetched in ONE bulk tensor copy into the scratch SA (the
+// tensor map's out-of-bounds fill is zero -- exactly the zero boundary), then copied into
+// S0's padded (odd-stride) layout, divided by `div` when it is not 1.  The 4-D tensor is
+// (cols, rows, columns, samples) with the caller's leading / batch strides.
+struct TmaSrc {
+  const CUtensorMap* map;  // nullptr: scalar loads
+  int col, b;              // tensor coordinates 2 and 3 of the vector
+  double div;
+  uint64_t* mbar;          // shared-memory mbarrier (initialised with count 1)
+  uint32_t* phase;         // its current phase parity (shared)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ inline void tma_mbar_init(uint64_t* mbar, uint32_t* phase) {
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    *phase = 0;
+  }
+  __syncthreads();
+}
+
+__device__ inline void tma_load_region(const TmaSrc& t, const Geom& g, int y0, int x0, double* stage, double* S0) {
+  const int BW = TW + 2 * g.H;
+  if (threadIdx.x == 0) {
+    const uint32_t bytes = (uint32_t)(g.RH * BW * sizeof(double));
+    // generic-proxy accesses of the staging buffer (the previous tile's passes) before the
+    // async-proxy writes of the bulk copy
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(t.mbar)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(smem_u32(stage)),
+        "l"(t.map), "r"(x0 - g.H), "r"(y0 - g.H), "r"(t.col), "r"(t.b), "r"(smem_u32(t.mbar))
+        : "memory");
+  }
+  const uint32_t ph = *t.phase;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tKR_TMA_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra KR_TMA_WAIT;\n\t}" ::"r"(smem_u32(t.mbar)),
+      "r"(ph)
+      : "memory");
+  const double div = t.div;
+  for (int i = threadIdx.x; i < g.RH * BW; i += blockDim.x) {
+    const int yy = i / BW, xx = i - yy * BW;
+    const double v = stage[i];
+    S0[yy * g.RW + xx] = div == 1.0 ? v : v / div;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *t.phase = ph ^ 1u;
+}
 
 __device__ inline void load_region(const kr_op& op, const Geom& g, const TileIn& in, int y0, int x0,
                                    double* S0) {
@@ -620,14 +677,16 @@ __device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, 
 }
 
 template <int Q>
-__device__ inline void tile_hvp_t(const kr_op& op, const Geom& g, Smem& sm, int b, const TileIn& in, int tile);
+__device__ inline void tile_hvp_t(const kr_op& op, const Geom& g, Smem& sm, int b, const TileIn& in, int tile,
+                                  const TmaSrc* tma = nullptr);
 
 __device__ inline void tile_hvp(const kr_op& op, const Geom& g, Smem& sm, int b, const TileIn& in, int tile) {
   tile_hvp_t<0>(op, g, sm, b, in, tile);
 }
 
 template <int Q>
-__device__ inline void tile_hvp_t(const kr_op& op, const Geom& g, Smem& sm, int b, const TileIn& in, int tile) {
+__device__ inline void tile_hvp_t(const kr_op& op, const Geom& g, Smem& sm, int b, const TileIn& in, int tile,
+                                  const TmaSrc* tma) {
   if (op.data_kind == KR_DATA_DENSE) {
     tile_hvp_dense(op, b, in, tile, sm.res);
     return;
@@ -639,8 +698,12 @@ __device__ inline void tile_hvp_t(const kr_op& op, const Geom& g, Smem& sm, int 
 #ifdef KR_RMINRES_TIMING
   unsigned long long slast = kr_gtime0();
 #endif
-  load_region(op, g, in, y0, x0, sm.S0);
-  block_barrier();
+  if (tma && tma->map) {
+    tma_load_region(*tma, g, y0, x0, sm.SA, sm.S0);
+  } else {
+    load_region(op, g, in, y0, x0, sm.S0);
+    block_barrier();
+  }
   KR_SMARK(0, slast);
 
   // pointwise part: mask data term + ridge

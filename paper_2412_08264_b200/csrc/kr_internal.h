@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cublas_v2.h>
+#include <cuda.h>
 #include <cusolverDn.h>
 #include <cuda_runtime.h>
 
@@ -21,6 +22,11 @@ int device_sms();
 int cublas_handle(cublasHandle_t* out, cudaStream_t st);
 int cusolver_handle(cusolverDnHandle_t* out, cudaStream_t st);
 int cublas_check(cublasStatus_t s, const char* what);
+// 4-D fp64 tensor map (cols, rows, ncols, batch) with leading / batch strides ld, bs (elements)
+// and box (box_w, box_h, 1, 1) for the TMA-staged stencil regions; false when the layout is not
+// expressible (odd widths or strides, misaligned base) or the driver entry point is missing
+bool make_region_tmap(CUtensorMap* map, const double* base, int cols, int rows, int64_t ncols, int64_t batch,
+                      int64_t ld, int64_t bs, int box_w, int box_h);
 
 }  // namespace kr
 

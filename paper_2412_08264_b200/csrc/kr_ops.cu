@@ -74,8 +74,11 @@ __global__ void prepare_tv_kernel(kr_op op) {
 template <int Q>
 __global__ void __launch_bounds__(NT) hvp_kernel(kr_op op, const double* __restrict__ V, int64_t ldv,
                                                  int64_t bsv, double* __restrict__ HV, int64_t ldo,
-                                                 int64_t bso, const int32_t* __restrict__ dims) {
-  extern __shared__ double smem[];
+                                                 int64_t bso, const int32_t* __restrict__ dims,
+                                                 const __grid_constant__ CUtensorMap tmap, int use_tma) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t mphase;
   const int tile = blockIdx.x, col = blockIdx.y, b = blockIdx.z;
   if (dims && col >= dims[b]) {  // zero pad column of a batch padded to its widest sample: H 0 = 0
     double* out = HV + b * bso + col * ldo;
@@ -87,9 +90,11 @@ __global__ void __launch_bounds__(NT) hvp_kernel(kr_op op, const double* __restr
   }
   const Geom g = make_geom(op);
   Smem sm = carve(g, smem);
+  if (use_tma) tma_mbar_init(&mbar, &mphase);
   load_weights(op, g, sm);
   const double* in = V + b * bsv + col * ldv;
-  tile_hvp_t<Q>(op, g, sm, b, TileIn{in, 1.0, nullptr, 0.0}, tile);
+  const TmaSrc t{&tmap, col, b, 1.0, &mbar, &mphase};
+  tile_hvp_t<Q>(op, g, sm, b, TileIn{in, 1.0, nullptr, 0.0}, tile, use_tma ? &t : nullptr);
   double* out = HV + b * bso + col * ldo;
   for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
     int64_t p = tile_pixel(op, tile, l);
@@ -442,7 +447,12 @@ int kr::hvp_cols(const kr_op* op, const double* V, int64_t ldv, int64_t bsv, int
   KR_TRY(ensure_smem(fn, smem));
   dim3 grid(num_tiles(*op), ncols, op->batch);
   kr_op opv = *op;
-  void* args[] = {&opv, (void*)&V, &ldv, &bsv, &HV, &ldo, &bso, (void*)&dims};
+  alignas(64) CUtensorMap tmap;
+  int use_tma = (op->data_kind != KR_DATA_DENSE && g.RH * (TW + 2 * g.H) <= g.sa &&
+                 make_region_tmap(&tmap, V, op->cols, op->rows, ncols, op->batch, ldv, bsv, TW + 2 * g.H, g.RH))
+                    ? 1 : 0;
+  if (!use_tma) memset(&tmap, 0, sizeof tmap);
+  void* args[] = {&opv, (void*)&V, &ldv, &bsv, &HV, &ldo, &bso, (void*)&dims, &tmap, &use_tma};
   cudaError_t e = cudaLaunchKernel(fn, grid, dim3(NT), args, smem, (cudaStream_t)stream);
   if (e != cudaSuccess) return fail(KR_ECUDA, std::string("kr_hvp launch: ") + cudaGetErrorString(e));
   return check_launch("kr_hvp");

@@ -27,6 +27,7 @@
 //  * The stop decision of iteration k is taken right after it (end of phase B), so a
 //    finished sample's blocks never run another stencil.
 
+#include <cstring>
 #include <string>
 
 #include "kr_common.cuh"
@@ -74,6 +75,8 @@ struct DParams {
   int track;                   // residual vector requested (hv keeps every column)
   int vec2;                    // even image width and 16-byte aligned columns: pixel pairs as double2
   int pipe;                    // odd samples run one phase behind the even ones (A and B units overlap)
+  int use_tma;                 // the stencil's halo region comes in one bulk tensor copy (tmap over tmp)
+  CUtensorMap tmap;            // (cols, rows, 1, B) view of tmp
 };
 
 __device__ __forceinline__ double2 ld2cg(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
@@ -241,9 +244,11 @@ __device__ inline void solve_y(const DParams& P, int b, int K, double* scratch, 
 #define DYN_GRID_SYNC() grid_barrier(P.bar, (unsigned)P.G, grid_target)
 
 template <int Q>
-__global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(DParams P) {
+__global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(const __grid_constant__ DParams P) {
   unsigned int grid_target = 0;
-  extern __shared__ double smem[];
+  extern __shared__ __align__(128) double smem[];
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t mphase;
   const kr_op& op = P.op;
   const kr_solve_args& A = P.a;
   const Geom g = make_geom(op);
@@ -261,6 +266,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(DParams P) {
   const int nt = P.ntiles, G = P.G;
   const int SL_CHV = 0, SL_CV = s, SL_VHV = 2 * s, SL_ZHV = 2 * s + 1;
   const int CH = (g.s0 + g.sa) / 5;  // solve_y / finalize staging chunk (entries)
+  if (P.use_tma) tma_mbar_init(&mbar, &mphase);
   load_weights(op, g, sm);
   unsigned ph = 0;
 
@@ -410,7 +416,8 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(DParams P) {
         const double* Z = ns ? A.Z + (int64_t)b * A.bs_z : nullptr;
         double* hvk = hvcol(P, b, k);
         double* vk = vcol(P, b, k);
-        tile_hvp_t<Q>(op, g, sm, b, TileIn{tb, beta, nullptr, 0.0}, tile);
+        const TmaSrc tsrc{&P.tmap, 0, b, beta, &mbar, &mphase};
+        tile_hvp_t<Q>(op, g, sm, b, TileIn{tb, beta, nullptr, 0.0}, tile, P.use_tma ? &tsrc : nullptr);
         if (deferred) {
           for (int i = threadIdx.x; i < npass * 25 * DEF_STRIDE; i += NT) red[i] = 0.0;
           block_barrier();
@@ -889,6 +896,13 @@ int rminres_dyn(const kr_op& op, const kr_solve_args& a, double* work, int64_t w
            a.ld_basis % 2 == 0 && a.bs_basis % 2 == 0 &&
            (a.s == 0 || (al16(a.C) && a.ld_uc % 2 == 0 && a.bs_uc % 2 == 0)) &&
            (ns == 0 || (al16(a.Z) && a.ld_z % 2 == 0 && a.bs_z % 2 == 0)) && getenv("KR_DYN_SCALAR") == nullptr;
+  {
+    const Geom g = make_geom(op);
+    P.use_tma = (op.data_kind != KR_DATA_DENSE && g.RH * (TW + 2 * g.H) <= g.sa &&
+                 make_region_tmap(&P.tmap, P.tmp, op.cols, op.rows, 1, B, n, n, TW + 2 * g.H, g.RH))
+                    ? 1 : 0;
+    if (!P.use_tma) memset(&P.tmap, 0, sizeof P.tmap);
+  }
   const void* kfn = KR_PICK_Q(rminres_dyn_kernel, q_variant(op));
   KR_TRY(ensure_smem(kfn, L.smem));
   cudaMemsetAsync(P.vecs, 0, sizeof(double) * (size_t)B * NVEC * MAX_S, st);
