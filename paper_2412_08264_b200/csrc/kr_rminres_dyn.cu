@@ -418,6 +418,14 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(const __grid_constan
         double* vk = vcol(P, b, k);
         const TmaSrc tsrc{&P.tmap, 0, b, beta, &mbar, &mphase};
         tile_hvp_t<Q>(op, g, sm, b, TileIn{tb, beta, nullptr, 0.0}, tile, P.use_tma ? &tsrc : nullptr);
+        if (P.use_tma && threadIdx.x == 0 && next_ticket < (unsigned)(na * nt)) {
+          // the next unit's halo region into L2 while this unit's dots run (its bulk copy then
+          // hits L2; a finalisation unit's region is only a wasted prefetch)
+          const int nb = list[next_ticket % na], ntl = next_ticket / na, tyc = tiles_x(op);
+          asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global [%0, {%1, %2, %3, %4}];" ::"l"(&P.tmap),
+                       "r"((ntl % tyc) * TW - g.H), "r"((ntl / tyc) * TH - g.H), "r"(0), "r"(nb)
+                       : "memory");
+        }
         if (deferred) {
           for (int i = threadIdx.x; i < npass * 25 * DEF_STRIDE; i += NT) red[i] = 0.0;
           block_barrier();
