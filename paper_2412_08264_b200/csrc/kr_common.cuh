@@ -364,8 +364,12 @@ __host__ __device__ constexpr int pick_run(int lanes, int len, int BS) {
 // (a sliding window: RUN + BS - 1 loads for RUN * BS FMAs).  Row passes map lanes to
 // rows (odd smem strides keep them conflict-free), column passes map lanes to columns.
 // Every output accumulates its taps in the order u = 0 .. BS-1 (the generic path's order).
-template <int BS>
-__device__ inline void blur_normal_bs(const kr_op& op, const Geom& g, Smem& sm, int y0, int x0) {
+// GRAD = true (the lower-level gradient, operators.py:329-353 generalised): pass 2's
+// A x gets y subtracted inside the image (residual A x - y) and the data cost
+// sum (A x - y)^2 of the tile's own pixels is accumulated into *dcost.
+template <int BS, bool GRAD = false>
+__device__ inline void blur_normal_bs(const kr_op& op, const Geom& g, Smem& sm, int y0, int x0,
+                                      const double* ydata = nullptr, double* dcost = nullptr) {
   constexpr int RB = BS / 2;
   constexpr int H1 = TH + 4 * RB, W1 = TW + 2 * RB, W1P = W1 + 1, H2 = TH + 2 * RB, W3P = TW + 1;
   constexpr int RX1 = pick_run(H1, W1, BS), RY2 = pick_run(W1, H2, BS), RX3 = pick_run(H2, TW, BS),
@@ -423,7 +427,17 @@ __device__ inline void blur_normal_bs(const kr_op& op, const Geom& g, Smem& sm, 
 #pragma unroll
       for (int i = 0; i < RY2; ++i) {
         const int r = r0 + i, y = y0 - RB + r;
-        if (r < H2) S2[r * W1P + c] = (y >= 0 && y < rows && x >= 0 && x < cols) ? acc[i] : 0.0;
+        if (r < H2) {
+          const bool in = y >= 0 && y < rows && x >= 0 && x < cols;
+          double v = in ? acc[i] : 0.0;
+          if constexpr (GRAD) {
+            if (in) {
+              v -= ydata[(int64_t)y * cols + x];
+              if (r >= RB && r < RB + TH && c >= RB && c < RB + TW) *dcost += v * v;
+            }
+          }
+          S2[r * W1P + c] = v;
+        }
       }
     }
   }
@@ -557,8 +571,12 @@ __device__ inline void tile_blur_normal_generic(const kr_op& op, const Geom& g, 
 //            curvatures are loaded before the FMAs);
 //   stage 2: out_w += w_j corr(e_j, c_j) on the tile, a lane RB2 rows of 4 columns;
 // then the per-warp sums are added in warp order (fixed, deterministic) to sm.res.
-template <int Q>
-__device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, int b, int y0, int x0) {
+// GRAD = true: the lower-level gradient's regulariser term sum_j w_j C_j^T phi'(C_j x)
+// (stage 1 applies phi' instead of the curvature) and the cost sum_j w_j sum_p phi(C_j x)
+// over the tile's own pixels into *rcost.
+template <int Q, bool GRAD = false>
+__device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, int b, int y0, int x0,
+                                      double* rcost = nullptr) {
   constexpr int R = Q / 2;
   constexpr int EW = TW + 2 * R, EH = TH + 2 * R, ES = EW * EH;
 #ifndef KR_RB1_Q5
@@ -586,9 +604,14 @@ __device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, 
     for (int a = 0; a < Q; ++a)
 #pragma unroll
       for (int bb = 0; bb < Q; ++bb) k[a][bb] = kj[a * Q + bb];
-    const double* cj = quad ? nullptr : op.curv + ((int64_t)b * op.num_filters + j) * n;
+    const double* cj = (quad || GRAD) ? nullptr : op.curv + ((int64_t)b * op.num_filters + j) * n;
     // curvature of a strip: loaded one item ahead (the L2 latency overlaps the FMAs)
     auto load_cv = [&](int item, double (&cv)[RB1]) {
+      if constexpr (GRAD) {
+#pragma unroll
+        for (int i = 0; i < RB1; ++i) cv[i] = 0.0;
+        return;
+      }
       const int c = item % EW, r0 = (item / EW) * RB1;
       const int x = x0 - R + c;
 #pragma unroll
@@ -626,7 +649,30 @@ __device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, 
       }
 #pragma unroll
       for (int i = 0; i < RB1; ++i)
-        if (r0 + i < EH) S4[(r0 + i) * EW + c] = cv[i] * acc[i];
+        if (r0 + i < EH) {
+          if constexpr (GRAD) {
+            // phi' and phi of u = (c_j * x) (the potential, operators.py:5-7 / DESIGN section 2);
+            // zero outside the image like the curvature path
+            const int y = y0 - R + r0 + i, x = x0 - R + c;
+            const bool in = y >= 0 && y < rows && x >= 0 && x < cols;
+            const double u = acc[i];
+            double e = 0.0;
+            if (in) {
+              const bool own = r0 + i >= R && r0 + i < R + TH && c >= R && c < R + TW;
+              if (quad) {
+                e = 2.0 * u;
+                if (own) *rcost += sm.fw[j] * (u * u);
+              } else {
+                const double sq = sqrt(u * u + op.eps * op.eps);
+                e = u / sq;
+                if (own) *rcost += sm.fw[j] * sq;
+              }
+            }
+            S4[(r0 + i) * EW + c] = e;
+          } else {
+            S4[(r0 + i) * EW + c] = cv[i] * acc[i];
+          }
+        }
     }
     __syncwarp();
     const double wj = sm.fw[j];

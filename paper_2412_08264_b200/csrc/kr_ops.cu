@@ -4,6 +4,7 @@
 //   kr_jadj        J W for t columns x B samples     (operators.py:290-298, 386-444)
 //   kr_lower_eval  lower cost + gradient             (operators.py:329-353)
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -378,6 +379,51 @@ __global__ void __launch_bounds__(NT) lower_eval_kernel(kr_op op, const double* 
   double* gout = grad + (int64_t)b * n;
   for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
     int64_t p = tile_pixel(op, tile, l);
+    if (p >= 0) gout[p] = sm.res[l];
+  }
+  double v3[3] = {c_data, c_ridge, c_reg};
+  block_sum<3>(v3, red);
+  if (threadIdx.x < 3) part[((int64_t)b * ntiles + tile) * 3 + threadIdx.x] = red[threadIdx.x];
+}
+
+// Lower-level cost and gradient for the configs' model family (blur 9/15/21 + learned
+// filters q = 3/5/7, smooth-|.| or quadratic potential) through the HVP's templated tile
+// machinery: the separable register-blocked blur with the residual A x - y formed in its
+// second pass, and the one-filter-per-warp stage with phi' in place of the curvature
+// (operators.py:329-353 generalised; same partial layout as lower_eval_kernel).
+template <int Q, int BS>
+__global__ void __launch_bounds__(NT) lower_eval_fast_kernel(kr_op op, const double* __restrict__ X,
+                                                             const double* __restrict__ Y, double* __restrict__ grad,
+                                                             double* __restrict__ part) {
+  extern __shared__ __align__(128) double smem[];
+  const Geom g = make_geom(op);
+  Smem sm = carve(g, smem);
+  __shared__ double red[4 * 33 + 4];
+  load_weights(op, g, sm);
+  const int tile = blockIdx.x, b = blockIdx.z, ntiles = gridDim.x;
+  const int tyc = tiles_x(op);
+  const int y0 = (tile / tyc) * TH, x0 = (tile % tyc) * TW;
+  const int rows = op.rows, cols = op.cols, H = g.H;
+  const int64_t n = op_n(op);
+  load_region(op, g, TileIn{X + (int64_t)b * n, 1.0, nullptr, 0.0}, y0, x0, sm.S0);
+  block_barrier();
+  double c_data = 0.0, c_ridge = 0.0, c_reg = 0.0;
+  for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
+    const int ty = l / TW, tx = l - ty * TW;
+    const double v = sm.S0[(ty + H) * g.RW + tx + H];
+    double acc = 0.0;
+    if (y0 + ty < rows && x0 + tx < cols) {
+      acc = op.ridge * v;
+      c_ridge += v * v;
+    }
+    sm.res[l] = acc;
+  }
+  block_barrier();
+  blur_normal_bs<BS, true>(op, g, sm, y0, x0, Y + (int64_t)b * n, &c_data);
+  tile_filters_q<Q, true>(op, g, sm, b, y0, x0, &c_reg);
+  double* gout = grad + (int64_t)b * n;
+  for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
+    const int64_t p = tile_pixel(op, tile, l);
     if (p >= 0) gout[p] = sm.res[l];
   }
   double v3[3] = {c_data, c_ridge, c_reg};
@@ -830,10 +876,27 @@ extern "C" int kr_lower_eval(const kr_op* op, const double* X, const double* Y, 
   KR_CHECK_ARG(work_len >= kr_lower_workspace(op), "lower workspace too small");
   Geom g = make_geom(*op);
   size_t smem = (size_t)g.total * sizeof(double);
-  KR_TRY(ensure_smem((const void*)lower_eval_kernel, smem));
   const int ntiles = num_tiles(*op);
   cudaStream_t st = (cudaStream_t)stream;
-  lower_eval_kernel<<<dim3(ntiles, 1, op->batch), NT, smem, st>>>(*op, X, Y, grad, work);
+  const void* fast = nullptr;
+  static const bool generic_only = getenv("KR_LOWER_GENERIC") != nullptr;
+  if (!generic_only && op->data_kind == KR_DATA_BLUR && op->reg_kind == KR_REG_FILTERS) {
+#define KR_LFAST(QQ, BB) \
+    if (op->ksize == QQ && op->blur_size == BB) fast = (const void*)lower_eval_fast_kernel<QQ, BB>;
+    KR_LFAST(3, 9) KR_LFAST(3, 15) KR_LFAST(3, 21) KR_LFAST(5, 9) KR_LFAST(5, 15) KR_LFAST(5, 21)
+    KR_LFAST(7, 9) KR_LFAST(7, 15) KR_LFAST(7, 21)
+#undef KR_LFAST
+  }
+  if (fast) {
+    KR_TRY(ensure_smem(fast, smem));
+    kr_op opv = *op;
+    void* args[] = {&opv, (void*)&X, (void*)&Y, &grad, &work};
+    const cudaError_t e = cudaLaunchKernel(fast, dim3(ntiles, 1, op->batch), dim3(NT), args, smem, st);
+    if (e != cudaSuccess) return fail(KR_ECUDA, std::string("kr_lower_eval launch: ") + cudaGetErrorString(e));
+  } else {
+    KR_TRY(ensure_smem((const void*)lower_eval_kernel, smem));
+    lower_eval_kernel<<<dim3(ntiles, 1, op->batch), NT, smem, st>>>(*op, X, Y, grad, work);
+  }
   KR_TRY(check_launch("kr_lower_eval"));
   lower_reduce_kernel<<<op->batch, 32, 0, st>>>(*op, work, ntiles, cost);
   return check_launch("kr_lower_eval reduce");
