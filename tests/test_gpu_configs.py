@@ -104,3 +104,48 @@ def test_sequence_matches_oracle_at_config_size(name, cuda):
     if diverged:
         print(f"   rank-drop decisions at the 1e-10 threshold differed for samples {sorted(diverged)}")
     assert not failures, failures
+
+
+def test_solved_sequence_replay_matches_oracle(cuda):
+    """The bench's kind of frozen sequence -- x_hat_i = the device L-BFGS minimiser at each
+    theta of the path (sequence.solve_path) -- saved / loaded as krecycle-sequence-v1 and
+    replayed through the device SequenceSolver (RGen-L(R)-NSC) against the CPU oracle's
+    replay of the SAME loaded systems (experiments.py:390-463): C2's operators, two
+    samples, four systems; iterations within +-1, hypergradients within 1e-8 where the
+    counts agree (or the oracle's adjacent-iterate / perturbed spread otherwise)."""
+    import tempfile
+
+    from oracle import cpu_bilevel as ob
+    from oracle import cpu_fast as cf
+    from oracle import cpu_imaging as im
+    from paper_2412_08264_b200 import HessianSolveConfig, SequenceSolver
+    from paper_2412_08264_b200.bilevel import hypergradients
+    from paper_2412_08264_b200.problems import CONFIGS, synthetic_sequence
+    from paper_2412_08264_b200.sequence import load_sequence, save_sequence, solve_path
+
+    cfg = dataclasses.replace(CONFIGS["C2"], batch=2)
+    thetas, _ = synthetic_sequence(cfg, np.zeros((1, cfg.size * cfg.size)), 4)
+    with tempfile.TemporaryDirectory() as tmp:
+        seq = load_sequence(save_sequence(solve_path(cfg, thetas, count=2, lower_gtol=1e-6, device=cuda), tmp))
+    model = seq.model(cuda)
+    kw = dict(recycle_dim=cfg.recycle_dim, delta=1e-6, max_iter=cfg.max_iter)
+    gpu = SequenceSolver(HessianSolveConfig.from_strategy("RGen-L(R)-NSC", **kw))
+    ocfg = dataclasses.replace(im.CONFIGS["C2"])
+    omodels = [im.deblur_sample(ocfg, k)[0] for k in range(2)]
+    cpus = [ob.SequenceSolver(ob.SolveConfig.from_strategy("RGen-L(R)-NSC", **kw)) for _ in range(2)]
+    ctls = [ob.SequenceSolver(ob.SolveConfig.from_strategy("RGen-L(R)-NSC", **kw)) for _ in range(2)]
+    for i, rec in enumerate(seq.systems):
+        hg, res, _ = hypergradients(model, rec.theta, torch.as_tensor(rec.x_hats, device=cuda), gpu)
+        for b in range(2):
+            xh = rec.x_hats[b]
+            H, J = cf.hessian(omodels[b], rec.theta, xh), cf.jacobian(omodels[b], rec.theta, xh)
+            r, _ = cpus[b].solve(H, xh - seq.x_true[b], J)
+            rc, _ = ctls[b].solve(im.perturbed(H, 2e-16, seed=10 * i + b), xh - seq.x_true[b], J)
+            ref = J.apply_adjoint(r.solution)
+            floor = np.linalg.norm(J.apply_adjoint(rc.solution) - ref) / np.linalg.norm(ref)
+            err = np.linalg.norm(hg[b].cpu().numpy() - ref) / np.linalg.norm(ref)
+            print(f"system {i} sample {b}: iterations gpu {res[b].iterations} oracle {r.iterations} "
+                  f"(control {rc.iterations}), hg err {err:.2e} floor {floor:.2e}")
+            assert abs(res[b].iterations - r.iterations) <= max(1, abs(rc.iterations - r.iterations) + 1)
+            if res[b].iterations == r.iterations:
+                assert err <= max(1e-8, 10 * floor), (i, b, err, floor)
