@@ -50,7 +50,7 @@ extern "C" {
 
 typedef struct CUstream_st* kr_stream_t; /* == cudaStream_t */
 
-#define KR_ABI_VERSION 4
+#define KR_ABI_VERSION 5
 
 /* Largest candidate width t = k_prev + s_prev of the small dense kernels and the recycle
  * update: BASELINE C5 with s = 80 and 500 iterations (t <= 580), with margin. */
@@ -111,7 +111,8 @@ typedef struct kr_solve_args {
   const double* U;         /* [batch][s][ld_uc] */
   const double* C;         /* [batch][s][ld_uc], C^T C = I */
   int64_t ld_uc, bs_uc;
-  int32_t stop_kind;       /* 0 = residual norm (stopping.py:93-99), 1 = NSC (stopping.py:102-118) */
+  int32_t stop_kind;       /* 0 = residual norm (stopping.py:93-99), 1 = NSC (stopping.py:102-118),
+                              2 = true hypergradient error (stopping.py:121-185; see nsc_r0) */
   double delta;            /* strict: stop when value < delta (stopping.py:89-90) */
   int32_t nsc_s;           /* NSC columns */
   const double* Z;         /* [batch][nsc_s][ld_z]: Z = W V_H,sel diag(mu_sel) (nsc_value, stopping.py:69-72) */
@@ -127,6 +128,10 @@ typedef struct kr_solve_args {
   int32_t* iters;          /* out [batch] */
   int32_t* reasons;        /* out [batch]: 0 tolerance, 1 max_iter, 2 breakdown, 3 non-SPD */
   const double* Minv;      /* [batch][s][s] (U^T C)^{-1}, row-major: kr_cg deflation (recycled CG); NULL = plain CG */
+  const double* nsc_r0;    /* stop_kind 2 (true hypergradient error, stopping.py:121-185): [batch][nsc_s]
+                              J w* - J w0 with w* = H^-1 g; Z then holds the rows of J (nsc_s = p <= 128),
+                              ZtC = J U, and the value ||J H^-1 r_k|| follows the residual recurrence
+                              with Z^T hv_k replaced by J v_k (= J H^-1 H v_k).  Needs a kept basis. */
 } kr_solve_args;
 
 int kr_abi_version(void);

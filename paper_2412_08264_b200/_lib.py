@@ -39,7 +39,7 @@ class KrOp(ctypes.Structure):
     ]
 
 
-ABI_VERSION = 4  # KR_ABI_VERSION of include/krecycle_b200.h
+ABI_VERSION = 5  # KR_ABI_VERSION of include/krecycle_b200.h
 
 
 class KrSolveArgs(ctypes.Structure):
@@ -53,7 +53,7 @@ class KrSolveArgs(ctypes.Structure):
         ("track_residual", _c_i32),
         ("w", _c_p), ("r", _c_p), ("basis", _c_p), ("ld_basis", _c_i64), ("bs_basis", _c_i64),
         ("res_norms", _c_p), ("stop_vals", _c_p), ("iters", _c_p), ("reasons", _c_p),
-        ("Minv", _c_p),
+        ("Minv", _c_p), ("nsc_r0", _c_p),
     ]
 
 

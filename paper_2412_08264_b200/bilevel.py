@@ -21,7 +21,7 @@ from .krylov import SolveOptions, SolveResult, rcg, rminres
 from .operators import (DenseOperator, FoEParams, HessianOperator, ImageVector, InpaintingProblem, Model,
                         StencilJacobian, as_device, _foe_model)
 from .recycling import RecycleSpace, StrategyDescriptor, next_recycle
-from .stopping import ConfigurationError, NscRule, ResidualNormRule
+from .stopping import ConfigurationError, NscRule, ResidualNormRule, TrueHgErrorRule
 
 __all__ = ["HessianSolveConfig", "SequenceSolver", "hypergradient", "hypergradients"]
 
@@ -130,8 +130,6 @@ class SequenceSolver:
     """
 
     def __init__(self, cfg: HessianSolveConfig):
-        if cfg.stop == "true-hg":
-            raise NotImplementedError("the true-hypergradient rule is an oracle; use the CPU oracle for it")
         self.cfg = cfg
         self._first = True
         self._prev_basis: list | None = None
@@ -420,12 +418,17 @@ class SequenceSolver:
             main.wait_stream(self._streams[b])
         return recs
 
-    def _options(self, recycles, init):
+    def _options(self, recycles, init, hessian=None, jac=None):
         """Stop rules per sample (bilevel.py:264-276) and the solve options."""
         cfg = self.cfg
         rules = []
-        for rec in recycles:
-            if cfg.stop == "nsc" and rec.nsc_data is not None:
+        B = len(recycles)
+        for b, rec in enumerate(recycles):
+            if cfg.stop == "true-hg":  # bilevel.py:267-268 (an experiment oracle)
+                hb = hessian if B == 1 else hessian.sample(b)
+                jb = jac if B == 1 else jac.sample(b)
+                rules.append(TrueHgErrorRule(cfg.delta, jb, hb, cfg.inner_tol, cfg.dense_limit))
+            elif cfg.stop == "nsc" and rec.nsc_data is not None:
                 rules.append(NscRule(cfg.delta, rec.nsc_data))
             else:  # res, or nsc on the first system (bilevel.py:269-273)
                 rules.append(ResidualNormRule(cfg.delta))
@@ -457,7 +460,7 @@ class SequenceSolver:
             def then(lo, hi, recs):
                 hs = hessian.slice(lo, hi)
                 w0 = None if init is None else init[lo:hi].contiguous()
-                return solve(hs, g[lo:hi], recs, self._options(recs, w0))
+                return solve(hs, g[lo:hi], recs, self._options(recs, w0, hs, jac.slice(lo, hi)))
 
             recycles, results = self._recycle_batched(hessian, jac, B, then=then)
         else:
@@ -465,7 +468,8 @@ class SequenceSolver:
         t1 = _phase_clock()
         self._first = False
         if results is None:
-            results = solve(hessian, g, recycles if B > 1 else recycles[0], self._options(recycles, init))
+            results = solve(hessian, g, recycles if B > 1 else recycles[0],
+                            self._options(recycles, init, hessian, jac))
         if t0 is not None:
             t2 = _phase_clock()
             import sys

@@ -721,9 +721,12 @@ int check_args(const kr_op& op, const kr_solve_args& a, bool dyn) {
   KR_CHECK_ARG(a.max_iter >= 1, "max_iter must be >= 1");
   KR_CHECK_ARG(a.s >= 0 && a.s <= MAX_S, "recycle dimension must be in [0, 128]");
   KR_CHECK_ARG(a.s == 0 || (a.U && a.C && a.ld_uc >= op_n(op)), "recycle space U/C missing or bad ld");
-  KR_CHECK_ARG(a.stop_kind == 0 || a.stop_kind == 1, "stop_kind must be 0 (residual) or 1 (NSC)");
+  KR_CHECK_ARG(a.stop_kind >= 0 && a.stop_kind <= 2, "stop_kind must be 0 (residual), 1 (NSC) or 2 (true hg)");
+  KR_CHECK_ARG(a.stop_kind != 2 || (dyn && a.nsc_r0 && a.Z && a.nsc_s >= 1 && a.nsc_s <= MAX_NSC &&
+                                    (a.s == 0 || a.ZtC)),
+               "the true-hypergradient stop needs a kept basis, J's rows (p <= 128), J U and J w* - J w0");
   KR_CHECK_ARG(a.delta > 0.0, "tolerance must be positive");
-  if (a.stop_kind == 1) {
+  if (a.stop_kind == 1 || a.stop_kind == 2) {
     KR_CHECK_ARG(a.nsc_s >= 1 && a.nsc_s <= MAX_NSC, "NSC needs 1..128 columns");
     KR_CHECK_ARG(a.Z && a.ld_z >= op_n(op), "NSC needs Z");
     KR_CHECK_ARG(a.s == 0 || a.ZtC, "NSC with recycling needs Z^T C");

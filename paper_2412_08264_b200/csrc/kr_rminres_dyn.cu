@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(const __grid_constan
   __shared__ int s_unit;
   __shared__ double sc[8];
   const int64_t n = P.n;
-  const int s = A.s, ns = A.stop_kind == 1 ? A.nsc_s : 0;
+  const int s = A.s, ns = A.stop_kind >= 1 ? A.nsc_s : 0;
   const int nt = P.ntiles, G = P.G;
   const int SL_CHV = 0, SL_CV = s, SL_VHV = 2 * s, SL_ZHV = 2 * s + 1;
   const int CH = (g.s0 + g.sa) / 5;  // solve_y / finalize staging chunk (entries)
@@ -338,14 +338,27 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(const __grid_constan
     block_sum<1>(v, red);
     if (threadIdx.x == 0) partp(P, b, 0)[tile] = red[0];
     block_barrier();
-    if (ns) {
+    if (ns && A.stop_kind == 1) {
       const double* Z = A.Z + (int64_t)b * A.bs_z;
       tile_mdots(P, b, tile, Z, A.ld_z, ns, 1, [&](int, int64_t p) { return tb[p]; }, red);
     }
     if (arrive(P, b, &s_flag)) {
-      reduce_tiles(P, b, 0, 1 + ns, slot);
+      reduce_tiles(P, b, 0, A.stop_kind == 1 ? 1 + ns : 1, slot);
       double* zrv = vecp(P, b, V_ZRV);
-      for (int i = threadIdx.x; i < ns; i += NT) zrv[i] = slot[1 + i];
+      if (A.stop_kind == 2) {
+        // G r0' = J H^-1 (g - H w0 - C t0) = (J w* - J w0) - (J U) t0
+        const double* t0 = vecp(P, b, V_T0);
+        const double* ZtC = s ? A.ZtC + (int64_t)b * ns * s : nullptr;
+        for (int i = threadIdx.x; i < ns; i += NT) {
+          double z = A.nsc_r0[(int64_t)b * ns + i];
+          for (int l = 0; l < s; ++l) z -= ZtC[(int64_t)i * s + l] * t0[l];
+          zrv[i] = z;
+          slot[1 + i] = z;
+        }
+        block_barrier();
+      } else {
+        for (int i = threadIdx.x; i < ns; i += NT) zrv[i] = slot[1 + i];
+      }
       if (threadIdx.x == 0) {
         St& S = P.st[b];
         const double beta = sqrt(slot[0]);
@@ -383,6 +396,9 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(const __grid_constan
   // ---------------- iterations ----------------
   const int npass = (s > ns ? s : ns) > 0 ? ((s > ns ? s : ns) + 7) / 8 : 1;
   const bool deferred = npass <= DEF_PASSES;
+  // true hypergradient error: the "Z" rows are J's and the per-iteration dots are J v_k
+  // (= J H^-1 H v_k, the G hv_k of the residual recurrence applied to G = J H^-1)
+  const bool zhv_on_v = A.stop_kind == 2;
   for (;;) {
     // One super-phase: every sample with work takes its next step -- phase A (M_RUN: stencil
     // + dots of v_k), phase B (M_RUNB: u, ||u||^2, finish iteration k) or the finalisation
@@ -456,7 +472,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(const __grid_constan
             for (int i = 0; i < 8; ++i) {
               v25[i] = cc[i].x * h2.x + cc[i].y * h2.y;
               v25[8 + i] = cc[i].x * v2.x + cc[i].y * v2.y;
-              v25[16 + i] = zz[i].x * h2.x + zz[i].y * h2.y;
+              v25[16 + i] = zhv_on_v ? zz[i].x * v2.x + zz[i].y * v2.y : zz[i].x * h2.x + zz[i].y * h2.y;
             }
             if (deferred) {
               def_add<25>(MultiSum<25>::reduce(v25, threadIdx.x & 31), base / 8, red);
@@ -517,7 +533,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(const __grid_constan
             for (int i = 0; i < 8; ++i) {
               v25[i] += cc[uu][i] * h;
               v25[8 + i] += cc[uu][i] * v;
-              v25[16 + i] += zz[uu][i] * h;
+              v25[16 + i] += zz[uu][i] * (zhv_on_v ? v : h);
             }
           }
           if (deferred) {
@@ -829,7 +845,7 @@ void dyn_plan(const kr_op& op, const kr_solve_args& a, DynLayout& L) {
   const int B = op.batch;
   L.smem = sizeof(double) * ((size_t)g.total + MAX_SLOTS + MAX_S + RED_DOUBLES);
   L.ntiles = num_tiles(op);
-  const int ns = a.stop_kind == 1 ? a.nsc_s : 0;
+  const int ns = a.stop_kind >= 1 ? a.nsc_s : 0;
   L.nslot = imax(imax(2 * a.s + 1 + ns, a.s + 1), 1 + ns);
   L.track = a.track_residual && a.r;
   int sms = device_sms(), per_sm = 0;
@@ -899,7 +915,7 @@ int rminres_dyn(const kr_op& op, const kr_solve_args& a, double* work, int64_t w
   const char* pe = getenv("KR_DYN_PIPE");
   P.pipe = pe ? (pe[0] == '1') : 0;  // measured: no gain once units are ticketed (C3: 1326 vs 1315 ms)
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
-  const int ns = a.stop_kind == 1 ? a.nsc_s : 0;
+  const int ns = a.stop_kind >= 1 ? a.nsc_s : 0;
   P.vec2 = op.data_kind != KR_DATA_DENSE && op.cols % 2 == 0 && al16(P.tmp) && al16(P.hv) && al16(a.basis) &&
            a.ld_basis % 2 == 0 && a.bs_basis % 2 == 0 &&
            (a.s == 0 || (al16(a.C) && a.ld_uc % 2 == 0 && a.bs_uc % 2 == 0)) &&

@@ -159,10 +159,14 @@ def _per_sample(x, B):
 
 
 def _rule_kind(rule) -> int:
+    from .stopping import TrueHgErrorRule
+
     if isinstance(rule, NscRule):
         return 1
     if isinstance(rule, ResidualNormRule):
         return 0
+    if isinstance(rule, TrueHgErrorRule):
+        return 2
     raise NotImplementedError(f"the device solver evaluates residual and NSC rules only, got {type(rule).__name__}")
 
 
@@ -257,9 +261,25 @@ class _Launch:
         # cg always returns its final residual (krylov.py:482: residual_vector=r.copy());
         # (r)minres tracks it when asked or when NSC needs it (krylov.py:214-215) -- unless the
         # caller waived it and the basis is kept (then the kernel keeps Z^T r in s-space)
-        want_r = opts.track_residual_vector or (kind == 1 and opts.residual_vector is not False)
+        want_r = opts.track_residual_vector or (kind >= 1 and opts.residual_vector is not False)
         track = want_r or plain_cg or (kind == 1 and not want_basis)
         a.track_residual = int(track)
+        if kind == 2:
+            # true hypergradient error: Z = J's rows, Z^T C -> J U, nsc_r0 = J w* - J w0
+            data = [r.device_data(G[b]) for b, r in enumerate(rules)]
+            p = data[0][0].shape[0]
+            Z = torch.stack([d[0] for d in data]).contiguous()            # (B, p, n)
+            r0 = torch.stack([d[1] for d in data])                        # (B, p)
+            if w0 is not None:
+                r0 = r0 - torch.bmm(Z, w0.unsqueeze(2)).squeeze(2)
+            r0 = r0.contiguous()
+            a.nsc_s, a.Z, a.ld_z, a.bs_z = p, Z.data_ptr(), n, p * n
+            a.nsc_r0 = r0.data_ptr()
+            self.keep += [Z, r0]
+            if s:
+                ZtC = torch.bmm(Z, self.U.transpose(1, 2)).contiguous()   # J U (B, p, s)
+                a.ZtC = ZtC.data_ptr()
+                self.keep.append(ZtC)
         if kind == 1:
             zs = [r.data.z_block() for r in rules]
             ns = max(z.shape[1] for z in zs)
@@ -289,7 +309,8 @@ class _Launch:
         if track:
             a.r = self.r.data_ptr()
         self.basis = None
-        if want_basis:
+        self.want_basis = want_basis
+        if want_basis or kind == 2:  # the true-hg rule runs in the shared-block kernel (basis kept)
             self.basis = _buf("basis", B, opts.max_iter, n, dev=dev)
             a.basis, a.ld_basis, a.bs_basis = self.basis.data_ptr(), n, opts.max_iter * n
         self.res = _buf("res", B, opts.max_iter + 1, dev=dev)
@@ -345,7 +366,7 @@ class _Launch:
             if why == "nonspd":
                 raise NonSPDError(f"curvature p^T H p <= 0 at iteration {k}; operator is not SPD")
             basis = None
-            if self.basis is not None:
+            if self.basis is not None and self.want_basis:
                 basis = self.basis[b, :k].T  # (n, k), contiguous columns
             out.append(SolveResult(
                 solution=self.w[b], iterations=k, residual_norms=res[b, : k + 1].copy(),

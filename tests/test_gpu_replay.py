@@ -129,3 +129,39 @@ def test_remaining_strategies_match_oracle(cuda, strategy):
         assert abs(int(its[i]) - res.iterations) <= 1, (i, its[i], res.iterations)
         if its[i] == res.iterations:
             assert rel(hgs[i], ref) <= 1e-8, (i, rel(hgs[i], ref))
+
+
+@pytest.mark.parametrize("strategy", ["None", "Ritz-S", "RGen-L(R)"])
+def test_true_hypergradient_stop_matches_oracle(cuda, strategy):
+    """The true-hypergradient-error stop rule (stopping.py:121-185, bilevel.py:267-268),
+    evaluated every iteration inside the persistent solver (s-space recurrence of
+    J H^-1 r_k), over the reference's foe12 sequence against the CPU oracle's TrueHgRule
+    (dense Cholesky per iteration): iterations within +-1, stop values and hypergradients
+    within 1e-8 where the counts agree."""
+    from oracle import cpu_bilevel as ob
+    from oracle import cpu_imaging as im
+    from paper_2412_08264_b200 import HessianSolveConfig, ImageVector, InpaintingProblem, SequenceSolver
+    from paper_2412_08264_b200.operators import as_device
+
+    d = golden("foe12_seq.npz")
+    shape = tuple(int(v) for v in d["shape"])
+    prob = InpaintingProblem(d["mask_rows"], d["y"], float(d["ridge"]), shape, ImageVector(d["x_true"], shape))
+    model = prob.model()
+    model.num_filters, model.ksize = int(d["num_filters"]), int(d["kernel_size"])
+    kw = dict(recycle_dim=10, delta=1e-4, max_iter=500, stop="true-hg")
+    gpu = SequenceSolver(HessianSolveConfig.from_strategy(strategy, **kw))
+    data = im.DataTerm("mask", shape, d["y"], scale=1.0, ridge=float(d["ridge"]), mask_rows=d["mask_rows"],
+                       x_true=d["x_true"])
+    om = im.Model(data, im.Regularizer("filters", int(d["num_filters"]), int(d["kernel_size"]), "quadratic"))
+    cpu = ob.SequenceSolver(ob.SolveConfig.from_strategy(strategy, **kw))
+    for i in range(d["theta"].shape[0]):
+        H, J = model.at(d["theta"][i], d["x_hat"][i])
+        res, _ = gpu.solve(H, as_device(d["g"][i]), J)
+        hg = to_np(J.apply_adjoint(res.solution))
+        Ho, Jo = im.hessian(om, d["theta"][i], d["x_hat"][i]), im.jacobian(om, d["theta"][i], d["x_hat"][i])
+        r, _ = cpu.solve(Ho, d["g"][i], Jo)
+        ref = Jo.apply_adjoint(r.solution)
+        assert abs(res.iterations - r.iterations) <= 1, (i, res.iterations, r.iterations)
+        if res.iterations == r.iterations:
+            assert rel(hg, ref) <= 1e-8, (i, rel(hg, ref))
+            assert rel(res.stop_values, r.stop_values) <= 1e-8, (i, res.stop_values[-3:], r.stop_values[-3:])
