@@ -77,3 +77,53 @@ def test_gloo_allgather_sum_is_bitwise_single_process(world):
     for rank, total, cost in res:
         assert np.array_equal(total, ref), rank
         assert cost == sum(range(1, world + 1))
+
+
+def _ls_worker(rank, world, port, q):
+    """The upper loop's distributed pieces (lower.gradient_descent): per-sample costs of
+    this rank's shard gathered and summed in sample order for every Armijo trial
+    (backtracking_linesearch, bilevel.py:326-358), theta updated redundantly."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    q.put((rank,) + _upper_step(rank, world))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _upper_step(rank, world):
+    from paper_2412_08264_b200.lower import LinesearchParams, UpperState, backtracking_linesearch
+
+    B, p, n = 7, 5, 11
+    rng = np.random.default_rng(4)
+    A = rng.standard_normal((B, n, p))
+    xt = rng.standard_normal((B, n))
+    mine = list(shard(B, world, rank))
+
+    def evaluate(theta, warm):  # x_k(theta) = x_true_k + A_k theta: F = sum_k 1/2 |A_k theta|^2
+        x = torch.from_numpy(np.stack([xt[k] + A[k] @ theta for k in mine]))
+        per = 0.5 * ((x - torch.from_numpy(xt[mine])) ** 2).sum(dim=1)
+        return float(allgather_sum(per.unsqueeze(1), B)[0]), x
+
+    theta0 = rng.standard_normal(p)
+    c0, x0 = evaluate(theta0, None)
+    d = sum(A[k].T @ (A[k] @ theta0) for k in range(B))  # exact gradient of F
+    state, trials = backtracking_linesearch(UpperState(theta0, x0, c0, 8.0), d, LinesearchParams(beta=8.0), evaluate)
+    return state.theta, state.cost, trials
+
+
+def test_gloo_upper_linesearch_is_bitwise_single_process():
+    ref_theta, ref_cost, ref_trials = _upper_step(0, 1)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ls_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for pr in procs:
+        pr.join(timeout=60)
+    assert ref_trials > 1  # the step had to backtrack
+    for rank, theta, cost, trials in res:
+        assert np.array_equal(theta, ref_theta) and cost == ref_cost and trials == ref_trials, rank
