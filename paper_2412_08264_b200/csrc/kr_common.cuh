@@ -66,6 +66,12 @@ __host__ __device__ inline int imax(int a, int b) { return a > b ? a : b; }
 
 constexpr int NWARP = NT / 32;  // warps per tile block (the filter stage runs one filter per warp)
 
+// stride of one filter plane of the filter stage (tile_filters_q): = 2 (mod 8) doubles
+__host__ __device__ inline int filt_plane_stride(int rq) {
+  const int epix = (TW + 2 * rq) * (TH + 2 * rq);
+  return ((epix + 7) & ~7) + 2;
+}
+
 __host__ __device__ inline Geom make_geom(const kr_op& op) {
   Geom g;
   g.rb = (op.data_kind == KR_DATA_BLUR) ? op.blur_size / 2 : 0;
@@ -79,7 +85,7 @@ __host__ __device__ inline Geom make_geom(const kr_op& op) {
   const int w1p = TW + 2 * g.rb + 1;  // padded (odd) strides of the blur scratch
   int s1 = (op.data_kind == KR_DATA_BLUR) ? (TH + 4 * g.rb) * w1p : 0;
   int s3 = (op.data_kind == KR_DATA_BLUR) ? (TH + 2 * g.rb) * (TW + 1) : 0;
-  int s4 = (op.reg_kind == KR_REG_FILTERS) ? NWARP * (TH + 2 * g.rq) * (TW + 2 * g.rq) : 0;
+  int s4 = (op.reg_kind == KR_REG_FILTERS) ? NWARP * filt_plane_stride(g.rq) : 0;
   int s5 = (op.reg_kind == KR_REG_TV) ? 2 * (TH + 1) * (TW + 1) : 0;
   g.sa = imax(imax(s1, s3), imax(s4, s5));
   g.sb = (op.data_kind == KR_DATA_BLUR) ? (TH + 2 * g.rb) * w1p : 0;
@@ -563,155 +569,179 @@ __device__ inline void tile_blur_normal_generic(const kr_op& op, const Geom& g, 
   block_barrier();
 }
 
-// Learned-filter part of H v for a compile-time filter size Q.  The J filters run
-// concurrently, one per warp (filters j = warp, warp + NWARP, ...), each warp with its
-// own scratch S4_w in smem and only __syncwarp between its stages:
-//   stage 1: e_j = kappa_j . (c_j * v) on the (TH+2R) x (TW+2R) extended tile, a lane a
-//            strip of RB1 rows of one column (loads (RB1+Q-1)Q, FMAs RB1 Q^2; the strip's
-//            curvatures are loaded before the FMAs);
-//   stage 2: out_w += w_j corr(e_j, c_j) on the tile, a lane RB2 rows of 4 columns;
+// Learned-filter part of H v for a compile-time filter size Q, filters in groups of 8:
+//   stage 1 (fp64 tensor cores, mma.sync m8n8k4 f64 = DMMA): for the group's 8 filters at
+//            once, E[p][j] = kappa_j(p) . sum_tap A[p][tap] K[tap][j] on the (TH+2R) x (TW+2R)
+//            extended tile -- A the im2col of the loaded region (one LDS per lane per MMA),
+//            K the group's taps in registers (Q^2 taps padded to a multiple of 4 with zero
+//            weights), 8 region pixels per MMA row block; the warps share the region's 8-pixel
+//            blocks; E lands in 8 smem planes (plane stride = 2 mod 8 doubles: the epilogue's
+//            stores are conflict-free);
+//   stage 2 (DFMA, one filter per warp): acc += (w_j k_j) corr E_j on the tile, a lane an
+//            8-row x 2-column output block (taps in registers, each region row loaded once
+//            per lane as Q+1 doubles in double2 loads: conflict-free quarter warps); Q = 7
+//            runs its tap rows in two halves so the taps fit in registers;
 // then the per-warp sums are added in warp order (fixed, deterministic) to sm.res.
+// DMMA and DFMA share the fp64 pipe on sm_100 (scripts/fp64_mix.cu: 37 TF either way or
+// mixed); the MMA form issues one instruction per 256 FMAs instead of 8 and one shared
+// load per MMA, which is what bounded the scalar form (profiles/r2_ncu_hvp_c3*.txt).
 // GRAD = true: the lower-level gradient's regulariser term sum_j w_j C_j^T phi'(C_j x)
 // (stage 1 applies phi' instead of the curvature) and the cost sum_j w_j sum_p phi(C_j x)
 // over the tile's own pixels into *rcost.
+template <int Q>
+struct FiltGeo {
+  static constexpr int R = Q / 2, EW = TW + 2 * R, EH = TH + 2 * R, EPIX = EW * EH;
+  static constexpr int ESP = ((EPIX + 7) & ~7) + 2;  // plane stride, = 2 (mod 8)
+  static constexpr int NK = (Q * Q + 3) / 4;         // k-steps of 4 taps
+  static constexpr int NMT = (EPIX + 7) / 8;         // 8-pixel row blocks of the region
+};
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+// stage 2 over tap rows [A0, A1): acc[i][e] += sum_{a,bb} kk[a][bb] E[(8br + i + a) EW + 2bc + e + bb]
+template <int Q, int A0, int A1>
+__device__ inline void filt_stage2(const double* __restrict__ E, const double* __restrict__ kj, double wj, int br,
+                                   int bc, double (&acc)[8][2]) {
+  using F = FiltGeo<Q>;
+  constexpr int EW = F::EW, NA = A1 - A0, NW = Q + 1;
+  double kk[NA][Q];
+#pragma unroll
+  for (int a = 0; a < NA; ++a)
+#pragma unroll
+    for (int bb = 0; bb < Q; ++bb) kk[a][bb] = wj * kj[(A0 + a) * Q + bb];
+#pragma unroll
+  for (int sr = A0; sr < 7 + A1; ++sr) {  // region row 8br + sr feeds output rows i = sr - a
+    const double2* rp = reinterpret_cast<const double2*>(E + (8 * br + sr) * EW + 2 * bc);
+    double w[NW];
+#pragma unroll
+    for (int u = 0; u < NW / 2; ++u) {
+      const double2 v = rp[u];
+      w[2 * u] = v.x;
+      w[2 * u + 1] = v.y;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int a = sr - i;
+      if (a >= A0 && a < A1) {
+#pragma unroll
+        for (int bb = 0; bb < Q; ++bb) {
+          acc[i][0] = fma(kk[a - A0][bb], w[bb], acc[i][0]);
+          acc[i][1] = fma(kk[a - A0][bb], w[bb + 1], acc[i][1]);
+        }
+      }
+    }
+  }
+}
+
 template <int Q, bool GRAD = false>
 __device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, int b, int y0, int x0,
                                       double* rcost = nullptr) {
-  constexpr int R = Q / 2;
-  constexpr int EW = TW + 2 * R, EH = TH + 2 * R, ES = EW * EH;
-#ifndef KR_RB1_Q5
-#define KR_RB1_Q5 4  // measured: 4 > 5 > 3, 6 (C2, 10-step A/B on one box)
-#endif
-  constexpr int RB1 = Q <= 3 ? 6 : (Q <= 5 ? KR_RB1_Q5 : 4);  // taller strips: fewer smem loads per FMA
-  constexpr int NCH1 = (EH + RB1 - 1) / RB1;
-  constexpr int RB2 = 4;
-  constexpr int NI2 = TPX / RB2 / 32;  // stage-2 items per lane
-  static_assert(TPX % (RB2 * 32) == 0 && TH % RB2 == 0, "stage-2 partition");
-  const int rows = op.rows, cols = op.cols, H = g.H, RW = g.RW;
+  using F = FiltGeo<Q>;
+  constexpr int R = F::R, EW = F::EW, EPIX = F::EPIX, ESP = F::ESP, NK = F::NK, NMT = F::NMT, QQ = Q * Q;
+  static_assert(TH == 16 && TW == 32 && NWARP == 8, "stage-2 lane blocks assume a 16 x 32 tile and 8 warps");
+  const int rows = op.rows, cols = op.cols, H = g.H, RW = g.RW, J = op.num_filters;
   const int64_t n = op_n(op);
   const bool quad = op.potential == KR_POT_QUADRATIC;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* S4 = sm.SA + warp * ES;
-  double out[NI2][RB2];
+  const int kc = lane & 3, mr = lane >> 2;  // MMA fragment column (tap / filter pair) and row (pixel)
+  int aoff[NK];                             // im2col offsets of this lane's taps in the region
 #pragma unroll
-  for (int it = 0; it < NI2; ++it)
+  for (int ks = 0; ks < NK; ++ks) {
+    const int tap = 4 * ks + kc;
+    aoff[ks] = tap < QQ ? -((tap / Q) * RW + tap % Q) : 0;  // pad taps read the pixel itself (weight 0)
+  }
+  const int bc = lane & 15, br = lane >> 4;  // stage-2 block: rows 8br .. 8br+7, cols 2bc, 2bc+1
+  double acc[8][2];
 #pragma unroll
-    for (int i = 0; i < RB2; ++i) out[it][i] = 0.0;
-  for (int j = warp; j < op.num_filters; j += NWARP) {
-    double k[Q][Q];
-    const double* kj = sm.kw + j * Q * Q;
+  for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = 0.0;
+  for (int g0 = 0; g0 < J; g0 += 8) {
+    double bw[NK];  // B fragment: filter g0 + mr, taps 4 ks + kc
+    {
+      const int j = g0 + mr;
 #pragma unroll
-    for (int a = 0; a < Q; ++a)
-#pragma unroll
-      for (int bb = 0; bb < Q; ++bb) k[a][bb] = kj[a * Q + bb];
-    const double* cj = (quad || GRAD) ? nullptr : op.curv + ((int64_t)b * op.num_filters + j) * n;
-    // curvature of a strip: loaded one item ahead (the L2 latency overlaps the FMAs)
-    auto load_cv = [&](int item, double (&cv)[RB1]) {
-      if constexpr (GRAD) {
-#pragma unroll
-        for (int i = 0; i < RB1; ++i) cv[i] = 0.0;
-        return;
+      for (int ks = 0; ks < NK; ++ks) {
+        const int tap = 4 * ks + kc;
+        bw[ks] = (j < J && tap < QQ) ? sm.kw[j * QQ + tap] : 0.0;
       }
-      const int c = item % EW, r0 = (item / EW) * RB1;
-      const int x = x0 - R + c;
-#pragma unroll
-      for (int i = 0; i < RB1; ++i) {
-        const int y = y0 - R + r0 + i;
-        const bool in = item < EW * NCH1 && r0 + i < EH && y >= 0 && y < rows && x >= 0 && x < cols;
-        cv[i] = in ? (quad ? 2.0 : __ldg(cj + (int64_t)y * cols + x)) : 0.0;
-      }
-    };
-    double cvn[RB1];
-    load_cv(lane, cvn);
-    for (int item = lane; item < EW * NCH1; item += 32) {
-      const int c = item % EW, r0 = (item / EW) * RB1;
-      double cv[RB1];
-#pragma unroll
-      for (int i = 0; i < RB1; ++i) cv[i] = cvn[i];
-      load_cv(item + 32, cvn);
-      double acc[RB1];
-#pragma unroll
-      for (int i = 0; i < RB1; ++i) acc[i] = 0.0;
-#pragma unroll
-      for (int sr = 0; sr < RB1 + Q - 1; ++sr) {
-        const double* src = sm.S0 + (r0 + H - (Q - 1) + sr) * RW + c + H;
-        double v[Q];
-#pragma unroll
-        for (int bb = 0; bb < Q; ++bb) v[bb] = src[-bb];
-#pragma unroll
-        for (int i = 0; i < RB1; ++i) {
-          const int a = i + Q - 1 - sr;  // conv tap row: output row r0+i reads S0 row r0+i+H-a
-          if (a >= 0 && a < Q) {
-#pragma unroll
-            for (int bb = 0; bb < Q; ++bb) acc[i] = fma(k[a][bb], v[bb], acc[i]);
-          }
+    }
+    const int j0 = g0 + 2 * kc;  // this lane's accumulator filters j0, j0 + 1
+    const double* c0p = (quad || GRAD || j0 >= J) ? nullptr : op.curv + ((int64_t)b * J + j0) * n;
+    const double* c1p = (quad || GRAD || j0 + 1 >= J) ? nullptr : op.curv + ((int64_t)b * J + j0 + 1) * n;
+    double* S4 = sm.SA;
+    for (int mt = warp; mt < NMT; mt += NWARP) {
+      const int pe = 8 * mt + mr;
+      const int pc = pe < EPIX ? pe : EPIX - 1;
+      const int re = pc / EW, ce = pc - re * EW;
+      const int y = y0 - R + re, x = x0 - R + ce;
+      const bool in = pe < EPIX && y >= 0 && y < rows && x >= 0 && x < cols;
+      double cv0 = 0.0, cv1 = 0.0;
+      if constexpr (!GRAD) {
+        if (in) {
+          const int64_t p = (int64_t)y * cols + x;
+          cv0 = quad ? 2.0 : (c0p ? __ldg(c0p + p) : 0.0);
+          cv1 = quad ? 2.0 : (c1p ? __ldg(c1p + p) : 0.0);
         }
       }
+      const double* src = sm.S0 + (re + H) * RW + ce + H;
+      double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-      for (int i = 0; i < RB1; ++i)
-        if (r0 + i < EH) {
-          if constexpr (GRAD) {
-            // phi' and phi of u = (c_j * x) (the potential, operators.py:5-7 / DESIGN section 2);
-            // zero outside the image like the curvature path
-            const int y = y0 - R + r0 + i, x = x0 - R + c;
-            const bool in = y >= 0 && y < rows && x >= 0 && x < cols;
-            const double u = acc[i];
-            double e = 0.0;
-            if (in) {
-              const bool own = r0 + i >= R && r0 + i < R + TH && c >= R && c < R + TW;
+      for (int ks = 0; ks < NK; ++ks) dmma_8x8x4(d0, d1, src[aoff[ks]], bw[ks]);
+      if (pe < EPIX) {
+        double e0, e1;
+        if constexpr (GRAD) {
+          // phi' and phi of u = (c_j * x) (the potential, operators.py:5-7 / DESIGN section 2);
+          // zero outside the image like the curvature path
+          e0 = e1 = 0.0;
+          if (in) {
+            const bool own = re >= R && re < R + TH && ce >= R && ce < R + TW;
+            const double u[2] = {d0, d1};
+            double e[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const int j = j0 + k;
               if (quad) {
-                e = 2.0 * u;
-                if (own) *rcost += sm.fw[j] * (u * u);
+                e[k] = 2.0 * u[k];
+                if (own && j < J) *rcost += sm.fw[j] * (u[k] * u[k]);
               } else {
-                const double sq = sqrt(u * u + op.eps * op.eps);
-                e = u / sq;
-                if (own) *rcost += sm.fw[j] * sq;
+                const double sq = sqrt(u[k] * u[k] + op.eps * op.eps);
+                e[k] = u[k] / sq;
+                if (own && j < J) *rcost += sm.fw[j] * sq;
               }
             }
-            S4[(r0 + i) * EW + c] = e;
-          } else {
-            S4[(r0 + i) * EW + c] = cv[i] * acc[i];
+            e0 = e[0];
+            e1 = e[1];
           }
+        } else {
+          e0 = cv0 * d0;
+          e1 = cv1 * d1;
         }
-    }
-    __syncwarp();
-    const double wj = sm.fw[j];
-#pragma unroll
-    for (int it = 0; it < NI2; ++it) {
-      const int item = lane + 32 * it;
-      const int tx2 = item % TW, r2 = (item / TW) * RB2;
-      double acc2[RB2];
-#pragma unroll
-      for (int i = 0; i < RB2; ++i) acc2[i] = 0.0;
-#pragma unroll
-      for (int sr = 0; sr < RB2 + Q - 1; ++sr) {
-        const double* src = S4 + (r2 + sr) * EW + tx2;
-        double v[Q];
-#pragma unroll
-        for (int bb = 0; bb < Q; ++bb) v[bb] = src[bb];
-#pragma unroll
-        for (int i = 0; i < RB2; ++i) {
-          const int a = sr - i;  // correlation tap row
-          if (a >= 0 && a < Q) {
-#pragma unroll
-            for (int bb = 0; bb < Q; ++bb) acc2[i] = fma(k[a][bb], v[bb], acc2[i]);
-          }
-        }
+        S4[(2 * kc) * ESP + pe] = e0;
+        S4[(2 * kc + 1) * ESP + pe] = e1;
       }
-#pragma unroll
-      for (int i = 0; i < RB2; ++i) out[it][i] = fma(wj, acc2[i], out[it][i]);
     }
-    __syncwarp();
+    block_barrier();
+    const int j = g0 + warp;
+    if (j < J) {
+      const double* E = S4 + warp * ESP;
+      const double* kj = sm.kw + j * QQ;
+      const double wj = sm.fw[j];
+      if constexpr (Q <= 5) {
+        filt_stage2<Q, 0, Q>(E, kj, wj, br, bc, acc);
+      } else {
+        filt_stage2<Q, 0, Q / 2 + 1>(E, kj, wj, br, bc, acc);
+        filt_stage2<Q, Q / 2 + 1, Q>(E, kj, wj, br, bc, acc);
+      }
+    }
+    block_barrier();  // the planes are free again (next group / the per-warp sums)
   }
-  block_barrier();  // every warp is done with its S4: reuse SA for the per-warp sums
   double* P = sm.SA;
 #pragma unroll
-  for (int it = 0; it < NI2; ++it) {
-    const int item = lane + 32 * it;
-    const int tx2 = item % TW, r2 = (item / TW) * RB2;
-#pragma unroll
-    for (int i = 0; i < RB2; ++i) P[warp * TPX + (r2 + i) * TW + tx2] = out[it][i];
-  }
+  for (int i = 0; i < 8; ++i)
+    *reinterpret_cast<double2*>(P + warp * TPX + (8 * br + i) * TW + 2 * bc) = make_double2(acc[i][0], acc[i][1]);
   block_barrier();
   for (int l = threadIdx.x; l < TPX; l += NT) {
     double a = 0.0;
