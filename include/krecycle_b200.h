@@ -223,11 +223,21 @@ int kr_qrcp_small_cluster(double* M, const int32_t* dims, int32_t batch, int32_t
 /* Batched Gram of row blocks: G_b[i][j] = a_i . b_j (row-major G, ldg, bsg) for
  * A_b, B_b given as `rows` rows of length n (row stride ld, batch stride bs) -- the
  * (B, t, n) Grams of the recycle update's QRs and W^T H W (recycling.py:194, 250,
- * 333).  Split-K over the pixel dimension (pointer-array batched cuBLAS DGEMM),
- * partials summed in fixed order.  work: kr_gram_workspace doubles. */
+ * 333).  Hand-written fp64 tensor-core kernel (mma.m8n8k4 f64, kr_gemm.cu): split-K over
+ * the pixel dimension, tile partials summed in fixed order; a true Gram (A == B) computes
+ * the lower tile blocks only and mirrors them.  work: kr_gram_workspace doubles. */
 int64_t kr_gram_workspace(int32_t batch, int32_t rows, int64_t n);
 int kr_gram(const double* A, const double* B, int64_t ld, int64_t bs, int32_t batch, int32_t rows, int64_t n,
             double* G, int64_t ldg, int64_t bsg, double* work, int64_t work_len, kr_stream_t stream);
+
+/* Batched row-block product Y_b = alpha F_b X_b + beta Y_b with F_b (r2 x r1, row-major,
+ * ldf, bsf) and X_b / Y_b rows of length L (ldx / ldy, bsx / bsy): the W <- R^-T A passes of
+ * the Cholesky-QRs (recycling.py:194, 369), the basis recombinations U~ = W X, H U~ = (H W) X
+ * (recycling.py:362-383) and Z = W V_H diag(mu).  lower != 0: F is lower triangular (the k
+ * loop of a tile row stops at its diagonal block).  Same fp64 tensor-core kernel family. */
+int kr_rows_mul(const double* F, int64_t ldf, int64_t bsf, const double* X, int64_t ldx, int64_t bsx, double* Y,
+                int64_t ldy, int64_t bsy, int32_t r2, int32_t r1, int64_t L, int32_t batch, double alpha, double beta,
+                int32_t lower, kr_stream_t stream);
 
 /* Whole-batch recycle update (recycling.py:386-465 next_recycle for every sample of
  * the batch at once; outer or inner placement; RGen with size L -- rgen_select :316-359 +

@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB_NAME = os.environ.get("KR_LIB_NAME", "libkrecycle_b200.so")
-SOURCES = ["kr_capi.cu", "kr_ops.cu", "kr_rminres.cu", "kr_rminres_dyn.cu", "kr_cg.cu", "kr_eig.cu", "kr_small.cu", "kr_qrcp.cu", "kr_recycle.cu"]
+SOURCES = ["kr_capi.cu", "kr_ops.cu", "kr_rminres.cu", "kr_rminres_dyn.cu", "kr_cg.cu", "kr_eig.cu", "kr_small.cu", "kr_qrcp.cu", "kr_recycle.cu", "kr_gemm.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3"] + os.environ.get("KR_NVCC_FLAGS", "").split()
 

@@ -116,6 +116,8 @@ def _declare(lib):
         "kr_gram_workspace": (_c_i64, [_c_i32, _c_i32, _c_i64]),
         "kr_gram": (_c_i32, [_c_p, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_i64,
                              _c_p]),
+        "kr_rows_mul": (_c_i32, [_c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_i32, _c_i32,
+                                 _c_i64, _c_i32, ctypes.c_double, ctypes.c_double, _c_i32, _c_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -130,7 +132,7 @@ EXPORTED = (
     "kr_rminres_workspace", "kr_rminres", "kr_cg_workspace", "kr_cg",
     "kr_syev_select_workspace", "kr_syev_select", "kr_chol_inv_workspace", "kr_chol_inv", "kr_qrcp_small", "kr_qrcp_small_cluster",
     "kr_gram_workspace", "kr_gram", "kr_recycle_workspace", "kr_recycle_update", "kr_thread_warmup",
-    "kr_ordered_sum",
+    "kr_ordered_sum", "kr_rows_mul",
 )
 
 

@@ -28,6 +28,17 @@ int cublas_check(cublasStatus_t s, const char* what);
 bool make_region_tmap(CUtensorMap* map, const double* base, int cols, int rows, int64_t ncols, int64_t batch,
                       int64_t ld, int64_t bs, int box_w, int box_h);
 
+// fp64 tensor-core (DMMA) products of the recycle update (kr_gemm.cu).
+// gram: G_b[i][j] = x_i . y_j over n (row-major G; sym: lower tile blocks computed and mirrored).
+int64_t gram_dmma_workspace(int batch, int rx, int ry, int64_t n, bool sym);
+int gram_dmma(const double* X, int64_t ldx, int64_t bsx, const double* Y, int64_t ldy, int64_t bsy, int batch, int rx,
+              int ry, int64_t n, bool sym, double* G, int64_t ldg, int64_t bsg, double* work, int64_t work_len,
+              cudaStream_t st);
+// rows_mul: Y_b (R2 x L) = alpha F_b (R2 x R1) X_b (R1 x L) + beta Y_b; lower: F is lower triangular
+int rows_mul_dmma(const double* F, int64_t ldf, int64_t sF, const double* X, int64_t ldX, int64_t sX, double* Y,
+                  int64_t ldY, int64_t sY, int R2, int R1, int64_t L, int batch, double alpha, double beta, bool lower,
+                  cudaStream_t st);
+
 }  // namespace kr
 
 #define KR_CHECK_ARG(cond, msg)                      \

@@ -727,8 +727,10 @@ static int64_t jw_workspace(const kr_op& op, int ncols) {
 
 extern "C" int64_t kr_jadj_workspace(const kr_op* op, int32_t ncols) {
   if (!op || validate_op(*op) != KR_OK) return -1;
-  if (jw_jmat_path(*op, ncols))
-    return (int64_t)jmat_chunk(*op) * op->num_filters * (1 + op->ksize * op->ksize) * op_n(*op);
+  if (jw_jmat_path(*op, ncols)) {
+    const int P = op->num_filters * (1 + op->ksize * op->ksize);
+    return (int64_t)jmat_chunk(*op) * P * op_n(*op) + gram_dmma_workspace(jmat_chunk(*op), ncols, P, op_n(*op), false);
+  }
   if (jw_gemm_path(*op, ncols)) return jw_workspace(*op, ncols);
   int64_t P = (op->reg_kind == KR_REG_TV) ? 1 : (int64_t)op->num_filters * (1 + op->ksize * op->ksize);
   return (int64_t)op->batch * ncols * num_tiles(*op) * P;
@@ -803,10 +805,9 @@ static int jadj_jmat(const kr_op& op, const double* W, int64_t ldw, int64_t bsw,
   const int64_t bsm = (int64_t)P * n;
   const void* fn = q == 3 ? (const void*)jmat_kernel<3> : q == 5 ? (const void*)jmat_kernel<5>
                                                                : (const void*)jmat_kernel<7>;
-  cublasHandle_t h;
-  KR_TRY(cublas_handle(&h, st));
-  const double one = 1.0, zero = 0.0;
   const int chunk = jmat_chunk(op);
+  double* gws = work + (int64_t)chunk * bsm;  // tile partials of the product
+  const int64_t gwl = gram_dmma_workspace(chunk, ncols, P, n, false);
   for (int b0 = 0; b0 < op.batch; b0 += chunk) {
     const int nb = (op.batch - b0) < chunk ? (op.batch - b0) : chunk;
     kr_op opv = op;  // samples b0 .. b0+nb-1 as a batch of nb
@@ -820,11 +821,9 @@ static int jadj_jmat(const kr_op& op, const double* W, int64_t ldw, int64_t bsw,
     cudaError_t e = cudaLaunchKernel(fn, dim3(num_tiles(op), op.num_filters, nb), dim3(NT), args, 0, st);
     if (e != cudaSuccess) return fail(KR_ECUDA, std::string("jmat launch: ") + cudaGetErrorString(e));
     KR_TRY(check_launch("jmat"));
-    // column-major: out (P x cols, ld ldo) = Mt^T (P x n) * W (n x cols, ld ldw)
-    KR_TRY(cublas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_T, CUBLAS_OP_N, P, ncols, (int)n, &one, Mt, (int)n,
-                                                  bsm, W + (int64_t)b0 * bsw, (int)ldw, bsw, &zero,
-                                                  JW + (int64_t)b0 * bso, (int)ldo, bso, nb),
-                        "dgemm Mt W"));
+    // out (cols x P, row-major, ld ldo): out[c][j] = w_c . Mt_j over the pixels (DMMA, kr_gemm.cu)
+    KR_TRY(gram_dmma(W + (int64_t)b0 * bsw, ldw, bsw, Mt, n, bsm, nb, ncols, P, n, false, JW + (int64_t)b0 * bso, ldo,
+                     bso, gws, gwl, st));
   }
   return KR_OK;
 }

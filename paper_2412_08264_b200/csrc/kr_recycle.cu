@@ -204,34 +204,34 @@ struct Ctx {
   }
 };
 
-// Y rows (B, R2, L) = F rows (B, R2, R1) @ X rows (B, R1, L)  [+ beta Y]
+// Y rows (B, R2, L) = F rows (B, R2, R1) @ X rows (B, R1, L)  [+ beta Y]; lower: F is a
+// lower-triangular factor (the Cholesky-QR passes) -- half the products are skipped
 int rows_mul(Ctx& c, const double* F, int64_t sF, const double* X, int64_t ldX, int64_t sX, double* Y, int64_t ldY,
-             int64_t sY, int R2, int R1, int64_t L, int B, double alpha = 1.0, double beta = 0.0) {
-  if (B == 0 || R2 == 0 || L == 0) return KR_OK;
-  return cublas_check(cublasDgemmStridedBatched(c.h, CUBLAS_OP_N, CUBLAS_OP_N, (int)L, R2, R1, &alpha, X, (int)ldX,
-                                                sX, F, R1, sF, &beta, Y, (int)ldY, sY, B),
-                      "kr_recycle rows_mul");
+             int64_t sY, int R2, int R1, int64_t L, int B, double alpha = 1.0, double beta = 0.0, bool lower = false) {
+  return rows_mul_dmma(F, R1, sF, X, ldX, sX, Y, ldY, sY, R2, R1, L, B, alpha, beta, lower, c.st);
+}
+int rows_mul_lower(Ctx& c, const double* F, int64_t sF, const double* X, int64_t ldX, int64_t sX, double* Y,
+                   int64_t ldY, int64_t sY, int R2, int R1, int64_t L, int B) {
+  return rows_mul(c, F, sF, X, ldX, sX, Y, ldY, sY, R2, R1, L, B, 1.0, 0.0, true);
 }
 
-// G (B, R, R) = X rows (R, L) X^T for short rows (L small): col-major G = X_col^T X_col
-int small_gram(Ctx& c, const double* X, int64_t ldX, int64_t sX, double* G, int R, int64_t L, int B) {
-  const double one = 1.0, zero = 0.0;
-  return cublas_check(cublasDgemmStridedBatched(c.h, CUBLAS_OP_T, CUBLAS_OP_N, R, R, (int)L, &one, X, (int)ldX, sX, X,
-                                                (int)ldX, sX, &zero, G, R, (int64_t)R * R, B),
-                      "kr_recycle small_gram");
-}
-
-int gram(Ctx& c, const double* A, const double* Bm, int B, int R, int64_t n, double* G) {
-  if (n < 4096) {  // short rows: one batched GEMM
-    const double one = 1.0, zero = 0.0;
-    return cublas_check(cublasDgemmStridedBatched(c.h, CUBLAS_OP_T, CUBLAS_OP_N, R, R, (int)n, &one, Bm, (int)n,
-                                                  (int64_t)R * n, A, (int)n, (int64_t)R * n, &zero, G, R,
-                                                  (int64_t)R * R, B),
-                        "kr_recycle gram");
-  }
-  const int64_t wl = kr_gram_workspace(B, R, n);
+// G (B, Rx, Ry) = X rows (Rx, L) Y rows (Ry, L)^T, rows of stride ld; sym: the result is
+// symmetric (a Gram, or W^T H W up to roundoff) -- lower tile blocks computed and mirrored
+int gram_xy(Ctx& c, const double* X, const double* Y, int64_t ld, int64_t bs, int B, int Rx, int Ry, int64_t L,
+            bool sym, double* G, int64_t ldg, int64_t bsg) {
+  const int64_t wl = gram_dmma_workspace(B, Rx, Ry, L, sym);
   double* ws = c.take(wl);
-  return kr_gram(A, Bm, n, (int64_t)R * n, B, R, n, G, R, (int64_t)R * R, ws, wl, c.st);
+  return gram_dmma(X, ld, bs, Y, ld, bs, B, Rx, Ry, L, sym, G, ldg, bsg, ws, wl, c.st);
+}
+
+// G (B, R, R) = X rows (R, L) X^T for short rows (L small)
+int small_gram(Ctx& c, const double* X, int64_t ldX, int64_t sX, double* G, int R, int64_t L, int B) {
+  return gram_xy(c, X, X, ldX, sX, B, R, R, L, true, G, R, (int64_t)R * R);
+}
+
+// G[i][j] = a_i . b_j (row-major); symmetric in exact arithmetic at every call site
+int gram(Ctx& c, const double* A, const double* Bm, int B, int R, int64_t n, double* G) {
+  return gram_xy(c, A, Bm, n, (int64_t)R * n, B, R, R, n, true, G, R, (int64_t)R * R);
 }
 
 template <typename T>
@@ -457,11 +457,11 @@ int cholqr2(Ctx& c, const double* A, int B, int T, int64_t L, const int32_t* dim
   double* G = c.take((int64_t)B * T * T);
   KR_TRY(L >= 4096 ? gram(c, A, A, B, T, L, G) : small_gram(c, A, L, (int64_t)T * L, G, T, L, B));
   KR_TRY(chol(c, G, dims, B, T, true, nullptr, o.f1));
-  KR_TRY(rows_mul(c, o.f1.F, (int64_t)T * T, A, L, (int64_t)T * L, tmpQ, L, (int64_t)T * L, T, T, L, B));
+  KR_TRY(rows_mul_lower(c, o.f1.F, (int64_t)T * T, A, L, (int64_t)T * L, tmpQ, L, (int64_t)T * L, T, T, L, B));
   KR_TRY(L >= 4096 ? gram(c, tmpQ, tmpQ, B, T, L, G) : small_gram(c, tmpQ, L, (int64_t)T * L, G, T, L, B));
   KR_TRY(chol(c, G, dims, B, T, false, nullptr, o.f2));
-  KR_TRY(rows_mul(c, o.f2.F, (int64_t)T * T, tmpQ, L, (int64_t)T * L, o.Q, L, (int64_t)T * L, T, T, L, B));
-  return rows_mul(c, o.f2.F, (int64_t)T * T, o.f1.F, T, (int64_t)T * T, o.F, T, (int64_t)T * T, T, T, T, B);
+  KR_TRY(rows_mul_lower(c, o.f2.F, (int64_t)T * T, tmpQ, L, (int64_t)T * L, o.Q, L, (int64_t)T * L, T, T, L, B));
+  return rows_mul_lower(c, o.f2.F, (int64_t)T * T, o.f1.F, T, (int64_t)T * T, o.F, T, (int64_t)T * T, T, T, T, B);
 }
 
 Factor new_factor(Ctx& c, int B, int T) {
@@ -550,12 +550,13 @@ int block_house(Ctx& c, const double* Ab, int t, int k1, int64_t n, double* Wb, 
   // remainder rows, projected twice: Rem -= W1 (W1^T Rem)   (column-major n x m / n x k1 views)
   KR_TRY(cudaMemcpyAsync(Rem, Ab + (int64_t)k1 * n, sizeof(double) * m * n, cudaMemcpyDeviceToDevice, c.st) ==
                  cudaSuccess ? KR_OK : fail(KR_ECUDA, "block_house copy"));
+  const int64_t pwl = gram_dmma_workspace(1, m, k1, n, false);
+  double* pws = c.take(pwl);
   auto project = [&]() -> int {
     for (int pass = 0; pass < 2; ++pass) {
-      KR_TRY(cublas_check(cublasDgemm(c.h, CUBLAS_OP_T, CUBLAS_OP_N, k1, m, (int)n, &one, Wb, (int)n, Rem, (int)n,
-                                      &zero, Cp, k1), "block_house W1^T R"));
-      KR_TRY(cublas_check(cublasDgemm(c.h, CUBLAS_OP_N, CUBLAS_OP_N, (int)n, m, k1, &mone, Wb, (int)n, Cp, k1, &one,
-                                      Rem, (int)n), "block_house R -= W1 C"));
+      // Cp (m x k1, row-major) = Rem rows . W1 rows;  Rem -= Cp W1
+      KR_TRY(gram_dmma(Rem, n, 0, Wb, n, 0, 1, m, k1, n, false, Cp, k1, 0, pws, pwl, c.st));
+      KR_TRY(rows_mul(c, Cp, 0, Wb, n, 0, Rem, n, 0, m, k1, n, 1, -1.0, 1.0));
     }
     return KR_OK;
   };
@@ -577,10 +578,10 @@ int block_house(Ctx& c, const double* Ab, int t, int k1, int64_t n, double* Wb, 
   double* W2 = Wb + (int64_t)k1 * n;
   KR_TRY(gram(c, Rem, Rem, 1, m, n, G));
   KR_TRY(chol(c, G, dm, 1, m, false, nullptr, g1));
-  KR_TRY(rows_mul(c, g1.F, 0, Rem, n, 0, W2, n, 0, m, m, n, 1));
+  KR_TRY(rows_mul_lower(c, g1.F, 0, Rem, n, 0, W2, n, 0, m, m, n, 1));
   KR_TRY(gram(c, W2, W2, 1, m, n, G));
   KR_TRY(chol(c, G, dm, 1, m, false, nullptr, g2));
-  KR_TRY(rows_mul(c, g2.F, 0, W2, n, 0, Rem, n, 0, m, m, n, 1));
+  KR_TRY(rows_mul_lower(c, g2.F, 0, W2, n, 0, Rem, n, 0, m, m, n, 1));
   KR_TRY(cudaMemcpyAsync(W2, Rem, sizeof(double) * m * n, cudaMemcpyDeviceToDevice, c.st) == cudaSuccess
              ? KR_OK : fail(KR_ECUDA, "block_house copy"));
   std::vector<int32_t> b1, b2;
@@ -761,7 +762,7 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
   // first pass into tmpQ or W so that the last pass lands in W (no B x T x n copy back)
   const int npass = shifted ? 2 : 1;
   double* first = (npass % 2 == 1) ? tmpQ : W;
-  KR_TRY(rows_mul(c, f1.F, (int64_t)T * T, A, n, (int64_t)T * n, first, n, (int64_t)T * n, T, T, n, B));
+  KR_TRY(rows_mul_lower(c, f1.F, (int64_t)T * T, A, n, (int64_t)T * n, first, n, (int64_t)T * n, T, T, n, B));
   // second pass (and third when shifted)
   Factor* fp[2] = {&f2, &f3};
   double* cur = first;
@@ -771,8 +772,8 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
   for (int pass = 0; pass < npass; ++pass) {
     KR_TRY(gram(c, cur, cur, B, T, n, G));
     KR_TRY(chol(c, G, d_td, B, T, false, nullptr, *fp[pass], true));
-    KR_TRY(rows_mul(c, fp[pass]->F, (int64_t)T * T, cur, n, (int64_t)T * n, nxt, n, (int64_t)T * n, T, T, n, B));
-    KR_TRY(rows_mul(c, fp[pass]->F, (int64_t)T * T, F, T, (int64_t)T * T, Ft, T, (int64_t)T * T, T, T, T, B));
+    KR_TRY(rows_mul_lower(c, fp[pass]->F, (int64_t)T * T, cur, n, (int64_t)T * n, nxt, n, (int64_t)T * n, T, T, n, B));
+    KR_TRY(rows_mul_lower(c, fp[pass]->F, (int64_t)T * T, F, T, (int64_t)T * T, Ft, T, (int64_t)T * T, T, T, T, B));
     std::swap(F, Ft);
     std::swap(cur, nxt);
   }
@@ -874,9 +875,8 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
         }
       }
       if (!house) {  // M column-major R: M[j][i] = a_j . w_i  (col-major M (T x T) = W_col^T A_col)
-        KR_TRY(cublas_check(cublasDgemm(c.h, CUBLAS_OP_T, CUBLAS_OP_N, T, T, (int)n, &one, W + (int64_t)b * T * n,
-                                        (int)n, A + (int64_t)b * T * n, (int)n, &zero, M + (int64_t)i * T * T, T),
-                            "kr_recycle R"));
+        KR_TRY(gram_xy(c, A + (int64_t)b * T * n, W + (int64_t)b * T * n, n, 0, 1, T, T, n, false,
+                       M + (int64_t)i * T * T, T, 0));
       } else {  // Householder: geqrf/orgqr on A_b (n x t column-major == its rows), W_b = Q rows
         // rare path (rank-deficient candidates): the LAPACK work buffer is sized by cuSOLVER,
         // so it is allocated stream-ordered here instead of from the caller's workspace
@@ -960,11 +960,8 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
       double* FA = c.take((int64_t)B * T * T);
       double* Mh = c.take((int64_t)B * T * T);
       KR_TRY(rows_mul(c, fb.F, (int64_t)T * T, As, T, (int64_t)T * T, FA, T, (int64_t)T * T, T, T, T, B));
-      const double one = 1.0, zero = 0.0;  // Mh = F (F A)^T = F A F^T (symmetric)
-      KR_TRY(cublas_check(cublasDgemmStridedBatched(c.h, CUBLAS_OP_T, CUBLAS_OP_N, T, T, T, &one, fb.F, T,
-                                                    (int64_t)T * T, FA, T, (int64_t)T * T, &zero, Mh, T,
-                                                    (int64_t)T * T, B),
-                          "kr_recycle harmonic congruence"));
+      // Mh = (F A) F^T = F A F^T (symmetric): Mh[i][j] = (FA)_i . F_j
+      KR_TRY(gram_xy(c, FA, fb.F, T, (int64_t)T * T, B, T, T, T, false, Mh, T, (int64_t)T * T));
       Msel = Mh;
     }
     const int64_t el = kr_syev_select_workspace(B, T);

@@ -426,41 +426,8 @@ extern "C" int kr_chol_inv(const double* G, int64_t ldg, int64_t bsg, const int3
 // sample x chunk, pointers built on the device) and the partials are summed in
 // fixed chunk order (deterministic).
 
-namespace kr {
-namespace {
-
-__global__ void gram_ptrs_kernel(const double* A, const double* Bm, int64_t bs, int batch, int S, int64_t c,
-                                 double* part, int64_t tt, const double** pa, const double** pb, double** pc) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= batch * S) return;
-  const int b = i / S, s = i % S;
-  pa[i] = A + (int64_t)b * bs + (int64_t)s * c;
-  pb[i] = Bm + (int64_t)b * bs + (int64_t)s * c;
-  pc[i] = part + (int64_t)i * tt;
-}
-
-__global__ void gram_sum_kernel(const double* part, int S, int64_t tt, int rows, double* G, int64_t ldg,
-                                int64_t bsg) {
-  const int b = blockIdx.y;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tt; e += (int64_t)gridDim.x * blockDim.x) {
-    const double* p = part + (int64_t)b * S * tt + e;
-    double acc = 0.0;
-    for (int s = 0; s < S; ++s) acc += p[(int64_t)s * tt];
-    const int64_t i = e / rows, j = e % rows;  // partial is column-major: element (j, i) = row i of G
-    G[(int64_t)b * bsg + i * ldg + j] = acc;
-  }
-}
-
-}  // namespace
-}  // namespace kr
-
 extern "C" int64_t kr_gram_workspace(int32_t batch, int32_t rows, int64_t n) {
-  if (batch <= 0 || rows <= 0 || n <= 0) return 1;
-  int S = (32 + batch - 1) / batch;
-  if (S > 16) S = 16;
-  while (S > 1 && (n % S != 0 || n / S < 512)) --S;
-  const int64_t tt = (int64_t)rows * rows;
-  return (int64_t)batch * S * tt + 3 * ((int64_t)batch * S + 1);
+  return kr::gram_dmma_workspace(batch, rows, rows, n, false);
 }
 
 extern "C" int kr_gram(const double* A, const double* Bm, int64_t ld, int64_t bs, int32_t batch, int32_t rows,
@@ -471,27 +438,9 @@ extern "C" int kr_gram(const double* A, const double* Bm, int64_t ld, int64_t bs
   if (batch == 0 || rows == 0) return KR_OK;
   KR_CHECK_ARG(A && Bm && G && work, "null pointer");
   KR_CHECK_ARG(work_len >= kr_gram_workspace(batch, rows, n), "workspace too small");
-  cudaStream_t st = (cudaStream_t)stream;
-  int S = (32 + batch - 1) / batch;
-  if (S > 16) S = 16;
-  while (S > 1 && (n % S != 0 || n / S < 512)) --S;
-  const int64_t c = n / S, tt = (int64_t)rows * rows;
-  double* part = work;
-  char* slots = reinterpret_cast<char*>(work + (int64_t)batch * S * tt);
-  const double** pa = (const double**)slots;
-  const double** pb = (const double**)(slots + sizeof(void*) * batch * S);
-  double** pc = (double**)(slots + 2 * sizeof(void*) * batch * S);
-  gram_ptrs_kernel<<<(batch * S + 127) / 128, 128, 0, st>>>(A, Bm, bs, batch, S, c, part, tt, pa, pb, pc);
-  cublasHandle_t h;
-  KR_TRY(cublas_handle(&h, st));
-  const double one = 1.0, zero = 0.0;
-  // column-major C (rows x rows) = B_chunk^T A_chunk: C(j, i) = b_j . a_i
-  KR_TRY(cublas_check(cublasDgemmBatched(h, CUBLAS_OP_T, CUBLAS_OP_N, rows, rows, (int)c, &one, pb, (int)ld, pa,
-                                         (int)ld, &zero, pc, rows, batch * S),
-                      "kr_gram dgemm"));
-  dim3 grid((unsigned)((tt + 255) / 256 < 1024 ? (tt + 255) / 256 : 1024), batch);
-  gram_sum_kernel<<<grid, 256, 0, st>>>(part, S, tt, rows, G, ldg, bsg);
-  return check_launch("kr_gram");
+  // a true Gram (A == B) computes the lower tile blocks and mirrors them
+  return kr::gram_dmma(A, ld, bs, Bm, ld, bs, batch, rows, rows, n, A == Bm, G, ldg, bsg, work, work_len,
+                       (cudaStream_t)stream);
 }
 
 // ---------------------------------------------------------------------------
