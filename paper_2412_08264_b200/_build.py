@@ -62,7 +62,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if failed:
         raise RuntimeError("nvcc failed:\n" + "\n".join(failed))
     tmp = out.with_suffix(".so.tmp")
-    link = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", str(tmp), "-lcublas", "-lcusolver",
+    link = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", str(tmp), "-lcusolver",
             "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
     res = subprocess.run(link, capture_output=True, text=True)
     if res.returncode != 0:

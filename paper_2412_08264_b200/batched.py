@@ -97,7 +97,7 @@ def gram(A: torch.Tensor, Bm: torch.Tensor | None = None) -> torch.Tensor:
     ws = torch.empty(max(wl, 1), dtype=torch.float64, device=A.device)
     _lib.check(L.kr_gram(A.data_ptr(), Bm.data_ptr(), n, T * n, B, T, n, G.data_ptr(), T, T * T, ws.data_ptr(), wl,
                          _lib.stream_ptr()), "kr_gram")
-    _lib.note_launch("kr_gram", 3)
+    _lib.note_launch("kr_gram", 2)
     return G
 
 

@@ -96,7 +96,7 @@ def _warm_thread(shape=None):
     torch.linalg.eigh(g)
     torch.linalg.eigvalsh(g)
     torch.bmm(a.unsqueeze(0), a.unsqueeze(0))
-    # the library's own cuBLAS handle is per host thread as well (kr_gram, kr_jadj)
+    # the library's own cuSOLVER handle (rank-deficient Householder branch) is per host thread as well
     from . import _lib
     from .batched import gram
     gram(torch.zeros(1, 2, 4096, dtype=torch.float64, device="cuda"))

@@ -165,21 +165,7 @@ extern "C" int kr_struct_sizes(int64_t* op_size, int64_t* args_size) {
 
 namespace kr {
 
-// One cuBLAS handle per (host thread, device); the stream is rebound per call.
-int cublas_handle(cublasHandle_t* out, cudaStream_t st) {
-  static thread_local cublasHandle_t handles[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return fail(KR_ECUDA, "device index out of range");
-  if (!handles[dev]) {
-    cublasStatus_t s = cublasCreate(&handles[dev]);
-    if (s != CUBLAS_STATUS_SUCCESS) return fail(KR_ECUDA, "cublasCreate failed");
-  }
-  if (cublasSetStream(handles[dev], st) != CUBLAS_STATUS_SUCCESS) return fail(KR_ECUDA, "cublasSetStream failed");
-  *out = handles[dev];
-  return KR_OK;
-}
-
+// One cuSOLVER handle per (host thread, device); the stream is rebound per call.
 int cusolver_handle(cusolverDnHandle_t* out, cudaStream_t st) {
   static thread_local cusolverDnHandle_t handles[64] = {};
   int dev = 0;
@@ -193,9 +179,5 @@ int cusolver_handle(cusolverDnHandle_t* out, cudaStream_t st) {
   return KR_OK;
 }
 
-int cublas_check(cublasStatus_t s, const char* what) {
-  if (s == CUBLAS_STATUS_SUCCESS) return KR_OK;
-  return fail(KR_ECUDA, std::string(what) + ": cuBLAS status " + std::to_string((int)s));
-}
 
 }  // namespace kr

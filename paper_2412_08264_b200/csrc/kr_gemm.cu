@@ -40,16 +40,26 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// `cnt` consecutive doubles of a row from global to shared, zero-filled past `valid`
-// doubles (valid <= 0: all zero).  V16: 16-byte copies (both addresses 16-byte aligned).
+// Two consecutive doubles of a row from global to shared, zero-filled past `valid` doubles.
+// V16: one 16-byte copy (both addresses 16-byte aligned).  Dead pairs (valid <= 0: pad rows,
+// the tail of the k range) are plain shared stores: a zero-size cp.async still sends its
+// request, and thousands of them on one dummy address serialise in L2 (measured: an edge
+// tile with 10 live rows took as long as a full one).
 template <bool V16>
-__device__ __forceinline__ void cp_pair(double* s, const double* g, const double* safe, int64_t valid) {
-  if (V16) {
-    const int bytes = valid >= 2 ? 16 : valid == 1 ? 8 : 0;
-    cp16(s, bytes ? g : safe, bytes);
+__device__ __forceinline__ void cp_pair(double* s, const double* g, int64_t valid) {
+  if (valid <= 0) {
+    if (V16) {
+      *reinterpret_cast<double2*>(s) = make_double2(0.0, 0.0);
+    } else {
+      s[0] = 0.0;
+      s[1] = 0.0;
+    }
+  } else if (V16) {
+    cp16(s, g, valid >= 2 ? 16 : 8);
   } else {
-    cp8(s, valid >= 1 ? g : safe, valid >= 1 ? 8 : 0);
-    cp8(s + 1, valid >= 2 ? g + 1 : safe, valid >= 2 ? 8 : 0);
+    cp8(s, g, 8);
+    if (valid >= 2) cp8(s + 1, g + 1, 8);
+    else s[1] = 0.0;
   }
 }
 
@@ -71,6 +81,8 @@ struct GramParams {
   int tn;         // tile columns (general case)
   int ntile;      // tiles per (sample, split)
   double* part;   // [batch][S][ntile][GM * GN]
+  const int32_t* dims;  // nullable: per-sample live rows (the rows beyond are zero pad rows)
+  int dim_x, dim_y;     // dims bounds the rows of X / of Y
 };
 
 __device__ __forceinline__ void tile_of(const GramParams& P, int q, int& ti, int& tj) {
@@ -95,6 +107,27 @@ __global__ void __launch_bounds__(GT, 2) gram_dmma_kernel(const GramParams P) {
   const double* Xb = P.X + (int64_t)b * P.bsx;
   const double* Yb = P.Y + (int64_t)b * P.bsy;
   const bool same = P.X == P.Y && ti == tj;  // diagonal tile of a true Gram: one operand tile
+  // live extents: 8-row MMA blocks past them (tile padding, a sample's zero pad rows) are
+  // skipped.  A warp's blocks are dealt cyclically (row blocks wm + 2 mi, column blocks
+  // wn + 4 ni), so the live blocks of an edge tile spread evenly over the warps and over the
+  // SM's four schedulers (a warp is pinned to one)
+  int rx = P.rx, ry = P.ry;
+  if (P.dims) {
+    const int d = P.dims[b];
+    if (P.dim_x && d < rx) rx = d;
+    if (P.dim_y && d < ry) ry = d;
+  }
+  int mcnt = 0, ncnt = 0;  // live row / column blocks of this warp (prefixes: the blocks ascend)
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) mcnt += (ti * GM + (wm + 2 * mi) * 8 < rx) ? 1 : 0;
+#pragma unroll
+  for (int ni = 0; ni < 2; ++ni) ncnt += (tj * GN + (wn + 4 * ni) * 8 < ry) ? 1 : 0;
+  const bool full = mcnt == 4 && ncnt == 2;
+  if (ti * GM >= rx || tj * GN >= ry) {  // nothing live in this tile
+    double* out = P.part + (((int64_t)b * P.S + blockIdx.y) * P.ntile + blockIdx.x) * (GM * GN);
+    for (int e = tid; e < GM * GN; e += GT) out[e] = 0.0;
+    return;
+  }
   const int64_t k_begin = (int64_t)sp * P.chunk;
   const int64_t k_end = k_begin + P.chunk < P.n ? k_begin + P.chunk : P.n;
   const int nk = k_end > k_begin ? (int)((k_end - k_begin + GK - 1) / GK) : 0;
@@ -108,10 +141,10 @@ __global__ void __launch_bounds__(GT, 2) gram_dmma_kernel(const GramParams P) {
       const int c = tid + i * GT, row = c / (GK / 2), cc = (c % (GK / 2)) * 2;
       const int64_t pcol = k0 + cc;
       const int gx = ti * GM + row;
-      cp_pair<V16>(xs + row * GLD + cc, Xb + (int64_t)gx * P.ldx + pcol, P.X, gx < P.rx ? k_end - pcol : 0);
+      cp_pair<V16>(xs + row * GLD + cc, Xb + (int64_t)gx * P.ldx + pcol, gx < rx ? k_end - pcol : 0);
       if (!same) {
         const int gy = tj * GN + row;
-        cp_pair<V16>(ys + row * GLD + cc, Yb + (int64_t)gy * P.ldy + pcol, P.Y, gy < P.ry ? k_end - pcol : 0);
+        cp_pair<V16>(ys + row * GLD + cc, Yb + (int64_t)gy * P.ldy + pcol, gy < ry ? k_end - pcol : 0);
       }
     }
   };
@@ -133,19 +166,35 @@ __global__ void __launch_bounds__(GT, 2) gram_dmma_kernel(const GramParams P) {
     cp_commit();
     const double* xs = gsm + (kt % STAGES) * G_STAGE;
     const double* ys = same ? xs : xs + GM * GLD;
-    const double* xa = xs + (wm * 32 + (lane >> 2)) * GLD + (lane & 3);
-    const double* yb = ys + (wn * 16 + (lane >> 2)) * GLD + (lane & 3);
+    const double* xa = xs + (wm * 8 + (lane >> 2)) * GLD + (lane & 3);
+    const double* yb = ys + (wn * 8 + (lane >> 2)) * GLD + (lane & 3);
+    if (full) {
 #pragma unroll
-    for (int ks = 0; ks < GK / 4; ++ks) {
-      double a[4], bb[2];
+      for (int ks = 0; ks < GK / 4; ++ks) {
+        double a[4], bb[2];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) a[mi] = xa[mi * 8 * GLD + ks * 4];
+        for (int mi = 0; mi < 4; ++mi) a[mi] = xa[mi * 16 * GLD + ks * 4];
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni) bb[ni] = yb[ni * 8 * GLD + ks * 4];
+        for (int ni = 0; ni < 2; ++ni) bb[ni] = yb[ni * 32 * GLD + ks * 4];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
+        for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], bb[ni]);
+          for (int ni = 0; ni < 2; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], bb[ni]);
+      }
+    } else if (mcnt > 0 && ncnt > 0) {
+#pragma unroll
+      for (int ks = 0; ks < GK / 4; ++ks) {
+        double a[4], bb[2];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) a[mi] = mi < mcnt ? xa[mi * 16 * GLD + ks * 4] : 0.0;
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) bb[ni] = ni < ncnt ? yb[ni * 32 * GLD + ks * 4] : 0.0;
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni)
+            if (mi < mcnt && ni < ncnt) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], bb[ni]);
+      }
     }
   }
   cp_wait<0>();
@@ -154,7 +203,7 @@ __global__ void __launch_bounds__(GT, 2) gram_dmma_kernel(const GramParams P) {
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 2; ++ni) {
-      const int r = wm * 32 + mi * 8 + (lane >> 2), cidx = wn * 16 + ni * 8 + 2 * (lane & 3);
+      const int r = (wm + 2 * mi) * 8 + (lane >> 2), cidx = (wn + 4 * ni) * 8 + 2 * (lane & 3);
       *reinterpret_cast<double2*>(out + r * GN + cidx) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
     }
 }
@@ -171,9 +220,9 @@ __global__ void gram_tile_sum_kernel(const GramParams P, double* G, int64_t ldg,
     double acc = 0.0;
     for (int s = 0; s < P.S; ++s) acc += part[(int64_t)s * P.ntile * (GM * GN) + e];
     const int gi = ti * GM + e / GN, gj = tj * GN + e % GN;
-    if (gi < P.rx && gj < P.ry) {
+    if (gi < P.rx && gj < P.ry && !(P.sym && gj > gi)) {  // (the strict upper triangle is the mirror)
       Gb[(int64_t)gi * ldg + gj] = acc;
-      if (P.sym && ti != tj) Gb[(int64_t)gj * ldg + gi] = acc;
+      if (P.sym && gi != gj) Gb[(int64_t)gj * ldg + gi] = acc;
     }
   }
 }
@@ -227,6 +276,8 @@ struct MulParams {
   int lower;    // F lower triangular (zero above the diagonal): the k loop stops at the diagonal block
   int tiles_i;  // row tiles
   int st2;      // 16-byte stores allowed
+  const int32_t* dims;  // nullable: per-sample live extent
+  int dim_r, dim_k;     // dims bounds the output rows (the rest come out as beta Y) / the k extent
 };
 
 template <int BM, bool V16>
@@ -242,8 +293,26 @@ __global__ void __launch_bounds__(GT, 2) rows_mul_dmma_kernel(const MulParams P)
   const double* Fb = P.F + (int64_t)b * P.sF;
   const double* Xb = P.X + (int64_t)b * P.sX;
   double* Yb = P.Y + (int64_t)b * P.sY;
-  const int kend = (P.lower && i0 + BM < P.R1) ? i0 + BM : P.R1;
+  int R2 = P.R2, R1 = P.R1;
+  if (P.dims) {
+    const int d = P.dims[b];
+    if (P.dim_r && d < R2) R2 = d;
+    if (P.dim_k && d < R1) R1 = d;
+  }
+  int kend = (P.lower && i0 + BM < R1) ? i0 + BM : R1;
+  if (i0 >= R2) kend = 0;  // no live row: the tile is beta Y
   const int nk = (kend + MK - 1) / MK;
+  // per 8-row MMA block of this warp (dealt cyclically over the warp rows: block wm + WM mi,
+  // so live rows and the triangular k extents balance): the k extent (0 past the live rows; a
+  // triangular F stops at the block's last row)
+  int kmi[4], kw = 0, kall = 1 << 30;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int rb = i0 + (wm + Gm::WM * mi) * 8;
+    kmi[mi] = rb >= R2 ? 0 : (P.lower && rb + 8 < kend) ? rb + 8 : kend;
+    kw = kmi[mi] > kw ? kmi[mi] : kw;
+    kall = kmi[mi] < kall ? kmi[mi] : kall;
+  }
 
   auto load = [&](int stage, int kt) {
     double* fs = gsm + stage * Gm::STAGE;
@@ -253,15 +322,16 @@ __global__ void __launch_bounds__(GT, 2) rows_mul_dmma_kernel(const MulParams P)
     for (int i = 0; i < (BM * MK) / GT; ++i) {
       const int e = tid + i * GT, row = e / MK, col = e % MK;
       const int gi = i0 + row, gj = k0 + col;
-      const bool ok = gi < P.R2 && gj < kend;
-      cp8(fs + row * MLDF + col, ok ? Fb + (int64_t)gi * P.ldf + gj : P.F, ok ? 8 : 0);
+      const bool ok = gi < R2 && gj < kend;
+      if (ok) cp8(fs + row * MLDF + col, Fb + (int64_t)gi * P.ldf + gj, 8);
+      else fs[row * MLDF + col] = 0.0;
     }
 #pragma unroll
     for (int i = 0; i < (MK * MN / 2) / GT; ++i) {
       const int c = tid + i * GT, row = c / (MN / 2), cc = (c % (MN / 2)) * 2;
       const int gj = k0 + row;
       const int64_t pc = p0 + cc;
-      cp_pair<V16>(xs + row * MLDX + cc, Xb + (int64_t)gj * P.ldX + pc, P.X, gj < kend ? P.L - pc : 0);
+      cp_pair<V16>(xs + row * MLDX + cc, Xb + (int64_t)gj * P.ldX + pc, gj < kend ? P.L - pc : 0);
     }
   };
 
@@ -282,26 +352,39 @@ __global__ void __launch_bounds__(GT, 2) rows_mul_dmma_kernel(const MulParams P)
     cp_commit();
     const double* fs = gsm + (kt % STAGES) * Gm::STAGE;
     const double* xs = fs + BM * MLDF;
-    const double* fa = fs + (wm * 32 + (lane >> 2)) * MLDF + (lane & 3);
+    const double* fa = fs + (wm * 8 + (lane >> 2)) * MLDF + (lane & 3);
     const double* xb = xs + (lane & 3) * MLDX + wn * Gm::WCOLS + (lane >> 2);
 #pragma unroll
     for (int ks = 0; ks < MK / 4; ++ks) {
+      const int kg = kt * MK + ks * 4;
+      if (kg >= kw) break;
       double a[4], bb[Gm::NI];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) a[mi] = fa[mi * 8 * MLDF + ks * 4];
-#pragma unroll
       for (int ni = 0; ni < Gm::NI; ++ni) bb[ni] = xb[ks * 4 * MLDX + ni * 8];
+      if (kg + 4 <= kall) {  // every block live at this k-step: branch-free
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
+        for (int mi = 0; mi < 4; ++mi) a[mi] = fa[mi * Gm::WM * 8 * MLDF + ks * 4];
 #pragma unroll
-        for (int ni = 0; ni < Gm::NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], bb[ni]);
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < Gm::NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], bb[ni]);
+      } else {
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) a[mi] = kg < kmi[mi] ? fa[mi * Gm::WM * 8 * MLDF + ks * 4] : 0.0;
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+          if (kg < kmi[mi]) {
+#pragma unroll
+            for (int ni = 0; ni < Gm::NI; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], bb[ni]);
+          }
+      }
     }
   }
   cp_wait<0>();
   const double alpha = P.alpha, beta = P.beta;
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi) {
-    const int gi = i0 + wm * 32 + mi * 8 + (lane >> 2);
+    const int gi = i0 + (wm + Gm::WM * mi) * 8 + (lane >> 2);
     if (gi >= P.R2) continue;
 #pragma unroll
     for (int ni = 0; ni < Gm::NI; ++ni) {
@@ -351,7 +434,7 @@ int64_t gram_dmma_workspace(int batch, int rx, int ry, int64_t n, bool sym) {
 
 int gram_dmma(const double* X, int64_t ldx, int64_t bsx, const double* Y, int64_t ldy, int64_t bsy, int batch, int rx,
               int ry, int64_t n, bool sym, double* G, int64_t ldg, int64_t bsg, double* work, int64_t work_len,
-              cudaStream_t st) {
+              cudaStream_t st, const int32_t* dims, int dims_mask) {
   if (batch == 0 || rx == 0 || ry == 0) return KR_OK;
   KR_CHECK_ARG(!sym || rx == ry, "symmetric Gram needs equal row counts");
   GramParams P{};
@@ -364,6 +447,9 @@ int gram_dmma(const double* X, int64_t ldx, int64_t bsx, const double* Y, int64_
   P.ldy = ldy;
   P.bsy = bsy;
   P.part = work;
+  P.dims = dims;
+  P.dim_x = dims_mask & 1;
+  P.dim_y = (dims_mask >> 1) & 1;
   const bool v16 = al16(X) && al16(Y) && ldx % 2 == 0 && bsx % 2 == 0 && ldy % 2 == 0 && bsy % 2 == 0;
   const void* fn = v16 ? (const void*)gram_dmma_kernel<true> : (const void*)gram_dmma_kernel<false>;
   KR_TRY(ensure_smem(fn, G_SMEM));
@@ -376,7 +462,7 @@ int gram_dmma(const double* X, int64_t ldx, int64_t bsx, const double* Y, int64_
 
 int rows_mul_dmma(const double* F, int64_t ldf, int64_t sF, const double* X, int64_t ldX, int64_t sX, double* Y,
                   int64_t ldY, int64_t sY, int R2, int R1, int64_t L, int batch, double alpha, double beta, bool lower,
-                  cudaStream_t st) {
+                  cudaStream_t st, const int32_t* dims, int dims_mask) {
   if (batch == 0 || R2 == 0 || L == 0) return KR_OK;
   MulParams P{};
   P.F = F;
@@ -394,6 +480,9 @@ int rows_mul_dmma(const double* F, int64_t ldf, int64_t sF, const double* X, int
   P.alpha = alpha;
   P.beta = beta;
   P.lower = lower ? 1 : 0;
+  P.dims = dims;
+  P.dim_r = dims_mask & 1;
+  P.dim_k = (dims_mask >> 1) & 1;
   const bool v16 = al16(X) && ldX % 2 == 0 && sX % 2 == 0;
   P.st2 = (al16(Y) && ldY % 2 == 0 && sY % 2 == 0) ? 1 : 0;
   if (R2 <= 32) {
@@ -414,5 +503,5 @@ extern "C" int kr_rows_mul(const double* F, int64_t ldf, int64_t bsf, const doub
   KR_CHECK_ARG(F && X && Y, "null pointer");
   KR_CHECK_ARG(ldf >= r1 && ldx >= L && ldy >= L, "leading dimension too small");
   return kr::rows_mul_dmma(F, ldf, bsf, X, ldx, bsx, Y, ldy, bsy, r2, r1, L, batch, alpha, beta, lower != 0,
-                           (cudaStream_t)stream);
+                           (cudaStream_t)stream, nullptr, 0);
 }

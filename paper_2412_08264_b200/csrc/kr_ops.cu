@@ -505,128 +505,10 @@ int kr::hvp_cols(const kr_op* op, const double* V, int64_t ldv, int64_t bsv, int
 }
 
 // ---------------------------------------------------------------------------
-// J W for many columns as convolution + GEMM (the q^2 lag sums of _shift_dot,
-// operators.py:386-408, are (q^2 x n)(n x t) products):
-//   Y_j  = kappa_j . (c_j * W)                      (jw_conv_kernel, + theta0 head partials)
-//   G_j  = Phi_j^T W + Xs^T Y_j                      (two strided-batched DGEMMs, j = 0..J-1)
-//   with Phi_j[d][p] = phi'_j(p + delta_d), Xs[d][p] = xhat(p - delta_d)   (jw_shift_kernel)
-//   out  = -w_j [head_j ; G_j]                       (jw_finish_kernel)
+// J W for many columns through the materialised mixed Jacobian (the q^2 lag sums of
+// _shift_dot, operators.py:386-408, become rows of a p x n matrix):
 
 namespace kr {
-
-constexpr int JW_CHUNK = 256;  // columns per pass (bounds the workspace)
-
-template <int Q>
-__global__ void __launch_bounds__(NT) jw_conv_kernel(kr_op op, int b, const double* __restrict__ W, int64_t ldw,
-                                                    double* __restrict__ Y, double* __restrict__ hpart) {
-  // one block per (tile, column): the input region is staged once and reused by
-  // all J filters (the J filter loop was a grid dimension -- J region loads)
-  constexpr int R = Q / 2, RW = TW + 2 * R, RH = TH + 2 * R, RB = TPX / NT;
-  __shared__ double sw[RH * RW];
-  __shared__ double red[8 * 33 + 8];
-  const int tile = blockIdx.x, c = blockIdx.y, nc = gridDim.y, ntiles = gridDim.x;
-  const int J = op.num_filters;
-  const int tyc = tiles_x(op);
-  const int y0 = (tile / tyc) * TH, x0 = (tile % tyc) * TW;
-  const int64_t n = op_n(op);
-  const double* w = W + c * ldw;
-  for (int i = threadIdx.x; i < RH * RW; i += blockDim.x) {
-    int rr = i / RW, cc = i - rr * RW;
-    int y = y0 - R + rr, x = x0 - R + cc;
-    sw[i] = (y >= 0 && y < op.rows && x >= 0 && x < op.cols) ? w[(int64_t)y * op.cols + x] : 0.0;
-  }
-  block_barrier();
-  const int tx = threadIdx.x % TW, r0 = (threadIdx.x / TW) * RB;
-  const bool quad = op.potential == KR_POT_QUADRATIC;
-  for (int j0 = 0; j0 < J; j0 += 8) {
-    double head[8];
-#pragma unroll
-    for (int jj = 0; jj < 8; ++jj) head[jj] = 0.0;
-    for (int jj = 0; jj < 8 && j0 + jj < J; ++jj) {
-      const int j = j0 + jj;
-      double k[Q][Q];
-      const double* kj = op.kernels + j * Q * Q;
-#pragma unroll
-      for (int a = 0; a < Q; ++a)
-#pragma unroll
-        for (int bb = 0; bb < Q; ++bb) k[a][bb] = kj[a * Q + bb];
-      double acc[RB];
-#pragma unroll
-      for (int i = 0; i < RB; ++i) acc[i] = 0.0;
-#pragma unroll
-      for (int sr = 0; sr < RB + Q - 1; ++sr) {
-        const double* src = sw + (r0 + sr) * RW + tx + 2 * R;
-        double v[Q];
-#pragma unroll
-        for (int bb = 0; bb < Q; ++bb) v[bb] = src[-bb];
-#pragma unroll
-        for (int i = 0; i < RB; ++i) {
-          const int a = i + Q - 1 - sr;  // output row r0+i reads region row r0+i+2R-a
-          if (a >= 0 && a < Q) {
-#pragma unroll
-            for (int bb = 0; bb < Q; ++bb) acc[i] = fma(k[a][bb], v[bb], acc[i]);
-          }
-        }
-      }
-      const double* sl = op.slope + ((int64_t)b * J + j) * n;
-      const double* cv = quad ? nullptr : op.curv + ((int64_t)b * J + j) * n;
-      double* yo = Y + ((int64_t)j * nc + c) * n;
-      double h = 0.0;
-#pragma unroll
-      for (int i = 0; i < RB; ++i) {
-        int y = y0 + r0 + i, x = x0 + tx;
-        if (y < op.rows && x < op.cols) {
-          int64_t p = (int64_t)y * op.cols + x;
-          h = fma(sl[p], acc[i], h);
-          yo[p] = (quad ? 2.0 : cv[p]) * acc[i];
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q == jj) head[q] = h;
-    }
-    block_sum<8>(head, red);
-    if (threadIdx.x < 8 && j0 + threadIdx.x < J)
-      hpart[((int64_t)(j0 + threadIdx.x) * nc + c) * ntiles + tile] = red[threadIdx.x];
-    block_barrier();
-  }
-}
-
-// Phi[j][d][p] = phi'_j(p + delta_d) (j < J), Xs[d][p] = xhat(p - delta_d) (j == J); zero outside.
-__global__ void jw_shift_kernel(kr_op op, int b, double* __restrict__ Phi, double* __restrict__ Xs) {
-  const int q = op.ksize, R = q / 2, d = blockIdx.y, j = blockIdx.z, J = op.num_filters;
-  const int da = d / q - R, db = d % q - R;
-  const int64_t n = op_n(op);
-  const double* src = (j < J) ? op.slope + ((int64_t)b * J + j) * n : op.xhat + (int64_t)b * n;
-  double* dst = (j < J) ? Phi + ((int64_t)j * q * q + d) * n : Xs + (int64_t)d * n;
-  const int sgn = (j < J) ? 1 : -1;
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-    int y = (int)(p / op.cols) + sgn * da, x = (int)(p % op.cols) + sgn * db;
-    dst[p] = (y >= 0 && y < op.rows && x >= 0 && x < op.cols) ? src[(int64_t)y * op.cols + x] : 0.0;
-  }
-}
-
-// out[c][j(1+q2)] = -w_j sum_tiles hpart;  out[c][j(1+q2)+1+d] = -w_j (sum_kc G1 + sum_kc G2)
-__global__ void jw_finish_kernel(kr_op op, const double* __restrict__ G1, const double* __restrict__ G2,
-                                 int nk, const double* __restrict__ hpart, int ntiles, int nc,
-                                 double* __restrict__ out, int64_t ldo) {
-  const int q2 = op.ksize * op.ksize, J = op.num_filters, P = J * (1 + q2), JQ = J * q2;
-  const int c = blockIdx.x;
-  for (int i = threadIdx.x; i < P; i += blockDim.x) {
-    const int j = i / (1 + q2), d = i % (1 + q2);
-    double v = 0.0;
-    if (d == 0) {
-      const double* h = hpart + ((int64_t)j * nc + c) * ntiles;
-      for (int t = 0; t < ntiles; ++t) v += h[t];
-    } else {
-      double a = 0.0, bsum = 0.0;
-      for (int kc = 0; kc < nk; ++kc) a += G1[(int64_t)kc * JQ * nc + (j * q2 + d - 1) + (int64_t)c * JQ];
-      for (int kc = 0; kc < nk; ++kc) bsum += G2[(int64_t)kc * q2 * J * nc + (d - 1) + ((int64_t)j * nc + c) * q2];
-      v = a + bsum;
-    }
-    out[c * ldo + i] = -op.fweights[j] * v;
-  }
-}
 
 // The mixed Jacobian materialised: J w is linear in w, so J W for many columns is
 // one GEMM with the p x n matrix Mt = J (operators.py:411-444 restated per pixel):
@@ -703,26 +585,6 @@ static int jmat_chunk(const kr_op& op) {
   return (int)(c < op.batch ? c : op.batch);
 }
 
-static bool jw_gemm_path(const kr_op& op, int ncols) { return q_variant(op) > 0 && ncols >= 4; }
-
-// split-K chunking of the pixel dimension: kc full chunks of Kc pixels + one remainder
-static void jw_split(int64_t n, int64_t* Kc, int* nfull, int* ntot) {
-  int nk = (int)(n / 2048);
-  nk = nk < 1 ? 1 : (nk > 32 ? 32 : nk);
-  *Kc = n / nk;
-  *nfull = (int)(n / *Kc);
-  *ntot = *nfull + ((n % *Kc) ? 1 : 0);
-}
-
-static int64_t jw_workspace(const kr_op& op, int ncols) {
-  const int64_t n = op_n(op), J = op.num_filters, q2 = (int64_t)op.ksize * op.ksize;
-  const int64_t nc = ncols < JW_CHUNK ? ncols : JW_CHUNK;
-  int64_t Kc;
-  int nf, nt;
-  jw_split(n, &Kc, &nf, &nt);
-  return J * nc * n + J * nc * num_tiles(op) + (J + 1) * q2 * n + 2 * (int64_t)nt * J * q2 * nc;
-}
-
 }  // namespace kr
 
 extern "C" int64_t kr_jadj_workspace(const kr_op* op, int32_t ncols) {
@@ -731,68 +593,8 @@ extern "C" int64_t kr_jadj_workspace(const kr_op* op, int32_t ncols) {
     const int P = op->num_filters * (1 + op->ksize * op->ksize);
     return (int64_t)jmat_chunk(*op) * P * op_n(*op) + gram_dmma_workspace(jmat_chunk(*op), ncols, P, op_n(*op), false);
   }
-  if (jw_gemm_path(*op, ncols)) return jw_workspace(*op, ncols);
   int64_t P = (op->reg_kind == KR_REG_TV) ? 1 : (int64_t)op->num_filters * (1 + op->ksize * op->ksize);
   return (int64_t)op->batch * ncols * num_tiles(*op) * P;
-}
-
-static int jadj_gemm(const kr_op& op, const double* W, int64_t ldw, int64_t bsw, int32_t ncols, double* JW,
-                     int64_t ldo, int64_t bso, double* work, cudaStream_t st) {
-  const int64_t n = op_n(op);
-  const int J = op.num_filters, q = op.ksize, q2 = q * q, ntiles = num_tiles(op), JQ = J * q2;
-  const int P = J * (1 + q2);
-  KR_CHECK_ARG(ldo >= P, "output leading dimension smaller than p");
-  cublasHandle_t h;
-  KR_TRY(cublas_handle(&h, st));
-  const int nc_max = ncols < JW_CHUNK ? ncols : JW_CHUNK;
-  int64_t Kc;
-  int nfull, ntot;
-  jw_split(n, &Kc, &nfull, &ntot);
-  double* Y = work;                                   // [J][nc][n] = n x (J nc) column-major
-  double* hpart = Y + (int64_t)J * nc_max * n;        // [J][nc][tiles]
-  double* Phi = hpart + (int64_t)J * nc_max * ntiles; // [J][q2][n] = n x (J q2) column-major
-  double* Xs = Phi + (int64_t)J * q2 * n;             // [q2][n]    = n x q2 column-major
-  double* G1 = Xs + (int64_t)q2 * n;                  // [kc] (J q2) x nc
-  double* G2 = G1 + (int64_t)ntot * JQ * nc_max;      // [kc] q2 x (J nc)
-  const void* conv = q == 3 ? (const void*)jw_conv_kernel<3> : q == 5 ? (const void*)jw_conv_kernel<5>
-                                                                  : (const void*)jw_conv_kernel<7>;
-  const double one = 1.0, zero = 0.0;
-  for (int b = 0; b < op.batch; ++b) {
-    unsigned sb = (unsigned)((n + 255) / 256 > 512 ? 512 : (n + 255) / 256);
-    jw_shift_kernel<<<dim3(sb, q2, J + 1), 256, 0, st>>>(op, b, Phi, Xs);
-    KR_TRY(check_launch("jw_shift"));
-    for (int c0 = 0; c0 < ncols; c0 += JW_CHUNK) {
-      const int nc = (ncols - c0) < JW_CHUNK ? (ncols - c0) : JW_CHUNK;
-      const double* Wc = W + b * bsw + (int64_t)c0 * ldw;
-      kr_op opv = op;
-      int bb = b;
-      void* args[] = {&opv, &bb, (void*)&Wc, &ldw, &Y, &hpart};
-      cudaError_t e = cudaLaunchKernel(conv, dim3(ntiles, nc), dim3(NT), args, 0, st);
-      if (e != cudaSuccess) return fail(KR_ECUDA, std::string("jw_conv launch: ") + cudaGetErrorString(e));
-      // split-K over pixel chunks: G1[kc] = Phi[kc rows]^T W[kc rows]  ((J q2) x nc)
-      //                            G2[kc] = Xs[kc rows]^T Y[kc rows]   (q2 x (J nc))
-      KR_TRY(cublas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_T, CUBLAS_OP_N, JQ, nc, (int)Kc, &one, Phi, (int)n,
-                                                    Kc, Wc, (int)ldw, Kc, &zero, G1, JQ, (long long)JQ * nc, nfull),
-                          "dgemm Phi^T W"));
-      KR_TRY(cublas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_T, CUBLAS_OP_N, q2, J * nc, (int)Kc, &one, Xs,
-                                                    (int)n, Kc, Y, (int)n, Kc, &zero, G2, q2,
-                                                    (long long)q2 * J * nc, nfull),
-                          "dgemm Xs^T Y"));
-      if (ntot > nfull) {
-        const int64_t off = (int64_t)nfull * Kc, rem = n - off;
-        KR_TRY(cublas_check(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, JQ, nc, (int)rem, &one, Phi + off, (int)n,
-                                        Wc + off, (int)ldw, &zero, G1 + (int64_t)nfull * JQ * nc, JQ),
-                            "dgemm Phi^T W tail"));
-        KR_TRY(cublas_check(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, q2, J * nc, (int)rem, &one, Xs + off, (int)n,
-                                        Y + off, (int)n, &zero, G2 + (int64_t)nfull * q2 * J * nc, q2),
-                            "dgemm Xs^T Y tail"));
-      }
-      jw_finish_kernel<<<nc, 128, 0, st>>>(op, G1, G2, ntot, hpart, ntiles, nc, JW + b * bso + (int64_t)c0 * ldo,
-                                           ldo);
-      KR_TRY(check_launch("jw_finish"));
-    }
-  }
-  return KR_OK;
 }
 
 // J W through the materialised Jacobian: one jmat launch for all samples, then one
@@ -840,7 +642,6 @@ extern "C" int kr_jadj(const kr_op* op, const double* W, int64_t ldw, int64_t bs
   dim3 grid(ntiles, ncols, op->batch);
   cudaStream_t st = (cudaStream_t)stream;
   if (jw_jmat_path(*op, ncols)) return jadj_jmat(*op, W, ldw, bsw, ncols, JW, ldo, bso, work, st);
-  if (jw_gemm_path(*op, ncols)) return jadj_gemm(*op, W, ldw, bsw, ncols, JW, ldo, bso, work, st);
   int P;
   if (op->reg_kind == KR_REG_FILTERS) {
     const int q = op->ksize, rq = q / 2;

@@ -191,7 +191,6 @@ struct WorkspaceOverrun {
 
 struct Ctx {
   cudaStream_t st;
-  cublasHandle_t h;
   double* cur;
   double* end;
   double* base = cur;
@@ -206,22 +205,28 @@ struct Ctx {
 
 // Y rows (B, R2, L) = F rows (B, R2, R1) @ X rows (B, R1, L)  [+ beta Y]; lower: F is a
 // lower-triangular factor (the Cholesky-QR passes) -- half the products are skipped
+// kdims (device, nullable): per-sample live rows of X -- the k loop stops there (the rows past
+// them are zero pad rows)
 int rows_mul(Ctx& c, const double* F, int64_t sF, const double* X, int64_t ldX, int64_t sX, double* Y, int64_t ldY,
-             int64_t sY, int R2, int R1, int64_t L, int B, double alpha = 1.0, double beta = 0.0, bool lower = false) {
-  return rows_mul_dmma(F, R1, sF, X, ldX, sX, Y, ldY, sY, R2, R1, L, B, alpha, beta, lower, c.st);
+             int64_t sY, int R2, int R1, int64_t L, int B, double alpha = 1.0, double beta = 0.0, bool lower = false,
+             const int32_t* kdims = nullptr) {
+  return rows_mul_dmma(F, R1, sF, X, ldX, sX, Y, ldY, sY, R2, R1, L, B, alpha, beta, lower, c.st, kdims,
+                       kdims ? 2 : 0);
 }
+// F = L^-1 D^-1 of a Cholesky-QR pass (identity pad block); dims: per-sample live rows of the
+// square product (pad rows of X are zero, so the pad rows of Y come out zero either way)
 int rows_mul_lower(Ctx& c, const double* F, int64_t sF, const double* X, int64_t ldX, int64_t sX, double* Y,
-                   int64_t ldY, int64_t sY, int R2, int R1, int64_t L, int B) {
-  return rows_mul(c, F, sF, X, ldX, sX, Y, ldY, sY, R2, R1, L, B, 1.0, 0.0, true);
+                   int64_t ldY, int64_t sY, int R2, int R1, int64_t L, int B, const int32_t* dims = nullptr) {
+  return rows_mul_dmma(F, R1, sF, X, ldX, sX, Y, ldY, sY, R2, R1, L, B, 1.0, 0.0, true, c.st, dims, dims ? 3 : 0);
 }
 
 // G (B, Rx, Ry) = X rows (Rx, L) Y rows (Ry, L)^T, rows of stride ld; sym: the result is
 // symmetric (a Gram, or W^T H W up to roundoff) -- lower tile blocks computed and mirrored
 int gram_xy(Ctx& c, const double* X, const double* Y, int64_t ld, int64_t bs, int B, int Rx, int Ry, int64_t L,
-            bool sym, double* G, int64_t ldg, int64_t bsg) {
+            bool sym, double* G, int64_t ldg, int64_t bsg, const int32_t* dims = nullptr) {
   const int64_t wl = gram_dmma_workspace(B, Rx, Ry, L, sym);
   double* ws = c.take(wl);
-  return gram_dmma(X, ld, bs, Y, ld, bs, B, Rx, Ry, L, sym, G, ldg, bsg, ws, wl, c.st);
+  return gram_dmma(X, ld, bs, Y, ld, bs, B, Rx, Ry, L, sym, G, ldg, bsg, ws, wl, c.st, dims, dims ? 3 : 0);
 }
 
 // G (B, R, R) = X rows (R, L) X^T for short rows (L small)
@@ -230,8 +235,10 @@ int small_gram(Ctx& c, const double* X, int64_t ldX, int64_t sX, double* G, int 
 }
 
 // G[i][j] = a_i . b_j (row-major); symmetric in exact arithmetic at every call site
-int gram(Ctx& c, const double* A, const double* Bm, int B, int R, int64_t n, double* G) {
-  return gram_xy(c, A, Bm, n, (int64_t)R * n, B, R, R, n, true, G, R, (int64_t)R * R);
+// dims (device, nullable): per-sample live rows (zero pad rows past them)
+int gram(Ctx& c, const double* A, const double* Bm, int B, int R, int64_t n, double* G,
+         const int32_t* dims = nullptr) {
+  return gram_xy(c, A, Bm, n, (int64_t)R * n, B, R, R, n, true, G, R, (int64_t)R * R, dims);
 }
 
 template <typename T>
@@ -622,9 +629,7 @@ using namespace kr;
 
 
 extern "C" int kr_thread_warmup(void) {
-  cublasHandle_t h;
   cusolverDnHandle_t sh;
-  KR_TRY(cublas_handle(&h, nullptr));
   KR_TRY(cusolver_handle(&sh, nullptr));
   // one tiny Householder QR on this thread's handle (first-call setup off the hot path)
   const int m = 64, q = 8;
@@ -692,14 +697,13 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
                      pop->num_filters == op->num_filters && pop->ksize == op->ksize,
                  "op_proj must describe the same batch and model family as op");
   }
-  Ctx c{(cudaStream_t)stream, nullptr, work, work + work_len};
+  Ctx c{(cudaStream_t)stream, work, work + work_len};
   KR_TRY(up_ring().reset());
   static const bool debug = getenv("KR_RECYCLE_DEBUG") != nullptr;
   const auto t_start = std::chrono::steady_clock::now();
   int n_ill = 0, n_house = 0, n_exact = 0, n_block = 0;
   double house_ms = 0.0;
   bool was_shifted = false;
-  KR_TRY(cublas_handle(&c.h, c.st));
   std::vector<int32_t> t(B), status(B, 0);
   for (int b = 0; b < B; ++b) t[b] = a->kdims[b] + a->sdims[b];
 
@@ -731,7 +735,7 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
   double* G = c.take((int64_t)B * T * T);
   double* F = c.take((int64_t)B * T * T);
   double* Ft = c.take((int64_t)B * T * T);
-  KR_TRY(gram(c, A, A, B, T, n, G));
+  KR_TRY(gram(c, A, A, B, T, n, G, d_td));
   double* nrm = c.take(2 * B);  // ||A||_F^2 = tr(A A^T) (the Gram is reused below), ||R^-1||_F^2
   trace_kernel<<<B, 256, 0, c.st>>>(G, T, nrm);
   // (partial factors: a sample whose passes break down keeps its orthonormalised leading
@@ -762,7 +766,7 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
   // first pass into tmpQ or W so that the last pass lands in W (no B x T x n copy back)
   const int npass = shifted ? 2 : 1;
   double* first = (npass % 2 == 1) ? tmpQ : W;
-  KR_TRY(rows_mul_lower(c, f1.F, (int64_t)T * T, A, n, (int64_t)T * n, first, n, (int64_t)T * n, T, T, n, B));
+  KR_TRY(rows_mul_lower(c, f1.F, (int64_t)T * T, A, n, (int64_t)T * n, first, n, (int64_t)T * n, T, T, n, B, d_td));
   // second pass (and third when shifted)
   Factor* fp[2] = {&f2, &f3};
   double* cur = first;
@@ -770,9 +774,9 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
   KR_TRY(cudaMemcpyAsync(F, f1.F, sizeof(double) * B * T * T, cudaMemcpyDeviceToDevice, c.st) == cudaSuccess
              ? KR_OK : fail(KR_ECUDA, "kr_recycle copy"));
   for (int pass = 0; pass < npass; ++pass) {
-    KR_TRY(gram(c, cur, cur, B, T, n, G));
+    KR_TRY(gram(c, cur, cur, B, T, n, G, d_td));
     KR_TRY(chol(c, G, d_td, B, T, false, nullptr, *fp[pass], true));
-    KR_TRY(rows_mul_lower(c, fp[pass]->F, (int64_t)T * T, cur, n, (int64_t)T * n, nxt, n, (int64_t)T * n, T, T, n, B));
+    KR_TRY(rows_mul_lower(c, fp[pass]->F, (int64_t)T * T, cur, n, (int64_t)T * n, nxt, n, (int64_t)T * n, T, T, n, B, d_td));
     KR_TRY(rows_mul_lower(c, fp[pass]->F, (int64_t)T * T, F, T, (int64_t)T * T, Ft, T, (int64_t)T * T, T, T, T, B));
     std::swap(F, Ft);
     std::swap(cur, nxt);
@@ -932,7 +936,7 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
   else
     KR_TRY(hvp_cols(pop, W, n, (int64_t)T * n, T, d_td, HW, n, (int64_t)T * n, c.st));
   double* Ht = c.take((int64_t)B * T * T);
-  KR_TRY(gram(c, W, HW, B, T, n, Ht));
+  KR_TRY(gram(c, W, HW, B, T, n, Ht, d_td));
   double* coeffs = c.take((int64_t)B * s * T);
   double* Xc = nullptr;
   double* VHmu = nullptr;
@@ -1083,9 +1087,9 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
     normalize_rows_kernel<<<dim3(s, B), 256, 0, c.st>>>(cand, s, n);
     KR_TRY(kr_hvp(op, cand, n, (int64_t)s * n, s, HU, n, (int64_t)s * n, c.st));
   } else {
-    KR_TRY(rows_mul(c, coeffs, (int64_t)s * T, W, n, (int64_t)T * n, cand, n, (int64_t)s * n, s, T, n, B));
+    KR_TRY(rows_mul(c, coeffs, (int64_t)s * T, W, n, (int64_t)T * n, cand, n, (int64_t)s * n, s, T, n, B, 1.0, 0.0, false, d_td));
     if (a->reuse_products && !inner)  // (inner: H W is the previous H's, H U~ needs the upcoming one)
-      KR_TRY(rows_mul(c, coeffs, (int64_t)s * T, HW, n, (int64_t)T * n, HU, n, (int64_t)s * n, s, T, n, B));
+      KR_TRY(rows_mul(c, coeffs, (int64_t)s * T, HW, n, (int64_t)T * n, HU, n, (int64_t)s * n, s, T, n, B, 1.0, 0.0, false, d_td));
     else
       KR_TRY(kr_hvp(op, cand, n, (int64_t)s * n, s, HU, n, (int64_t)s * n, c.st));
   }
@@ -1097,7 +1101,7 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
   KR_TRY(cholqr2(c, HU, B, s, n, d_ns, c.take((int64_t)B * s * n), qu));
   KR_TRY(rows_mul(c, qu.F, (int64_t)s * s, cand, n, (int64_t)s * n, a->U, n, (int64_t)s * n, s, s, n, B));
   if (a->vec_type == 1)
-    KR_TRY(rows_mul(c, VHmu, (int64_t)s * T, W, n, (int64_t)T * n, a->Z, n, (int64_t)s * n, s, T, n, B));
+    KR_TRY(rows_mul(c, VHmu, (int64_t)s * T, W, n, (int64_t)T * n, a->Z, n, (int64_t)s * n, s, T, n, B, 1.0, 0.0, false, d_td));
 
   // ---- 6. per-sample outcome
   std::vector<int32_t> ns, ui1, ui2, bd;
