@@ -573,8 +573,9 @@ __device__ inline void tile_blur_normal_generic(const kr_op& op, const Geom& g, 
 //   stage 1 (fp64 tensor cores, mma.sync m8n8k4 f64 = DMMA): for the group's 8 filters at
 //            once, E[p][j] = kappa_j(p) . sum_tap A[p][tap] K[tap][j] on the (TH+2R) x (TW+2R)
 //            extended tile -- A the im2col of the loaded region (one LDS per lane per MMA),
-//            K the group's taps in registers (Q^2 taps padded to a multiple of 4 with zero
-//            weights), 8 region pixels per MMA row block; the warps share the region's 8-pixel
+//            K the group's taps in registers (Q^2 - 1 taps in k-steps of 4; the last tap
+//            is added by two DFMAs per lane on the accumulator fragment -- 4 pipe cycles
+//            instead of the 16 of a zero-padded MMA), 8 region pixels per MMA row block; the warps share the region's 8-pixel
 //            blocks; E lands in 8 smem planes (plane stride = 2 mod 8 doubles: the epilogue's
 //            stores are conflict-free);
 //   stage 2 (DFMA, one filter per warp): acc += (w_j k_j) corr E_j on the tile, a lane an
@@ -592,7 +593,8 @@ template <int Q>
 struct FiltGeo {
   static constexpr int R = Q / 2, EW = TW + 2 * R, EH = TH + 2 * R, EPIX = EW * EH;
   static constexpr int ESP = ((EPIX + 7) & ~7) + 2;  // plane stride, = 2 (mod 8)
-  static constexpr int NK = (Q * Q + 3) / 4;         // k-steps of 4 taps
+  static constexpr int NK = (Q * Q) / 4;             // full k-steps of 4 taps; Q^2 = 1 (mod 4) for odd Q: the
+                                                     // last tap is two DFMAs per lane instead of a zero-padded MMA
   static constexpr int NMT = (EPIX + 7) / 8;         // 8-pixel row blocks of the region
 };
 
@@ -642,33 +644,36 @@ __device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, 
                                       double* rcost = nullptr) {
   using F = FiltGeo<Q>;
   constexpr int R = F::R, EW = F::EW, EPIX = F::EPIX, ESP = F::ESP, NK = F::NK, NMT = F::NMT, QQ = Q * Q;
+  static_assert(QQ % 4 == 1, "odd filter size: Q^2 - 1 taps in k-steps of 4 plus one");
   static_assert(TH == 16 && TW == 32 && NWARP == 8, "stage-2 lane blocks assume a 16 x 32 tile and 8 warps");
   const int rows = op.rows, cols = op.cols, H = g.H, RW = g.RW, J = op.num_filters;
   const int64_t n = op_n(op);
   const bool quad = op.potential == KR_POT_QUADRATIC;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int kc = lane & 3, mr = lane >> 2;  // MMA fragment column (tap / filter pair) and row (pixel)
-  int aoff[NK];                             // im2col offsets of this lane's taps in the region
+  int aoff[NK > 0 ? NK : 1];                             // im2col offsets of this lane's taps in the region
 #pragma unroll
   for (int ks = 0; ks < NK; ++ks) {
     const int tap = 4 * ks + kc;
-    aoff[ks] = tap < QQ ? -((tap / Q) * RW + tap % Q) : 0;  // pad taps read the pixel itself (weight 0)
+    aoff[ks] = -((tap / Q) * RW + tap % Q);
   }
+  const int alast = -((Q - 1) * RW + (Q - 1));  // the last tap (Q^2 - 1)
   const int bc = lane & 15, br = lane >> 4;  // stage-2 block: rows 8br .. 8br+7, cols 2bc, 2bc+1
   double acc[8][2];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = 0.0;
   for (int g0 = 0; g0 < J; g0 += 8) {
-    double bw[NK];  // B fragment: filter g0 + mr, taps 4 ks + kc
+    double bw[NK > 0 ? NK : 1];  // B fragment: filter g0 + mr, taps 4 ks + kc
     {
       const int j = g0 + mr;
 #pragma unroll
       for (int ks = 0; ks < NK; ++ks) {
         const int tap = 4 * ks + kc;
-        bw[ks] = (j < J && tap < QQ) ? sm.kw[j * QQ + tap] : 0.0;
+        bw[ks] = j < J ? sm.kw[j * QQ + tap] : 0.0;
       }
     }
     const int j0 = g0 + 2 * kc;  // this lane's accumulator filters j0, j0 + 1
+    const double wl0 = j0 < J ? sm.kw[j0 * QQ + QQ - 1] : 0.0, wl1 = j0 + 1 < J ? sm.kw[(j0 + 1) * QQ + QQ - 1] : 0.0;
     const double* c0p = (quad || GRAD || j0 >= J) ? nullptr : op.curv + ((int64_t)b * J + j0) * n;
     const double* c1p = (quad || GRAD || j0 + 1 >= J) ? nullptr : op.curv + ((int64_t)b * J + j0 + 1) * n;
     double* S4 = sm.SA;
@@ -690,6 +695,11 @@ __device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, 
       double d0 = 0.0, d1 = 0.0;
 #pragma unroll
       for (int ks = 0; ks < NK; ++ks) dmma_8x8x4(d0, d1, src[aoff[ks]], bw[ks]);
+      {
+        const double al = src[alast];
+        d0 = fma(al, wl0, d0);
+        d1 = fma(al, wl1, d1);
+      }
       if (pe < EPIX) {
         double e0, e1;
         if constexpr (GRAD) {

@@ -76,6 +76,7 @@ struct DParams {
   int vec2;                    // even image width and 16-byte aligned columns: pixel pairs as double2
   int pipe;                    // odd samples run one phase behind the even ones (A and B units overlap)
   int use_tma;                 // the stencil's halo region comes in one bulk tensor copy (tmap over tmp)
+  int window;                  // samples iterating at a time (the first `window` unfinished ones)
   CUtensorMap tmap;            // (cols, rows, 1, B) view of tmp
 };
 
@@ -405,7 +406,12 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(const __grid_constan
     // (M_FIN: w and r from the stored basis).  Without pipelining all samples are in step
     // (A, B, A, ...); with it the odd samples run one phase behind, so every super-phase
     // mixes compute-heavy A units with streaming B units on the same SMs.
-    const int na = build_list(P, ph, (1u << M_RUN) | (1u << M_FIN) | (1u << M_RUNB), list, wsum);
+    // Sample window: only the first `window` unfinished samples iterate; a finished sample's
+    // place goes to the next one.  Their recycle blocks C and Z (read every iteration) then
+    // stay L2-resident from one iteration to the next instead of streaming from HBM for the
+    // whole batch; per-sample arithmetic does not depend on the window (bitwise the same).
+    int na = build_list(P, ph, (1u << M_RUN) | (1u << M_FIN) | (1u << M_RUNB), list, wsum);
+    if (na > P.window) na = P.window;
     if (na == 0) break;  // identical in every block (M_WAIT only ever coexists with M_RUN samples)
     if (blockIdx.x == 0)
       for (int b = threadIdx.x; b < P.B; b += NT)
@@ -926,6 +932,11 @@ int rminres_dyn(const kr_op& op, const kr_solve_args& a, double* work, int64_t w
                  make_region_tmap(&P.tmap, P.tmp, op.cols, op.rows, 1, B, n, n, TW + 2 * g.H, g.RH))
                     ? 1 : 0;
     if (!P.use_tma) memset(&P.tmap, 0, sizeof P.tmap);
+  }
+  {
+    const char* we = getenv("KR_DYN_WINDOW");
+    int w = we ? atoi(we) : 0;
+    P.window = w > 0 ? w : MAX_B;
   }
   const void* kfn = KR_PICK_Q(rminres_dyn_kernel, q_variant(op));
   KR_TRY(ensure_smem(kfn, L.smem));
