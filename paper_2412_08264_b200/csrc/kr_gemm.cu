@@ -228,12 +228,26 @@ __global__ void gram_tile_sum_kernel(const GramParams P, double* G, int64_t ldg,
 }
 
 int gram_splits(int batch, int ntile, int64_t n) {
-  // enough CTAs for a few waves of 2 per SM; at least 8 k-steps per split
-  int S = (4 * 296 + batch * ntile - 1) / (batch * ntile);
-  const int64_t max_s = (n + 8 * GK - 1) / (8 * GK);
-  if (S > 32) S = 32;
-  if (S > max_s) S = (int)max_s;
-  return S < 1 ? 1 : S;
+  // The CTAs run in whole waves of 2 per SM, each CTA for n / S pixels: pick the split count
+  // that minimises waves x k-tiles per CTA (at t = 330, 16 samples: S = 7 fills 7.95 waves where
+  // S = 4 leaves the fifth wave half empty); at least 8 k-tiles per split, at most 32 splits
+  int sms = device_sms();
+  if (sms < 1) sms = 148;
+  const int64_t slots = 2 * (int64_t)sms, base = (int64_t)batch * ntile;
+  const int64_t kt = (n + GK - 1) / GK;
+  int best = 1;
+  int64_t best_cost = -1;
+  for (int S = 1; S <= 32; ++S) {
+    const int64_t per = (kt + S - 1) / S;
+    if (S > 1 && per < 8) break;
+    const int64_t waves = (base * S + slots - 1) / slots;
+    const int64_t cost = waves * (per + 6);  // + pipeline fill / epilogue of a CTA
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = S;
+    }
+  }
+  return best;
 }
 
 void gram_plan(GramParams& P, int batch, int rx, int ry, int64_t n, bool sym) {
