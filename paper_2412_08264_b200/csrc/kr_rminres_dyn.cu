@@ -37,6 +37,23 @@
 namespace kr {
 namespace dyn {
 
+#ifdef KR_DYN_TIMING
+// block 0's time by section of the unit loop (ns): 0 draw / wait for work, 1 stencil, 2 dots,
+// 3 arrive + last-block reduction (A), 4 phase B unit, 5 finalisation, 6 publish; 7 = A units
+__device__ unsigned long long g_dyn_ns[8];
+#define KR_DMARK(i, last)                                         \
+  do {                                                            \
+    if (threadIdx.x == 0 && blockIdx.x == 0) {                    \
+      unsigned long long t_;                                      \
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));       \
+      g_dyn_ns[i] += t_ - last;                                   \
+      last = t_;                                                  \
+    }                                                             \
+  } while (0)
+#else
+#define KR_DMARK(i, last) ((void)0)
+#endif
+
 // M_RUN: next step is phase A (stencil + dots) of iteration k; M_RUNB: phase B of k;
 // M_FIN: finalisation (w, r); M_WAIT: skips one super-phase (pipelining offset)
 enum Mode : unsigned { M_DONE = 0, M_RUN = 1, M_FIN = 2, M_RUNB = 3, M_WAIT = 4, M_INIT = 0xff };
@@ -77,6 +94,11 @@ struct DParams {
   int pipe;                    // odd samples run one phase behind the even ones (A and B units overlap)
   int use_tma;                 // the stencil's halo region comes in one bulk tensor copy (tmap over tmp)
   int window;                  // samples iterating at a time (the first `window` unfinished ones)
+  int dataflow;                // barrier-free schedule: per-sample phase tickets instead of grid barriers
+  int group_b;                 // tiles per draw of a phase-B unit (dataflow schedule)
+  int prio;                    // dataflow schedule: draw from the lowest unfinished sample first
+  unsigned long long* tick;    // [B] kind << 56 | phase sequence << 32 | tiles dispensed in the current phase
+  int* sched;                  // [2] head (first sample that may be unfinished), samples done
   CUtensorMap tmap;            // (cols, rows, 1, B) view of tmp
 };
 
@@ -244,6 +266,72 @@ __device__ inline void solve_y(const DParams& P, int b, int K, double* scratch, 
 
 #define DYN_GRID_SYNC() grid_barrier(P.bar, (unsigned)P.G, grid_target)
 
+// Barrier-free schedule: every sample carries a ticket word
+//   [63:56] kind of its current phase (M_RUN / M_RUNB / M_FIN / M_DONE)
+//   [55:32] phase sequence number     [31:0] tiles dispensed in this phase.
+// A block draws tiles of the current phase of one of the first `window` unfinished samples
+// (a group of `group_b` tiles for the short streaming phase B, one tile otherwise); the block
+// that completes a phase (last arrival) does the sample's reduction and scalar step and then
+// publishes the next phase's word.  No block ever waits for another except by looking for
+// work, so samples drift apart and one sample's serial tail (reduction, scalar recurrences)
+// overlaps the others' tiles.  Warp 0 collectively: the 32 lanes look at the 32 samples from
+// the head in one round trip, one lane draws.  Returns false when every sample is done.
+__device__ __forceinline__ unsigned long long tick_word(unsigned kind, unsigned seq, unsigned lo) {
+  return ((unsigned long long)kind << 56) | ((unsigned long long)(seq & 0xffffffu) << 32) | lo;
+}
+constexpr unsigned TICK_DONE_LO = 0x7fffffffu;
+__device__ __noinline__ bool grab_unit(const DParams& P, int* b_out, int* tile_out, int* cnt_out, unsigned* md_out,
+                                       unsigned* seq_out) {
+  const int lane = threadIdx.x & 31;
+  unsigned spin = 0;
+  for (;;) {
+    const int done = *reinterpret_cast<volatile int*>(P.sched + 1);
+    const int head = *reinterpret_cast<volatile int*>(P.sched);
+    if (done >= P.B) return false;
+    const int bb = head + lane;
+    const unsigned long long w = bb < P.B ? *reinterpret_cast<volatile unsigned long long*>(P.tick + bb)
+                                          : tick_word(M_DONE, 0, TICK_DONE_LO);
+    const unsigned kind = (unsigned)(w >> 56), lo = (unsigned)w;
+    const bool fin = kind == M_DONE;
+    const unsigned fm = __ballot_sync(0xffffffffu, fin);
+    const int lead = fm == 0xffffffffu ? 32 : __ffs(~fm) - 1;  // leading finished samples: the head moves on
+    if (lane == 0 && lead > 0) atomicMax(P.sched, head + lead < P.B ? head + lead : P.B);
+    const int rank = __popc(~fm & ((1u << lane) - 1u));        // unfinished samples before this one
+    const bool avail = !fin && rank < P.window && lo < (unsigned)P.ntiles;
+    const unsigned am = __ballot_sync(0xffffffffu, avail);
+    if (am == 0) {
+      if (!(fm == 0xffffffffu && head + 32 < P.B)) __nanosleep(64);
+      ++spin;
+      continue;
+    }
+    // prio: lowest unfinished sample first (depth-first: the few leading samples get every
+    // block they can use and stay L2-resident, the rest of the window takes the overflow);
+    // otherwise a block-dependent start spreads the blocks over the window
+    const int start = P.prio ? 0 : (int)((blockIdx.x + spin) & 31u);
+    const unsigned rot = start ? ((am >> start) | (am << (32 - start))) : am;
+    const int pick = (__ffs(rot) - 1 + start) & 31;
+    unsigned long long old = 0;
+    int G = 1;
+    if (lane == pick) {
+      G = kind == M_RUNB ? P.group_b : 1;
+      old = atomicAdd(P.tick + bb, (unsigned long long)G);
+    }
+    old = __shfl_sync(0xffffffffu, old, pick);
+    G = __shfl_sync(0xffffffffu, G, pick);
+    const unsigned okind = (unsigned)(old >> 56), olo = (unsigned)old;
+    if (okind != M_DONE && olo < (unsigned)P.ntiles) {
+      __threadfence();
+      *b_out = head + pick;
+      *tile_out = (int)olo;
+      *cnt_out = (int)olo + G <= P.ntiles ? G : P.ntiles - (int)olo;
+      *md_out = okind;
+      *seq_out = (unsigned)(old >> 32) & 0xffffffu;
+      return true;
+    }
+    ++spin;
+  }
+}
+
 template <int Q>
 __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(const __grid_constant__ DParams P) {
   unsigned int grid_target = 0;
@@ -261,6 +349,8 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(const __grid_constan
   __shared__ int wsum[NWARP];
   __shared__ int s_flag;
   __shared__ int s_unit;
+  __shared__ int s_b, s_tile, s_cnt;   // dataflow schedule: the drawn unit
+  __shared__ unsigned s_md, s_seq, s_pub;
   __shared__ double sc[8];
   const int64_t n = P.n;
   const int s = A.s, ns = A.stop_kind >= 1 ? A.nsc_s : 0;
@@ -382,6 +472,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(const __grid_constan
         if (m == M_RUN && P.pipe && (b & 1)) m = M_WAIT;
         S.k = 1;
         mode_set(P, b, ph, M_INIT, m);
+        if (P.dataflow) P.tick[b] = tick_word(m, 1, 0);
       }
       block_barrier();
       // t0 - Omega (Omega = 0) for a sample that finishes here
@@ -410,26 +501,64 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(const __grid_constan
     // place goes to the next one.  Their recycle blocks C and Z (read every iteration) then
     // stay L2-resident from one iteration to the next instead of streaming from HBM for the
     // whole batch; per-sample arithmetic does not depend on the window (bitwise the same).
-    int na = build_list(P, ph, (1u << M_RUN) | (1u << M_FIN) | (1u << M_RUNB), list, wsum);
-    if (na > P.window) na = P.window;
-    if (na == 0) break;  // identical in every block (M_WAIT only ever coexists with M_RUN samples)
-    if (blockIdx.x == 0)
-      for (int b = threadIdx.x; b < P.B; b += NT)
-        if (mode_at(P, b, ph) == M_WAIT) mode_set(P, b, ph, M_WAIT, M_RUN);
+    int na = 0;
+    if (!P.dataflow) {
+      na = build_list(P, ph, (1u << M_RUN) | (1u << M_FIN) | (1u << M_RUNB), list, wsum);
+      if (na > P.window) na = P.window;
+      if (na == 0) break;  // identical in every block (M_WAIT only ever coexists with M_RUN samples)
+      if (blockIdx.x == 0)
+        for (int b = threadIdx.x; b < P.B; b += NT)
+          if (mode_at(P, b, ph) == M_WAIT) mode_set(P, b, ph, M_WAIT, M_RUN);
+    }
     // units are taken from a ticket counter (the next ticket requested while the current
     // unit runs): blocks that drew heavy units take fewer -- the super-phase ends when the
     // work does, not when the unluckiest block's fixed share does.  Unit u is tile u / na
     // of list sample u % na (samples interleaved: A and B units mix on every SM, and
     // neighbouring tiles of a sample run concurrently for the halo's L2 reuse).
     unsigned int* tickets = P.grab + (ph & 1);
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(P.grab + ((ph + 1) & 1), 0u);
-    if (threadIdx.x == 0) s_unit = (int)atomicAdd(tickets, 1u);
-    block_barrier();
-    for (int u = s_unit; u < na * nt; u = s_unit) {
+    if (!P.dataflow) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(P.grab + ((ph + 1) & 1), 0u);
+      if (threadIdx.x == 0) s_unit = (int)atomicAdd(tickets, 1u);
+      block_barrier();
+    }
+#ifdef KR_DYN_TIMING
+    unsigned long long dlast = 0;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(dlast));
+#endif
+    for (;;) {
       unsigned int next_ticket = 0;
-      if (threadIdx.x == 0) next_ticket = atomicAdd(tickets, 1u);
-      const int b = list[u % na], tile = u / na;
-      const unsigned md = mode_at(P, b, ph);
+      int b, tile0, tcount = 1;
+      unsigned md;
+      if (P.dataflow) {
+        if (threadIdx.x < 32) {
+          int gb = -1, gt = 0, gc = 1;
+          unsigned gm = 0, gs = 0;
+          if (!grab_unit(P, &gb, &gt, &gc, &gm, &gs)) gb = -1;
+          if (threadIdx.x == 0) {
+            s_b = gb;
+            s_tile = gt;
+            s_cnt = gc;
+            s_md = gm;
+            s_seq = gs;
+            s_pub = 0xffu;
+          }
+        }
+        block_barrier();
+        if (s_b < 0) break;
+        b = s_b;
+        tile0 = s_tile;
+        tcount = s_cnt;
+        md = s_md;
+      } else {
+        const int u = s_unit;
+        if (u >= na * nt) break;
+        if (threadIdx.x == 0) next_ticket = atomicAdd(tickets, 1u);
+        b = list[u % na];
+        tile0 = u / na;
+        md = mode_at(P, b, ph);
+      }
+      KR_DMARK(0, dlast);
+      for (int tile = tile0; tile < tile0 + tcount; ++tile) {
       if (md == M_RUN) {
         const double beta = __ldcg(&P.st[b].beta);
         const int k = *reinterpret_cast<volatile int*>(&P.st[b].k);
@@ -440,7 +569,8 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(const __grid_constan
         double* vk = vcol(P, b, k);
         const TmaSrc tsrc{&P.tmap, 0, b, beta, &mbar, &mphase};
         tile_hvp_t<Q>(op, g, sm, b, TileIn{tb, beta, nullptr, 0.0}, tile, P.use_tma ? &tsrc : nullptr);
-        if (P.use_tma && threadIdx.x == 0 && next_ticket < (unsigned)(na * nt)) {
+        KR_DMARK(1, dlast);
+        if (P.use_tma && !P.dataflow && threadIdx.x == 0 && next_ticket < (unsigned)(na * nt)) {
           // the next unit's halo region into L2 while this unit's dots run (its bulk copy then
           // hits L2; a finalisation unit's region is only a wasted prefetch)
           const int nb = list[next_ticket % na], ntl = next_ticket / na, tyc = tiles_x(op);
@@ -565,6 +695,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(const __grid_constan
           for (int c = threadIdx.x; c < ns; c += NT) partp(P, b, SL_ZHV + c)[tile] = def_sum(red, (c / 8) * 25 + 16 + c % 8);
           if (threadIdx.x == 0) partp(P, b, SL_VHV)[tile] = def_sum(red, 24);
         }
+        KR_DMARK(2, dlast);
         if (arrive(P, b, &s_flag)) {
           reduce_tiles(P, b, 0, 2 * s + 1 + ns, slot);
           double* chv = vecp(P, b, V_CHV);
@@ -580,9 +711,14 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(const __grid_constan
             for (int i = 0; i < s; ++i) corr += slot[SL_CV + i] * slot[SL_CHV + i];
             P.st[b].alpha = slot[SL_VHV] - corr;
             mode_set(P, b, ph, M_RUN, M_RUNB);
+            s_pub = M_RUNB;
           }
         }
         block_barrier();
+        KR_DMARK(3, dlast);
+#ifdef KR_DYN_TIMING
+        if (threadIdx.x == 0 && blockIdx.x == 0) g_dyn_ns[7] += 1;
+#endif
       } else if (md == M_RUNB) {
         // ===== phase B: u = hv_k - C chv - alpha v_k - beta_k v_{k-1}, ||u||^2; then finish iteration k =====
       St* S = P.st + b;
@@ -737,6 +873,7 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(const __grid_constan
           }
           sc[6] = (double)m;
           mode_set(P, b, ph, M_RUNB, m);
+          s_pub = m;
         }
         block_barrier();
         if (sc[6] == (double)M_FIN) {
@@ -817,14 +954,36 @@ __global__ void __launch_bounds__(NT, 2) rminres_dyn_kernel(const __grid_constan
             A.iters[b] = P.st[b].iters;
             A.reasons[b] = P.st[b].reason;
             mode_set(P, b, ph, M_FIN, M_DONE);
+            s_pub = M_DONE;
           }
         }
         block_barrier();
       }
       block_barrier();
-      if (threadIdx.x == 0) s_unit = (int)next_ticket;
+      if (md == M_RUNB) KR_DMARK(4, dlast);
+      else if (md != M_RUN) KR_DMARK(5, dlast);
+      }  // tiles of the drawn unit
+      if (P.dataflow) {
+        // the block that completed the sample's phase publishes the next one (after all of
+        // its own post-processing above: the barrier orders the block's writes, the fence
+        // makes them visible before the word)
+        if (threadIdx.x == 0 && s_pub != 0xffu) {
+          __threadfence();
+          if (s_pub == M_DONE) {
+            atomicExch(P.tick + b, tick_word(M_DONE, 0, TICK_DONE_LO));
+            __threadfence();
+            atomicAdd(P.sched + 1, 1);
+          } else {
+            atomicExch(P.tick + b, tick_word(s_pub, s_seq + 1, 0));
+          }
+        }
+      } else {
+        if (threadIdx.x == 0) s_unit = (int)next_ticket;
+      }
       block_barrier();
+      KR_DMARK(6, dlast);
     }
+    if (P.dataflow) break;
     DYN_GRID_SYNC();
     ++ph;
   }
@@ -866,7 +1025,7 @@ void dyn_plan(const kr_op& op, const kr_solve_args& a, DynLayout& L) {
   const int64_t hv = L.track ? (int64_t)B * a.max_iter * n : (int64_t)B * n;
   L.total = (int64_t)B * n + hv + ((a.w0 && L.track) ? (int64_t)B * n : 0) + (int64_t)B * L.nslot * L.ntiles +
             (int64_t)B * (sizeof(St) / 8) + (int64_t)B * NVEC * MAX_S + (int64_t)B * (a.max_iter + 1) * 4 +
-            (int64_t)B * a.max_iter + B /*mode*/ + (B + 2) /*cnt, bar (as doubles)*/ + 8;
+            (int64_t)B * a.max_iter + B /*mode*/ + (B + 2) /*cnt, bar (as doubles)*/ + B /*tick*/ + 2 /*sched*/ + 8;
 }
 
 }  // namespace
@@ -917,6 +1076,8 @@ int rminres_dyn(const kr_op& op, const kr_solve_args& a, double* work, int64_t w
   P.cnt = reinterpret_cast<int*>(take(B + 2));
   P.bar = reinterpret_cast<unsigned int*>(P.cnt + B + 1);
   P.grab = reinterpret_cast<unsigned int*>(P.cnt + B + 2);
+  P.tick = reinterpret_cast<unsigned long long*>(take(B));
+  P.sched = reinterpret_cast<int*>(take(2));
   // pipelining pays when every super-phase still has several units per block
   const char* pe = getenv("KR_DYN_PIPE");
   P.pipe = pe ? (pe[0] == '1') : 0;  // measured: no gain once units are ticketed (C3: 1326 vs 1315 ms)
@@ -937,15 +1098,34 @@ int rminres_dyn(const kr_op& op, const kr_solve_args& a, double* work, int64_t w
     const char* we = getenv("KR_DYN_WINDOW");
     int w = we ? atoi(we) : 0;
     P.window = w > 0 ? w : MAX_B;
+    const char* de = getenv("KR_DYN_DATAFLOW");
+    P.dataflow = (de && de[0] == '1') ? 1 : 0;
+    if (P.dataflow) P.pipe = 0;
+    const char* ge = getenv("KR_DYN_GROUPB");
+    P.group_b = ge && atoi(ge) > 0 ? atoi(ge) : 4;
+    const char* pr = getenv("KR_DYN_PRIO");
+    P.prio = (pr && pr[0] == '1') ? 1 : 0;
   }
   const void* kfn = KR_PICK_Q(rminres_dyn_kernel, q_variant(op));
   KR_TRY(ensure_smem(kfn, L.smem));
   cudaMemsetAsync(P.vecs, 0, sizeof(double) * (size_t)B * NVEC * MAX_S, st);
   cudaMemsetAsync(P.mode, 0xff, sizeof(unsigned long long) * (size_t)B, st);
   cudaMemsetAsync(P.cnt, 0, sizeof(double) * (size_t)(B + 2), st);
+  cudaMemsetAsync(P.tick, 0, sizeof(double) * (size_t)(B + 2), st);
   void* args[] = {&P};
   cudaError_t e = cudaLaunchCooperativeKernel(kfn, dim3(P.G), dim3(NT), args, L.smem, st);
   if (e != cudaSuccess) return fail(KR_ECUDA, std::string("rminres cooperative launch: ") + cudaGetErrorString(e));
+#ifdef KR_DYN_TIMING
+  {
+    cudaStreamSynchronize(st);
+    unsigned long long h[8] = {};
+    cudaMemcpyFromSymbol(h, kr::dyn::g_dyn_ns, sizeof h);
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(kr::dyn::g_dyn_ns, z, sizeof z);
+    fprintf(stderr, "dyn block0 us: draw %.0f stencil %.0f dots %.0f arriveA %.0f phaseB %.0f fin %.0f publish %.0f; A units %llu\n",
+            h[0] / 1e3, h[1] / 1e3, h[2] / 1e3, h[3] / 1e3, h[4] / 1e3, h[5] / 1e3, h[6] / 1e3, h[7]);
+  }
+#endif
   return check_launch("kr_rminres (dyn)");
 }
 
