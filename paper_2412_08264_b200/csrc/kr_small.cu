@@ -427,7 +427,11 @@ extern "C" int kr_chol_inv(const double* G, int64_t ldg, int64_t bsg, const int3
 // fixed chunk order (deterministic).
 
 extern "C" int64_t kr_gram_workspace(int32_t batch, int32_t rows, int64_t n) {
-  return kr::gram_dmma_workspace(batch, rows, rows, n, false);
+  // kr_gram plans a true Gram (A == B) on the lower tile blocks and a general product on all
+  // tiles; their split counts differ, so the workspace covers both
+  const int64_t a = kr::gram_dmma_workspace(batch, rows, rows, n, false);
+  const int64_t b = kr::gram_dmma_workspace(batch, rows, rows, n, true);
+  return a > b ? a : b;
 }
 
 extern "C" int kr_gram(const double* A, const double* Bm, int64_t ld, int64_t bs, int32_t batch, int32_t rows,
