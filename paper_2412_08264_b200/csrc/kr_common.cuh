@@ -373,9 +373,10 @@ __host__ __device__ constexpr int pick_run(int lanes, int len, int BS) {
 // GRAD = true (the lower-level gradient, operators.py:329-353 generalised): pass 2's
 // A x gets y subtracted inside the image (residual A x - y) and the data cost
 // sum (A x - y)^2 of the tile's own pixels is accumulated into *dcost.
+// init = true: pass 4 writes res instead of accumulating into it (no pointwise term before it).
 template <int BS, bool GRAD = false>
 __device__ inline void blur_normal_bs(const kr_op& op, const Geom& g, Smem& sm, int y0, int x0,
-                                      const double* ydata = nullptr, double* dcost = nullptr) {
+                                      const double* ydata = nullptr, double* dcost = nullptr, bool init = false) {
   constexpr int RB = BS / 2;
   constexpr int H1 = TH + 4 * RB, W1 = TW + 2 * RB, W1P = W1 + 1, H2 = TH + 2 * RB, W3P = TW + 1;
   constexpr int RX1 = pick_run(H1, W1, BS), RY2 = pick_run(W1, H2, BS), RX3 = pick_run(H2, TW, BS),
@@ -494,7 +495,10 @@ __device__ inline void blur_normal_bs(const kr_op& op, const Geom& g, Smem& sm, 
       }
 #pragma unroll
       for (int i = 0; i < RY4; ++i)
-        if (r0 + i < TH) sm.res[(r0 + i) * TW + c] += ds * acc[i];
+        if (r0 + i < TH) {
+          double* o = sm.res + (r0 + i) * TW + c;
+          *o = init ? ds * acc[i] : *o + ds * acc[i];
+        }
     }
   }
   block_barrier();
@@ -506,13 +510,11 @@ __device__ inline void tile_blur_normal_generic(const kr_op& op, const Geom& g, 
 // Blur data term on the loaded region: res (+)= data_scale * A^T A v.
 __device__ inline void tile_blur_normal(const kr_op& op, const Geom& g, Smem& sm, int y0, int x0,
                                         bool accumulate) {
-  if (accumulate) {
-    switch (op.blur_size) {
-      case 9: blur_normal_bs<9>(op, g, sm, y0, x0); return;
-      case 15: blur_normal_bs<15>(op, g, sm, y0, x0); return;
-      case 21: blur_normal_bs<21>(op, g, sm, y0, x0); return;
-      default: break;
-    }
+  switch (op.blur_size) {
+    case 9: blur_normal_bs<9>(op, g, sm, y0, x0, nullptr, nullptr, !accumulate); return;
+    case 15: blur_normal_bs<15>(op, g, sm, y0, x0, nullptr, nullptr, !accumulate); return;
+    case 21: blur_normal_bs<21>(op, g, sm, y0, x0, nullptr, nullptr, !accumulate); return;
+    default: break;
   }
   tile_blur_normal_generic(op, g, sm, y0, x0, accumulate);
 }
@@ -792,22 +794,26 @@ __device__ inline void tile_hvp_t(const kr_op& op, const Geom& g, Smem& sm, int 
   }
   KR_SMARK(0, slast);
 
-  // pointwise part: mask data term + ridge
-  const double* mask = (op.data_kind == KR_DATA_MASK) ? op.mask + (int64_t)b * op.mask_bstride : nullptr;
-  for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
-    int ty = l / TW, tx = l - ty * TW;
-    int y = y0 + ty, x = x0 + tx;
-    double v = sm.S0[(ty + H) * g.RW + tx + H];
-    double acc = 0.0;
-    if (y < rows && x < cols) {
-      if (mask) acc = (op.data_scale == 1.0 ? mask[(int64_t)y * cols + x] : op.data_scale * mask[(int64_t)y * cols + x]) * v;
-      acc += op.ridge * v;
+  // pointwise part: mask data term + ridge (a blur data term without ridge has none: the
+  // blur's last pass then writes res instead of accumulating -- 0 + x = x, bitwise the same)
+  const bool pointwise = !(op.data_kind == KR_DATA_BLUR && op.ridge == 0.0);
+  if (pointwise) {
+    const double* mask = (op.data_kind == KR_DATA_MASK) ? op.mask + (int64_t)b * op.mask_bstride : nullptr;
+    for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
+      int ty = l / TW, tx = l - ty * TW;
+      int y = y0 + ty, x = x0 + tx;
+      double v = sm.S0[(ty + H) * g.RW + tx + H];
+      double acc = 0.0;
+      if (y < rows && x < cols) {
+        if (mask) acc = (op.data_scale == 1.0 ? mask[(int64_t)y * cols + x] : op.data_scale * mask[(int64_t)y * cols + x]) * v;
+        acc += op.ridge * v;
+      }
+      sm.res[l] = acc;
     }
-    sm.res[l] = acc;
+    block_barrier();
   }
-  block_barrier();
   KR_SMARK(1, slast);
-  if (op.data_kind == KR_DATA_BLUR) tile_blur_normal(op, g, sm, y0, x0, true);
+  if (op.data_kind == KR_DATA_BLUR) tile_blur_normal(op, g, sm, y0, x0, pointwise);
   KR_SMARK(2, slast);
 
   if (Q > 0 && op.reg_kind == KR_REG_FILTERS) {
