@@ -50,7 +50,7 @@ extern "C" {
 
 typedef struct CUstream_st* kr_stream_t; /* == cudaStream_t */
 
-#define KR_ABI_VERSION 5
+#define KR_ABI_VERSION 6
 
 /* Largest candidate width t = k_prev + s_prev of the small dense kernels and the recycle
  * update: BASELINE C5 with s = 80 and 500 iterations (t <= 580), with margin. */

@@ -39,7 +39,7 @@ class KrOp(ctypes.Structure):
     ]
 
 
-ABI_VERSION = 5  # KR_ABI_VERSION of include/krecycle_b200.h
+ABI_VERSION = 6  # KR_ABI_VERSION of include/krecycle_b200.h
 
 
 class KrSolveArgs(ctypes.Structure):

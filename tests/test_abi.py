@@ -24,7 +24,7 @@ def declared_functions():
 def test_library_builds_and_loads():
     assert lib_path().exists(), "run __graft_entry__.build() first"
     L = _lib.load_library()
-    assert L.kr_abi_version() == _lib.ABI_VERSION == 5
+    assert L.kr_abi_version() == _lib.ABI_VERSION == 6
 
 
 def test_every_declared_symbol_is_exported():
