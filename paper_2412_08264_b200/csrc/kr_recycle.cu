@@ -174,6 +174,58 @@ __global__ void normalize_rows_kernel(double* X, int R, int64_t L) {
   for (int64_t i = threadIdx.x; i < L; i += blockDim.x) x[i] *= sc;
 }
 
+// Unit rows with the eigensolver's sign convention (largest-|component| positive)
+__global__ void normalize_sign_rows_kernel(double* X, int R, int64_t L) {
+  const int r = blockIdx.x, b = blockIdx.y;
+  double* x = X + ((int64_t)b * R + r) * L;
+  __shared__ double red[8 * 33 + 8];
+  __shared__ double smax[256];
+  __shared__ int64_t simax[256];
+  double v[1] = {0.0};
+  double best = -1.0;
+  int64_t bi = 0;
+  for (int64_t i = threadIdx.x; i < L; i += blockDim.x) {
+    v[0] += x[i] * x[i];
+    if (fabs(x[i]) > best) {
+      best = fabs(x[i]);
+      bi = i;
+    }
+  }
+  smax[threadIdx.x] = best;
+  simax[threadIdx.x] = bi;
+  block_sum<1>(v, red);
+  if (threadIdx.x == 0) {  // first index of the largest magnitude
+    for (int t = 1; t < (int)blockDim.x; ++t)
+      if (smax[t] > smax[0] || (smax[t] == smax[0] && simax[t] < simax[0])) {
+        smax[0] = smax[t];
+        simax[0] = simax[t];
+      }
+  }
+  __syncthreads();
+  const double nr = sqrt(red[0]);
+  const double sc = (nr > 0.0 ? 1.0 / nr : 1.0) * (x[simax[0]] < 0.0 ? -1.0 : 1.0);
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < L; i += blockDim.x) x[i] *= sc;
+}
+
+// Q1t[b][c][i] = QS[b][i][c] for c < p: the first p entries of the rows of QS, transposed
+__global__ void transpose_head_kernel(const double* QS, int P, int T, int p, double* Q1t) {
+  __shared__ double tile[32][33];
+  const int b = blockIdx.z;
+  const double* src = QS + (int64_t)b * T * P;
+  double* dst = Q1t + (int64_t)b * p * T;
+  const int i0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = i0 + r, cc = c0 + threadIdx.x;
+    tile[r][threadIdx.x] = (i < T && cc < p) ? src[(int64_t)i * P + cc] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int cc = c0 + r, i = i0 + threadIdx.x;
+    if (cc < p && i < T) dst[(int64_t)cc * T + i] = tile[threadIdx.x][r];
+  }
+}
+
 // M (column-major, ld T) <- upper triangle of the t x t R held column-major in A (ld n)
 __global__ void copy_r_kernel(const double* A, int64_t n, int t, double* M, int T) {
   const int j = blockIdx.x;
@@ -1017,13 +1069,42 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
     qs.f1 = new_factor(c, B, T);
     qs.f2 = new_factor(c, B, T);
     KR_TRY(cholqr2(c, S, B, T, P, d_td, c.take((int64_t)B * T * P), qs));
-    // Q1^T Q1 (Q1 = first p entries of every row of QS)
-    double* Mq = c.take((int64_t)B * T * T);
-    KR_TRY(small_gram(c, qs.Q, P, (int64_t)T * P, Mq, T, p, B));
-    const int64_t el = kr_syev_select_workspace(B, T);
+    // Right singular vectors of Q1 (= first p entries of every row of QS) for the s largest
+    // alpha: eigenvectors of Q1^T Q1 (t x t).  When every sample has more candidates than
+    // parameters (t_b > p: Q1^T Q1 has rank <= p) and the t x t problem is beyond the
+    // shared-memory eigensolver while p x p is not, the same vectors come from the p x p dual
+    // Q1 Q1^T y = alpha^2 y as z = Q1^T y / alpha (well conditioned for the LARGEST alpha, the
+    // only ones size L selects): C3 at steady state t = 330, p = 208 -- 13 ms of one-CTA-per-
+    // matrix eigensolver on the update's critical chain become ~1.5 ms.
+    int tmin = T;
+    for (int b = 0; b < B; ++b) tmin = t[b] < tmin ? t[b] : tmin;
+    static const bool dual_off = getenv("KR_GSVD_DUAL") && getenv("KR_GSVD_DUAL")[0] == '0';
+    const bool dual = !dual_off && T > 228 && p <= 228 && p >= s && tmin > p;
+    const int64_t el = kr_syev_select_workspace(B, dual ? p : T);
     double* Zs = c.take((int64_t)B * s * T);
-    KR_TRY(hi_stream().run(c.st, [&](cudaStream_t st) { return kr_syev_select(Mq, T, (int64_t)T * T, d_td, B, T, 1, s, nullptr, 0, Zs, T, (int64_t)s * T, d_ns,
-                          c.take(el), el, st); }));
+    if (!dual) {
+      double* Mq = c.take((int64_t)B * T * T);
+      KR_TRY(small_gram(c, qs.Q, P, (int64_t)T * P, Mq, T, p, B));
+      KR_TRY(hi_stream().run(c.st, [&](cudaStream_t st) { return kr_syev_select(Mq, T, (int64_t)T * T, d_td, B, T, 1, s, nullptr, 0, Zs, T, (int64_t)s * T, d_ns,
+                            c.take(el), el, st); }));
+    } else {
+      double* Q1t = c.take((int64_t)B * p * T);
+      transpose_head_kernel<<<dim3((T + 31) / 32, (p + 31) / 32, B), dim3(32, 8), 0, c.st>>>(qs.Q, P, T, p, Q1t);
+      KR_TRY(check_launch("transpose_head"));
+      double* Md = c.take((int64_t)B * p * p);  // Q1 Q1^T
+      KR_TRY(rows_mul(c, Q1t, (int64_t)p * T, qs.Q, P, (int64_t)T * P, Md, p, (int64_t)p * p, p, T, p, B));
+      int32_t* d_pd = reinterpret_cast<int32_t*>(c.take((B + 1) / 2 + 1));
+      {
+        std::vector<int32_t> hp(B, p);
+        KR_TRY(h2d(c, d_pd, hp.data(), B));
+      }
+      double* Yd = c.take((int64_t)B * s * p);
+      KR_TRY(hi_stream().run(c.st, [&](cudaStream_t st) { return kr_syev_select(Md, p, (int64_t)p * p, d_pd, B, p, 1, s, nullptr, 0, Yd, p, (int64_t)s * p, d_ns,
+                            c.take(el), el, st); }));
+      KR_TRY(rows_mul(c, Yd, (int64_t)s * p, Q1t, T, (int64_t)p * T, Zs, T, (int64_t)s * T, s, p, T, B));
+      normalize_sign_rows_kernel<<<dim3(s, B), 256, 0, c.st>>>(Zs, s, T);
+      KR_TRY(check_launch("normalize_sign_rows"));
+    }
     // the bracket decision (host), overlapping the eigen kernel
     if (!joined) {
       KR_TRY(ss.wait(c.st));
@@ -1043,8 +1124,9 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
     if (!exact.empty()) {  // exact extreme eigenvalues where the bracket straddles the limit
       double* ext = c.take(2 * (int64_t)B);
       double* zz = c.take(2 * (int64_t)B * T);
+      const int64_t elT = kr_syev_select_workspace(B, T);
       KR_TRY(hi_stream().run(c.st, [&](cudaStream_t st) { return kr_syev_select(Ht, T, (int64_t)T * T, d_td, B, T, 2, 2, ext, 2, zz, T, 2 * (int64_t)T, nullptr,
-                            c.take(el), el, st); }));
+                            c.take(elT), elT, st); }));
       std::vector<double> ex;
       KR_TRY(d2h(c, ex, ext, 2 * B));
       for (int b : exact) {
