@@ -1078,7 +1078,8 @@ static int recycle_update_impl(const kr_op* op, const kr_recycle_args* a, double
     // matrix eigensolver on the update's critical chain become ~1.5 ms.
     int tmin = T;
     for (int b = 0; b < B; ++b) tmin = t[b] < tmin ? t[b] : tmin;
-    static const bool dual_off = getenv("KR_GSVD_DUAL") && getenv("KR_GSVD_DUAL")[0] == '0';
+    const char* de = getenv("KR_GSVD_DUAL");  // (read per call: the tests run both forms)
+    const bool dual_off = de && de[0] == '0';
     const bool dual = !dual_off && T > 228 && p <= 228 && p >= s && tmin > p;
     const int64_t el = kr_syev_select_workspace(B, dual ? p : T);
     double* Zs = c.take((int64_t)B * s * T);

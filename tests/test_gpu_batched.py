@@ -387,11 +387,14 @@ def test_recycle_update_rank_drop_block_householder():
         assert torch.allclose(got[0].nsc_data.values, ref.nsc_data.values, rtol=1e-8)
 
 
-@pytest.mark.parametrize("strategy", ["RGen-L(R)-NSC", "Ritz-L"])
-def test_recycle_update_wide_candidates(strategy):
+@pytest.mark.parametrize("strategy,dual", [("RGen-L(R)-NSC", "1"), ("RGen-L(R)-NSC", "0"), ("Ritz-L", "1")])
+def test_recycle_update_wide_candidates(strategy, dual, monkeypatch):
     """Candidate widths beyond the shared-memory kernels (t ~ 330, the C3 regime): the
     native orchestrator (global-workspace Cholesky / eigen-select, 8-CTA cluster QRCP)
-    against the per-sample reference-semantics path."""
+    against the per-sample reference-semantics path.  RGen runs both forms of the GSVD's
+    eigen step: the t x t problem Q1^T Q1 (KR_GSVD_DUAL=0) and, since t > p = 208 here, the
+    p x p dual Q1 Q1^T (default)."""
+    monkeypatch.setenv("KR_GSVD_DUAL", dual)
     from paper_2412_08264_b200 import HessianSolveConfig, SequenceSolver, batched
     from paper_2412_08264_b200.bilevel import hypergradients
     from paper_2412_08264_b200.problems import DeblurConfig, make_batch, synthetic_sequence
