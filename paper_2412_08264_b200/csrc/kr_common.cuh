@@ -311,10 +311,22 @@ __device__ inline void tma_load_region(const TmaSrc& t, const Geom& g, int y0, i
       "r"(ph)
       : "memory");
   const double div = t.div;
-  for (int i = threadIdx.x; i < g.RH * BW; i += blockDim.x) {
-    const int yy = i / BW, xx = i - yy * BW;
-    const double v = stage[i];
-    S0[yy * g.RW + xx] = div == 1.0 ? v : v / div;
+  {
+    // (row, column) of the thread's elements carried incrementally: one division per thread
+    const int nt = (int)blockDim.x, dq = nt / BW, dm = nt - dq * BW;
+    int yy = (int)threadIdx.x / BW, xx = (int)threadIdx.x - yy * BW;
+    int o = yy * g.RW + xx;
+    const int dro = dq * g.RW + dm, wrap = g.RW - BW;
+    for (int i = threadIdx.x; i < g.RH * BW; i += nt) {
+      const double v = stage[i];
+      S0[o] = div == 1.0 ? v : v / div;
+      xx += dm;
+      o += dro;
+      if (xx >= BW) {
+        xx -= BW;
+        o += wrap;
+      }
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) *t.phase = ph ^ 1u;
@@ -645,7 +657,7 @@ template <int Q, bool GRAD = false>
 __device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, int b, int y0, int x0,
                                       double* rcost = nullptr) {
   using F = FiltGeo<Q>;
-  constexpr int R = F::R, EW = F::EW, EPIX = F::EPIX, ESP = F::ESP, NK = F::NK, NMT = F::NMT, QQ = Q * Q;
+  constexpr int R = F::R, EW = F::EW, EH_ = F::EH, EPIX = F::EPIX, ESP = F::ESP, NK = F::NK, NMT = F::NMT, QQ = Q * Q;
   static_assert(QQ % 4 == 1, "odd filter size: Q^2 - 1 taps in k-steps of 4 plus one");
   static_assert(TH == 16 && TW == 32 && NWARP == 8, "stage-2 lane blocks assume a 16 x 32 tile and 8 warps");
   const int rows = op.rows, cols = op.cols, H = g.H, RW = g.RW, J = op.num_filters;
@@ -679,21 +691,29 @@ __device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, 
     const double* c0p = (quad || GRAD || j0 >= J) ? nullptr : op.curv + ((int64_t)b * J + j0) * n;
     const double* c1p = (quad || GRAD || j0 + 1 >= J) ? nullptr : op.curv + ((int64_t)b * J + j0 + 1) * n;
     double* S4 = sm.SA;
+    // this lane's region pixel pe = 8 mt + mr advances by 8 NWARP = 64 pixels per iteration:
+    // its row / column in the extended tile, its offset in the loaded region, its global
+    // pixel index and its plane slot are carried incrementally (no division, no 64-bit
+    // products in the loop)
+    constexpr int STEP = 8 * NWARP, DR = STEP / EW, DC = STEP - DR * EW;
+    int pe = 8 * warp + mr;
+    int re = pe / EW, ce = pe - re * EW;
+    int soff = (re + H) * RW + ce + H;                            // offset of the pixel in S0
+    int64_t gp = (int64_t)(y0 - R + re) * cols + (x0 - R + ce);   // global pixel index
+    double* e0p = S4 + (2 * kc) * ESP + pe;
     for (int mt = warp; mt < NMT; mt += NWARP) {
-      const int pe = 8 * mt + mr;
-      const int pc = pe < EPIX ? pe : EPIX - 1;
-      const int re = pc / EW, ce = pc - re * EW;
+      const bool live = pe < EPIX;
       const int y = y0 - R + re, x = x0 - R + ce;
-      const bool in = pe < EPIX && y >= 0 && y < rows && x >= 0 && x < cols;
+      const bool in = live && (unsigned)y < (unsigned)rows && (unsigned)x < (unsigned)cols;
       double cv0 = 0.0, cv1 = 0.0;
       if constexpr (!GRAD) {
         if (in) {
-          const int64_t p = (int64_t)y * cols + x;
-          cv0 = quad ? 2.0 : (c0p ? __ldg(c0p + p) : 0.0);
-          cv1 = quad ? 2.0 : (c1p ? __ldg(c1p + p) : 0.0);
+          cv0 = quad ? 2.0 : (c0p ? __ldg(c0p + gp) : 0.0);
+          cv1 = quad ? 2.0 : (c1p ? __ldg(c1p + gp) : 0.0);
         }
       }
-      const double* src = sm.S0 + (re + H) * RW + ce + H;
+      // (a padded slot past the region reads the region's last pixel, like the clamp it replaces)
+      const double* src = sm.S0 + (live ? soff : (EH_ - 1 + H) * RW + (EW - 1) + H);
       double d0 = 0.0, d1 = 0.0;
 #pragma unroll
       for (int ks = 0; ks < NK; ++ks) dmma_8x8x4(d0, d1, src[aoff[ks]], bw[ks]);
@@ -702,7 +722,7 @@ __device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, 
         d0 = fma(al, wl0, d0);
         d1 = fma(al, wl1, d1);
       }
-      if (pe < EPIX) {
+      if (live) {
         double e0, e1;
         if constexpr (GRAD) {
           // phi' and phi of u = (c_j * x) (the potential, operators.py:5-7 / DESIGN section 2);
@@ -731,8 +751,20 @@ __device__ inline void tile_filters_q(const kr_op& op, const Geom& g, Smem& sm, 
           e0 = cv0 * d0;
           e1 = cv1 * d1;
         }
-        S4[(2 * kc) * ESP + pe] = e0;
-        S4[(2 * kc + 1) * ESP + pe] = e1;
+        e0p[0] = e0;
+        e0p[ESP] = e1;
+      }
+      pe += STEP;
+      e0p += STEP;
+      ce += DC;
+      re += DR;
+      soff += DR * RW + DC;
+      gp += (int64_t)DR * cols + DC;
+      if (ce >= EW) {
+        ce -= EW;
+        re += 1;
+        soff += RW - EW;
+        gp += cols - EW;
       }
     }
     block_barrier();
