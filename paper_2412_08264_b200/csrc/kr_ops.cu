@@ -97,9 +97,18 @@ __global__ void __launch_bounds__(NT) hvp_kernel(kr_op op, const double* __restr
   const TmaSrc t{&tmap, col, b, 1.0, &mbar, &mphase};
   tile_hvp_t<Q>(op, g, sm, b, TileIn{in, 1.0, nullptr, 0.0}, tile, use_tma ? &t : nullptr);
   double* out = HV + b * bso + col * ldo;
-  for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
-    int64_t p = tile_pixel(op, tile, l);
-    if (p >= 0) out[p] = sm.res[l];
+  if (op.data_kind == KR_DATA_DENSE) {
+    for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
+      int64_t p = tile_pixel(op, tile, l);
+      if (p >= 0) out[p] = sm.res[l];
+    }
+  } else {  // the tile's origin once, not per element
+    const int tyc = tiles_x(op);
+    const int y0 = (tile / tyc) * TH, x0 = (tile % tyc) * TW;
+    for (int l = threadIdx.x; l < TPX; l += blockDim.x) {
+      const int y = y0 + l / TW, x = x0 + l % TW;
+      if (y < op.rows && x < op.cols) out[(int64_t)y * op.cols + x] = sm.res[l];
+    }
   }
 }
 
