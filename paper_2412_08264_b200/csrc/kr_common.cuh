@@ -380,7 +380,10 @@ __host__ __device__ constexpr int pick_run(int lanes, int len, int BS) {
     const long long items = (long long)lanes * ((len + r - 1) / r);
     const long long rounds = (items + NT - 1) / NT;
     const long long cost = rounds * (r * BS + r + BS - 1);
-    if (cost * 100 <= best_cost * 103) return r;
+#ifndef KR_PICK_SLACK
+#define KR_PICK_SLACK 3
+#endif
+    if (cost * 100 <= best_cost * (100 + KR_PICK_SLACK)) return r;
   }
   return best;
 }
